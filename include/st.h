@@ -1,0 +1,173 @@
+/*
+ * st.h — C ABI of the B200-native all-at-once space-time solver (libst.so).
+ *
+ * Method: arxiv 2508.09589 (Alexandersen & Appel). The library solves the stabilised
+ * continuous-Galerkin space-time finite-element system of transient heat conduction
+ *     K(rho) T = f            (sec. 3.1.2; weak form PAPER.md:338-353)
+ * its adjoint (transposed) system
+ *     K(rho)^T lambda = dphi/dT   (sec. 3.3.3)
+ * and the element sensitivities
+ *     dphi/drho_e = -lambda^T (dK/drho_e) T
+ * with FGMRES right-preconditioned by one space-time geometric multigrid
+ * V-cycle per iteration on the semi-coarsened hierarchy of Algorithm 1,
+ * Galerkin coarse operators J_{l+1} = P_l^T J_l P_l.
+ *
+ * Conventions:
+ *  - All floating point is IEEE fp64.
+ *  - Coordinates are the rescaled ones: x in [0,1]^sdim, t in [0,1];
+ *    k~ = k tau / L^2, Q~ = Q tau (Delta T = 1).
+ *  - Node layout: index = i1 + (n+1)*(i2 + (n+1)*([i3 + (n+1)*] it)), x1 fastest, t slowest.
+ *    N_n = (n+1)^sdim (nt+1) doubles per nodal vector (T, lambda, dJdT, f).
+ *  - Element layout of rho and dJ: space-time design (ST_SPACE_TIME): [nt][n]..[n] (x1
+ *    fastest), n^sdim nt doubles; time-constant design (ST_TIME_CONSTANT, the extruded design
+ *    of PAPER.md:262, 604-608): [n]..[n], n^sdim doubles, and dJ is summed through time.
+ *  - Pointers may be DEVICE pointers (current device of the context) or HOST pointers;
+ *    the library detects host memory (cudaPointerGetAttributes) and stages it through
+ *    device buffers inside the call. Caller owns every vector; the context owns workspaces.
+ *  - Every call enqueues on the context's stream and returns after completion.
+ *  - Dirichlet data (R-1..R-4): T = T0 on the t = 0 node plane (initial
+ *    condition); T = 0 on the sink patch of the face x1 = 0 (all t) whose transverse
+ *    coordinates lie within halfwidth of center. Symmetric elimination with unit diagonal.
+ *  - Return value: ST_OK or a negative ST_E_* code; st_strerror() gives text.
+ *    No C++ exception crosses this boundary.
+ */
+#ifndef ST_H_
+#define ST_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ST_ABI_VERSION 1
+
+enum {
+  ST_OK = 0,
+  ST_E_INVALID_ARG = -1,   /* bad size, null pointer, non-square grid, n < 2      */
+  ST_E_DIVISIBILITY = -2,  /* a level cannot be halved in the direction Algorithm 1 picks      */
+  ST_E_NOT_CONVERGED = -3, /* maxit reached; best iterate written and stats filled             */
+  ST_E_BREAKDOWN = -4,     /* Krylov breakdown (zero norm / non-finite value)                   */
+  ST_E_OOM = -5,           /* device allocation failed                                          */
+  ST_E_CUDA = -6,          /* CUDA runtime error (text via st_strerror / st_last_error)         */
+  ST_E_NCCL = -7,          /* communicator error                                                */
+  ST_E_UNSUPPORTED = -8    /* option combination not implemented                                */
+};
+
+enum { ST_TIME_CONSTANT = 0, ST_SPACE_TIME = 1 };
+enum { ST_SRC_UNIFORM = 0, ST_SRC_SIN = 1 };
+enum { ST_SMOOTH_JACOBI = 0, ST_SMOOTH_CHEBYSHEV = 1 };
+
+/* Regular space-time mesh of n^sdim x nt elements. L, tau only rescale. */
+typedef struct {
+  int32_t sdim;   /* 2 ((2+1)D, 8-node trilinear hex) or 3 ((3+1)D, 16-node element)   */
+  int64_t n;      /* elements per spatial direction (square/cubic elements)            */
+  int64_t nt;     /* time elements                                                     */
+  double L, tau;  /* characteristic length and final time           */
+} st_grid_t;
+
+/* Modified SIMP: C = C_ins + (C_con-C_ins) rho^p_c,
+ * k = k_ins + (k_con-k_ins) rho^p_k; k~ = k tau / L^2. */
+typedef struct { double C_ins, C_con, p_c, k_ins, k_con, p_k; } st_materials_t;
+
+/* Dirichlet data. face: 0 = x1 = 0 (only face implemented). */
+typedef struct {
+  double T0;          /* value on the t = 0 node plane                                   */
+  int32_t has_patch;  /* 0 => insulated everywhere except the IC                         */
+  int32_t face;
+  double center, halfwidth; /* fractions of L; BASELINE default 0.5, 0.05               */
+} st_bcs_t;
+
+/* Source Q (physical units): UNIFORM Q0;  SIN: Q0 (1 + a sin(w t_phys)), t_phys = tau t. */
+typedef struct { int32_t kind; double Q0, a, w; } st_source_t;
+
+typedef struct {
+  int32_t design_mode;      /* ST_TIME_CONSTANT | ST_SPACE_TIME                          */
+  double rtol;              /* FGMRES stop: true ||b - K T|| / ||b|| <= rtol              */
+  int32_t maxit;            /* max outer iterations (total over restarts)                */
+  int32_t restart;          /* FGMRES restart length m                                   */
+  int32_t smoother;         /* ST_SMOOTH_JACOBI                                          */
+  int32_t nu_pre, nu_post;  /* smoothing sweeps                                          */
+  double omega;             /* Jacobi damping                                            */
+  double lambda_crit;       /* Algorithm 1 threshold (0.5)                 */
+  int64_t coarse_max_nodes; /* stop coarsening at <= this many nodes (R-19)     */
+  int32_t max_levels;       /* 0 = unlimited                                             */
+  int32_t full_coarsening;  /* 1 = coarsen space and time together    */
+  int32_t use_graphs;       /* capture the V-cycle in a CUDA graph                        */
+  int32_t verbose;
+} st_options_t;
+
+/* Distribution (time slabs). NULL or size == 1 => one GPU. */
+typedef struct { void* nccl_comm; int32_t rank, size; void* cuda_stream; int32_t device; } st_dist_t;
+
+typedef struct st_ctx st_ctx_t;
+
+typedef struct {
+  int32_t iterations;        /* outer FGMRES iterations of the last solve                 */
+  int32_t restarts;
+  double rel_residual;       /* final TRUE relative residual ||b - K x|| / ||b||          */
+  double setup_ms, solve_ms; /* last rho-dependent setup and last solve, device ms         */
+  int32_t n_levels;
+  int32_t converged;
+} st_stats_t;
+
+typedef struct {
+  int32_t n_levels;
+  int64_t n[32], nt[32];     /* elements per level                                        */
+  int32_t kind[32];          /* 0 fine, 1 space, 2 time, 3 full                            */
+  int32_t form[32];          /* operator storage: 0 matrix-free (rho), 1 MK, 2 block-4, 3 dense */
+  int64_t nodes[32];
+} st_hierarchy_t;
+
+/* Fill `o` with the library defaults (rtol 1e-8, restart 30, Jacobi nu 2/2 omega 0.7,
+ * lambda_crit 0.5, coarse_max_nodes 400). */
+void st_default_options(st_options_t* o);
+
+/* Validate, run Algorithm 1, allocate all workspaces, assemble f on the device.
+ * Errors: ST_E_INVALID_ARG, ST_E_DIVISIBILITY, ST_E_OOM, ST_E_CUDA. */
+int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* bcs,
+             const st_source_t* src, const st_options_t* opts, const st_dist_t* dist,
+             st_ctx_t** out);
+
+void st_destroy(st_ctx_t* ctx);
+
+/* Forward solve K_bc(rho) T = b. T: in = initial guess (warm start,
+ * PAPER.md:385), out = solution with prescribed values at constrained nodes.
+ * rho: element densities (layout above). Returns ST_OK or ST_E_NOT_CONVERGED (best
+ * iterate written). */
+int st_solve(st_ctx_t* ctx, const double* rho, double* T);
+
+/* Adjoint solve K_bc(rho)^T lambda = m_f .* dJdT. lambda: in = initial
+ * guess, out = solution (0 at constrained nodes). dJdT at constrained nodes is ignored. */
+int st_adjoint(st_ctx_t* ctx, const double* rho, const double* dJdT, double* lambda);
+
+/* Sensitivities dJ_e = -lambda_e^T (dC/drho G + dk~/drho Kx) T_e,
+ * summed through time for a time-constant design. */
+int st_sensitivity(st_ctx_t* ctx, const double* rho, const double* T, const double* lambda,
+                   double* dJ);
+
+/* Test hook: y = K x (transpose = 0) or K^T x (1); bc = 1 applies the eliminated
+ * operator m_f K m_f + m_c, bc = 0 the unconstrained K. */
+int st_apply(st_ctx_t* ctx, const double* rho, const double* x, double* y, int transpose, int bc);
+
+/* Source vector f and the eliminated right-hand side b. */
+int st_rhs(st_ctx_t* ctx, const double* rho, double* f, double* b);
+
+/* Multigrid test hooks on level l (0 = finest): y = A_l x (masked, Galerkin operator). */
+int st_level_apply(st_ctx_t* ctx, const double* rho, int level, const double* x, double* y,
+                   int transpose);
+
+int st_get_stats(const st_ctx_t* ctx, st_stats_t* s);
+int st_get_hierarchy(const st_ctx_t* ctx, st_hierarchy_t* h);
+int64_t st_num_nodes(const st_ctx_t* ctx);
+int64_t st_num_design(const st_ctx_t* ctx);
+/* Number of kernels this library launched since setup (bench evidence). */
+int64_t st_kernel_launches(const st_ctx_t* ctx);
+const char* st_strerror(int code);
+const char* st_last_error(void);
+int st_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ST_H_ */

@@ -1,0 +1,846 @@
+// api.cu — the C ABI of libst (include/st.h): context, Algorithm-1 hierarchy, rho-dependent
+// Galerkin setup, V-cycle, FGMRES, adjoint, sensitivities. Host orchestration in C++;
+// every arithmetic step of the path runs in the CUDA kernels of ops/transfer/krylov/misc.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "st.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace st;
+
+namespace {
+thread_local std::string g_last_error;
+
+struct StErr {
+  int code;
+  std::string msg;
+};
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      throw StErr{e_ == cudaErrorMemoryAllocation ? ST_E_OOM : ST_E_CUDA,               \
+                  std::string(#call) + ": " + cudaGetErrorString(e_)};                  \
+  } while (0)
+
+struct Level {
+  Geom g{};
+  int kind = KIND_FINE;
+  OpDesc op{};
+  double* st = nullptr;  // owned stencil storage (null if shared / RHO)
+  bool st_owned = false;
+  long long st_elems = 0;
+  double *x = nullptr, *b = nullptr, *r = nullptr, *t = nullptr;
+  bool dense = false;
+  double *A = nullptr, *Ainv = nullptr;
+  int* info = nullptr;
+};
+}  // namespace
+
+struct st_ctx {
+  st_grid_t grid{};
+  st_materials_t mats{};
+  st_bcs_t bcs{};
+  st_source_t src{};
+  st_options_t opt{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sd = 2;
+  bool tc = true;
+  MatsDev md{};
+  std::vector<Level> lv;
+  long long N = 0, ndesign = 0, ld = 0;
+  double *f = nullptr, *b = nullptr, *tmpN = nullptr, *tmpN2 = nullptr;
+  double *V = nullptr, *Z = nullptr;
+  RedWs ws{};
+  double* dsmall = nullptr;
+  double* hsmall = nullptr;
+  double* rho_stage = nullptr;
+  double* io_stage[4] = {nullptr, nullptr, nullptr, nullptr};
+  long long io_n[4] = {0, 0, 0, 0};
+  double rho_ck[2] = {0.0, 0.0};
+  bool have_ops = false;
+  st_stats_t stats{};
+  long long launches = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+namespace {
+
+void L(st_ctx* c, long long n = 1) { c->launches += n; }
+
+void check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw StErr{ST_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e)};
+}
+
+template <class T> void dalloc(T** p, size_t count) {
+  CK(cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T)));
+}
+
+Geom make_geom(int sd, int n, int nt, int plo, int phi) {
+  Geom g{};
+  g.sd = sd;
+  g.n = n;
+  g.nn = n + 1;
+  g.nt = nt;
+  g.P = 1;
+  for (int d = 0; d < sd; ++d) g.P *= g.nn;
+  g.N = g.P * (nt + 1);
+  g.plo = plo;
+  g.phi = phi;
+  g.dx = 1.0 / n;
+  g.dt = 1.0 / nt;
+  return g;
+}
+
+int nc_of(int sd) { return sd == 2 ? 5 : 14; }
+
+// E' = W0^T E W0 + W1^T E W1 (linear-in-time prolongation, two fine layers per coarse layer)
+void time_coarsen_factor(const double E[2][2], double out[2][2]) {
+  const double W[2][2][2] = {{{1.0, 0.0}, {0.5, 0.5}}, {{0.5, 0.5}, {0.0, 1.0}}};
+  for (int A = 0; A < 2; ++A)
+    for (int B = 0; B < 2; ++B) {
+      double v = 0.0;
+      for (int f = 0; f < 2; ++f)
+        for (int a = 0; a < 2; ++a)
+          for (int b = 0; b < 2; ++b) v += W[f][a][A] * W[f][b][B] * E[a][b];
+      out[A][B] = v;
+    }
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a{};
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+double* stage(st_ctx* c, int slot, long long n) {
+  if (c->io_n[slot] < n) {
+    if (c->io_stage[slot]) cudaFree(c->io_stage[slot]);
+    dalloc(&c->io_stage[slot], (size_t)n);
+    c->io_n[slot] = n;
+  }
+  return c->io_stage[slot];
+}
+
+const double* in_ptr(st_ctx* c, const double* p, long long n, int slot) {
+  if (!p) throw StErr{ST_E_INVALID_ARG, "null pointer"};
+  if (is_device_ptr(p)) return p;
+  double* d = stage(c, slot, n);
+  CK(cudaMemcpyAsync(d, p, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  return d;
+}
+
+// ---------------------------------------------------------------------------------------
+// Algorithm 1
+void build_hierarchy(st_ctx* c) {
+  const st_materials_t& m = c->mats;
+  const double scale = c->grid.tau / (c->grid.L * c->grid.L);
+  const double kc = m.k_con * scale, ki = m.k_ins * scale;
+  const double D = std::sqrt(kc * ki / (m.C_con * m.C_ins));
+  int n = (int)c->grid.n, nt = (int)c->grid.nt;
+  // sink patch on the fine level: nodes j with |j/n - center| <= halfwidth (R-4)
+  int plo = 1, phi = 0;
+  if (c->bcs.has_patch) {
+    plo = n + 1;
+    phi = -1;
+    for (int j = 0; j <= n; ++j) {
+      if (std::fabs((double)j / n - c->bcs.center) <= c->bcs.halfwidth * (1.0 + 1e-12)) {
+        plo = std::min(plo, j);
+        phi = std::max(phi, j);
+      }
+    }
+  }
+  c->lv.clear();
+  Level L0;
+  L0.g = make_geom(c->sd, n, nt, plo, phi);
+  L0.kind = KIND_FINE;
+  c->lv.push_back(L0);
+  const int maxl = c->opt.max_levels > 0 ? c->opt.max_levels : 64;
+  while ((int)c->lv.size() < maxl) {
+    const Geom& g = c->lv.back().g;
+    if (g.N <= c->opt.coarse_max_nodes) break;
+    double lam = D * g.dt / (g.dx * g.dx);
+    int kind;
+    bool ok;
+    if (c->opt.full_coarsening) {
+      kind = KIND_FULL;
+      ok = (g.n % 2 == 0) && (g.nt % 2 == 0) && g.n >= 2 && g.nt >= 2;
+    } else if (lam < c->opt.lambda_crit) {
+      kind = KIND_TIME;
+      ok = (g.nt % 2 == 0) && g.nt >= 2;
+    } else {
+      kind = KIND_SPACE;
+      ok = (g.n % 2 == 0) && g.n >= 2;
+    }
+    if (!ok) break;
+    int n2 = g.n, nt2 = g.nt, plo2 = g.plo, phi2 = g.phi;
+    if (kind == KIND_SPACE || kind == KIND_FULL) {
+      n2 /= 2;
+      plo2 = (g.plo + 1) / 2;  // coarse J with 2J in [plo, phi] (injection)
+      phi2 = g.phi >= 0 ? g.phi / 2 : -1;
+    }
+    if (kind == KIND_TIME || kind == KIND_FULL) nt2 /= 2;
+    Level Ln;
+    Ln.g = make_geom(c->sd, n2, nt2, plo2, phi2);
+    Ln.kind = kind;
+    c->lv.push_back(Ln);
+  }
+  if (c->lv.back().g.N > 8192)
+    throw StErr{ST_E_DIVISIBILITY, "coarsest level too large for the dense solve (" +
+                                       std::to_string(c->lv.back().g.N) + " nodes): grid not divisible enough"};
+}
+
+void setup_forms(st_ctx* c) {
+  const int NC = nc_of(c->sd);
+  for (size_t l = 0; l < c->lv.size(); ++l) {
+    Level& Lv = c->lv[l];
+    OpDesc& op = Lv.op;
+    op.g = Lv.g;
+    op.m = c->md;
+    if (l == 0) {
+      op.form = FORM_RHO;
+      op.nl = c->tc ? 1 : Lv.g.nt;
+      op.rho_tc = c->tc ? 1 : 0;
+      op.U[0][0] = 0.0; op.U[0][1] = 0.0; op.U[1][0] = -1.0; op.U[1][1] = 1.0;
+      double s = Lv.g.dt / 6.0;
+      op.Tm[0][0] = 2 * s; op.Tm[0][1] = s; op.Tm[1][0] = s; op.Tm[1][1] = 2 * s;
+      continue;
+    }
+    const Level& Pv = c->lv[l - 1];
+    const OpDesc& po = Pv.op;
+    if (Lv.kind == KIND_FULL) throw StErr{ST_E_UNSUPPORTED, "full space-time coarsening not implemented"};
+    if (Lv.kind == KIND_SPACE) {
+      op.nl = po.nl;
+      if (po.form == FORM_RHO || po.form == FORM_MK) {
+        op.form = FORM_MK;
+        memcpy(op.U, po.U, sizeof(op.U));
+        memcpy(op.Tm, po.Tm, sizeof(op.Tm));
+        Lv.st_elems = (long long)op.nl * 2 * NC * Lv.g.P;
+      } else {
+        op.form = FORM_B4;
+        Lv.st_elems = (long long)op.nl * 4 * NC * Lv.g.P;
+      }
+      Lv.st_owned = true;
+    } else {  // KIND_TIME
+      if (po.nl == 1) {
+        op.form = FORM_MK;
+        op.nl = 1;
+        time_coarsen_factor(po.U, op.U);
+        time_coarsen_factor(po.Tm, op.Tm);
+        if (po.form == FORM_RHO) {
+          Lv.st_elems = 2LL * NC * Lv.g.P;
+          Lv.st_owned = true;
+        } else {
+          Lv.st_owned = false;  // same spatial stencils as the finer level
+        }
+      } else {
+        op.form = FORM_B4;
+        op.nl = po.nl / 2;
+        Lv.st_elems = (long long)op.nl * 4 * NC * Lv.g.P;
+        Lv.st_owned = true;
+      }
+    }
+  }
+}
+
+void allocate(st_ctx* c) {
+  const long long N = c->N;
+  const int m = c->opt.restart;
+  c->ld = (N + 31) / 32 * 32;
+  dalloc(&c->f, N);
+  dalloc(&c->b, N);
+  dalloc(&c->tmpN, N);
+  dalloc(&c->tmpN2, N);
+  dalloc(&c->V, (size_t)(m + 1) * c->ld);
+  dalloc(&c->Z, (size_t)m * c->ld);
+  dalloc(&c->ws.partial, (size_t)kRedBlocks * 16);
+  dalloc(&c->ws.counter, 1);
+  CK(cudaMemsetAsync(c->ws.counter, 0, sizeof(unsigned), c->stream));
+  dalloc(&c->dsmall, 512);
+  CK(cudaMallocHost((void**)&c->hsmall, 512 * sizeof(double)));
+  for (size_t l = 0; l < c->lv.size(); ++l) {
+    Level& Lv = c->lv[l];
+    const long long n = Lv.g.N;
+    if (l == 0) {
+      dalloc(&Lv.r, n);
+      dalloc(&Lv.t, n);
+    } else {
+      dalloc(&Lv.x, n);
+      dalloc(&Lv.b, n);
+      dalloc(&Lv.r, n);
+      dalloc(&Lv.t, n);
+      if (Lv.st_owned) {
+        dalloc(&Lv.st, Lv.st_elems);
+        Lv.op.st = Lv.st;
+      } else {
+        Lv.op.st = c->lv[l - 1].op.st;  // resolved again after build (shared)
+      }
+    }
+  }
+  Level& Lc = c->lv.back();
+  Lc.dense = true;
+  dalloc(&Lc.A, (size_t)Lc.g.N * Lc.g.N);
+  dalloc(&Lc.Ainv, (size_t)Lc.g.N * Lc.g.N);
+  dalloc(&Lc.info, 1);
+  CK(cudaEventCreate(&c->e0));
+  CK(cudaEventCreate(&c->e1));
+}
+
+void op_launch(st_ctx* c, int l, int mode, bool trans, bool mask, const double* x, const double* b, double* y) {
+  launch_op(c->lv[l].op, mode, trans, mask, x, b, y, c->opt.omega, c->stream);
+  L(c);
+}
+
+// rho -> level-0 operator pointer; returns true if rho changed since the last full setup
+bool bind_rho(st_ctx* c, const double* rho_in) {
+  const double* rho = rho_in;
+  if (!is_device_ptr(rho_in)) {
+    CK(cudaMemcpyAsync(c->rho_stage, rho_in, c->ndesign * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    rho = c->rho_stage;
+  }
+  c->lv[0].op.rho = rho;
+  launch_checksum(rho, c->ndesign, c->dsmall + 500, c->ws, c->stream);
+  L(c);
+  CK(cudaMemcpyAsync(c->hsmall + 500, c->dsmall + 500, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  bool changed = !(c->have_ops && c->hsmall[500] == c->rho_ck[0] && c->hsmall[501] == c->rho_ck[1]);
+  c->rho_ck[0] = c->hsmall[500];
+  c->rho_ck[1] = c->hsmall[501];
+  return changed;
+}
+
+// rho-dependent setup: Galerkin coarse operators, dense coarsest inverse,
+// eliminated right-hand side b.
+void build_ops(st_ctx* c) {
+  CK(cudaEventRecord(c->e0, c->stream));
+  for (size_t l = 1; l < c->lv.size(); ++l) {
+    Level& Lv = c->lv[l];
+    const Level& Pv = c->lv[l - 1];
+    if (Lv.kind == KIND_SPACE) {
+      launch_rap_space(Pv.op, Lv.g, Lv.op.nl, Lv.op.form == FORM_MK ? 2 : 4, Lv.st, c->stream);
+      L(c);
+    } else if (Lv.kind == KIND_TIME) {
+      if (Pv.op.nl == 1) {
+        if (Pv.op.form == FORM_RHO) {
+          launch_rho_to_mk(Pv.op, 0, Lv.st, c->stream);
+          L(c);
+        } else {
+          Lv.op.st = Pv.op.st;
+        }
+      } else {
+        launch_rap_time(Pv.op, Lv.op.nl, Lv.st, c->stream);
+        L(c);
+      }
+    }
+    check_launch();
+  }
+  Level& Lc = c->lv.back();
+  const long long Nc = Lc.g.N;
+  CK(cudaMemsetAsync(Lc.A, 0, (size_t)Nc * Nc * sizeof(double), c->stream));
+  launch_dense_assemble(Lc.op, Lc.A, c->stream);
+  launch_dense_invert(Lc.A, Lc.Ainv, (int)Nc, Lc.info, c->stream);
+  L(c, 2);
+  check_launch();
+  // eliminated RHS b = m_f (f - K xD) + m_c xD (R-1)
+  const Geom& g0 = c->lv[0].g;
+  if (c->bcs.T0 != 0.0) {
+    launch_xd(g0, c->bcs.T0, c->tmpN, c->stream);
+    op_launch(c, 0, MODE_APPLY, false, false, c->tmpN, nullptr, c->tmpN2);
+    launch_rhs_combine(g0, c->f, c->tmpN2, c->bcs.T0, c->b, c->stream);
+    L(c, 2);
+  } else {
+    launch_rhs_combine(g0, c->f, nullptr, 0.0, c->b, c->stream);
+    L(c);
+  }
+  check_launch();
+  CK(cudaEventRecord(c->e1, c->stream));
+  CK(cudaEventSynchronize(c->e1));
+  int info = 0;
+  CK(cudaMemcpy(&info, Lc.info, sizeof(int), cudaMemcpyDeviceToHost));
+  if (info != 0) throw StErr{ST_E_BREAKDOWN, "coarsest-level matrix singular (pivot " + std::to_string(info) + ")"};
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+  c->stats.setup_ms = ms;
+  c->have_ops = true;
+}
+
+void prepare(st_ctx* c, const double* rho) {
+  if (bind_rho(c, rho)) build_ops(c);
+}
+
+// ---------------------------------------------------------------------------------------
+// V-cycle: damped-Jacobi pre-smoothing from zero, residual,
+// restriction, recursion, prolongation + correction, post-smoothing; coarsest: exact.
+void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x) {
+  Level& Lv = c->lv[l];
+  if (Lv.dense) {
+    launch_dense_solve(Lv.Ainv, (int)Lv.g.N, trans, b, x, c->stream);
+    L(c);
+    return;
+  }
+  Level& Nx = c->lv[l + 1];
+  const int npre = c->opt.nu_pre, npost = c->opt.nu_post;
+  const int total = npre + npost;
+  double* cur = (total % 2 == 1) ? x : Lv.t;
+  double* oth = (cur == x) ? Lv.t : x;
+  op_launch(c, l, MODE_JAC0, trans, true, nullptr, b, cur);
+  for (int s = 1; s < npre; ++s) {
+    op_launch(c, l, MODE_JAC, trans, true, cur, b, oth);
+    std::swap(cur, oth);
+  }
+  op_launch(c, l, MODE_RESID, trans, true, cur, b, Lv.r);
+  launch_restrict(Lv.g, Nx.g, Nx.kind, Lv.r, Nx.b, c->stream);
+  L(c);
+  vcycle(c, l + 1, trans, Nx.b, Nx.x);
+  launch_prolong_add(Lv.g, Nx.g, Nx.kind, Nx.x, cur, c->stream);
+  L(c);
+  for (int s = 0; s < npost; ++s) {
+    op_launch(c, l, MODE_JAC, trans, true, cur, b, oth);
+    std::swap(cur, oth);
+  }
+}
+
+void sync_small(st_ctx* c, int off, int n) {
+  CK(cudaMemcpyAsync(c->hsmall + off, c->dsmall + off, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+// FGMRES(m), right preconditioned by one V-cycle (Saad 1993). Classical
+// Gram-Schmidt with one conditional re-orthogonalisation (DGKS). Convergence on the TRUE
+// relative residual ||b - A x|| / ||b|| <= rtol (R-14).
+int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
+  const long long N = c->N;
+  const int m = c->opt.restart;
+  const double rtol = c->opt.rtol;
+  const long long ld = c->ld;
+  double* dh = c->dsmall;        // [0..63] h, [64..127] reorth h, [128..191] y
+  double* hh = c->hsmall;
+  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), gv(m + 1), y(m);
+  CK(cudaEventRecord(c->e0, c->stream));
+  // ||b||
+  launch_mdot(b, nullptr, 0, 0, N, dh + 200, c->ws, c->stream);
+  L(c);
+  sync_small(c, 200, 1);
+  const double bnorm = std::sqrt(hh[200]);
+  int its = 0, restarts = 0, status = ST_OK;
+  double relres = 0.0;
+  bool conv = false;
+  if (bnorm == 0.0) {
+    CK(cudaMemsetAsync(x, 0, N * sizeof(double), c->stream));
+    conv = true;
+  }
+  while (!conv) {
+    // true residual r = b - A x into V_0
+    op_launch(c, 0, MODE_RESID, trans, true, x, b, c->V);
+    launch_mdot(c->V, nullptr, 0, 0, N, dh + 200, c->ws, c->stream);
+    L(c);
+    sync_small(c, 200, 1);
+    const double beta = std::sqrt(hh[200]);
+    relres = beta / bnorm;
+    if (!std::isfinite(beta)) { status = ST_E_BREAKDOWN; break; }
+    if (relres <= rtol) { conv = true; break; }
+    if (its >= c->opt.maxit) { status = ST_E_NOT_CONVERGED; break; }
+    launch_scale(c->V, c->V, 1.0 / beta, N, c->stream);
+    L(c);
+    std::fill(gv.begin(), gv.end(), 0.0);
+    gv[0] = beta;
+    int jend = 0;
+    for (int j = 0; j < m; ++j) {
+      double* vj = c->V + (long long)j * ld;
+      double* zj = c->Z + (long long)j * ld;
+      double* w = c->V + (long long)(j + 1) * ld;
+      vcycle(c, 0, trans, vj, zj);
+      op_launch(c, 0, MODE_APPLY, trans, true, zj, nullptr, w);
+      launch_mdot(w, c->V, ld, j + 1, N, dh, c->ws, c->stream);
+      launch_maxpy_norm(w, c->V, ld, j + 1, dh, N, dh + 196, c->ws, c->stream);
+      L(c, (j + 8) / 8 + 1);
+      check_launch();
+      CK(cudaMemcpyAsync(hh, dh, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(hh + 196, dh + 196, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      double* hcol = &H[(size_t)j * (m + 1)];
+      for (int i = 0; i <= j; ++i) hcol[i] = hh[i];
+      double ww = hh[j + 1], w2 = hh[196];
+      if (w2 < 0.5 * ww) {  // DGKS re-orthogonalisation
+        launch_mdot(w, c->V, ld, j + 1, N, dh + 64, c->ws, c->stream);
+        launch_maxpy_norm(w, c->V, ld, j + 1, dh + 64, N, dh + 196, c->ws, c->stream);
+        L(c, (j + 8) / 8 + 1);
+        CK(cudaMemcpyAsync(hh + 64, dh + 64, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(hh + 196, dh + 196, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int i = 0; i <= j; ++i) hcol[i] += hh[64 + i];
+        w2 = hh[196];
+      }
+      const double hn = std::sqrt(std::max(w2, 0.0));
+      hcol[j + 1] = hn;
+      ++its;
+      if (hn > 0.0) {
+        launch_scale(w, w, 1.0 / hn, N, c->stream);
+        L(c);
+      }
+      // Givens rotations
+      for (int i = 0; i < j; ++i) {
+        double t = cs[i] * hcol[i] + sn[i] * hcol[i + 1];
+        hcol[i + 1] = -sn[i] * hcol[i] + cs[i] * hcol[i + 1];
+        hcol[i] = t;
+      }
+      double den = std::hypot(hcol[j], hcol[j + 1]);
+      if (den == 0.0) { status = ST_E_BREAKDOWN; jend = j; break; }
+      cs[j] = hcol[j] / den;
+      sn[j] = hcol[j + 1] / den;
+      hcol[j] = den;
+      hcol[j + 1] = 0.0;
+      gv[j + 1] = -sn[j] * gv[j];
+      gv[j] = cs[j] * gv[j];
+      jend = j + 1;
+      if (!std::isfinite(gv[j + 1])) { status = ST_E_BREAKDOWN; break; }
+      if (std::fabs(gv[j + 1]) <= rtol * bnorm || hn == 0.0 || its >= c->opt.maxit) break;
+    }
+    if (status == ST_E_BREAKDOWN && jend == 0) break;
+    // back substitution H y = g, x += Z y
+    for (int i = jend - 1; i >= 0; --i) {
+      double s = gv[i];
+      for (int k = i + 1; k < jend; ++k) s -= H[(size_t)k * (m + 1) + i] * y[k];
+      y[i] = s / H[(size_t)i * (m + 1) + i];
+    }
+    for (int i = 0; i < jend; ++i) hh[128 + i] = y[i];
+    CK(cudaMemcpyAsync(dh + 128, hh + 128, jend * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    launch_lincomb(x, c->Z, ld, jend, dh + 128, N, c->stream);
+    L(c);
+    check_launch();
+    ++restarts;
+    if (status == ST_E_BREAKDOWN) status = ST_OK;  // lucky/hard breakdown: re-check true residual
+  }
+  CK(cudaEventRecord(c->e1, c->stream));
+  CK(cudaEventSynchronize(c->e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+  c->stats.solve_ms = ms;
+  c->stats.iterations = its;
+  c->stats.restarts = restarts;
+  c->stats.rel_residual = relres;
+  c->stats.converged = conv ? 1 : 0;
+  c->stats.n_levels = (int)c->lv.size();
+  if (!conv && status == ST_OK) status = ST_E_NOT_CONVERGED;
+  return conv ? ST_OK : status;
+}
+
+double* out_ptr(st_ctx* c, double* p, long long n, int slot, bool copy_in, bool* staged) {
+  if (!p) throw StErr{ST_E_INVALID_ARG, "null pointer"};
+  if (is_device_ptr(p)) {
+    *staged = false;
+    return p;
+  }
+  double* d = stage(c, slot, n);
+  if (copy_in) CK(cudaMemcpyAsync(d, p, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  *staged = true;
+  return d;
+}
+
+void copy_back(st_ctx* c, double* host, const double* dev, long long n) {
+  CK(cudaMemcpyAsync(host, dev, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+template <class F> int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const StErr& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return ST_E_CUDA;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return ST_E_CUDA;
+  }
+}
+
+void free_ctx(st_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  for (auto& Lv : c->lv) {
+    if (Lv.st_owned && Lv.st) cudaFree(Lv.st);
+    cudaFree(Lv.x); cudaFree(Lv.b); cudaFree(Lv.r); cudaFree(Lv.t);
+    cudaFree(Lv.A); cudaFree(Lv.Ainv); cudaFree(Lv.info);
+  }
+  cudaFree(c->f); cudaFree(c->b); cudaFree(c->tmpN); cudaFree(c->tmpN2);
+  cudaFree(c->V); cudaFree(c->Z); cudaFree(c->ws.partial); cudaFree(c->ws.counter);
+  cudaFree(c->dsmall);
+  if (c->hsmall) cudaFreeHost(c->hsmall);
+  cudaFree(c->rho_stage);
+  for (int i = 0; i < 4; ++i) cudaFree(c->io_stage[i]);
+  if (c->e0) cudaEventDestroy(c->e0);
+  if (c->e1) cudaEventDestroy(c->e1);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+}  // namespace
+
+// =======================================================================================
+extern "C" {
+
+int st_abi_version(void) { return ST_ABI_VERSION; }
+
+void st_default_options(st_options_t* o) {
+  if (!o) return;
+  memset(o, 0, sizeof(*o));
+  o->design_mode = ST_SPACE_TIME;
+  o->rtol = 1e-8;
+  o->maxit = 500;
+  o->restart = 30;
+  o->smoother = ST_SMOOTH_JACOBI;
+  o->nu_pre = 2;
+  o->nu_post = 2;
+  o->omega = 0.7;
+  o->lambda_crit = 0.5;
+  o->coarse_max_nodes = 400;
+  o->max_levels = 0;
+  o->full_coarsening = 0;
+  o->use_graphs = 0;
+  o->verbose = 0;
+}
+
+const char* st_strerror(int code) {
+  switch (code) {
+    case ST_OK: return "ok";
+    case ST_E_INVALID_ARG: return "invalid argument";
+    case ST_E_DIVISIBILITY: return "grid not divisible along the coarsening direction";
+    case ST_E_NOT_CONVERGED: return "solver did not converge";
+    case ST_E_BREAKDOWN: return "Krylov breakdown";
+    case ST_E_OOM: return "out of device memory";
+    case ST_E_CUDA: return "CUDA error";
+    case ST_E_NCCL: return "NCCL error";
+    case ST_E_UNSUPPORTED: return "unsupported option";
+    default: return "unknown";
+  }
+}
+
+const char* st_last_error(void) { return g_last_error.c_str(); }
+
+int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* bcs, const st_source_t* src,
+             const st_options_t* opts, const st_dist_t* dist, st_ctx_t** out) {
+  return guarded([&]() -> int {
+    if (!grid || !mats || !bcs || !src || !out) throw StErr{ST_E_INVALID_ARG, "null argument"};
+    *out = nullptr;
+    if (grid->sdim != 2 && grid->sdim != 3) throw StErr{ST_E_INVALID_ARG, "sdim must be 2 or 3"};
+    if (grid->n < 2 || grid->nt < 2) throw StErr{ST_E_INVALID_ARG, "n and nt must be >= 2"};
+    if (!(grid->L > 0) || !(grid->tau > 0)) throw StErr{ST_E_INVALID_ARG, "L and tau must be > 0"};
+    if (grid->n > (1 << 20) || grid->nt > (1 << 24)) throw StErr{ST_E_INVALID_ARG, "grid too large"};
+    if (!(mats->C_ins > 0) || !(mats->C_con > 0) || !(mats->k_ins > 0) || !(mats->k_con > 0))
+      throw StErr{ST_E_INVALID_ARG, "material constants must be > 0"};
+    if (bcs->has_patch && bcs->face != 0) throw StErr{ST_E_UNSUPPORTED, "only face 0 (x1 = 0) supported"};
+    if (src->kind != ST_SRC_UNIFORM && src->kind != ST_SRC_SIN) throw StErr{ST_E_UNSUPPORTED, "source kind"};
+    if (dist && dist->size > 1) throw StErr{ST_E_UNSUPPORTED, "multi-GPU time slabs: not in this build"};
+    st_ctx* c = new st_ctx();
+    try {
+      c->grid = *grid;
+      c->mats = *mats;
+      c->bcs = *bcs;
+      c->src = *src;
+      if (opts) c->opt = *opts;
+      else st_default_options(&c->opt);
+      if (c->opt.restart < 1 || c->opt.restart > 60) throw StErr{ST_E_INVALID_ARG, "restart must be in [1, 60]"};
+      if (c->opt.nu_pre < 1 || c->opt.nu_post < 0) throw StErr{ST_E_INVALID_ARG, "nu_pre >= 1, nu_post >= 0"};
+      if (c->opt.coarse_max_nodes < 8) c->opt.coarse_max_nodes = 8;
+      CK(cudaGetDevice(&c->device));
+      if (dist && dist->device >= 0) {
+        c->device = dist->device;
+        CK(cudaSetDevice(c->device));
+      }
+      if (dist && dist->cuda_stream) {
+        c->stream = (cudaStream_t)dist->cuda_stream;
+      } else {
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+      }
+      c->sd = grid->sdim;
+      c->tc = (c->opt.design_mode == ST_TIME_CONSTANT);
+      const double scale = grid->tau / (grid->L * grid->L);
+      c->md.Cins = mats->C_ins;
+      c->md.dC = mats->C_con - mats->C_ins;
+      c->md.pc = mats->p_c;
+      c->md.kins = mats->k_ins * scale;
+      c->md.dk = (mats->k_con - mats->k_ins) * scale;
+      c->md.pk = mats->p_k;
+      build_hierarchy(c);
+      setup_forms(c);
+      c->N = c->lv[0].g.N;
+      long long nsp = 1;
+      for (int d = 0; d < c->sd; ++d) nsp *= grid->n;
+      c->ndesign = c->tc ? nsp : nsp * grid->nt;
+      allocate(c);
+      dalloc(&c->rho_stage, c->ndesign);
+      // source vector f: Q~ = Q tau
+      launch_source(c->lv[0].g, src->kind, src->Q0 * grid->tau, src->a, src->w, grid->tau, c->f, c->stream);
+      L(c);
+      check_launch();
+      CK(cudaStreamSynchronize(c->stream));
+    } catch (...) {
+      free_ctx(c);
+      throw;
+    }
+    *out = c;
+    return ST_OK;
+  });
+}
+
+void st_destroy(st_ctx_t* ctx) { free_ctx(ctx); }
+
+int st_solve(st_ctx_t* c, const double* rho, double* T) {
+  return guarded([&]() -> int {
+    if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
+    CK(cudaSetDevice(c->device));
+    prepare(c, rho);
+    bool staged = false;
+    double* x = out_ptr(c, T, c->N, 0, true, &staged);
+    launch_set_bc_values(c->lv[0].g, c->bcs.T0, x, c->stream);  // x_c = xD
+    L(c);
+    int rc = fgmres(c, false, c->b, x);
+    if (staged) copy_back(c, T, x, c->N);
+    return rc;
+  });
+}
+
+int st_adjoint(st_ctx_t* c, const double* rho, const double* dJdT, double* lambda) {
+  return guarded([&]() -> int {
+    if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
+    CK(cudaSetDevice(c->device));
+    prepare(c, rho);
+    const double* g = in_ptr(c, dJdT, c->N, 1);
+    launch_mask_free(c->lv[0].g, g, c->tmpN2, c->stream);  // RHS m_f g
+    L(c);
+    bool staged = false;
+    double* x = out_ptr(c, lambda, c->N, 0, true, &staged);
+    launch_set_bc_values(c->lv[0].g, 0.0, x, c->stream);  // lambda_c = 0
+    L(c);
+    int rc = fgmres(c, true, c->tmpN2, x);
+    if (staged) copy_back(c, lambda, x, c->N);
+    return rc;
+  });
+}
+
+int st_sensitivity(st_ctx_t* c, const double* rho, const double* T, const double* lambda, double* dJ) {
+  return guarded([&]() -> int {
+    if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
+    CK(cudaSetDevice(c->device));
+    const double* r = rho;
+    if (!is_device_ptr(rho)) {
+      CK(cudaMemcpyAsync(c->rho_stage, rho, c->ndesign * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      r = c->rho_stage;
+    }
+    OpDesc op = c->lv[0].op;
+    op.rho = r;
+    const double* Td = in_ptr(c, T, c->N, 1);
+    const double* Ld = in_ptr(c, lambda, c->N, 2);
+    bool staged = false;
+    double* dj = out_ptr(c, dJ, c->ndesign, 3, false, &staged);
+    launch_sensitivity(op, Td, Ld, dj, c->stream);
+    L(c);
+    check_launch();
+    if (staged) copy_back(c, dJ, dj, c->ndesign);
+    else CK(cudaStreamSynchronize(c->stream));
+    return ST_OK;
+  });
+}
+
+int st_apply(st_ctx_t* c, const double* rho, const double* x, double* y, int transpose, int bc) {
+  return guarded([&]() -> int {
+    if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
+    CK(cudaSetDevice(c->device));
+    const double* r = rho;
+    if (!is_device_ptr(rho)) {
+      CK(cudaMemcpyAsync(c->rho_stage, rho, c->ndesign * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      r = c->rho_stage;
+    }
+    c->lv[0].op.rho = r;
+    const double* xd = in_ptr(c, x, c->N, 1);
+    bool staged = false;
+    double* yd = out_ptr(c, y, c->N, 2, false, &staged);
+    op_launch(c, 0, MODE_APPLY, transpose != 0, bc != 0, xd, nullptr, yd);
+    check_launch();
+    if (staged) copy_back(c, y, yd, c->N);
+    else CK(cudaStreamSynchronize(c->stream));
+    return ST_OK;
+  });
+}
+
+int st_level_apply(st_ctx_t* c, const double* rho, int level, const double* x, double* y, int transpose) {
+  return guarded([&]() -> int {
+    if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
+    if (level < 0 || level >= (int)c->lv.size()) throw StErr{ST_E_INVALID_ARG, "level out of range"};
+    CK(cudaSetDevice(c->device));
+    prepare(c, rho);
+    const long long n = c->lv[level].g.N;
+    const double* xd = in_ptr(c, x, n, 1);
+    bool staged = false;
+    double* yd = out_ptr(c, y, n, 2, false, &staged);
+    op_launch(c, level, MODE_APPLY, transpose != 0, true, xd, nullptr, yd);
+    check_launch();
+    if (staged) copy_back(c, y, yd, n);
+    else CK(cudaStreamSynchronize(c->stream));
+    return ST_OK;
+  });
+}
+
+int st_rhs(st_ctx_t* c, const double* rho, double* f, double* b) {
+  return guarded([&]() -> int {
+    if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
+    CK(cudaSetDevice(c->device));
+    prepare(c, rho);
+    if (f) {
+      if (is_device_ptr(f)) CK(cudaMemcpyAsync(f, c->f, c->N * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      else CK(cudaMemcpyAsync(f, c->f, c->N * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    }
+    if (b) {
+      if (is_device_ptr(b)) CK(cudaMemcpyAsync(b, c->b, c->N * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      else CK(cudaMemcpyAsync(b, c->b, c->N * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return ST_OK;
+  });
+}
+
+int st_get_stats(const st_ctx_t* c, st_stats_t* s) {
+  if (!c || !s) return ST_E_INVALID_ARG;
+  *s = c->stats;
+  return ST_OK;
+}
+
+int st_get_hierarchy(const st_ctx_t* c, st_hierarchy_t* h) {
+  if (!c || !h) return ST_E_INVALID_ARG;
+  memset(h, 0, sizeof(*h));
+  h->n_levels = (int)std::min<size_t>(c->lv.size(), 32);
+  for (int l = 0; l < h->n_levels; ++l) {
+    h->n[l] = c->lv[l].g.n;
+    h->nt[l] = c->lv[l].g.nt;
+    h->kind[l] = c->lv[l].kind;
+    h->form[l] = c->lv[l].dense ? FORM_DENSE : c->lv[l].op.form;
+    h->nodes[l] = c->lv[l].g.N;
+  }
+  return ST_OK;
+}
+
+int64_t st_num_nodes(const st_ctx_t* c) { return c ? c->N : -1; }
+int64_t st_num_design(const st_ctx_t* c) { return c ? c->ndesign : -1; }
+int64_t st_kernel_launches(const st_ctx_t* c) { return c ? c->launches : -1; }
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+// common.cuh — internal types and device helpers of libst (B200, sm_100a, fp64).
+//
+// Operator algebra (derivation in DESIGN.md "Plane form"): the element matrix of the
+// stabilised CG space-time element factorises as
+//     A_e = C_e (U (x) M_sp) + k~_e (Tm (x) K_sp),  U = [[0,0],[-1,1]], Tm = dt/6 [[2,1],[1,2]]
+// (time index: row = test, col = trial; bottom = 0, top = 1). Every multigrid level of the
+// Galerkin hierarchy is stored per element LAYER tau (planes tau, tau+1)
+// as a 2x2 time block of symmetric spatial stencils S^{ab}_tau:
+//     (K x)_p = S^{tb}_{p-1} x_{p-1} + S^{tt}_{p-1} x_p + S^{bb}_p x_p + S^{bt}_p x_{p+1}.
+// Forms: RHO (fine level, matrix-free: M, K stencils from rho on the fly), MK (S^{ab} =
+// U[a][b] M_tau + Tm[a][b] K_tau, stored M, K), B4 (four stored stencils per layer).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace st {
+
+enum Form { FORM_RHO = 0, FORM_MK = 1, FORM_B4 = 2, FORM_DENSE = 3 };
+enum Kind { KIND_FINE = 0, KIND_SPACE = 1, KIND_TIME = 2, KIND_FULL = 3 };
+enum Mode { MODE_APPLY = 0, MODE_RESID = 1, MODE_JAC = 2, MODE_JAC0 = 3 };
+
+// Level geometry: n^sd x nt elements, (n+1)^sd (nt+1) nodes.
+struct Geom {
+  int sd;
+  int n, nn, nt;
+  long long P;   // nodes per time plane
+  long long N;   // all nodes
+  int plo, phi;  // sink patch: transverse node range at x1 = 0 (plo > phi: none)
+  double dx, dt;
+};
+
+struct MatsDev {
+  double Cins, dC, pc;   // C = Cins + dC rho^pc
+  double kins, dk, pk;   // k~ = kins + dk rho^pk   (already rescaled by tau/L^2)
+};
+
+// Operator descriptor, passed by value to kernels.
+struct OpDesc {
+  Geom g;
+  int form;
+  int nl;                 // stored layers: 1 (time-constant) or nt
+  double U[2][2], Tm[2][2];
+  const double* rho;      // FORM_RHO
+  int rho_tc;             // rho time-constant
+  MatsDev m;
+  const double* st;       // MK: [nl][2][NC][P]; B4: [nl][4][NC][P]
+};
+
+template <int SD> struct SG {
+  static constexpr int NOFF = SD == 2 ? 9 : 27;
+  static constexpr int CEN = SD == 2 ? 4 : 13;
+  static constexpr int NC = SD == 2 ? 5 : 14;     // center + forward offsets
+  static constexpr int NE = SD == 2 ? 4 : 8;      // elements around a node
+  // offset component d (0 = x1) of stencil index k = (dz+1)*9 + (dy+1)*3 + (dx+1)
+  __host__ __device__ static constexpr int od(int k, int d) {
+    return d == 0 ? (k % 3) - 1 : (d == 1 ? ((k / 3) % 3) - 1 : (k / 9) - 1);
+  }
+};
+
+// spatial element-matrix entries by Hamming distance h between local corners
+// 2D: M = dx^2/36 [4,2,1], K = 1/6 [4,-1,-2];  3D: M = dx^3/216 [8,4,2,1], K = dx [1/3,0,-1/12,-1/12]
+template <int SD> __device__ __forceinline__ double mtab(int h, double dx) {
+  if (SD == 2) return (h == 0 ? 4.0 : (h == 1 ? 2.0 : 1.0)) * (dx * dx / 36.0);
+  return (h == 0 ? 8.0 : (h == 1 ? 4.0 : (h == 2 ? 2.0 : 1.0))) * (dx * dx * dx / 216.0);
+}
+template <int SD> __device__ __forceinline__ double ktab(int h, double dx) {
+  if (SD == 2) return (h == 0 ? 4.0 : (h == 1 ? -1.0 : -2.0)) * (1.0 / 6.0);
+  return (h == 0 ? (1.0 / 3.0) : (h == 1 ? 0.0 : (-1.0 / 12.0))) * dx;
+}
+
+__device__ __forceinline__ double powp(double r, double p) {
+  if (p == 3.0) return r * r * r;
+  if (p == 1.0) return r;
+  if (p == 2.0) return r * r;
+  if (p == 4.0) { double q = r * r; return q * q; }
+  if (p == 0.0) return 1.0;
+  return pow(r, p);
+}
+__device__ __forceinline__ double dpowp(double r, double p) {  // d/dr r^p
+  if (p == 3.0) return 3.0 * r * r;
+  if (p == 1.0) return 1.0;
+  if (p == 2.0) return 2.0 * r;
+  if (p == 4.0) return 4.0 * r * r * r;
+  if (p == 0.0) return 0.0;
+  return p * pow(r, p - 1.0);
+}
+
+// constrained node test (R-2, R-4): t = 0 plane, or sink patch at x1 = 0
+template <int SD> __device__ __forceinline__ bool is_cons(const Geom& g, const int* c, int p) {
+  if (p == 0) return true;
+  if (c[0] != 0) return false;
+  bool in = (c[1] >= g.plo && c[1] <= g.phi);
+  if (SD == 3) in = in && (c[2] >= g.plo && c[2] <= g.phi);
+  return in;
+}
+template <int SD> __device__ __forceinline__ bool is_patch(const Geom& g, const int* c) {
+  if (c[0] != 0) return false;
+  bool in = (c[1] >= g.plo && c[1] <= g.phi);
+  if (SD == 3) in = in && (c[2] >= g.plo && c[2] <= g.phi);
+  return in;
+}
+
+template <int SD> __device__ __forceinline__ long long pidx(const Geom& g, const int* c) {
+  long long r = c[0] + (long long)g.nn * c[1];
+  if (SD == 3) r += (long long)g.nn * g.nn * c[2];
+  return r;
+}
+
+}  // namespace st

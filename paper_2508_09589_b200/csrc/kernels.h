@@ -1,0 +1,50 @@
+// kernels.h — host launchers of libst's CUDA kernels (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include "common.cuh"
+
+namespace st {
+
+// ops.cu
+void launch_op(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
+               double omega, cudaStream_t s);
+void launch_rap_space(const OpDesc& fop, const Geom& gc, int nl, int ns, double* out, cudaStream_t s);
+void launch_rap_time(const OpDesc& fop, int nlc, double* out, cudaStream_t s);
+void launch_rho_to_mk(const OpDesc& fop, int tau, double* out, cudaStream_t s);
+void launch_dense_assemble(const OpDesc& op, double* A, cudaStream_t s);
+
+// transfer.cu — restriction r_c = m_f^c P^T r_f, prolongation x_f += m_f P e_c
+void launch_restrict(const Geom& gf, const Geom& gc, int kind, const double* rf, double* rc, cudaStream_t s);
+void launch_prolong_add(const Geom& gf, const Geom& gc, int kind, const double* ec, double* xf, cudaStream_t s);
+
+// krylov.cu — deterministic reductions (fixed block count, last-block finalisation)
+struct RedWs {
+  double* partial;      // [kMaxBlocks * kMaxK]
+  unsigned int* counter;
+};
+constexpr int kRedBlocks = 296;
+constexpr int kMaxDots = 9;
+// out[0..k-1] = V_j . w (j < k), out[k] = w . w ; k <= 8
+void launch_mdot(const double* w, const double* V, long long ldv, int k, long long n, double* out, RedWs ws,
+                 cudaStream_t s);
+// w -= sum_j h[j] V_j (h on device); out[0] = ||w||^2 after
+void launch_maxpy_norm(double* w, const double* V, long long ldv, int k, const double* h, long long n,
+                       double* out, RedWs ws, cudaStream_t s);
+// x += sum_j y[j] Z_j (y on device)
+void launch_lincomb(double* x, const double* Z, long long ldz, int k, const double* y, long long n, cudaStream_t s);
+// v = w / sqrt(nrm2[0]) (nrm2 on device) or v = alpha * w
+void launch_scale_dev(const double* w, double* v, const double* nrm2, long long n, cudaStream_t s);
+void launch_scale(const double* w, double* v, double alpha, long long n, cudaStream_t s);
+void launch_checksum(const double* a, long long n, double* out, RedWs ws, cudaStream_t s);
+
+// misc.cu
+void launch_source(const Geom& g, int kind, double qscale, double a, double w, double tau, double* f, cudaStream_t s);
+void launch_mask_free(const Geom& g, const double* in, double* out, cudaStream_t s);       // out = m_f .* in
+void launch_set_bc_values(const Geom& g, double T0, double* x, cudaStream_t s);          // x_c = xD
+void launch_rhs_combine(const Geom& g, const double* f, const double* KxD, double T0, double* b, cudaStream_t s);
+void launch_xd(const Geom& g, double T0, double* x, cudaStream_t s);                      // x = xD (0 off plane 0)
+void launch_sensitivity(const OpDesc& op, const double* T, const double* lam, double* dJ, cudaStream_t s);
+void launch_dense_invert(double* A, double* Ainv, int n, int* info, cudaStream_t s);
+void launch_dense_solve(const double* Ainv, int n, bool trans, const double* b, double* x, cudaStream_t s);
+
+}  // namespace st

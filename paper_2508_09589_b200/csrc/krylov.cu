@@ -1,0 +1,192 @@
+// krylov.cu — FGMRES building blocks (Saad 1993): fused multi-dot
+// (classical Gram-Schmidt column h = V^T w together with ||w||^2), multi-AXPY with the new
+// norm, the solution update x += Z y, scaling. HBM-bound; reductions are deterministic
+// (fixed grid, per-block partials, last-block finalisation in fixed order).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace st {
+
+constexpr int kRedThreads = 256;
+
+template <int NV>
+__device__ __forceinline__ void block_partials(double (&acc)[NV], double* __restrict__ partial, RedWs ws,
+                                               double* __restrict__ out) {
+  __shared__ double sm[kRedThreads / 32][NV > 0 ? NV : 1];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double a = acc[v];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+    if (lane == 0) sm[wid][v] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double a = 0.0;
+#pragma unroll
+    for (int w = 0; w < kRedThreads / 32; ++w) a += sm[w][threadIdx.x];
+    partial[(long long)blockIdx.x * NV + threadIdx.x] = a;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = atomicAdd(ws.counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // last block: sum partials over blocks in fixed order
+  for (int v = 0; v < NV; ++v) {
+    double a = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += kRedThreads) a += ((volatile double*)partial)[(long long)b * NV + v];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+    __syncthreads();
+    if (lane == 0) sm[wid][0] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kRedThreads / 32; ++w) s += sm[w][0];
+      out[v] = s;
+    }
+  }
+  if (threadIdx.x == 0) *ws.counter = 0u;
+}
+
+template <int J, bool NRM>
+__global__ void __launch_bounds__(kRedThreads) mdot_kernel(const double* __restrict__ w, const double* __restrict__ V,
+                                                           long long ldv, long long n, double* out, RedWs ws) {
+  constexpr int NV = J + (NRM ? 1 : 0);
+  double acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double wi = __ldg(w + i);
+#pragma unroll
+    for (int j = 0; j < J; ++j) acc[j] += __ldg(V + j * ldv + i) * wi;
+    if (NRM) acc[NV - 1] += wi * wi;
+  }
+  block_partials<NV>(acc, ws.partial, ws, out);
+}
+
+__global__ void __launch_bounds__(kRedThreads) maxpy_norm_kernel(double* __restrict__ w, const double* __restrict__ V,
+                                                                 long long ldv, int k, const double* __restrict__ h,
+                                                                 long long n, double* out, RedWs ws) {
+  __shared__ double hs[128];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) hs[j] = h[j];
+  __syncthreads();
+  double acc[1] = {0.0};
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double wi = w[i];
+    for (int j = 0; j < k; ++j) wi -= hs[j] * __ldg(V + j * ldv + i);
+    w[i] = wi;
+    acc[0] += wi * wi;
+  }
+  block_partials<1>(acc, ws.partial, ws, out);
+}
+
+__global__ void lincomb_kernel(double* __restrict__ x, const double* __restrict__ Z, long long ldz, int k,
+                               const double* __restrict__ y, long long n) {
+  __shared__ double ys[128];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) ys[j] = y[j];
+  __syncthreads();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double xi = x[i];
+    for (int j = 0; j < k; ++j) xi += ys[j] * __ldg(Z + j * ldz + i);
+    x[i] = xi;
+  }
+}
+
+__global__ void scale_dev_kernel(const double* __restrict__ w, double* __restrict__ v, const double* nrm2, long long n) {
+  double a = 1.0 / sqrt(nrm2[0]);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) v[i] = a * w[i];
+}
+
+__global__ void scale_kernel(const double* __restrict__ w, double* __restrict__ v, double a, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) v[i] = a * w[i];
+}
+
+__device__ __forceinline__ double hash_weight(long long i) {
+  unsigned long long z = (unsigned long long)i * 0x9E3779B97F4A7C15ull;
+  z ^= z >> 31; z *= 0xBF58476D1CE4E5B9ull; z ^= z >> 27;
+  return 0.5 + (double)(z >> 11) * (1.0 / 9007199254740992.0);
+}
+
+__global__ void __launch_bounds__(kRedThreads) checksum_kernel(const double* __restrict__ a, long long n, double* out,
+                                                               RedWs ws) {
+  double acc[2] = {0.0, 0.0};
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double v = __ldg(a + i);
+    acc[0] += v;
+    acc[1] += v * hash_weight(i);
+  }
+  block_partials<2>(acc, ws.partial, ws, out);
+}
+
+static unsigned red_blocks(long long n) {
+  long long b = (n + kRedThreads - 1) / kRedThreads;
+  if (b > kRedBlocks) b = kRedBlocks;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+void launch_mdot(const double* w, const double* V, long long ldv, int k, long long n, double* out, RedWs ws,
+                 cudaStream_t s) {
+  // k dots + ||w||^2 in chunks of <= 8 vectors; the norm rides on the last chunk
+  unsigned g = red_blocks(n);
+  int done = 0;
+  do {
+    int J = k - done;
+    if (J > 8) J = 8;
+    bool nrm = (done + J == k);
+    const double* Vj = V + (long long)done * ldv;
+    double* o = out + done;
+#define MD(JJ)                                                                                 \
+  case JJ:                                                                                     \
+    if (nrm) mdot_kernel<JJ, true><<<g, kRedThreads, 0, s>>>(w, Vj, ldv, n, o, ws);            \
+    else mdot_kernel<JJ, false><<<g, kRedThreads, 0, s>>>(w, Vj, ldv, n, o, ws);               \
+    break;
+    switch (J) {
+      case 0: mdot_kernel<0, true><<<g, kRedThreads, 0, s>>>(w, Vj, ldv, n, o, ws); break;
+      MD(1) MD(2) MD(3) MD(4) MD(5) MD(6) MD(7) MD(8)
+    }
+#undef MD
+    done += J;
+  } while (done < k);
+}
+
+void launch_maxpy_norm(double* w, const double* V, long long ldv, int k, const double* h, long long n, double* out,
+                       RedWs ws, cudaStream_t s) {
+  maxpy_norm_kernel<<<red_blocks(n), kRedThreads, 0, s>>>(w, V, ldv, k, h, n, out, ws);
+}
+
+static unsigned ew_blocks(long long n) {
+  long long b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+void launch_lincomb(double* x, const double* Z, long long ldz, int k, const double* y, long long n, cudaStream_t s) {
+  lincomb_kernel<<<ew_blocks(n), 256, 0, s>>>(x, Z, ldz, k, y, n);
+}
+void launch_scale_dev(const double* w, double* v, const double* nrm2, long long n, cudaStream_t s) {
+  scale_dev_kernel<<<ew_blocks(n), 256, 0, s>>>(w, v, nrm2, n);
+}
+void launch_scale(const double* w, double* v, double alpha, long long n, cudaStream_t s) {
+  scale_kernel<<<ew_blocks(n), 256, 0, s>>>(w, v, alpha, n);
+}
+void launch_checksum(const double* a, long long n, double* out, RedWs ws, cudaStream_t s) {
+  checksum_kernel<<<red_blocks(n), kRedThreads, 0, s>>>(a, n, out, ws);
+}
+
+}  // namespace st

@@ -1,0 +1,260 @@
+// misc.cu — source assembly, Dirichlet helpers, element sensitivities, dense coarsest solve.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace st {
+
+// ---------------------------------------------------------------------------------------
+// f_a = sum_e int N_a Q~ dV for a spatially uniform source: exact spatial
+// integrals (dx/2 per adjacent element and direction) times 2-point Gauss in time per
+// element layer (R-5).
+template <int SD>
+__global__ void source_kernel(Geom g, int kind, double qscale, double a, double w, double tau, double* __restrict__ f) {
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= g.N) return;
+  int p = (int)(idx / g.P);
+  long long pn = idx % g.P;
+  double sx = 1.0;
+  long long t = pn;
+  for (int d = 0; d < SD; ++d) {
+    int c = (int)(t % g.nn);
+    t /= g.nn;
+    sx *= 0.5 * g.dx * ((c == 0 || c == g.n) ? 1.0 : 2.0);
+  }
+  const double s = 0.5 / sqrt(3.0);
+  double ft = 0.0;
+  for (int side = 0; side < 2; ++side) {
+    int l = side == 0 ? p - 1 : p;       // layer; node is its top (side 0) or bottom (side 1)
+    if (l < 0 || l >= g.nt) continue;
+    for (int gp = 0; gp < 2; ++gp) {
+      double sg = gp == 0 ? -s : s;
+      double tt = (l + 0.5 + sg) * g.dt;
+      double N = side == 0 ? (0.5 + sg) : (0.5 - sg);
+      double Q = qscale * ((kind == 1) ? (1.0 + a * sin(w * tau * tt)) : 1.0);
+      ft += 0.5 * g.dt * N * Q;
+    }
+  }
+  f[idx] = sx * ft;
+}
+
+void launch_source(const Geom& g, int kind, double qscale, double a, double w, double tau, double* f, cudaStream_t s) {
+  unsigned grd = (unsigned)((g.N + 255) / 256);
+  if (g.sd == 2) source_kernel<2><<<grd, 256, 0, s>>>(g, kind, qscale, a, w, tau, f);
+  else source_kernel<3><<<grd, 256, 0, s>>>(g, kind, qscale, a, w, tau, f);
+}
+
+// ---------------------------------------------------------------------------------------
+template <int SD> __device__ __forceinline__ void node_of(const Geom& g, long long idx, int* c, int& p) {
+  p = (int)(idx / g.P);
+  long long t = idx % g.P;
+  for (int d = 0; d < SD; ++d) { c[d] = (int)(t % g.nn); t /= g.nn; }
+}
+
+template <int SD> __global__ void mask_free_kernel(Geom g, const double* __restrict__ in, double* __restrict__ out) {
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= g.N) return;
+  int c[3] = {0, 0, 0}, p;
+  node_of<SD>(g, idx, c, p);
+  out[idx] = is_cons<SD>(g, c, p) ? 0.0 : in[idx];
+}
+template <int SD> __global__ void set_bc_kernel(Geom g, double T0, double* __restrict__ x) {
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= g.N) return;
+  int c[3] = {0, 0, 0}, p;
+  node_of<SD>(g, idx, c, p);
+  if (is_cons<SD>(g, c, p)) x[idx] = (p == 0) ? T0 : 0.0;
+}
+template <int SD> __global__ void xd_kernel(Geom g, double T0, double* __restrict__ x) {
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= g.N) return;
+  x[idx] = (idx < g.P) ? T0 : 0.0;
+}
+template <int SD>
+__global__ void rhs_kernel(Geom g, const double* __restrict__ f, const double* __restrict__ KxD, double T0,
+                           double* __restrict__ b) {
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= g.N) return;
+  int c[3] = {0, 0, 0}, p;
+  node_of<SD>(g, idx, c, p);
+  if (is_cons<SD>(g, c, p)) b[idx] = (p == 0) ? T0 : 0.0;
+  else b[idx] = f[idx] - (KxD ? KxD[idx] : 0.0);
+}
+
+#define EW_LAUNCH(K, ...)                                                   \
+  do {                                                                      \
+    unsigned grd = (unsigned)((g.N + 255) / 256);                           \
+    if (g.sd == 2) K<2><<<grd, 256, 0, s>>>(g, __VA_ARGS__);                \
+    else K<3><<<grd, 256, 0, s>>>(g, __VA_ARGS__);                          \
+  } while (0)
+
+void launch_mask_free(const Geom& g, const double* in, double* out, cudaStream_t s) { EW_LAUNCH(mask_free_kernel, in, out); }
+void launch_set_bc_values(const Geom& g, double T0, double* x, cudaStream_t s) { EW_LAUNCH(set_bc_kernel, T0, x); }
+void launch_xd(const Geom& g, double T0, double* x, cudaStream_t s) { EW_LAUNCH(xd_kernel, T0, x); }
+void launch_rhs_combine(const Geom& g, const double* f, const double* KxD, double T0, double* b, cudaStream_t s) {
+  EW_LAUNCH(rhs_kernel, f, KxD, T0, b);
+}
+
+// ---------------------------------------------------------------------------------------
+// Element sensitivities: dJ_e = -lambda_e^T (C' U(x)M_sp + k~' Tm(x)K_sp) T_e
+// with lambda = 0 on constrained nodes and full T. Time-constant rho: sum over layers
+// (transposed extrusion).
+template <int SD>
+__device__ double elem_sens(const OpDesc& op, const double* __restrict__ T, const double* __restrict__ lam,
+                            const int* a, int tau, double r) {
+  constexpr int NE = SG<SD>::NE;
+  const Geom& g = op.g;
+  double Tb[NE], Tt[NE], Lb[NE], Lt[NE];
+#pragma unroll
+  for (int b = 0; b < NE; ++b) {
+    int c[3] = {0, 0, 0};
+#pragma unroll
+    for (int d = 0; d < SD; ++d) c[d] = a[d] + ((b >> d) & 1);
+    long long pn = pidx<SD>(g, c);
+    long long ib = (long long)tau * g.P + pn, it = ib + g.P;
+    Tb[b] = __ldg(T + ib);
+    Tt[b] = __ldg(T + it);
+    Lb[b] = is_cons<SD>(g, c, tau) ? 0.0 : __ldg(lam + ib);
+    Lt[b] = is_cons<SD>(g, c, tau + 1) ? 0.0 : __ldg(lam + it);
+  }
+  double gG = 0.0, gK1 = 0.0, gK2 = 0.0;
+#pragma unroll
+  for (int b = 0; b < NE; ++b) {
+#pragma unroll
+    for (int q = 0; q < NE; ++q) {
+      int h = __popc((unsigned)(b ^ q));
+      double m = mtab<SD>(h, g.dx), k = ktab<SD>(h, g.dx);
+      gG += Lt[b] * m * (Tt[q] - Tb[q]);
+      gK1 += Lb[b] * k * (2.0 * Tb[q] + Tt[q]);
+      gK2 += Lt[b] * k * (Tb[q] + 2.0 * Tt[q]);
+    }
+  }
+  double gK = (g.dt / 6.0) * (gK1 + gK2);
+  double dC = op.m.dC * dpowp(r, op.m.pc);
+  double dk = op.m.dk * dpowp(r, op.m.pk);
+  return -(dC * gG + dk * gK);
+}
+
+template <int SD>
+__global__ void sens_kernel(OpDesc op, const double* __restrict__ T, const double* __restrict__ lam,
+                            double* __restrict__ dJ) {
+  const Geom& g = op.g;
+  long long ne_sp = 1;
+  for (int d = 0; d < SD; ++d) ne_sp *= g.n;
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long total = op.rho_tc ? ne_sp : ne_sp * g.nt;
+  if (idx >= total) return;
+  long long e = idx % ne_sp;
+  int a[3] = {0, 0, 0};
+  long long t = e;
+  for (int d = 0; d < SD; ++d) { a[d] = (int)(t % g.n); t /= g.n; }
+  if (op.rho_tc) {
+    double r = __ldg(op.rho + e);
+    double acc = 0.0;
+    for (int tau = 0; tau < g.nt; ++tau) acc += elem_sens<SD>(op, T, lam, a, tau, r);
+    dJ[e] = acc;
+  } else {
+    int tau = (int)(idx / ne_sp);
+    dJ[idx] = elem_sens<SD>(op, T, lam, a, tau, __ldg(op.rho + idx));
+  }
+}
+
+void launch_sensitivity(const OpDesc& op, const double* T, const double* lam, double* dJ, cudaStream_t s) {
+  long long ne_sp = 1;
+  for (int d = 0; d < op.g.sd; ++d) ne_sp *= op.g.n;
+  long long total = op.rho_tc ? ne_sp : ne_sp * op.g.nt;
+  unsigned grd = (unsigned)((total + 127) / 128);
+  if (op.g.sd == 2) sens_kernel<2><<<grd, 128, 0, s>>>(op, T, lam, dJ);
+  else sens_kernel<3><<<grd, 128, 0, s>>>(op, T, lam, dJ);
+}
+
+// ---------------------------------------------------------------------------------------
+// Dense coarsest level: Gauss-Jordan inverse with partial pivoting in one CTA (the level
+// has <= coarse_max_nodes nodes), then x = A^-1 b per V-cycle.
+__global__ void __launch_bounds__(1024) dense_invert_kernel(double* __restrict__ W, double* __restrict__ Ainv, int n,
+                                                            int* info) {
+  extern __shared__ double fac[];
+  __shared__ double bv[32];
+  __shared__ int bi[32];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  for (long long i = tid; i < (long long)n * n; i += nth) Ainv[i] = ((i / n) == (i % n)) ? 1.0 : 0.0;
+  if (tid == 0) *info = 0;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    // pivot search
+    double best = -1.0;
+    int bidx = k;
+    for (int i = k + tid; i < n; i += nth) {
+      double v = fabs(W[(long long)i * n + k]);
+      if (v > best) { best = v; bidx = i; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_down_sync(0xffffffffu, best, o);
+      int oi = __shfl_down_sync(0xffffffffu, bidx, o);
+      if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+    }
+    if ((tid & 31) == 0) { bv[tid >> 5] = best; bi[tid >> 5] = bidx; }
+    __syncthreads();
+    if (tid == 0) {
+      double bb = bv[0];
+      int ii = bi[0];
+      for (int w = 1; w < nth / 32; ++w)
+        if (bv[w] > bb || (bv[w] == bb && bi[w] < ii)) { bb = bv[w]; ii = bi[w]; }
+      bi[0] = ii;
+      if (!(bb > 0.0)) *info = k + 1;
+    }
+    __syncthreads();
+    const int piv = bi[0];
+    if (piv != k) {
+      for (int j = tid; j < n; j += nth) {
+        double t1 = W[(long long)k * n + j]; W[(long long)k * n + j] = W[(long long)piv * n + j]; W[(long long)piv * n + j] = t1;
+        double t2 = Ainv[(long long)k * n + j]; Ainv[(long long)k * n + j] = Ainv[(long long)piv * n + j]; Ainv[(long long)piv * n + j] = t2;
+      }
+    }
+    __syncthreads();
+    const double d = W[(long long)k * n + k];
+    const double inv = (d != 0.0) ? 1.0 / d : 0.0;
+    __syncthreads();
+    for (int j = tid; j < n; j += nth) {
+      W[(long long)k * n + j] *= inv;
+      Ainv[(long long)k * n + j] *= inv;
+    }
+    for (int i = tid; i < n; i += nth) fac[i] = (i == k) ? 0.0 : W[(long long)i * n + k];
+    __syncthreads();
+    for (long long e = tid; e < (long long)n * n; e += nth) {
+      int i = (int)(e / n), j = (int)(e % n);
+      double f = fac[i];
+      if (f != 0.0) {
+        W[e] -= f * W[(long long)k * n + j];
+        Ainv[e] -= f * Ainv[(long long)k * n + j];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+void launch_dense_invert(double* A, double* Ainv, int n, int* info, cudaStream_t s) {
+  dense_invert_kernel<<<1, 1024, n * sizeof(double), s>>>(A, Ainv, n, info);
+}
+
+__global__ void dense_solve_kernel(const double* __restrict__ Ainv, int n, int trans, const double* __restrict__ b,
+                                   double* __restrict__ x) {
+  // one warp per output entry
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  double acc = 0.0;
+  if (!trans)
+    for (int j = lane; j < n; j += 32) acc += Ainv[(long long)warp * n + j] * b[j];
+  else
+    for (int j = lane; j < n; j += 32) acc += Ainv[(long long)j * n + warp] * b[j];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if (lane == 0) x[warp] = acc;
+}
+
+void launch_dense_solve(const double* Ainv, int n, bool trans, const double* b, double* x, cudaStream_t s) {
+  int thr = 256;
+  unsigned grd = (unsigned)((n * 32 + thr - 1) / thr);
+  dense_solve_kernel<<<grd, thr, 0, s>>>(Ainv, n, trans ? 1 : 0, b, x);
+}
+
+}  // namespace st

@@ -1,0 +1,593 @@
+// ops.cu — level operators of the space-time system (2D+t and 3D+t), fp64, sm_100a.
+//
+// One kernel family evaluates, for every node of a level, the row of the (masked) operator
+//   (K x)_p = S^{tb}_{p-1} x_{p-1} + S^{tt}_{p-1} x_p + S^{bb}_p x_p + S^{bt}_p x_{p+1}
+// (transpose: swap S^{bt} <-> S^{tb}; spatial stencils are symmetric), marching in time so
+// that each element layer is evaluated once per node: the layer-p evaluation yields the
+// bottom part of row p and the top part of row p+1 (carried in a register).
+// Modes: APPLY y = A x; RESID y = b - A x; JAC y = x + w D^-1 (b - A x); JAC0 y = w D^-1 b.
+// Dirichlet elimination (R-1): A = m_f K m_f + m_c.
+// Fine level (FORM_RHO) is matrix-free: C_e, k~_e from rho by SIMP on the
+// fly, element matrices C (U (x) M_sp) + k~ (Tm (x) K_sp) (F1).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace st {
+
+// ---------------------------------------------------------------------------------------
+// element coefficients around a node (layer tau)
+template <int SD>
+__device__ __forceinline__ void elem_ck(const OpDesc& op, const int* c, int tau, double* ce, double* ke) {
+  const Geom& g = op.g;
+#pragma unroll
+  for (int e = 0; e < SG<SD>::NE; ++e) {
+    bool valid = (tau >= 0 && tau < g.nt);
+    long long eidx = 0, mul = 1;
+#pragma unroll
+    for (int d = 0; d < SD; ++d) {
+      int a = c[d] + ((e >> d) & 1) - 1;
+      valid = valid && (a >= 0 && a < g.n);
+      eidx += (long long)a * mul;
+      mul *= g.n;
+    }
+    if (valid) {
+      long long ri = op.rho_tc ? eidx : (long long)tau * mul + eidx;
+      double r = __ldg(op.rho + ri);
+      ce[e] = op.m.Cins + op.m.dC * powp(r, op.m.pc);
+      ke[e] = op.m.kins + op.m.dk * powp(r, op.m.pk);
+    } else {
+      ce[e] = 0.0;
+      ke[e] = 0.0;
+    }
+  }
+}
+
+// normalised spatial tables: M = sM * mh[h], K = sK * kh[h]
+template <int SD> __device__ __forceinline__ double mh(int h) {
+  return SD == 2 ? (h == 0 ? 4.0 : (h == 1 ? 2.0 : 1.0)) : (h == 0 ? 8.0 : (h == 1 ? 4.0 : (h == 2 ? 2.0 : 1.0)));
+}
+template <int SD> __device__ __forceinline__ double kh(int h) {
+  return SD == 2 ? (h == 0 ? 4.0 : (h == 1 ? -1.0 : -2.0)) : (h == 0 ? 4.0 : (h == 1 ? 0.0 : -1.0));
+}
+template <int SD> __device__ __forceinline__ double sM(double dx) {
+  return SD == 2 ? dx * dx / 36.0 : dx * dx * dx / 216.0;
+}
+template <int SD> __device__ __forceinline__ double sK(double dx) {
+  return SD == 2 ? 1.0 / 6.0 : dx / 12.0;
+}
+
+// weighted mass / stiffness applied at the node: sum_e coef_e * (element row . x)
+template <int SD>
+__device__ __forceinline__ void rho_MK(const double* ce, const double* ke, const double* xs, double dx,
+                                       double& Mx, double& Kx) {
+  double m = 0.0, k = 0.0;
+#pragma unroll
+  for (int e = 0; e < SG<SD>::NE; ++e) {
+    double pm = 0.0, pk = 0.0;
+#pragma unroll
+    for (int b = 0; b < SG<SD>::NE; ++b) {
+      int kk = 0, h = 0, mul = 1;
+#pragma unroll
+      for (int d = 0; d < SD; ++d) {
+        int bit = (e >> d) & 1, be = (b >> d) & 1;
+        int o = bit - 1 + be;
+        kk += (o + 1) * mul;
+        mul *= 3;
+        h += (be != 1 - bit) ? 1 : 0;
+      }
+      pm += mh<SD>(h) * xs[kk];
+      if (kh<SD>(h) != 0.0) pk += kh<SD>(h) * xs[kk];
+    }
+    m += ce[e] * pm;
+    k += ke[e] * pk;
+  }
+  Mx = m * sM<SD>(dx);
+  Kx = k * sK<SD>(dx);
+}
+
+// full stencil weight of offset k for the RHO form (s = 0: M, 1: K)
+template <int SD>
+__device__ __forceinline__ double rho_weight(const double* ce, const double* ke, int k, int s, double dx) {
+  double w = 0.0;
+  int h = 0;
+#pragma unroll
+  for (int d = 0; d < SD; ++d) h += SG<SD>::od(k, d) != 0;
+#pragma unroll
+  for (int e = 0; e < SG<SD>::NE; ++e) {
+    bool in = true;
+#pragma unroll
+    for (int d = 0; d < SD; ++d) {
+      int o = SG<SD>::od(k, d), bit = (e >> d) & 1;
+      if (o == 1 && bit != 1) in = false;
+      if (o == -1 && bit != 0) in = false;
+    }
+    if (in) w += (s == 0 ? ce[e] : ke[e]);
+  }
+  return s == 0 ? w * mh<SD>(h) * sM<SD>(dx) : w * kh<SD>(h) * sK<SD>(dx);
+}
+
+// stored symmetric stencil: weight of offset k at node c (base = layer/stencil origin)
+template <int SD>
+__device__ __forceinline__ double st_weight(const Geom& g, const double* __restrict__ base, const int* c,
+                                            long long pn, int k) {
+  constexpr int CEN = SG<SD>::CEN, NOFF = SG<SD>::NOFF;
+  if (k >= CEN) return __ldg(base + (long long)(k - CEN) * g.P + pn);
+  int nb[3] = {0, 0, 0};
+#pragma unroll
+  for (int d = 0; d < SD; ++d) {
+    nb[d] = c[d] + SG<SD>::od(k, d);
+    if (nb[d] < 0 || nb[d] >= g.nn) return 0.0;
+  }
+  return __ldg(base + (long long)(NOFF - 1 - k - CEN) * g.P + pidx<SD>(g, nb));
+}
+
+template <int SD>
+__device__ __forceinline__ double st_apply(const Geom& g, const double* __restrict__ base, const int* c,
+                                           long long pn, const double* xs) {
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < SG<SD>::NOFF; ++k) acc += st_weight<SD>(g, base, c, pn, k) * xs[k];
+  return acc;
+}
+
+template <bool TRANS>
+__device__ __forceinline__ void combine_mk(const OpDesc& op, double Mb, double Mt, double Kb, double Kt,
+                                           double& bot, double& top) {
+  if (!TRANS) {
+    bot = op.U[0][0] * Mb + op.U[0][1] * Mt + op.Tm[0][0] * Kb + op.Tm[0][1] * Kt;
+    top = op.U[1][0] * Mb + op.U[1][1] * Mt + op.Tm[1][0] * Kb + op.Tm[1][1] * Kt;
+  } else {
+    bot = op.U[0][0] * Mb + op.U[1][0] * Mt + op.Tm[0][0] * Kb + op.Tm[1][0] * Kt;
+    top = op.U[0][1] * Mb + op.U[1][1] * Mt + op.Tm[0][1] * Kb + op.Tm[1][1] * Kt;
+  }
+}
+
+// evaluate layer tau at node c: contributions to row tau (bot) and row tau+1 (top), plus
+// the diagonal parts S^{bb}_center (dbot) and S^{tt}_center (dtop)
+template <int SD, int FORM, bool TRANS, bool NEEDX, bool NEEDD>
+__device__ __forceinline__ void layer_eval(const OpDesc& op, const int* c, long long pn, int tau,
+                                           const double* xb, const double* xt, double& bot, double& top,
+                                           double& dbot, double& dtop) {
+  constexpr int NC = SG<SD>::NC, CEN = SG<SD>::CEN;
+  const Geom& g = op.g;
+  bot = top = dbot = dtop = 0.0;
+  if (FORM == FORM_RHO) {
+    double ce[SG<SD>::NE], ke[SG<SD>::NE];
+    elem_ck<SD>(op, c, tau, ce, ke);
+    if (NEEDX) {
+      double Mb, Kb, Mt, Kt;
+      rho_MK<SD>(ce, ke, xb, g.dx, Mb, Kb);
+      rho_MK<SD>(ce, ke, xt, g.dx, Mt, Kt);
+      combine_mk<TRANS>(op, Mb, Mt, Kb, Kt, bot, top);
+    }
+    if (NEEDD) {
+      double Mc = rho_weight<SD>(ce, ke, CEN, 0, g.dx), Kc = rho_weight<SD>(ce, ke, CEN, 1, g.dx);
+      dbot = op.U[0][0] * Mc + op.Tm[0][0] * Kc;
+      dtop = op.U[1][1] * Mc + op.Tm[1][1] * Kc;
+    }
+  } else if (FORM == FORM_MK) {
+    const double* Mbase = op.st + (long long)(op.nl == 1 ? 0 : tau) * 2 * NC * g.P;
+    const double* Kbase = Mbase + (long long)NC * g.P;
+    if (NEEDX) {
+      double Mb = st_apply<SD>(g, Mbase, c, pn, xb), Mt = st_apply<SD>(g, Mbase, c, pn, xt);
+      double Kb = st_apply<SD>(g, Kbase, c, pn, xb), Kt = st_apply<SD>(g, Kbase, c, pn, xt);
+      combine_mk<TRANS>(op, Mb, Mt, Kb, Kt, bot, top);
+    }
+    if (NEEDD) {
+      double Mc = __ldg(Mbase + pn), Kc = __ldg(Kbase + pn);
+      dbot = op.U[0][0] * Mc + op.Tm[0][0] * Kc;
+      dtop = op.U[1][1] * Mc + op.Tm[1][1] * Kc;
+    }
+  } else {  // FORM_B4
+    const double* base = op.st + (long long)(op.nl == 1 ? 0 : tau) * 4 * NC * g.P;
+    const double* Sbb = base;
+    const double* Sbt = base + (long long)NC * g.P;
+    const double* Stb = base + 2LL * NC * g.P;
+    const double* Stt = base + 3LL * NC * g.P;
+    if (NEEDX) {
+      if (!TRANS) {
+        bot = st_apply<SD>(g, Sbb, c, pn, xb) + st_apply<SD>(g, Sbt, c, pn, xt);
+        top = st_apply<SD>(g, Stb, c, pn, xb) + st_apply<SD>(g, Stt, c, pn, xt);
+      } else {
+        bot = st_apply<SD>(g, Sbb, c, pn, xb) + st_apply<SD>(g, Stb, c, pn, xt);
+        top = st_apply<SD>(g, Sbt, c, pn, xb) + st_apply<SD>(g, Stt, c, pn, xt);
+      }
+    }
+    if (NEEDD) {
+      dbot = __ldg(Sbb + pn);
+      dtop = __ldg(Stt + pn);
+    }
+  }
+}
+
+template <int SD, bool MASK>
+__device__ __forceinline__ void load_nb(const Geom& g, const double* __restrict__ x, const int* c, int q,
+                                        double* xs) {
+  const double* xp = x + (long long)q * g.P;
+#pragma unroll
+  for (int k = 0; k < SG<SD>::NOFF; ++k) {
+    int nb[3] = {0, 0, 0};
+    bool valid = true;
+#pragma unroll
+    for (int d = 0; d < SD; ++d) {
+      nb[d] = c[d] + SG<SD>::od(k, d);
+      valid = valid && nb[d] >= 0 && nb[d] < g.nn;
+    }
+    double v = 0.0;
+    if (valid) {
+      v = __ldg(xp + pidx<SD>(g, nb));
+      if (MASK && is_cons<SD>(g, nb, q)) v = 0.0;
+    }
+    xs[k] = v;
+  }
+}
+
+template <int SD, int FORM, int MODE, bool TRANS, bool MASK>
+__global__ void __launch_bounds__(128) op_kernel(OpDesc op, const double* __restrict__ x,
+                                                 const double* __restrict__ b, double* __restrict__ y,
+                                                 double omega, int chunk) {
+  constexpr int NOFF = SG<SD>::NOFF;
+  constexpr bool NEEDX = (MODE != MODE_JAC0);
+  constexpr bool NEEDD = (MODE == MODE_JAC || MODE == MODE_JAC0);
+  const Geom& g = op.g;
+  const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y * blockDim.y + threadIdx.y;
+  const int rows = (SD == 2) ? g.nn : g.nn * g.nn;
+  if (i0 >= g.nn || r >= rows) return;
+  int c[3];
+  c[0] = i0;
+  c[1] = (SD == 2) ? r : r % g.nn;
+  c[2] = (SD == 2) ? 0 : r / g.nn;
+  const long long pn = i0 + (long long)g.nn * r;
+  const int p0 = blockIdx.z * chunk;
+  const int p1 = min(p0 + chunk, g.nt + 1);
+  if (p0 > g.nt) return;
+  const bool patch = MASK && is_patch<SD>(g, c);
+
+  double xb[NOFF], xt[NOFF];
+  double carry = 0.0, dcarry = 0.0;
+  if (NEEDX) {
+    if (p0 >= 1) {
+      load_nb<SD, MASK>(g, x, c, p0 - 1, xb);
+      load_nb<SD, MASK>(g, x, c, p0, xt);
+    } else {
+      load_nb<SD, MASK>(g, x, c, p0, xt);
+    }
+  }
+  if (p0 >= 1) {
+    double bt, tp, db, dt;
+    layer_eval<SD, FORM, TRANS, NEEDX, NEEDD>(op, c, pn, p0 - 1, xb, xt, bt, tp, db, dt);
+    carry = tp;
+    dcarry = dt;
+  }
+  for (int p = p0; p < p1; ++p) {
+    if (NEEDX) {
+#pragma unroll
+      for (int k = 0; k < NOFF; ++k) xb[k] = xt[k];
+    }
+    double bot = 0.0, top = 0.0, dbot = 0.0, dtop = 0.0;
+    if (p < g.nt) {
+      if (NEEDX) load_nb<SD, MASK>(g, x, c, p + 1, xt);
+      layer_eval<SD, FORM, TRANS, NEEDX, NEEDD>(op, c, pn, p, xb, xt, bot, top, dbot, dtop);
+    }
+    const long long gi = (long long)p * g.P + pn;
+    const bool cons = MASK && (p == 0 || patch);
+    double Ax = carry + bot;
+    double D = dcarry + dbot;
+    if (cons) {
+      Ax = NEEDX ? __ldg(x + gi) : 0.0;
+      D = 1.0;
+    }
+    double out;
+    if (MODE == MODE_APPLY) out = Ax;
+    else if (MODE == MODE_RESID) out = __ldg(b + gi) - Ax;
+    else if (MODE == MODE_JAC) out = __ldg(x + gi) + omega * (__ldg(b + gi) - Ax) / D;
+    else out = omega * __ldg(b + gi) / D;
+    y[gi] = out;
+    carry = top;
+    dcarry = dtop;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+static int choose_chunk(const Geom& g) {
+  long long per_plane = g.P;
+  long long target = 148LL * 2048 * 2;
+  long long chunks = (target + per_plane - 1) / per_plane;
+  if (chunks < 1) chunks = 1;
+  if (chunks > g.nt + 1) chunks = g.nt + 1;
+  return (int)((g.nt + 1 + chunks - 1) / chunks);
+}
+
+template <int SD, int FORM, int MODE, bool TRANS, bool MASK>
+static void launch_t(const OpDesc& op, const double* x, const double* b, double* y, double omega, cudaStream_t s) {
+  const Geom& g = op.g;
+  dim3 blk(32, 4, 1);
+  int rows = SD == 2 ? g.nn : g.nn * g.nn;
+  int chunk = choose_chunk(g);
+  dim3 grd((g.nn + 31) / 32, (rows + 3) / 4, (g.nt + 1 + chunk - 1) / chunk);
+  op_kernel<SD, FORM, MODE, TRANS, MASK><<<grd, blk, 0, s>>>(op, x, b, y, omega, chunk);
+}
+
+template <int SD, int FORM>
+static void launch_f(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b,
+                     double* y, double omega, cudaStream_t s) {
+  if (!mask) {
+    if (trans) launch_t<SD, FORM, MODE_APPLY, true, false>(op, x, b, y, omega, s);
+    else launch_t<SD, FORM, MODE_APPLY, false, false>(op, x, b, y, omega, s);
+    return;
+  }
+#define ST_CASE(M)                                                              \
+  case M:                                                                       \
+    if (trans) launch_t<SD, FORM, M, true, true>(op, x, b, y, omega, s);        \
+    else launch_t<SD, FORM, M, false, true>(op, x, b, y, omega, s);             \
+    break;
+  switch (mode) {
+    ST_CASE(MODE_APPLY)
+    ST_CASE(MODE_RESID)
+    ST_CASE(MODE_JAC)
+    ST_CASE(MODE_JAC0)
+  }
+#undef ST_CASE
+}
+
+void launch_op(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
+               double omega, cudaStream_t s) {
+  if (op.g.sd == 2) {
+    if (op.form == FORM_RHO) launch_f<2, FORM_RHO>(op, mode, trans, mask, x, b, y, omega, s);
+    else if (op.form == FORM_MK) launch_f<2, FORM_MK>(op, mode, trans, mask, x, b, y, omega, s);
+    else launch_f<2, FORM_B4>(op, mode, trans, mask, x, b, y, omega, s);
+  } else {
+    if (op.form == FORM_RHO) launch_f<3, FORM_RHO>(op, mode, trans, mask, x, b, y, omega, s);
+    else if (op.form == FORM_MK) launch_f<3, FORM_MK>(op, mode, trans, mask, x, b, y, omega, s);
+    else launch_f<3, FORM_B4>(op, mode, trans, mask, x, b, y, omega, s);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Weight accessor used by the Galerkin and dense-assembly kernels: full weight of offset k
+// of time block (a,b) in layer tau at node c.
+template <int SD, int FORM>
+__device__ double block_weight(const OpDesc& op, const int* c, long long pn, int tau, int a, int bb, int k) {
+  constexpr int NC = SG<SD>::NC;
+  const Geom& g = op.g;
+  if (FORM == FORM_RHO) {
+    double ce[SG<SD>::NE], ke[SG<SD>::NE];
+    elem_ck<SD>(op, c, tau, ce, ke);
+    return op.U[a][bb] * rho_weight<SD>(ce, ke, k, 0, g.dx) + op.Tm[a][bb] * rho_weight<SD>(ce, ke, k, 1, g.dx);
+  } else if (FORM == FORM_MK) {
+    const double* Mbase = op.st + (long long)(op.nl == 1 ? 0 : tau) * 2 * NC * g.P;
+    const double* Kbase = Mbase + (long long)NC * g.P;
+    return op.U[a][bb] * st_weight<SD>(g, Mbase, c, pn, k) + op.Tm[a][bb] * st_weight<SD>(g, Kbase, c, pn, k);
+  } else {
+    const double* base = op.st + (long long)(op.nl == 1 ? 0 : tau) * 4 * NC * g.P + (long long)(2 * a + bb) * NC * g.P;
+    return st_weight<SD>(g, base, c, pn, k);
+  }
+}
+
+// MK weight of stencil s (0 = M, 1 = K) — only for RHO / MK forms
+template <int SD, int FORM>
+__device__ double mk_weight(const OpDesc& op, const int* c, long long pn, int tau, int s, int k) {
+  constexpr int NC = SG<SD>::NC;
+  const Geom& g = op.g;
+  if (FORM == FORM_RHO) {
+    double ce[SG<SD>::NE], ke[SG<SD>::NE];
+    elem_ck<SD>(op, c, tau, ce, ke);
+    return rho_weight<SD>(ce, ke, k, s, g.dx);
+  } else {
+    const double* base = op.st + (long long)(op.nl == 1 ? 0 : tau) * 2 * NC * g.P + (long long)s * NC * g.P;
+    return st_weight<SD>(g, base, c, pn, k);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Galerkin coarse operators, structured.
+// Spatial coarsening: every stored stencil of the coarse level is P_x^T S P_x with the
+// bilinear/trilinear interpolation P_x (weights 1, 1/2 per direction), per layer.
+// NS stencils: MK -> 2 (M, K), B4 -> 4. Fine op provides weights through mk_/block_weight.
+template <int SD, int FFORM, int NS>
+__global__ void rap_space_kernel(OpDesc fop, Geom gc, int nl, double* __restrict__ out) {
+  constexpr int NOFF = SG<SD>::NOFF, NC = SG<SD>::NC, CEN = SG<SD>::CEN;
+  const Geom& gf = fop.g;
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long total = gc.P * nl * NS;
+  if (idx >= total) return;
+  long long pc = idx % gc.P;
+  int s = (int)((idx / gc.P) % NS);
+  int tau = (int)(idx / (gc.P * NS));
+  int C[3] = {0, 0, 0};
+  {
+    long long t = pc;
+    for (int d = 0; d < SD; ++d) { C[d] = (int)(t % gc.nn); t /= gc.nn; }
+  }
+  double acc[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) acc[q] = 0.0;
+  // loop over fine nodes f in supp(C)
+  for (int fa = 0; fa < NOFF; ++fa) {
+    int f[3] = {0, 0, 0};
+    bool ok = true;
+    double wf = 1.0;
+    for (int d = 0; d < SD; ++d) {
+      int o = SG<SD>::od(fa, d);
+      f[d] = 2 * C[d] + o;
+      ok = ok && f[d] >= 0 && f[d] < gf.nn;
+      wf *= (o == 0) ? 1.0 : 0.5;
+    }
+    if (!ok) continue;
+    long long pf = pidx<SD>(gf, f);
+    for (int k = 0; k < NOFF; ++k) {
+      int gg[3] = {0, 0, 0};
+      bool okg = true;
+      for (int d = 0; d < SD; ++d) {
+        gg[d] = f[d] + SG<SD>::od(k, d);
+        okg = okg && gg[d] >= 0 && gg[d] < gf.nn;
+      }
+      if (!okg) continue;
+      double w;
+      if (NS == 2) w = mk_weight<SD, FFORM>(fop, f, pf, tau, s, k);
+      else w = block_weight<SD, FFORM>(fop, f, pf, tau, s >> 1, s & 1, k);
+      if (w == 0.0) continue;
+      // interpolation weight of g from coarse node C + off(q), q >= CEN
+#pragma unroll
+      for (int q = 0; q < NC; ++q) {
+        int kq = q + CEN;
+        double wg = 1.0;
+        for (int d = 0; d < SD; ++d) {
+          int diff = gg[d] - 2 * (C[d] + SG<SD>::od(kq, d));
+          if (diff < -1 || diff > 1) { wg = 0.0; break; }
+          wg *= (diff == 0) ? 1.0 : 0.5;
+        }
+        acc[q] += wf * w * wg;
+      }
+    }
+  }
+  double* o = out + ((long long)tau * NS + s) * NC * gc.P;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) o[(long long)q * gc.P + pc] = acc[q];
+}
+
+// Time coarsening: coarse layer T from fine layers 2T, 2T+1 with the linear-in-time
+// interpolation (fine plane 2T+1 = (coarse T + coarse T+1)/2):
+//   S'^{AB} = sum_f sum_{a,b} W_f[a][A] W_f[b][B] S_{2T+f}^{ab},  W_0 = [[1,0],[.5,.5]], W_1 = [[.5,.5],[0,1]].
+template <int SD, int FFORM>
+__global__ void rap_time_kernel(OpDesc fop, int nlc, double* __restrict__ out) {
+  constexpr int NC = SG<SD>::NC, CEN = SG<SD>::CEN;
+  const Geom& g = fop.g;
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long total = g.P * nlc;
+  if (idx >= total) return;
+  long long pn = idx % g.P;
+  int T = (int)(idx / g.P);
+  int c[3] = {0, 0, 0};
+  {
+    long long t = pn;
+    for (int d = 0; d < SD; ++d) { c[d] = (int)(t % g.nn); t /= g.nn; }
+  }
+  const double W[2][2][2] = {{{1.0, 0.0}, {0.5, 0.5}}, {{0.5, 0.5}, {0.0, 1.0}}};
+  for (int q = 0; q < NC; ++q) {
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int f = 0; f < 2; ++f) {
+      int tau = (fop.nl == 1 && FFORM != FORM_RHO) ? 0 : 2 * T + f;
+      if (FFORM == FORM_RHO && fop.rho_tc) tau = 0;
+      double s[2][2];
+      for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) s[a][b] = block_weight<SD, FFORM>(fop, c, pn, tau, a, b, q + CEN);
+      for (int A = 0; A < 2; ++A)
+        for (int B = 0; B < 2; ++B) {
+          double v = 0.0;
+          for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b) v += W[f][a][A] * W[f][b][B] * s[a][b];
+          acc[A][B] += v;
+        }
+    }
+    for (int A = 0; A < 2; ++A)
+      for (int B = 0; B < 2; ++B) out[((long long)T * 4 + 2 * A + B) * NC * g.P + (long long)q * g.P + pn] = acc[A][B];
+  }
+}
+
+// Materialise the M, K stencils of the fine RHO operator for one layer (time-constant
+// design): out[2][NC][P].
+template <int SD>
+__global__ void rho_to_mk_kernel(OpDesc fop, int tau, double* __restrict__ out) {
+  constexpr int NC = SG<SD>::NC, CEN = SG<SD>::CEN;
+  const Geom& g = fop.g;
+  long long pn = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (pn >= g.P) return;
+  int c[3] = {0, 0, 0};
+  long long t = pn;
+  for (int d = 0; d < SD; ++d) { c[d] = (int)(t % g.nn); t /= g.nn; }
+  double ce[SG<SD>::NE], ke[SG<SD>::NE];
+  elem_ck<SD>(fop, c, tau, ce, ke);
+  for (int q = 0; q < NC; ++q) {
+    out[(long long)q * g.P + pn] = rho_weight<SD>(ce, ke, q + CEN, 0, g.dx);
+    out[(long long)(NC + q) * g.P + pn] = rho_weight<SD>(ce, ke, q + CEN, 1, g.dx);
+  }
+}
+
+void launch_rap_space(const OpDesc& fop, const Geom& gc, int nl, int ns, double* out, cudaStream_t s) {
+  long long total = gc.P * nl * ns;
+  int blk = 128;
+  long long grd = (total + blk - 1) / blk;
+#define RS(SD, F, NS) rap_space_kernel<SD, F, NS><<<(unsigned)grd, blk, 0, s>>>(fop, gc, nl, out)
+  if (fop.g.sd == 2) {
+    if (ns == 2) { if (fop.form == FORM_RHO) RS(2, FORM_RHO, 2); else RS(2, FORM_MK, 2); }
+    else { if (fop.form == FORM_RHO) RS(2, FORM_RHO, 4); else if (fop.form == FORM_MK) RS(2, FORM_MK, 4); else RS(2, FORM_B4, 4); }
+  } else {
+    if (ns == 2) { if (fop.form == FORM_RHO) RS(3, FORM_RHO, 2); else RS(3, FORM_MK, 2); }
+    else { if (fop.form == FORM_RHO) RS(3, FORM_RHO, 4); else if (fop.form == FORM_MK) RS(3, FORM_MK, 4); else RS(3, FORM_B4, 4); }
+  }
+#undef RS
+}
+
+void launch_rap_time(const OpDesc& fop, int nlc, double* out, cudaStream_t s) {
+  long long total = fop.g.P * nlc;
+  int blk = 128;
+  long long grd = (total + blk - 1) / blk;
+#define RT(SD, F) rap_time_kernel<SD, F><<<(unsigned)grd, blk, 0, s>>>(fop, nlc, out)
+  if (fop.g.sd == 2) {
+    if (fop.form == FORM_RHO) RT(2, FORM_RHO); else if (fop.form == FORM_MK) RT(2, FORM_MK); else RT(2, FORM_B4);
+  } else {
+    if (fop.form == FORM_RHO) RT(3, FORM_RHO); else if (fop.form == FORM_MK) RT(3, FORM_MK); else RT(3, FORM_B4);
+  }
+#undef RT
+}
+
+void launch_rho_to_mk(const OpDesc& fop, int tau, double* out, cudaStream_t s) {
+  int blk = 128;
+  long long grd = (fop.g.P + blk - 1) / blk;
+  if (fop.g.sd == 2) rho_to_mk_kernel<2><<<(unsigned)grd, blk, 0, s>>>(fop, tau, out);
+  else rho_to_mk_kernel<3><<<(unsigned)grd, blk, 0, s>>>(fop, tau, out);
+}
+
+// ---------------------------------------------------------------------------------------
+// Dense coarsest operator: A[row][col] of the masked level operator (row-major, N x N).
+template <int SD, int FORM>
+__global__ void dense_assemble_kernel(OpDesc op, double* __restrict__ A) {
+  constexpr int NOFF = SG<SD>::NOFF;
+  const Geom& g = op.g;
+  long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (row >= g.N) return;
+  int p = (int)(row / g.P);
+  long long pn = row % g.P;
+  int c[3] = {0, 0, 0};
+  long long t = pn;
+  for (int d = 0; d < SD; ++d) { c[d] = (int)(t % g.nn); t /= g.nn; }
+  double* Ar = A + row * g.N;
+  if (is_cons<SD>(g, c, p)) { Ar[row] = 1.0; return; }
+  // layer p-1 (top rows: S^{tb} -> plane p-1, S^{tt} -> plane p); layer p (bottom rows)
+  for (int side = 0; side < 2; ++side) {
+    int tau = side == 0 ? p - 1 : p;
+    if (tau < 0 || tau >= g.nt) continue;
+    int a = side == 0 ? 1 : 0;
+    for (int bb = 0; bb < 2; ++bb) {
+      int q = tau + bb;  // plane of the trial node
+      for (int k = 0; k < NOFF; ++k) {
+        int nb[3] = {0, 0, 0};
+        bool ok = true;
+        for (int d = 0; d < SD; ++d) {
+          nb[d] = c[d] + SG<SD>::od(k, d);
+          ok = ok && nb[d] >= 0 && nb[d] < g.nn;
+        }
+        if (!ok) continue;
+        if (is_cons<SD>(g, nb, q)) continue;
+        double w = block_weight<SD, FORM>(op, c, pn, tau, a, bb, k);
+        Ar[(long long)q * g.P + pidx<SD>(g, nb)] += w;
+      }
+    }
+  }
+}
+
+void launch_dense_assemble(const OpDesc& op, double* A, cudaStream_t s) {
+  int blk = 128;
+  long long grd = (op.g.N + blk - 1) / blk;
+#define DA(SD, F) dense_assemble_kernel<SD, F><<<(unsigned)grd, blk, 0, s>>>(op, A)
+  if (op.g.sd == 2) {
+    if (op.form == FORM_RHO) DA(2, FORM_RHO); else if (op.form == FORM_MK) DA(2, FORM_MK); else DA(2, FORM_B4);
+  } else {
+    if (op.form == FORM_RHO) DA(3, FORM_RHO); else if (op.form == FORM_MK) DA(3, FORM_MK); else DA(3, FORM_B4);
+  }
+#undef DA
+}
+
+}  // namespace st

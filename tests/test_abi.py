@@ -1,0 +1,66 @@
+"""CPU-side checks of the boundary: libst.so builds for sm_100a, loads, and exports every
+function include/st.h declares (no compute calls without a GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "st.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(st_[a-z_]+)\s*\(", src)))
+
+
+def test_library_builds_and_exports_all_declared_symbols():
+    from paper_2508_09589_b200 import build
+    path = build.build()
+    lib = ctypes.CDLL(path)
+    names = _declared()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+
+
+def test_binding_exports_match_header():
+    from paper_2508_09589_b200 import st
+    assert set(st.EXPORTS) <= set(_declared())
+
+
+def test_default_options_and_errors():
+    from paper_2508_09589_b200 import st
+    lib = st.load_library()
+    o = st.Options()
+    lib.st_default_options(ctypes.byref(o))
+    assert o.rtol == 1e-8 and o.lambda_crit == 0.5 and o.restart == 30
+    assert lib.st_abi_version() == 1
+    assert lib.st_strerror(-2).decode().startswith("grid not divisible")
+
+
+def test_setup_rejects_bad_args_without_gpu():
+    """Validation happens before any device call: n < 2 must fail with ST_E_INVALID_ARG."""
+    from paper_2508_09589_b200 import st
+    lib = st.load_library()
+    g = st.Grid(2, 1, 4, 1.0, 1.0)
+    m = st.Materials(1, 1, 1, 1e-3, 1, 3)
+    b = st.BCs(0.0, 1, 0, 0.5, 0.05)
+    s = st.Source(0, 1.0, 0.0, 0.0)
+    h = ctypes.c_void_p()
+    rc = lib.st_setup(ctypes.byref(g), ctypes.byref(m), ctypes.byref(b), ctypes.byref(s), None, None, ctypes.byref(h))
+    assert rc == -1
+
+
+def test_cubin_is_sm100a():
+    """The fatbinary carries sm_100a SASS (cuobjdump)."""
+    import shutil
+    import subprocess
+    from paper_2508_09589_b200 import build
+    path = build.build()
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([tool, "--list-elf", path], capture_output=True, text=True).stdout
+    assert "sm_100a" in out

@@ -1,0 +1,196 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element, on
+the same seeded inputs (north_star tolerances: operator <= 1e-12, solution <= 1e-8 at
+rtol 1e-10, sensitivities <= 1e-7, all fp64, normwise relative; R-15, R-16)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import oracle as O
+import st_inputs as I
+from tests.gpu_util import CFG1_MATS, CFG4_MATS, make_pair, rel
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+DEV = torch.device("cuda:0")
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=DEV)
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+OP_CASES = [
+    # (sdim, n, nt, mats, T0, design, seed, tc)
+    (2, 16, 16, CFG1_MATS, 0.0, "uniform", 0, False),
+    (2, 16, 16, CFG1_MATS, 0.0, "uniform", 3, False),
+    (2, 12, 20, CFG4_MATS, 0.3, "uniform", 1, False),
+    (2, 32, 32, CFG1_MATS, 0.0, "smooth_tc", 0, True),
+    (2, 2, 2, CFG1_MATS, 0.5, "uniform", 2, False),
+    (2, 7, 5, CFG4_MATS, 0.0, "uniform", 4, False),
+    (3, 4, 6, CFG4_MATS, 0.2, "uniform", 0, False),
+    (3, 6, 12, CFG4_MATS, 0.0, "smooth_tc", 0, True),
+]
+
+
+def _rho(sdim, n, nt, design, seed, tc):
+    if design == "uniform":
+        shape = (n,) * sdim if tc else (nt,) + (n,) * sdim
+        return I.rho_uniform(shape, seed)
+    return I.design_for(sdim, n, nt, design, seed)
+
+
+@pytest.mark.parametrize("case", OP_CASES, ids=lambda c: f"{c[0]}d-{c[1]}x{c[2]}-s{c[6]}-{'tc' if c[7] else 'st'}")
+def test_operator_parity(case):
+    sdim, n, nt, mats, T0, design, seed, tc = case
+    solver, prob = make_pair(sdim, n, nt, mats=mats, T0=T0, time_constant=tc)
+    rho = _rho(sdim, n, nt, design, seed, tc)
+    K = prob.K(rho)
+    Kbc, _, _, _ = prob.system(rho)
+    x = I.rand_vector(prob.mesh.n_nodes, seed + 1)
+    xd, yd = dev(x), torch.empty(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+    rd = dev(rho)
+    for trans in (False, True):
+        for bc in (False, True):
+            A = (Kbc if bc else K)
+            ref = (A.T if trans else A) @ x
+            solver.apply(rd, xd, yd, transpose=trans, bc=bc)
+            assert rel(host(yd), ref) <= 1e-12, (trans, bc, rel(host(yd), ref))
+    solver.close()
+
+
+@pytest.mark.parametrize("src,T0", [(("uniform", 1.0, 0.0, 0.0), 0.0), (("sin", 1.0, 1.0, 2 * np.pi), 0.4)])
+def test_rhs_parity(src, T0):
+    solver, prob = make_pair(2, 12, 10, mats=CFG4_MATS, T0=T0, source=src)
+    rho = I.rho_uniform((10, 12, 12), 5)
+    _, b_ref, _, _ = prob.system(rho)
+    f = torch.empty(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+    b = torch.empty_like(f)
+    solver.rhs(dev(rho), f, b)
+    assert rel(host(f), prob.f()) <= 1e-13
+    assert rel(host(b), b_ref) <= 1e-12
+
+
+SOLVE_CASES = [
+    # name, sdim, n, nt, mats, T0, source, tau, design, tc
+    ("cfg1", 2, 16, 16, CFG1_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0), 1.0, "uniform", False),
+    ("cfg2-replica", 2, 32, 32, CFG1_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0), 1.0, "smooth_tc", True),
+    ("cfg3-replica", 2, 32, 32, CFG1_MATS, 0.0, ("sin", 1.0, 1.0, 2 * np.pi), 1.0, "smooth_layers", False),
+    ("cfg4-replica", 3, 6, 12, CFG4_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0), 1.0, "smooth_tc", True),
+    ("cfg5-replica-G2", 2, 16, 32, CFG1_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0), 2.0, "const", False),
+    ("nonzero-T0", 2, 12, 20, CFG4_MATS, 0.7, ("sin", 1.0, 1.0, 2 * np.pi), 1.0, "uniform", False),
+]
+
+
+@pytest.mark.parametrize("case", SOLVE_CASES, ids=lambda c: c[0])
+def test_solve_adjoint_sensitivity_parity(case):
+    name, sdim, n, nt, mats, T0, src, tau, design, tc = case
+    solver, prob = make_pair(sdim, n, nt, mats=mats, T0=T0, source=src, tau=tau, time_constant=tc,
+                             rtol=1e-10, maxit=400)
+    if design == "uniform":
+        rho = _rho(sdim, n, nt, "uniform", 0, tc)
+    else:
+        rho = I.design_for(sdim, n, nt, design, 0)
+    T_ref, lam_ref = prob.solve_both(rho)
+    dJ_ref = prob.sensitivity(rho, T_ref, lam_ref)
+    rd = dev(rho)
+    T = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+    solver.solve(rd, T)
+    st = solver.stats()
+    assert st["converged"] == 1 and st["rel_residual"] <= 1e-10
+    assert rel(host(T), T_ref) <= 1e-8, rel(host(T), T_ref)
+    g = dev(prob.compliance_rhs())
+    lam = torch.zeros_like(T)
+    solver.adjoint(rd, g, lam)
+    assert solver.stats()["converged"] == 1
+    assert rel(host(lam), lam_ref) <= 1e-8, rel(host(lam), lam_ref)
+    dJ = torch.empty(rho.size, dtype=torch.float64, device=DEV)
+    solver.sensitivity(rd, T, lam, dJ)
+    assert rel(host(dJ).reshape(dJ_ref.shape), dJ_ref) <= 1e-7, rel(host(dJ).reshape(dJ_ref.shape), dJ_ref)
+    solver.close()
+
+
+def test_host_pointer_path_and_warm_start():
+    """C ABI with HOST buffers (library stages them) gives the same result; a warm start
+    from the solution converges in zero iterations."""
+    solver, prob = make_pair(2, 16, 16, rtol=1e-10)
+    rho = I.rho_uniform((16, 16, 16), 0)
+    T_ref = prob.forward(rho)
+    T = np.zeros(prob.mesh.n_nodes)
+    solver.solve(rho, T)
+    assert rel(T, T_ref) <= 1e-8
+    solver.solve(rho, T)
+    assert solver.stats()["iterations"] == 0
+    lam = np.zeros_like(T)
+    solver.adjoint(rho, prob.compliance_rhs(), lam)
+    dJ = np.zeros(rho.size)
+    solver.sensitivity(rho, T, lam, dJ)
+    _, lam_ref = prob.solve_both(rho)
+    assert rel(dJ.reshape(rho.shape), prob.sensitivity(rho, T_ref, lam_ref)) <= 1e-7
+    solver.close()
+
+
+def _P1(nf, kind):
+    """1D linear interpolation coarse(n/2) -> fine(n) nodes."""
+    nc = nf // 2
+    P = np.zeros((nf + 1, nc + 1))
+    for i in range(nf + 1):
+        if i % 2 == 0:
+            P[i, i // 2] = 1.0
+        else:
+            P[i, i // 2] = P[i, i // 2 + 1] = 0.5
+    return P
+
+
+@pytest.mark.parametrize("sdim,n,nt,tc", [(2, 16, 16, False), (2, 32, 32, True), (3, 4, 8, False)])
+def test_galerkin_coarse_operators(sdim, n, nt, tc):
+    """Each stored coarse level equals the masked Galerkin product P^T A_{l-1} P of the
+    unconstrained operator, with P the
+    space/time linear interpolation of the level pair, built here independently."""
+    solver, prob = make_pair(sdim, n, nt, mats=CFG4_MATS, time_constant=tc)
+    rho = I.rho_uniform((n,) * sdim if tc else (nt,) + (n,) * sdim, 3)
+    H = solver.hierarchy()
+    Kl = prob.K(rho).tocsr()
+    dims = [(H[0]["n"], H[0]["nt"])]
+    for l in range(1, len(H)):
+        nf, ntf = dims[-1]
+        if H[l]["kind"] == "space":
+            Px = sp.csr_matrix(_P1(nf, "s"))
+            Ps = Px
+            for _ in range(sdim - 1):
+                Ps = sp.kron(Px, Ps)
+            P = sp.kron(sp.identity(ntf + 1), Ps).tocsr()
+        else:
+            Ps = sp.identity((nf + 1) ** sdim)
+            P = sp.kron(sp.csr_matrix(_P1(ntf, "t")), Ps).tocsr()
+        Kl = (P.T @ Kl @ P).tocsr()
+        dims.append((H[l]["n"], H[l]["nt"]))
+        # masked reference
+        mesh_l = O.Mesh(sdim, H[l]["n"], H[l]["nt"])
+        # constrained set at level l: t=0 plane + patch injected (range halves per space step)
+        cons, _ = O.dirichlet(mesh_l, O.BCs())
+        free = (~cons).astype(float)
+        Aref = sp.diags(free) @ Kl @ sp.diags(free) + sp.diags(cons.astype(float))
+        x = I.rand_vector(mesh_l.n_nodes, 7 + l)
+        y = torch.empty(mesh_l.n_nodes, dtype=torch.float64, device=DEV)
+        for trans in (False, True):
+            solver.level_apply(dev(rho), l, dev(x), y, transpose=trans)
+            ref = (Aref.T if trans else Aref) @ x
+            assert rel(host(y), ref) <= 1e-12, (l, trans, rel(host(y), ref))
+    solver.close()
+
+
+def test_iteration_counts_reasonable():
+    """Config-1 forward/adjoint converge in a modest number of outer iterations."""
+    solver, prob = make_pair(2, 16, 16)
+    rho = dev(I.rho_uniform((16, 16, 16), 0))
+    T = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+    solver.solve(rho, T)
+    assert solver.stats()["iterations"] <= 40
+    solver.close()
