@@ -74,7 +74,8 @@ def backward_euler(n: int, sdim: int, C_e, k_e, q_of_t, nsteps: int, T0: float,
     Mf = sp.diags(free)
     A = (Mf @ (M / dt + K) @ Mf + sp.diags(cons.astype(np.float64))).tocsc()
     lu = spla.splu(A)
-    T = np.full(N, float(T0))  # T^0 = T0 everywhere (IC); the sink holds 0 for t > 0
+    T = np.full(N, float(T0))  # T^0 = T0 (IC) except on the sink, which holds 0 (R-2)
+    T[cons] = 0.0
     out = [T.copy()]
     for m in range(nsteps):
         t1 = (m + 1) * dt

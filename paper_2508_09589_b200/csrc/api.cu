@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -234,14 +235,15 @@ void setup_forms(st_ctx* c) {
         Lv.st_elems = (long long)op.nl * 2 * NC * Lv.g.P;
       } else {
         op.form = FORM_B4;
-        Lv.st_elems = (long long)op.nl * 4 * NC * Lv.g.P;
+        memcpy(op.U, po.U, sizeof(op.U));
+        Lv.st_elems = (long long)op.nl * 5 * NC * Lv.g.P;
       }
       Lv.st_owned = true;
-    } else {  // KIND_TIME
+    } else {  // KIND_TIME: Galerkin conduction, re-stabilised (upwind) capacity in time
+      op.U[0][0] = 0.0; op.U[0][1] = 0.0; op.U[1][0] = -1.0; op.U[1][1] = 1.0;
       if (po.nl == 1) {
         op.form = FORM_MK;
         op.nl = 1;
-        time_coarsen_factor(po.U, op.U);
         time_coarsen_factor(po.Tm, op.Tm);
         if (po.form == FORM_RHO) {
           Lv.st_elems = 2LL * NC * Lv.g.P;
@@ -252,7 +254,7 @@ void setup_forms(st_ctx* c) {
       } else {
         op.form = FORM_B4;
         op.nl = po.nl / 2;
-        Lv.st_elems = (long long)op.nl * 4 * NC * Lv.g.P;
+        Lv.st_elems = (long long)op.nl * 5 * NC * Lv.g.P;
         Lv.st_owned = true;
       }
     }
@@ -333,7 +335,7 @@ void build_ops(st_ctx* c) {
     Level& Lv = c->lv[l];
     const Level& Pv = c->lv[l - 1];
     if (Lv.kind == KIND_SPACE) {
-      launch_rap_space(Pv.op, Lv.g, Lv.op.nl, Lv.op.form == FORM_MK ? 2 : 4, Lv.st, c->stream);
+      launch_rap_space(Pv.op, Lv.g, Lv.op.nl, Lv.op.form == FORM_MK ? 2 : 5, Lv.st, c->stream);
       L(c);
     } else if (Lv.kind == KIND_TIME) {
       if (Pv.op.nl == 1) {
@@ -610,7 +612,7 @@ void st_default_options(st_options_t* o) {
   o->smoother = ST_SMOOTH_JACOBI;
   o->nu_pre = 2;
   o->nu_post = 2;
-  o->omega = 0.7;
+  o->omega = 0.6;
   o->lambda_crit = 0.5;
   o->coarse_max_nodes = 400;
   o->max_levels = 0;
@@ -661,6 +663,7 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       if (c->opt.restart < 1 || c->opt.restart > 60) throw StErr{ST_E_INVALID_ARG, "restart must be in [1, 60]"};
       if (c->opt.nu_pre < 1 || c->opt.nu_post < 0) throw StErr{ST_E_INVALID_ARG, "nu_pre >= 1, nu_post >= 0"};
       if (c->opt.coarse_max_nodes < 8) c->opt.coarse_max_nodes = 8;
+      if (const char* e = getenv("ST_NO_FAST")) g_use_fast = (e[0] == '0');
       CK(cudaGetDevice(&c->device));
       if (dist && dist->device >= 0) {
         c->device = dist->device;

@@ -8,7 +8,8 @@
 // as a 2x2 time block of symmetric spatial stencils S^{ab}_tau:
 //     (K x)_p = S^{tb}_{p-1} x_{p-1} + S^{tt}_{p-1} x_p + S^{bb}_p x_p + S^{bt}_p x_{p+1}.
 // Forms: RHO (fine level, matrix-free: M, K stencils from rho on the fly), MK (S^{ab} =
-// U[a][b] M_tau + Tm[a][b] K_tau, stored M, K), B4 (four stored stencils per layer).
+// U[a][b] M_tau + Tm[a][b] K_tau, stored M, K), B4 (S^{ab} = U[a][b] M_tau + K^{ab}_tau: five
+// stored stencils per layer, time-varying levels below a time coarsening).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -43,7 +44,7 @@ struct OpDesc {
   const double* rho;      // FORM_RHO
   int rho_tc;             // rho time-constant
   MatsDev m;
-  const double* st;       // MK: [nl][2][NC][P]; B4: [nl][4][NC][P]
+  const double* st;       // MK: [nl][2][NC][P]; B4: [nl][5][NC][P] = M, Kbb, Kbt, Ktb, Ktt
 };
 
 template <int SD> struct SG {

@@ -62,12 +62,14 @@ template <int SD> __global__ void set_bc_kernel(Geom g, double T0, double* __res
   if (idx >= g.N) return;
   int c[3] = {0, 0, 0}, p;
   node_of<SD>(g, idx, c, p);
-  if (is_cons<SD>(g, c, p)) x[idx] = (p == 0) ? T0 : 0.0;
+  if (is_cons<SD>(g, c, p)) x[idx] = (p == 0 && !is_patch<SD>(g, c)) ? T0 : 0.0;
 }
 template <int SD> __global__ void xd_kernel(Geom g, double T0, double* __restrict__ x) {
   long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= g.N) return;
-  x[idx] = (idx < g.P) ? T0 : 0.0;
+  int c[3] = {0, 0, 0}, p;
+  node_of<SD>(g, idx, c, p);
+  x[idx] = (p == 0 && !is_patch<SD>(g, c)) ? T0 : 0.0;
 }
 template <int SD>
 __global__ void rhs_kernel(Geom g, const double* __restrict__ f, const double* __restrict__ KxD, double T0,
@@ -76,7 +78,7 @@ __global__ void rhs_kernel(Geom g, const double* __restrict__ f, const double* _
   if (idx >= g.N) return;
   int c[3] = {0, 0, 0}, p;
   node_of<SD>(g, idx, c, p);
-  if (is_cons<SD>(g, c, p)) b[idx] = (p == 0) ? T0 : 0.0;
+  if (is_cons<SD>(g, c, p)) b[idx] = (p == 0 && !is_patch<SD>(g, c)) ? T0 : 0.0;
   else b[idx] = f[idx] - (KxD ? KxD[idx] : 0.0);
 }
 
@@ -89,7 +91,7 @@ __global__ void rhs_kernel(Geom g, const double* __restrict__ f, const double* _
 
 void launch_mask_free(const Geom& g, const double* in, double* out, cudaStream_t s) { EW_LAUNCH(mask_free_kernel, in, out); }
 void launch_set_bc_values(const Geom& g, double T0, double* x, cudaStream_t s) { EW_LAUNCH(set_bc_kernel, T0, x); }
-void launch_xd(const Geom& g, double T0, double* x, cudaStream_t s) { EW_LAUNCH(xd_kernel, T0, x); }
+void launch_xd(const Geom& g, double T0, double* x, cudaStream_t s) { EW_LAUNCH(xd_kernel, T0, x); }  // x = xD
 void launch_rhs_combine(const Geom& g, const double* f, const double* KxD, double T0, double* b, cudaStream_t s) {
   EW_LAUNCH(rhs_kernel, f, KxD, T0, b);
 }

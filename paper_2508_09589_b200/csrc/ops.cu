@@ -178,24 +178,27 @@ __device__ __forceinline__ void layer_eval(const OpDesc& op, const int* c, long 
       dbot = op.U[0][0] * Mc + op.Tm[0][0] * Kc;
       dtop = op.U[1][1] * Mc + op.Tm[1][1] * Kc;
     }
-  } else {  // FORM_B4
-    const double* base = op.st + (long long)(op.nl == 1 ? 0 : tau) * 4 * NC * g.P;
-    const double* Sbb = base;
-    const double* Sbt = base + (long long)NC * g.P;
-    const double* Stb = base + 2LL * NC * g.P;
-    const double* Stt = base + 3LL * NC * g.P;
+  } else {  // FORM_B4: [M, Kbb, Kbt, Ktb, Ktt], S^{ab} = U[a][b] M + K^{ab}
+    const double* base = op.st + (long long)(op.nl == 1 ? 0 : tau) * 5 * NC * g.P;
+    const double* Mst = base;
+    const double* Kbb = base + (long long)NC * g.P;
+    const double* Kbt = base + 2LL * NC * g.P;
+    const double* Ktb = base + 3LL * NC * g.P;
+    const double* Ktt = base + 4LL * NC * g.P;
     if (NEEDX) {
+      double Mb = st_apply<SD>(g, Mst, c, pn, xb), Mt = st_apply<SD>(g, Mst, c, pn, xt);
       if (!TRANS) {
-        bot = st_apply<SD>(g, Sbb, c, pn, xb) + st_apply<SD>(g, Sbt, c, pn, xt);
-        top = st_apply<SD>(g, Stb, c, pn, xb) + st_apply<SD>(g, Stt, c, pn, xt);
+        bot = op.U[0][0] * Mb + op.U[0][1] * Mt + st_apply<SD>(g, Kbb, c, pn, xb) + st_apply<SD>(g, Kbt, c, pn, xt);
+        top = op.U[1][0] * Mb + op.U[1][1] * Mt + st_apply<SD>(g, Ktb, c, pn, xb) + st_apply<SD>(g, Ktt, c, pn, xt);
       } else {
-        bot = st_apply<SD>(g, Sbb, c, pn, xb) + st_apply<SD>(g, Stb, c, pn, xt);
-        top = st_apply<SD>(g, Sbt, c, pn, xb) + st_apply<SD>(g, Stt, c, pn, xt);
+        bot = op.U[0][0] * Mb + op.U[1][0] * Mt + st_apply<SD>(g, Kbb, c, pn, xb) + st_apply<SD>(g, Ktb, c, pn, xt);
+        top = op.U[0][1] * Mb + op.U[1][1] * Mt + st_apply<SD>(g, Kbt, c, pn, xb) + st_apply<SD>(g, Ktt, c, pn, xt);
       }
     }
     if (NEEDD) {
-      dbot = __ldg(Sbb + pn);
-      dtop = __ldg(Stt + pn);
+      double Mc = __ldg(Mst + pn);
+      dbot = op.U[0][0] * Mc + __ldg(Kbb + pn);
+      dtop = op.U[1][1] * Mc + __ldg(Ktt + pn);
     }
   }
 }
@@ -331,8 +334,11 @@ static void launch_f(const OpDesc& op, int mode, bool trans, bool mask, const do
 #undef ST_CASE
 }
 
+bool g_use_fast = true;
+
 void launch_op(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                double omega, cudaStream_t s) {
+  if (g_use_fast && launch_op_fast2d(op, mode, trans, mask, x, b, y, omega, s)) return;
   if (op.g.sd == 2) {
     if (op.form == FORM_RHO) launch_f<2, FORM_RHO>(op, mode, trans, mask, x, b, y, omega, s);
     else if (op.form == FORM_MK) launch_f<2, FORM_MK>(op, mode, trans, mask, x, b, y, omega, s);
@@ -345,24 +351,43 @@ void launch_op(const OpDesc& op, int mode, bool trans, bool mask, const double* 
 }
 
 // ---------------------------------------------------------------------------------------
-// Weight accessor used by the Galerkin and dense-assembly kernels: full weight of offset k
-// of time block (a,b) in layer tau at node c.
+// Weight accessors used by the Galerkin and dense-assembly kernels (full weight of offset k
+// at node c, layer tau): capacity part M (time factor op.U) and conduction blocks K^{ab}.
 template <int SD, int FORM>
-__device__ double block_weight(const OpDesc& op, const int* c, long long pn, int tau, int a, int bb, int k) {
+__device__ double mpart_weight(const OpDesc& op, const int* c, long long pn, int tau, int k) {
   constexpr int NC = SG<SD>::NC;
   const Geom& g = op.g;
   if (FORM == FORM_RHO) {
     double ce[SG<SD>::NE], ke[SG<SD>::NE];
     elem_ck<SD>(op, c, tau, ce, ke);
-    return op.U[a][bb] * rho_weight<SD>(ce, ke, k, 0, g.dx) + op.Tm[a][bb] * rho_weight<SD>(ce, ke, k, 1, g.dx);
+    return rho_weight<SD>(ce, ke, k, 0, g.dx);
   } else if (FORM == FORM_MK) {
-    const double* Mbase = op.st + (long long)(op.nl == 1 ? 0 : tau) * 2 * NC * g.P;
-    const double* Kbase = Mbase + (long long)NC * g.P;
-    return op.U[a][bb] * st_weight<SD>(g, Mbase, c, pn, k) + op.Tm[a][bb] * st_weight<SD>(g, Kbase, c, pn, k);
+    return st_weight<SD>(g, op.st + (long long)(op.nl == 1 ? 0 : tau) * 2 * NC * g.P, c, pn, k);
   } else {
-    const double* base = op.st + (long long)(op.nl == 1 ? 0 : tau) * 4 * NC * g.P + (long long)(2 * a + bb) * NC * g.P;
-    return st_weight<SD>(g, base, c, pn, k);
+    return st_weight<SD>(g, op.st + (long long)(op.nl == 1 ? 0 : tau) * 5 * NC * g.P, c, pn, k);
   }
+}
+
+template <int SD, int FORM>
+__device__ double kblock_weight(const OpDesc& op, const int* c, long long pn, int tau, int a, int bb, int k) {
+  constexpr int NC = SG<SD>::NC;
+  const Geom& g = op.g;
+  if (FORM == FORM_RHO) {
+    double ce[SG<SD>::NE], ke[SG<SD>::NE];
+    elem_ck<SD>(op, c, tau, ce, ke);
+    return op.Tm[a][bb] * rho_weight<SD>(ce, ke, k, 1, g.dx);
+  } else if (FORM == FORM_MK) {
+    const double* Kb = op.st + (long long)(op.nl == 1 ? 0 : tau) * 2 * NC * g.P + (long long)NC * g.P;
+    return op.Tm[a][bb] * st_weight<SD>(g, Kb, c, pn, k);
+  } else {
+    const double* Kb = op.st + (long long)(op.nl == 1 ? 0 : tau) * 5 * NC * g.P + (long long)(1 + 2 * a + bb) * NC * g.P;
+    return st_weight<SD>(g, Kb, c, pn, k);
+  }
+}
+
+template <int SD, int FORM>
+__device__ double block_weight(const OpDesc& op, const int* c, long long pn, int tau, int a, int bb, int k) {
+  return op.U[a][bb] * mpart_weight<SD, FORM>(op, c, pn, tau, k) + kblock_weight<SD, FORM>(op, c, pn, tau, a, bb, k);
 }
 
 // MK weight of stencil s (0 = M, 1 = K) — only for RHO / MK forms
@@ -384,7 +409,7 @@ __device__ double mk_weight(const OpDesc& op, const int* c, long long pn, int ta
 // Galerkin coarse operators, structured.
 // Spatial coarsening: every stored stencil of the coarse level is P_x^T S P_x with the
 // bilinear/trilinear interpolation P_x (weights 1, 1/2 per direction), per layer.
-// NS stencils: MK -> 2 (M, K), B4 -> 4. Fine op provides weights through mk_/block_weight.
+// NS stencils: MK -> 2 (M, K), B4 -> 5 (M, K^{bb}, K^{bt}, K^{tb}, K^{tt}).
 template <int SD, int FFORM, int NS>
 __global__ void rap_space_kernel(OpDesc fop, Geom gc, int nl, double* __restrict__ out) {
   constexpr int NOFF = SG<SD>::NOFF, NC = SG<SD>::NC, CEN = SG<SD>::CEN;
@@ -426,7 +451,8 @@ __global__ void rap_space_kernel(OpDesc fop, Geom gc, int nl, double* __restrict
       if (!okg) continue;
       double w;
       if (NS == 2) w = mk_weight<SD, FFORM>(fop, f, pf, tau, s, k);
-      else w = block_weight<SD, FFORM>(fop, f, pf, tau, s >> 1, s & 1, k);
+      else if (s == 0) w = mpart_weight<SD, FFORM>(fop, f, pf, tau, k);
+      else w = kblock_weight<SD, FFORM>(fop, f, pf, tau, (s - 1) >> 1, (s - 1) & 1, k);
       if (w == 0.0) continue;
       // interpolation weight of g from coarse node C + off(q), q >= CEN
 #pragma unroll
@@ -447,9 +473,11 @@ __global__ void rap_space_kernel(OpDesc fop, Geom gc, int nl, double* __restrict
   for (int q = 0; q < NC; ++q) o[(long long)q * gc.P + pc] = acc[q];
 }
 
-// Time coarsening: coarse layer T from fine layers 2T, 2T+1 with the linear-in-time
-// interpolation (fine plane 2T+1 = (coarse T + coarse T+1)/2):
-//   S'^{AB} = sum_f sum_{a,b} W_f[a][A] W_f[b][B] S_{2T+f}^{ab},  W_0 = [[1,0],[.5,.5]], W_1 = [[.5,.5],[0,1]].
+// Time coarsening: coarse layer T from fine layers 2T, 2T+1:
+// conduction blocks by Galerkin with the linear-in-time interpolation (fine plane 2T+1 =
+// (coarse T + coarse T+1)/2): K'^{AB} = sum_f sum_{a,b} W_f[a][A] W_f[b][B] K_f^{ab},
+// W_0 = [[1,0],[.5,.5]], W_1 = [[.5,.5],[0,1]]; capacity part re-stabilised (rediscretised
+// upwind time factor, coefficient = mean of the two layers): M' = (M_{2T} + M_{2T+1}) / 2.
 template <int SD, int FFORM>
 __global__ void rap_time_kernel(OpDesc fop, int nlc, double* __restrict__ out) {
   constexpr int NC = SG<SD>::NC, CEN = SG<SD>::CEN;
@@ -465,14 +493,17 @@ __global__ void rap_time_kernel(OpDesc fop, int nlc, double* __restrict__ out) {
     for (int d = 0; d < SD; ++d) { c[d] = (int)(t % g.nn); t /= g.nn; }
   }
   const double W[2][2][2] = {{{1.0, 0.0}, {0.5, 0.5}}, {{0.5, 0.5}, {0.0, 1.0}}};
+  double* o = out + (long long)T * 5 * NC * g.P;
   for (int q = 0; q < NC; ++q) {
     double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    double macc = 0.0;
     for (int f = 0; f < 2; ++f) {
-      int tau = (fop.nl == 1 && FFORM != FORM_RHO) ? 0 : 2 * T + f;
-      if (FFORM == FORM_RHO && fop.rho_tc) tau = 0;
+      int tau = 2 * T + f;
+      if ((FFORM == FORM_RHO && fop.rho_tc) || (FFORM != FORM_RHO && fop.nl == 1)) tau = 0;
+      macc += 0.5 * mpart_weight<SD, FFORM>(fop, c, pn, tau, q + CEN);
       double s[2][2];
       for (int a = 0; a < 2; ++a)
-        for (int b = 0; b < 2; ++b) s[a][b] = block_weight<SD, FFORM>(fop, c, pn, tau, a, b, q + CEN);
+        for (int b = 0; b < 2; ++b) s[a][b] = kblock_weight<SD, FFORM>(fop, c, pn, tau, a, b, q + CEN);
       for (int A = 0; A < 2; ++A)
         for (int B = 0; B < 2; ++B) {
           double v = 0.0;
@@ -481,8 +512,9 @@ __global__ void rap_time_kernel(OpDesc fop, int nlc, double* __restrict__ out) {
           acc[A][B] += v;
         }
     }
+    o[(long long)q * g.P + pn] = macc;
     for (int A = 0; A < 2; ++A)
-      for (int B = 0; B < 2; ++B) out[((long long)T * 4 + 2 * A + B) * NC * g.P + (long long)q * g.P + pn] = acc[A][B];
+      for (int B = 0; B < 2; ++B) o[(long long)(1 + 2 * A + B) * NC * g.P + (long long)q * g.P + pn] = acc[A][B];
   }
 }
 
@@ -512,10 +544,10 @@ void launch_rap_space(const OpDesc& fop, const Geom& gc, int nl, int ns, double*
 #define RS(SD, F, NS) rap_space_kernel<SD, F, NS><<<(unsigned)grd, blk, 0, s>>>(fop, gc, nl, out)
   if (fop.g.sd == 2) {
     if (ns == 2) { if (fop.form == FORM_RHO) RS(2, FORM_RHO, 2); else RS(2, FORM_MK, 2); }
-    else { if (fop.form == FORM_RHO) RS(2, FORM_RHO, 4); else if (fop.form == FORM_MK) RS(2, FORM_MK, 4); else RS(2, FORM_B4, 4); }
+    else { if (fop.form == FORM_RHO) RS(2, FORM_RHO, 5); else if (fop.form == FORM_MK) RS(2, FORM_MK, 5); else RS(2, FORM_B4, 5); }
   } else {
     if (ns == 2) { if (fop.form == FORM_RHO) RS(3, FORM_RHO, 2); else RS(3, FORM_MK, 2); }
-    else { if (fop.form == FORM_RHO) RS(3, FORM_RHO, 4); else if (fop.form == FORM_MK) RS(3, FORM_MK, 4); else RS(3, FORM_B4, 4); }
+    else { if (fop.form == FORM_RHO) RS(3, FORM_RHO, 5); else if (fop.form == FORM_MK) RS(3, FORM_MK, 5); else RS(3, FORM_B4, 5); }
   }
 #undef RS
 }

@@ -7,7 +7,7 @@ import scipy.sparse as sp
 
 import oracle as O
 import st_inputs as I
-from tests.gpu_util import CFG1_MATS, CFG4_MATS, make_pair, rel
+from gpu_util import CFG1_MATS, CFG4_MATS, make_pair, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -148,41 +148,59 @@ def _P1(nf, kind):
     return P
 
 
-@pytest.mark.parametrize("sdim,n,nt,tc", [(2, 16, 16, False), (2, 32, 32, True), (3, 4, 8, False)])
-def test_galerkin_coarse_operators(sdim, n, nt, tc):
-    """Each stored coarse level equals the masked Galerkin product P^T A_{l-1} P of the
-    unconstrained operator, with P the
-    space/time linear interpolation of the level pair, built here independently."""
+@pytest.mark.parametrize("sdim,n,nt,tc", [(2, 16, 16, False), (2, 32, 32, True), (3, 4, 8, False), (2, 8, 32, False)])
+def test_coarse_operators(sdim, n, nt, tc):
+    """Each coarse level equals, with the Dirichlet masks of its own grid, the operator built
+    here independently from assembled matrices: conduction part
+    by Galerkin P^T A P with the space/time linear interpolation P; capacity
+    part by Galerkin under space coarsening and re-stabilised (upwind U, layer-mean capacity)
+    under time coarsening."""
     solver, prob = make_pair(sdim, n, nt, mats=CFG4_MATS, time_constant=tc)
     rho = I.rho_uniform((n,) * sdim if tc else (nt,) + (n,) * sdim, 3)
     H = solver.hierarchy()
-    Kl = prob.K(rho).tocsr()
-    dims = [(H[0]["n"], H[0]["nt"])]
+    C, k, _, _, _ = prob.coefficients(rho)
+    Kcap = O.assemble_K(prob.mesh, C, np.zeros_like(k)).tocsr()
+    Kcon = O.assemble_K(prob.mesh, np.zeros_like(C), k).tocsr()
+    nf, ntf = H[0]["n"], H[0]["nt"]
     for l in range(1, len(H)):
-        nf, ntf = dims[-1]
+        Psp = (nf + 1) ** sdim
         if H[l]["kind"] == "space":
             Px = sp.csr_matrix(_P1(nf, "s"))
             Ps = Px
             for _ in range(sdim - 1):
                 Ps = sp.kron(Px, Ps)
             P = sp.kron(sp.identity(ntf + 1), Ps).tocsr()
+            Kcap = (P.T @ Kcap @ P).tocsr()
         else:
-            Ps = sp.identity((nf + 1) ** sdim)
-            P = sp.kron(sp.csr_matrix(_P1(ntf, "t")), Ps).tocsr()
-        Kl = (P.T @ Kl @ P).tocsr()
-        dims.append((H[l]["n"], H[l]["nt"]))
-        # masked reference
-        mesh_l = O.Mesh(sdim, H[l]["n"], H[l]["nt"])
-        # constrained set at level l: t=0 plane + patch injected (range halves per space step)
+            P = sp.kron(sp.csr_matrix(_P1(ntf, "t")), sp.identity(Psp)).tocsr()
+            # layer masses M_tau = -block(tau+1, tau) of the capacity part (U[1][0] = -1)
+            ntc = ntf // 2
+            U = np.array([[0.0, 0.0], [-1.0, 1.0]])
+            blocks = []
+            for T in range(ntc):
+                M0 = -Kcap[(2 * T + 1) * Psp:(2 * T + 2) * Psp, (2 * T) * Psp:(2 * T + 1) * Psp]
+                M1 = -Kcap[(2 * T + 2) * Psp:(2 * T + 3) * Psp, (2 * T + 1) * Psp:(2 * T + 2) * Psp]
+                Mb = 0.5 * (M0 + M1)
+                E = sp.lil_matrix((ntc + 1, ntc + 1))
+                for a in range(2):
+                    for b in range(2):
+                        E[T + a, T + b] = U[a, b]
+                blocks.append(sp.kron(E.tocsr(), Mb))
+            Kcap = sum(blocks).tocsr()
+        Kcon = (P.T @ Kcon @ P).tocsr()
+        nf, ntf = H[l]["n"], H[l]["nt"]
+        mesh_l = O.Mesh(sdim, nf, max(ntf, 2))
         cons, _ = O.dirichlet(mesh_l, O.BCs())
+        cons = cons[:(nf + 1) ** sdim * (ntf + 1)]
         free = (~cons).astype(float)
+        Kl = Kcap + Kcon
         Aref = sp.diags(free) @ Kl @ sp.diags(free) + sp.diags(cons.astype(float))
-        x = I.rand_vector(mesh_l.n_nodes, 7 + l)
-        y = torch.empty(mesh_l.n_nodes, dtype=torch.float64, device=DEV)
+        x = I.rand_vector(Aref.shape[0], 7 + l)
+        y = torch.empty(Aref.shape[0], dtype=torch.float64, device=DEV)
         for trans in (False, True):
             solver.level_apply(dev(rho), l, dev(x), y, transpose=trans)
             ref = (Aref.T if trans else Aref) @ x
-            assert rel(host(y), ref) <= 1e-12, (l, trans, rel(host(y), ref))
+            assert rel(host(y), ref) <= 1e-12, (l, H[l], trans, rel(host(y), ref))
     solver.close()
 
 
