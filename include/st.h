@@ -26,8 +26,9 @@
  *    device buffers inside the call. Caller owns every vector; the context owns workspaces.
  *  - Every call enqueues on the context's stream and returns after completion.
  *  - Dirichlet data (R-1..R-4): T = T0 on the t = 0 node plane (initial
- *    condition); T = 0 on the sink patch of the face x1 = 0 (all t) whose transverse
- *    coordinates lie within halfwidth of center. Symmetric elimination with unit diagonal.
+ *    condition); T = 0 on the sink patch of the face x1 = 0 (all t, including t = 0) whose
+ *    transverse coordinates lie within halfwidth of center. Symmetric elimination with
+ *    unit diagonal.
  *  - Return value: ST_OK or a negative ST_E_* code; st_strerror() gives text.
  *    No C++ exception crosses this boundary.
  */
@@ -119,7 +120,7 @@ typedef struct {
   int64_t nodes[32];
 } st_hierarchy_t;
 
-/* Fill `o` with the library defaults (rtol 1e-8, restart 30, Jacobi nu 2/2 omega 0.7,
+/* Fill `o` with the library defaults (rtol 1e-8, restart 30, Jacobi nu 2/2 omega 0.6,
  * lambda_crit 0.5, coarse_max_nodes 400). */
 void st_default_options(st_options_t* o);
 
@@ -156,6 +157,13 @@ int st_rhs(st_ctx_t* ctx, const double* rho, double* f, double* b);
 /* Multigrid test hooks on level l (0 = finest): y = A_l x (masked, Galerkin operator). */
 int st_level_apply(st_ctx_t* ctx, const double* rho, int level, const double* x, double* y,
                    int transpose);
+
+/* Benchmark hook: enqueue `reps` back-to-back launches of the level-l operator kernel in
+ * mode (0 apply, 1 residual y = b - A x, 2 damped-Jacobi sweep, 3 first sweep from zero)
+ * on the context stream and return WITHOUT synchronising (the caller brackets them with
+ * events on that stream). Device pointers only. */
+int st_bench_op(st_ctx_t* ctx, const double* rho, int level, int mode, int transpose, const double* x,
+                const double* b, double* y, int reps);
 
 int st_get_stats(const st_ctx_t* ctx, st_stats_t* s);
 int st_get_hierarchy(const st_ctx_t* ctx, st_hierarchy_t* h);

@@ -822,6 +822,27 @@ int st_rhs(st_ctx_t* c, const double* rho, double* f, double* b) {
   });
 }
 
+int st_bench_op(st_ctx_t* c, const double* rho, int level, int mode, int transpose, const double* x,
+                const double* b, double* y, int reps) {
+  return guarded([&]() -> int {
+    if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
+    if (level < 0 || level >= (int)c->lv.size() || c->lv[level].dense) throw StErr{ST_E_INVALID_ARG, "level"};
+    if (mode < 0 || mode > 3 || reps < 0) throw StErr{ST_E_INVALID_ARG, "mode/reps"};
+    if (!is_device_ptr(y) || (mode != 3 && !is_device_ptr(x)) || (mode != 0 && !is_device_ptr(b)))
+      throw StErr{ST_E_INVALID_ARG, "st_bench_op takes device pointers"};
+    CK(cudaSetDevice(c->device));
+    if (level == 0) {
+      if (!is_device_ptr(rho)) throw StErr{ST_E_INVALID_ARG, "rho must be a device pointer"};
+      c->lv[0].op.rho = rho;
+    } else {
+      prepare(c, rho);
+    }
+    for (int r = 0; r < reps; ++r) op_launch(c, level, mode, transpose != 0, true, x, b, y);
+    check_launch();
+    return ST_OK;
+  });
+}
+
 int st_get_stats(const st_ctx_t* c, st_stats_t* s) {
   if (!c || !s) return ST_E_INVALID_ARG;
   *s = c->stats;

@@ -18,13 +18,17 @@
 #include "kernels.h"
 
 namespace st {
+#ifndef ST_CUNI_MINB
+#define ST_CUNI_MINB 3
+#endif
 namespace f2 {
 
 constexpr int TX = 32, TYT = 4, RY = 2, TY = TYT * RY;   // node tile 32 x 8
 constexpr int HX = TX + 2, HY = TY + 2, PT = HX * HY;    // plane tile with halo: 34 x 10
 constexpr int EX = TX + 1, EY = TY + 1, ET = EX * EY;    // element tile: 33 x 9
-constexpr int NB = 5;                                     // ring slots
+constexpr int NB = 6;                                     // ring slots (NB-2 planes in flight)
 constexpr int NTH = TX * TYT;
+constexpr int BT = TX * TY;                               // interior (b) tile
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -79,13 +83,19 @@ template <bool TRANS> __device__ __forceinline__ Fac make_fac(const OpDesc& op, 
   return f;
 }
 
-// SRC: 0 = RHO, 1 = MK stored (TC only)
-template <bool TC, int SRC, int MODE, bool TRANS, bool MASK>
-__global__ void __launch_bounds__(NTH, 3) op2d_kernel(OpDesc op, const double* __restrict__ x,
+// SRC: 0 = RHO, 1 = MK stored (TC only). CUNI: uniform capacity (C_ins = C_con) on the RHO
+// time-constant level: the spatial mass is the tensor product of the 1D assembled masses,
+// M = C dx^2/36 (My (x) Mx) with 1D patterns [1,4,1] (interior), [0,2,1] / [1,2,0] (ends), applied
+// separably; only the 9 stiffness weights are held in registers.
+template <bool TC, int SRC, bool CUNI, int MODE, bool TRANS, bool MASK>
+__global__ void __launch_bounds__(NTH, CUNI ? ST_CUNI_MINB : 3) op2d_kernel(OpDesc op, const double* __restrict__ x,
                                                       const double* __restrict__ b, double* __restrict__ y,
                                                       double omega, int chunk) {
   constexpr bool TVR = (!TC) && SRC == 0;
-  __shared__ __align__(16) double xs[NB][PT];
+  constexpr bool NX = (MODE != MODE_JAC0);   // reads x
+  constexpr bool NBV = (MODE != MODE_APPLY); // reads b
+  __shared__ __align__(16) double xs[NX ? NB : 1][NX ? PT : 1];
+  __shared__ __align__(16) double bs[NBV ? NB : 1][NBV ? BT : 1];
   __shared__ __align__(16) double rs[TVR ? NB : 1][TVR ? ET : 1];
   __shared__ double cC[TVR ? ET : 1], cK[TVR ? ET : 1];
 
@@ -99,7 +109,7 @@ __global__ void __launch_bounds__(NTH, 3) op2d_kernel(OpDesc op, const double* _
   const int i = x0 + tx;
   const int n = g.n, nn = g.nn;
   const long long P = g.P;
-  const double sm = (SRC == 0) ? g.dx * g.dx * (1.0 / 36.0) : 1.0;
+  const double sm = (SRC == 0) ? g.dx * g.dx * (1.0 / 36.0) * (CUNI ? op.m.Cins : 1.0) : 1.0;
   const double sk = (SRC == 0) ? (1.0 / 6.0) : 1.0;
   const Fac F = make_fac<TRANS>(op, sm, sk);
   int jr[RY];
@@ -110,36 +120,87 @@ __global__ void __launch_bounds__(NTH, 3) op2d_kernel(OpDesc op, const double* _
     act[r] = (i <= n) && (jr[r] <= n);
   }
 
-  // --- plane / layer loaders -------------------------------------------------------
-  auto issue_plane = [&](int q) {
-    double* dst = xs[q % NB];
-    const double* src = x + (long long)q * P;
-    for (int e = tid; e < PT; e += NTH) {
-      int ly = e / HX, lx = e - ly * HX;
+  // --- per-thread copy descriptors (computed once; every plane only bumps a pointer) ---
+  constexpr int XPT = (PT + NTH - 1) / NTH;   // x elements per thread (3)
+  constexpr int BPT = (BT + NTH - 1) / NTH;   // b elements per thread (2)
+  constexpr int RPT = (ET + NTH - 1) / NTH;   // rho elements per thread (3)
+  int xoff[XPT], xsm[XPT];
+  unsigned xval = 0u, xpatch = 0u;
+#pragma unroll
+  for (int k = 0; k < XPT; ++k) {
+    int e = tid + k * NTH;
+    int ly = e / HX, lx = e - ly * HX;
+    int gi = x0 - 1 + lx, gj = y0 - 1 + ly;
+    bool v = (e < PT) && (gi >= 0 && gi <= n && gj >= 0 && gj <= n);
+    xoff[k] = v ? gj * nn + gi : 0;
+    xsm[k] = e < PT ? e : 0;
+    if (v) xval |= 1u << k;
+    if (v && gi == 0 && gj >= g.plo && gj <= g.phi) xpatch |= 1u << k;
+  }
+  int boff[BPT];
+  unsigned bval = 0u;
+#pragma unroll
+  for (int k = 0; k < BPT; ++k) {
+    int e = tid + k * NTH;
+    int ly = e / TX, lx = e - ly * TX;
+    int gi = x0 + lx, gj = y0 + ly;
+    bool v = (e < BT) && gi <= n && gj <= n;
+    boff[k] = v ? gj * nn + gi : 0;
+    if (v) bval |= 1u << k;
+  }
+  int roff[RPT];
+  unsigned rval = 0u;
+  if (TVR) {
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      int e = tid + k * NTH;
+      int ly = e / EX, lx = e - ly * EX;
       int gi = x0 - 1 + lx, gj = y0 - 1 + ly;
-      bool v = (gi >= 0 && gi <= n && gj >= 0 && gj <= n);
-      if (MASK && v && (q == 0 || (gi == 0 && gj >= g.plo && gj <= g.phi))) v = false;
-      const double* s = v ? src + (long long)gj * nn + gi : x;
-      cp_async8(&dst[e], s, v);
+      bool v = (e < ET) && gi >= 0 && gi < n && gj >= 0 && gj < n;
+      roff[k] = v ? gj * n + gi : 0;
+      if (v) rval |= 1u << k;
+    }
+  }
+
+  // --- plane / layer loaders -------------------------------------------------------
+  auto issue_plane = [&](int q, int slot, const double* xq, const double* bq) {
+    if (NX) {
+      double* dst = xs[slot];
+      const double* src = xq;
+      unsigned vm = xval & (MASK ? (q == 0 ? 0u : ~xpatch) : ~0u);
+#pragma unroll
+      for (int k = 0; k < XPT; ++k)
+        if (k < XPT - 1 || tid + k * NTH < PT) cp_async8(&dst[xsm[k]], src + xoff[k], (vm >> k) & 1u);
+    }
+    if (NBV && q >= p0 && q < p1) {  // b of row q (interior tile)
+      double* dst = bs[slot];
+      const double* src = bq;
+#pragma unroll
+      for (int k = 0; k < BPT; ++k) cp_async8(&dst[tid + k * NTH], src + boff[k], (bval >> k) & 1u);
     }
     if (TVR) {
       int tau = q - 1;  // layer needed when plane q arrives
       if (tau >= qs) {
-        double* rd = rs[q % NB];
+        double* rd = rs[slot];
         const double* rsrc = op.rho + (long long)tau * n * n;
-        for (int e = tid; e < ET; e += NTH) {
-          int ly = e / EX, lx = e - ly * EX;
-          int gi = x0 - 1 + lx, gj = y0 - 1 + ly;
-          bool v = (gi >= 0 && gi < n && gj >= 0 && gj < n);
-          const double* s = v ? rsrc + (long long)gj * n + gi : op.rho;
-          cp_async8(&rd[e], s, v);
-        }
+#pragma unroll
+        for (int k = 0; k < RPT; ++k)
+          if (k < RPT - 1 || tid + k * NTH < ET) cp_async8(&rd[tid + k * NTH], rsrc + roff[k], (rval >> k) & 1u);
       }
     }
   };
 
   // --- time-constant weights in registers ------------------------------------------
-  double wM[RY][9], wK[RY][9];
+  double wM[CUNI ? 1 : RY][9], wK[RY][9];
+  double wx[3], wy[RY][3];
+  if (CUNI) {
+    wx[0] = (i == 0) ? 0.0 : 1.0; wx[1] = (i == 0 || i == n) ? 2.0 : 4.0; wx[2] = (i >= n) ? 0.0 : 1.0;
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      const int j = jr[r];
+      wy[r][0] = (j == 0) ? 0.0 : 1.0; wy[r][1] = (j == 0 || j == n) ? 2.0 : 4.0; wy[r][2] = (j >= n) ? 0.0 : 1.0;
+    }
+  }
   if (TC) {
 #pragma unroll
     for (int r = 0; r < RY; ++r) {
@@ -153,7 +214,7 @@ __global__ void __launch_bounds__(NTH, 3) op2d_kernel(OpDesc op, const double* _
           ce[e] = v ? op.m.Cins + op.m.dC * powp(rho, op.m.pc) : 0.0;
           ke[e] = v ? op.m.kins + op.m.dk * powp(rho, op.m.pk) : 0.0;
         }
-        wM_from(ce[0], ce[1], ce[2], ce[3], wM[r]);
+        if (!CUNI) wM_from(ce[0], ce[1], ce[2], ce[3], wM[r]);
         wK_from(ke[0], ke[1], ke[2], ke[3], wK[r]);
       } else {
         // stored symmetric stencils: own forward coefs (k >= 4) + neighbours' mirrored ones
@@ -179,12 +240,15 @@ __global__ void __launch_bounds__(NTH, 3) op2d_kernel(OpDesc op, const double* _
   }
 
   // diagonal parts (TC: loop invariant)
-  double dbotC[RY], dtopC[RY];
-  if (TC) {
+  double odI[RY], odT[RY];  // omega / D for interior rows and for the last row (top part only)
+  if (TC && (MODE == MODE_JAC || MODE == MODE_JAC0)) {
 #pragma unroll
     for (int r = 0; r < RY; ++r) {
-      dbotC[r] = F.u00 * wM[r][4] + F.t00 * wK[r][4];
-      dtopC[r] = F.u11 * wM[r][4] + F.t11 * wK[r][4];
+      const double mc = CUNI ? wx[1] * wy[r][1] : wM[CUNI ? 0 : r][4];
+      double db = F.u00 * mc + F.t00 * wK[r][4];
+      double dt = F.u11 * mc + F.t11 * wK[r][4];
+      odI[r] = act[r] ? omega / (db + dt) : 0.0;
+      odT[r] = act[r] ? omega / dt : 0.0;
     }
   }
 
@@ -192,29 +256,45 @@ __global__ void __launch_bounds__(NTH, 3) op2d_kernel(OpDesc op, const double* _
 #pragma unroll
   for (int k = 0; k < NB - 2; ++k) {
     int q = qs + k;
-    if (q <= qe) issue_plane(q);
+    if (q <= qe) issue_plane(q, q % NB, x + (long long)q * P, b + (long long)q * P);
     cp_commit();
   }
+  // running plane pointers of the next plane to issue (qs + NB - 2)
+  const double* xnext = x + (long long)(qs + NB - 2) * P;
+  const double* bnext = b + (long long)(qs + NB - 2) * P;
+  // ring slots: cur = slot of plane q, prv = slot of plane q-1, nxt = slot of plane q+NB-2
+  int cur = qs % NB;
+  int prv = (cur + NB - 1) % NB;
+  int nxt = (cur + NB - 2) % NB;
+  const int nodeoff0 = jr[0] * nn + i;
+  double* yrow = y + (long long)(qs - 1) * P + nodeoff0;   // row q-1 of the current iteration
 
-  double Mprev[RY], Kprev[RY], carry[RY], dcarry[RY], bnext[RY];
+  double Mprev[RY], Kprev[RY], carry[RY], dcarry[RY];
 #pragma unroll
-  for (int r = 0; r < RY; ++r) { Mprev[r] = Kprev[r] = carry[r] = dcarry[r] = 0.0; bnext[r] = 0.0; }
+  for (int r = 0; r < RY; ++r) { Mprev[r] = Kprev[r] = carry[r] = dcarry[r] = 0.0; }
 
-  auto out_row = [&](int p, int r, double Ax, double D) {
+  // out_row: od = omega / D (JAC, JAC0); slot = ring slot of plane p
+  const bool patchr[RY] = {MASK && i == 0 && jr[0] >= g.plo && jr[0] <= g.phi,
+                           MASK && i == 0 && jr[1] >= g.plo && jr[1] <= g.phi};
+  auto out_row = [&](int p, int slot, int r, double Ax, double od) {
     if (p < p0 || p >= p1 || !act[r]) return;
-    const long long gi = (long long)p * P + (long long)jr[r] * nn + i;
-    const bool cons = MASK && (p == 0 || (i == 0 && jr[r] >= g.plo && jr[r] <= g.phi));
+    const long long gi = (long long)p * P + nodeoff0 + r * nn;
+    const bool cons = MASK && (p == 0 || patchr[r]);
+    double* yo = yrow + r * nn;
+    const double bv = NBV ? bs[slot][(ty * RY + r) * TX + tx] : 0.0;
     double o;
     if (MODE == MODE_APPLY) {
       o = cons ? __ldg(x + gi) : Ax;
     } else if (MODE == MODE_RESID) {
-      o = bnext[r] - (cons ? __ldg(x + gi) : Ax);
-    } else {  // JAC
-      double xc = xs[p % NB][(ty * RY + r + 1) * HX + tx + 1];
-      if (cons) { xc = __ldg(x + gi); Ax = xc; D = 1.0; }
-      o = xc + omega * (bnext[r] - Ax) / D;
+      o = bv - (cons ? __ldg(x + gi) : Ax);
+    } else if (MODE == MODE_JAC) {
+      double xc = xs[slot][(ty * RY + r + 1) * HX + tx + 1];
+      if (cons) { xc = __ldg(x + gi); Ax = xc; od = omega; }
+      o = fma(od, bv - Ax, xc);
+    } else {  // JAC0
+      o = (cons ? omega : od) * bv;
     }
-    y[gi] = o;
+    *yo = o;
   };
 
   for (int q = qs; q <= qe; ++q) {
@@ -224,14 +304,16 @@ __global__ void __launch_bounds__(NTH, 3) op2d_kernel(OpDesc op, const double* _
       __syncthreads();  // previous iteration finished reading cC / cK
       int tau = q - 1;
       if (tau >= qs) {
-        const double* rd = rs[q % NB];
-        for (int e = tid; e < ET; e += NTH) {
-          int ly = e / EX, lx = e - ly * EX;
-          int gi = x0 - 1 + lx, gj = y0 - 1 + ly;
-          bool v = (gi >= 0 && gi < n && gj >= 0 && gj < n);
-          double rho = rd[e];
-          cC[e] = v ? op.m.Cins + op.m.dC * powp(rho, op.m.pc) : 0.0;
-          cK[e] = v ? op.m.kins + op.m.dk * powp(rho, op.m.pk) : 0.0;
+        const double* rd = rs[cur];
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+          const int e = tid + k * NTH;
+          if (k < RPT - 1 || e < ET) {
+            const bool v = (rval >> k) & 1u;
+            const double rho = rd[e];
+            cC[e] = v ? op.m.Cins + op.m.dC * powp(rho, op.m.pc) : 0.0;
+            cK[e] = v ? op.m.kins + op.m.dk * powp(rho, op.m.pk) : 0.0;
+          }
         }
       }
     }
@@ -239,34 +321,40 @@ __global__ void __launch_bounds__(NTH, 3) op2d_kernel(OpDesc op, const double* _
     // refill: plane q + NB - 2 into the slot of plane q - 2
     {
       int qn = q + NB - 2;
-      if (qn <= qe) issue_plane(qn);
+      if (qn <= qe) issue_plane(qn, nxt, xnext, bnext);
       cp_commit();
+      xnext += P;
+      bnext += P;
     }
-    // b for the row output in this iteration (row q-1) — RESID/JAC
-    const int prow = q - 1;
-    if (MODE == MODE_RESID || MODE == MODE_JAC) {
-#pragma unroll
-      for (int r = 0; r < RY; ++r)
-        bnext[r] = (act[r] && prow >= p0 && prow < p1) ? __ldg(b + (long long)prow * P + (long long)jr[r] * nn + i) : 0.0;
-    }
+    const int prow = q - 1;  // row completed in this iteration
     // gather 3 x (RY+2) neighbourhood of plane q
     double nbq[RY + 2][3];
-    {
-      const double* t = xs[q % NB] + (ty * RY) * HX + tx;
+    if (NX) {
+      const double* t = xs[cur] + (ty * RY) * HX + tx;
 #pragma unroll
       for (int s = 0; s < RY + 2; ++s)
 #pragma unroll
         for (int c = 0; c < 3; ++c) nbq[s][c] = t[s * HX + c];
     }
     if (TC) {
+      double rsum[RY + 2];
+      if (CUNI && NX) {
+#pragma unroll
+        for (int s2 = 0; s2 < RY + 2; ++s2) rsum[s2] = fma(wx[0], nbq[s2][0], fma(wx[1], nbq[s2][1], wx[2] * nbq[s2][2]));
+      }
 #pragma unroll
       for (int r = 0; r < RY; ++r) {
-        double Mq = ap9(wM[r], nbq, r), Kq = ap9(wK[r], nbq, r);
+        if (!NX) {
+          if (q > qs) out_row(prow, prv, r, 0.0, odI[r]);
+          continue;
+        }
+        double Mq = CUNI ? fma(wy[r][0], rsum[r], fma(wy[r][1], rsum[r + 1], wy[r][2] * rsum[r + 2]))
+                         : ap9(wM[CUNI ? 0 : r], nbq, r);
+        double Kq = ap9(wK[r], nbq, r);
         if (q > qs) {  // layer tau = q-1: planes q-1 (prev) and q
           double bot = F.u00 * Mprev[r] + F.u01 * Mq + F.t00 * Kprev[r] + F.t01 * Kq;
           double top = F.u10 * Mprev[r] + F.u11 * Mq + F.t10 * Kprev[r] + F.t11 * Kq;
-          double D = (prow >= 1 ? dtopC[r] : 0.0) + dbotC[r];
-          out_row(prow, r, carry[r] + bot, D);
+          out_row(prow, prv, r, carry[r] + bot, odI[r]);
           carry[r] = top;
         }
         Mprev[r] = Mq;
@@ -275,11 +363,13 @@ __global__ void __launch_bounds__(NTH, 3) op2d_kernel(OpDesc op, const double* _
     } else {
       if (q > qs) {
         double nbp[RY + 2][3];
-        const double* t = xs[(q - 1) % NB] + (ty * RY) * HX + tx;
+        if (NX) {
+          const double* t = xs[prv] + (ty * RY) * HX + tx;
 #pragma unroll
-        for (int s = 0; s < RY + 2; ++s)
+          for (int s = 0; s < RY + 2; ++s)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) nbp[s][c] = t[s * HX + c];
+            for (int c = 0; c < 3; ++c) nbp[s][c] = t[s * HX + c];
+        }
         // element coefficients of the thread's column: rows s = 0..RY, cols W (tx), E (tx+1)
         double cw[RY + 1], ckw[RY + 1], ce_[RY + 1], cke[RY + 1];
 #pragma unroll
@@ -293,123 +383,82 @@ __global__ void __launch_bounds__(NTH, 3) op2d_kernel(OpDesc op, const double* _
           double w1[9], w2[9];
           wM_from(cw[r], ce_[r], cw[r + 1], ce_[r + 1], w1);
           wK_from(ckw[r], cke[r], ckw[r + 1], cke[r + 1], w2);
-          double Mb = ap9(w1, nbp, r), Mt = ap9(w1, nbq, r);
-          double Kb = ap9(w2, nbp, r), Kt = ap9(w2, nbq, r);
-          double bot = F.u00 * Mb + F.u01 * Mt + F.t00 * Kb + F.t01 * Kt;
-          double top = F.u10 * Mb + F.u11 * Mt + F.t10 * Kb + F.t11 * Kt;
+          double bot = 0.0, top = 0.0;
+          if (NX) {
+            double Mb = ap9(w1, nbp, r), Mt = ap9(w1, nbq, r);
+            double Kb = ap9(w2, nbp, r), Kt = ap9(w2, nbq, r);
+            bot = F.u00 * Mb + F.u01 * Mt + F.t00 * Kb + F.t01 * Kt;
+            top = F.u10 * Mb + F.u11 * Mt + F.t10 * Kb + F.t11 * Kt;
+          }
           double db = F.u00 * w1[4] + F.t00 * w2[4];
           double dt = F.u11 * w1[4] + F.t11 * w2[4];
-          out_row(prow, r, carry[r] + bot, dcarry[r] + db);
+          double od = (MODE == MODE_JAC || MODE == MODE_JAC0) && act[r] ? omega / (dcarry[r] + db) : 0.0;
+          out_row(prow, prv, r, carry[r] + bot, od);
           carry[r] = top;
           dcarry[r] = dt;
         }
       }
     }
+    // ROTATE
+    yrow += P;
+    prv = cur;
+    cur = (cur + 1 == NB) ? 0 : cur + 1;
+    nxt = (nxt + 1 == NB) ? 0 : nxt + 1;
   }
+  // (ring slots rotate at the end of every iteration, see ROTATE)
   // last row nt: only the top part of layer nt-1
   if (p1 == g.nt + 1) {
     const int p = g.nt;
-    if (MODE == MODE_RESID || MODE == MODE_JAC) {
-#pragma unroll
-      for (int r = 0; r < RY; ++r)
-        bnext[r] = act[r] ? __ldg(b + (long long)p * P + (long long)jr[r] * nn + i) : 0.0;
-    }
 #pragma unroll
     for (int r = 0; r < RY; ++r) {
-      double D = TC ? dtopC[r] : dcarry[r];
-      out_row(p, r, carry[r], D);
+      double od = 0.0;
+      if (MODE == MODE_JAC || MODE == MODE_JAC0) od = TC ? odT[r] : (act[r] ? omega / dcarry[r] : 0.0);
+      out_row(p, prv, r, carry[r], od);
     }
   }
   cp_wait<0>();
 }
 
-// JAC0 (first sweep from zero): y = omega b / D, D = diag of the masked operator
-template <bool TC, int SRC>
-__global__ void jac0_2d_kernel(OpDesc op, const double* __restrict__ b, double* __restrict__ y, double omega) {
-  const Geom& g = op.g;
-  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= g.N) return;
-  const int p = (int)(idx / g.P);
-  const long long pn = idx - (long long)p * g.P;
-  const int i = (int)(pn % g.nn), j = (int)(pn / g.nn);
-  const bool cons = (p == 0 || (i == 0 && j >= g.plo && j <= g.phi));
-  double D = 1.0;
-  if (!cons) {
-    const int n = g.n;
-    double Dd = 0.0;
-    const double sm = (SRC == 0) ? g.dx * g.dx * (1.0 / 36.0) : 1.0;
-    const double sk = (SRC == 0) ? (1.0 / 6.0) : 1.0;
-    for (int side = 0; side < 2; ++side) {
-      int tau = side == 0 ? p - 1 : p;  // top of layer p-1, bottom of layer p
-      if (tau < 0 || tau >= g.nt) continue;
-      double Mc, Kc;
-      if (SRC == 0) {
-        double sc = 0.0, sk2 = 0.0;
-        for (int e = 0; e < 4; ++e) {
-          int a = i - 1 + (e & 1), bb = j - 1 + (e >> 1);
-          if (a < 0 || a >= n || bb < 0 || bb >= n) continue;
-          long long ri = (long long)bb * n + a + (TC ? 0 : (long long)tau * n * n);
-          double rho = __ldg(op.rho + ri);
-          sc += op.m.Cins + op.m.dC * powp(rho, op.m.pc);
-          sk2 += op.m.kins + op.m.dk * powp(rho, op.m.pk);
-        }
-        Mc = 4.0 * sc * sm;
-        Kc = 4.0 * sk2 * sk;
-      } else {
-        Mc = __ldg(op.st + pn);
-        Kc = __ldg(op.st + 5 * g.P + pn);
-      }
-      Dd += side == 0 ? (op.U[1][1] * Mc + op.Tm[1][1] * Kc) : (op.U[0][0] * Mc + op.Tm[0][0] * Kc);
-    }
-    D = Dd;
-  }
-  y[idx] = omega * __ldg(b + idx) / D;
-}
-
 }  // namespace f2
 
 static int choose_chunk2(const Geom& g, long long tiles) {
-  // aim for ~4 waves of CTAs over 148 SMs x 3 resident CTAs, chunks >= 8 planes
+  // ~4 waves of CTAs over 148 SMs x 3 resident CTAs; small levels: short chunks so that all
+  // planes proceed in parallel (latency), large levels: long chunks (1 extra plane per chunk)
   long long target = 148LL * 3 * 4;
   long long chunks = (target + tiles - 1) / tiles;
-  long long maxch = (g.nt + 1 + 7) / 8;
-  if (chunks > maxch) chunks = maxch;
+  if (chunks > g.nt + 1) chunks = g.nt + 1;
   if (chunks < 1) chunks = 1;
   return (int)((g.nt + 1 + chunks - 1) / chunks);
 }
 
-template <bool TC, int SRC, int MODE, bool TRANS, bool MASK>
+template <bool TC, int SRC, bool CUNI, int MODE, bool TRANS, bool MASK>
 static void l2d(const OpDesc& op, const double* x, const double* b, double* y, double omega, cudaStream_t s) {
   const Geom& g = op.g;
   dim3 blk(f2::TX, f2::TYT, 1);
   long long tx = (g.nn + f2::TX - 1) / f2::TX, ty = (g.nn + f2::TY - 1) / f2::TY;
   int chunk = choose_chunk2(g, tx * ty);
   dim3 grd((unsigned)tx, (unsigned)ty, (unsigned)((g.nt + 1 + chunk - 1) / chunk));
-  f2::op2d_kernel<TC, SRC, MODE, TRANS, MASK><<<grd, blk, 0, s>>>(op, x, b, y, omega, chunk);
+  f2::op2d_kernel<TC, SRC, CUNI, MODE, TRANS, MASK><<<grd, blk, 0, s>>>(op, x, b, y, omega, chunk);
 }
 
-template <bool TC, int SRC>
+template <bool TC, int SRC, bool CUNI>
 static void l2d_modes(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                       double omega, cudaStream_t s) {
-  if (mode == MODE_JAC0) {
-    unsigned grd = (unsigned)((op.g.N + 255) / 256);
-    f2::jac0_2d_kernel<TC, SRC><<<grd, 256, 0, s>>>(op, b, y, omega);
-    return;
-  }
   if (!mask) {
-    if (trans) l2d<TC, SRC, MODE_APPLY, true, false>(op, x, b, y, omega, s);
-    else l2d<TC, SRC, MODE_APPLY, false, false>(op, x, b, y, omega, s);
+    if (trans) l2d<TC, SRC, CUNI, MODE_APPLY, true, false>(op, x, b, y, omega, s);
+    else l2d<TC, SRC, CUNI, MODE_APPLY, false, false>(op, x, b, y, omega, s);
     return;
   }
 #define C2(M)                                                             \
   case M:                                                                 \
-    if (trans) l2d<TC, SRC, M, true, true>(op, x, b, y, omega, s);        \
-    else l2d<TC, SRC, M, false, true>(op, x, b, y, omega, s);             \
+    if (trans) l2d<TC, SRC, CUNI, M, true, true>(op, x, b, y, omega, s);  \
+    else l2d<TC, SRC, CUNI, M, false, true>(op, x, b, y, omega, s);       \
     break;
   switch (mode) {
     C2(MODE_APPLY)
     C2(MODE_RESID)
     C2(MODE_JAC)
+    C2(MODE_JAC0)
   }
 #undef C2
 }
@@ -420,12 +469,14 @@ bool launch_op_fast2d(const OpDesc& op, int mode, bool trans, bool mask, const d
   if (op.g.sd != 2) return false;
   if (mode == MODE_JAC0 && !mask) return false;
   if (op.form == FORM_RHO) {
-    if (op.rho_tc) l2d_modes<true, 0>(op, mode, trans, mask, x, b, y, omega, s);
-    else l2d_modes<false, 0>(op, mode, trans, mask, x, b, y, omega, s);
+    const bool cuni = (op.m.dC == 0.0);
+    if (op.rho_tc && cuni) l2d_modes<true, 0, true>(op, mode, trans, mask, x, b, y, omega, s);
+    else if (op.rho_tc) l2d_modes<true, 0, false>(op, mode, trans, mask, x, b, y, omega, s);
+    else l2d_modes<false, 0, false>(op, mode, trans, mask, x, b, y, omega, s);
     return true;
   }
   if (op.form == FORM_MK && op.nl == 1) {
-    l2d_modes<true, 1>(op, mode, trans, mask, x, b, y, omega, s);
+    l2d_modes<true, 1, false>(op, mode, trans, mask, x, b, y, omega, s);
     return true;
   }
   return false;

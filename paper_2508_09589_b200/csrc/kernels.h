@@ -26,7 +26,7 @@ struct RedWs {
   double* partial;      // [kMaxBlocks * kMaxK]
   unsigned int* counter;
 };
-constexpr int kRedBlocks = 296;
+constexpr int kRedBlocks = 148 * 6;
 constexpr int kMaxDots = 9;
 // out[0..k-1] = V_j . w (j < k), out[k] = w . w ; k <= 8
 void launch_mdot(const double* w, const double* V, long long ldv, int k, long long n, double* out, RedWs ws,

@@ -64,7 +64,18 @@ __global__ void __launch_bounds__(kRedThreads) mdot_kernel(const double* __restr
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  // two elements per iteration: 2 (J + 1) independent loads in flight per thread
+  for (; i + stride < n; i += 2 * stride) {
+    double w0 = __ldg(w + i), w1 = __ldg(w + i + stride);
+    double v0[J > 0 ? J : 1], v1[J > 0 ? J : 1];
+#pragma unroll
+    for (int j = 0; j < J; ++j) { v0[j] = __ldg(V + j * ldv + i); v1[j] = __ldg(V + j * ldv + i + stride); }
+#pragma unroll
+    for (int j = 0; j < J; ++j) acc[j] += v0[j] * w0 + v1[j] * w1;
+    if (NRM) acc[NV - 1] += w0 * w0 + w1 * w1;
+  }
+  if (i < n) {
     double wi = __ldg(w + i);
 #pragma unroll
     for (int j = 0; j < J; ++j) acc[j] += __ldg(V + j * ldv + i) * wi;
@@ -81,11 +92,30 @@ __global__ void __launch_bounds__(kRedThreads) maxpy_norm_kernel(double* __restr
   __syncthreads();
   double acc[1] = {0.0};
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
-    double wi = w[i];
-    for (int j = 0; j < k; ++j) wi -= hs[j] * __ldg(V + j * ldv + i);
-    w[i] = wi;
-    acc[0] += wi * wi;
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i + stride < n; i += 2 * stride) {
+    double a0 = w[i], a1 = w[i + stride];
+    int j = 0;
+    for (; j + 4 <= k; j += 4) {
+      double p0 = __ldg(V + (j + 0) * ldv + i), q0 = __ldg(V + (j + 0) * ldv + i + stride);
+      double p1 = __ldg(V + (j + 1) * ldv + i), q1 = __ldg(V + (j + 1) * ldv + i + stride);
+      double p2 = __ldg(V + (j + 2) * ldv + i), q2 = __ldg(V + (j + 2) * ldv + i + stride);
+      double p3 = __ldg(V + (j + 3) * ldv + i), q3 = __ldg(V + (j + 3) * ldv + i + stride);
+      a0 -= hs[j] * p0; a1 -= hs[j] * q0;
+      a0 -= hs[j + 1] * p1; a1 -= hs[j + 1] * q1;
+      a0 -= hs[j + 2] * p2; a1 -= hs[j + 2] * q2;
+      a0 -= hs[j + 3] * p3; a1 -= hs[j + 3] * q3;
+    }
+    for (; j < k; ++j) { a0 -= hs[j] * __ldg(V + j * ldv + i); a1 -= hs[j] * __ldg(V + j * ldv + i + stride); }
+    w[i] = a0;
+    w[i + stride] = a1;
+    acc[0] += a0 * a0 + a1 * a1;
+  }
+  if (i < n) {
+    double a0 = w[i];
+    for (int j = 0; j < k; ++j) a0 -= hs[j] * __ldg(V + j * ldv + i);
+    w[i] = a0;
+    acc[0] += a0 * a0;
   }
   block_partials<1>(acc, ws.partial, ws, out);
 }
@@ -98,7 +128,13 @@ __global__ void lincomb_kernel(double* __restrict__ x, const double* __restrict_
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
     double xi = x[i];
-    for (int j = 0; j < k; ++j) xi += ys[j] * __ldg(Z + j * ldz + i);
+    int j = 0;
+    for (; j + 4 <= k; j += 4) {
+      double z0 = __ldg(Z + (j + 0) * ldz + i), z1 = __ldg(Z + (j + 1) * ldz + i);
+      double z2 = __ldg(Z + (j + 2) * ldz + i), z3 = __ldg(Z + (j + 3) * ldz + i);
+      xi += ys[j] * z0 + ys[j + 1] * z1 + ys[j + 2] * z2 + ys[j + 3] * z3;
+    }
+    for (; j < k; ++j) xi += ys[j] * __ldg(Z + j * ldz + i);
     x[i] = xi;
   }
 }
@@ -133,7 +169,7 @@ __global__ void __launch_bounds__(kRedThreads) checksum_kernel(const double* __r
 }
 
 static unsigned red_blocks(long long n) {
-  long long b = (n + kRedThreads - 1) / kRedThreads;
+  long long b = (n + 2 * kRedThreads - 1) / (2 * kRedThreads);
   if (b > kRedBlocks) b = kRedBlocks;
   if (b < 1) b = 1;
   return (unsigned)b;
