@@ -160,10 +160,9 @@ int st_level_apply(st_ctx_t* ctx, const double* rho, int level, const double* x,
 
 /* Benchmark hook: enqueue `reps` back-to-back launches of the level-l operator kernel in
  * mode (0 apply, 1 residual y = b - A x, 2 damped-Jacobi sweep, 3 first sweep from zero)
- * on the context stream and return WITHOUT synchronising (the caller brackets them with
- * events on that stream). Device pointers only. */
-int st_bench_op(st_ctx_t* ctx, const double* rho, int level, int mode, int transpose, const double* x,
-                const double* b, double* y, int reps);
+ * on the context's internal work vectors and return WITHOUT synchronising (the caller
+ * brackets them with events on the context stream). rho: device pointer. */
+int st_bench_op(st_ctx_t* ctx, const double* rho, int level, int mode, int transpose, int reps);
 
 int st_get_stats(const st_ctx_t* ctx, st_stats_t* s);
 int st_get_hierarchy(const st_ctx_t* ctx, st_hierarchy_t* h);

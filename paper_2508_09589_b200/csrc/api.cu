@@ -60,8 +60,9 @@ struct st_ctx {
   bool tc = true;
   MatsDev md{};
   std::vector<Level> lv;
-  long long N = 0, ndesign = 0, ld = 0;
-  double *f = nullptr, *b = nullptr, *tmpN = nullptr, *tmpN2 = nullptr;
+  long long N = 0, Nd = 0, ndesign = 0, ld = 0;   // N: internal (padded) storage, Nd: nodes
+  Geom gd0{};                                      // level-0 geometry in the caller's dense layout
+  double *f = nullptr, *b = nullptr, *tmpN = nullptr, *tmpN2 = nullptr, *xint = nullptr;
   double *V = nullptr, *Z = nullptr;
   RedWs ws{};
   double* dsmall = nullptr;
@@ -88,15 +89,22 @@ void check_launch() {
 template <class T> void dalloc(T** p, size_t count) {
   CK(cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T)));
 }
+// zero-initialised (pad entries of internal vectors must stay zero)
+void dzalloc(double** p, size_t count) {
+  dalloc(p, count);
+  CK(cudaMemset(*p, 0, std::max<size_t>(count, 1) * sizeof(double)));
+}
 
-Geom make_geom(int sd, int n, int nt, int plo, int phi) {
+// pad = true: internal layout with an even x1 row pitch (16-byte aligned rows and planes)
+Geom make_geom(int sd, int n, int nt, int plo, int phi, bool pad = true) {
   Geom g{};
   g.sd = sd;
   g.n = n;
   g.nn = n + 1;
   g.nt = nt;
-  g.P = 1;
-  for (int d = 0; d < sd; ++d) g.P *= g.nn;
+  g.pr = (pad && (g.nn % 2 == 1)) ? g.nn + 1 : g.nn;
+  g.P = g.pr;
+  for (int d = 1; d < sd; ++d) g.P *= g.nn;
   g.N = g.P * (nt + 1);
   g.plo = plo;
   g.phi = phi;
@@ -106,6 +114,12 @@ Geom make_geom(int sd, int n, int nt, int plo, int phi) {
 }
 
 int nc_of(int sd) { return sd == 2 ? 5 : 14; }
+long long nodes_of(const Geom& g) {
+  long long v = g.nt + 1;
+  for (int d = 0; d < g.sd; ++d) v *= g.nn;
+  return v;
+}
+Geom dense_of(const Geom& g) { return make_geom(g.sd, g.n, g.nt, g.plo, g.phi, false); }
 
 // E' = W0^T E W0 + W1^T E W1 (linear-in-time prolongation, two fine layers per coarse layer)
 void time_coarsen_factor(const double E[2][2], double out[2][2]) {
@@ -175,7 +189,7 @@ void build_hierarchy(st_ctx* c) {
   const int maxl = c->opt.max_levels > 0 ? c->opt.max_levels : 64;
   while ((int)c->lv.size() < maxl) {
     const Geom& g = c->lv.back().g;
-    if (g.N <= c->opt.coarse_max_nodes) break;
+    if (nodes_of(g) <= c->opt.coarse_max_nodes) break;
     double lam = D * g.dt / (g.dx * g.dx);
     int kind;
     bool ok;
@@ -265,12 +279,13 @@ void allocate(st_ctx* c) {
   const long long N = c->N;
   const int m = c->opt.restart;
   c->ld = (N + 31) / 32 * 32;
-  dalloc(&c->f, N);
-  dalloc(&c->b, N);
-  dalloc(&c->tmpN, N);
-  dalloc(&c->tmpN2, N);
-  dalloc(&c->V, (size_t)(m + 1) * c->ld);
-  dalloc(&c->Z, (size_t)m * c->ld);
+  dzalloc(&c->f, N);
+  dzalloc(&c->b, N);
+  dzalloc(&c->tmpN, N);
+  dzalloc(&c->tmpN2, N);
+  dzalloc(&c->xint, N);
+  dzalloc(&c->V, (size_t)(m + 1) * c->ld);
+  dzalloc(&c->Z, (size_t)m * c->ld);
   dalloc(&c->ws.partial, (size_t)kRedBlocks * 16);
   dalloc(&c->ws.counter, 1);
   CK(cudaMemsetAsync(c->ws.counter, 0, sizeof(unsigned), c->stream));
@@ -280,13 +295,13 @@ void allocate(st_ctx* c) {
     Level& Lv = c->lv[l];
     const long long n = Lv.g.N;
     if (l == 0) {
-      dalloc(&Lv.r, n);
-      dalloc(&Lv.t, n);
+      dzalloc(&Lv.r, n);
+      dzalloc(&Lv.t, n);
     } else {
-      dalloc(&Lv.x, n);
-      dalloc(&Lv.b, n);
-      dalloc(&Lv.r, n);
-      dalloc(&Lv.t, n);
+      dzalloc(&Lv.x, n);
+      dzalloc(&Lv.b, n);
+      dzalloc(&Lv.r, n);
+      dzalloc(&Lv.t, n);
       if (Lv.st_owned) {
         dalloc(&Lv.st, Lv.st_elems);
         Lv.op.st = Lv.st;
@@ -560,6 +575,27 @@ void copy_back(st_ctx* c, double* host, const double* dev, long long n) {
   CK(cudaStreamSynchronize(c->stream));
 }
 
+// caller vector (dense layout, host or device) -> internal padded vector
+void pack_in(st_ctx* c, const double* user, double* internal, int slot) {
+  const double* d = in_ptr(c, user, c->Nd, slot);
+  launch_relayout(c->gd0, d, c->lv[0].g, internal, c->stream);
+  L(c);
+}
+// internal padded vector -> caller vector (dense layout, host or device); synchronises
+void unpack_out(st_ctx* c, const double* internal, double* user, int slot) {
+  if (!user) throw StErr{ST_E_INVALID_ARG, "null pointer"};
+  if (is_device_ptr(user)) {
+    launch_relayout(c->lv[0].g, internal, c->gd0, user, c->stream);
+    L(c);
+    CK(cudaStreamSynchronize(c->stream));
+  } else {
+    double* d = stage(c, slot, c->Nd);
+    launch_relayout(c->lv[0].g, internal, c->gd0, d, c->stream);
+    L(c);
+    copy_back(c, user, d, c->Nd);
+  }
+}
+
 template <class F> int guarded(F&& f) {
   try {
     return f();
@@ -583,7 +619,7 @@ void free_ctx(st_ctx* c) {
     cudaFree(Lv.x); cudaFree(Lv.b); cudaFree(Lv.r); cudaFree(Lv.t);
     cudaFree(Lv.A); cudaFree(Lv.Ainv); cudaFree(Lv.info);
   }
-  cudaFree(c->f); cudaFree(c->b); cudaFree(c->tmpN); cudaFree(c->tmpN2);
+  cudaFree(c->f); cudaFree(c->b); cudaFree(c->tmpN); cudaFree(c->tmpN2); cudaFree(c->xint);
   cudaFree(c->V); cudaFree(c->Z); cudaFree(c->ws.partial); cudaFree(c->ws.counter);
   cudaFree(c->dsmall);
   if (c->hsmall) cudaFreeHost(c->hsmall);
@@ -687,6 +723,8 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       build_hierarchy(c);
       setup_forms(c);
       c->N = c->lv[0].g.N;
+      c->Nd = nodes_of(c->lv[0].g);
+      c->gd0 = dense_of(c->lv[0].g);
       long long nsp = 1;
       for (int d = 0; d < c->sd; ++d) nsp *= grid->n;
       c->ndesign = c->tc ? nsp : nsp * grid->nt;
@@ -713,12 +751,11 @@ int st_solve(st_ctx_t* c, const double* rho, double* T) {
     if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
     CK(cudaSetDevice(c->device));
     prepare(c, rho);
-    bool staged = false;
-    double* x = out_ptr(c, T, c->N, 0, true, &staged);
-    launch_set_bc_values(c->lv[0].g, c->bcs.T0, x, c->stream);  // x_c = xD
-    L(c);
-    int rc = fgmres(c, false, c->b, x);
-    if (staged) copy_back(c, T, x, c->N);
+    pack_in(c, T, c->xint, 0);
+    launch_set_bc_values(c->lv[0].g, c->bcs.T0, c->xint, c->stream);  // x_c = xD
+    L(c, 2);
+    int rc = fgmres(c, false, c->b, c->xint);
+    unpack_out(c, c->xint, T, 0);
     return rc;
   });
 }
@@ -728,15 +765,13 @@ int st_adjoint(st_ctx_t* c, const double* rho, const double* dJdT, double* lambd
     if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
     CK(cudaSetDevice(c->device));
     prepare(c, rho);
-    const double* g = in_ptr(c, dJdT, c->N, 1);
-    launch_mask_free(c->lv[0].g, g, c->tmpN2, c->stream);  // RHS m_f g
-    L(c);
-    bool staged = false;
-    double* x = out_ptr(c, lambda, c->N, 0, true, &staged);
-    launch_set_bc_values(c->lv[0].g, 0.0, x, c->stream);  // lambda_c = 0
-    L(c);
-    int rc = fgmres(c, true, c->tmpN2, x);
-    if (staged) copy_back(c, lambda, x, c->N);
+    pack_in(c, dJdT, c->tmpN2, 1);
+    launch_mask_free(c->lv[0].g, c->tmpN2, c->tmpN2, c->stream);  // RHS m_f g
+    pack_in(c, lambda, c->xint, 0);
+    launch_set_bc_values(c->lv[0].g, 0.0, c->xint, c->stream);  // lambda_c = 0
+    L(c, 4);
+    int rc = fgmres(c, true, c->tmpN2, c->xint);
+    unpack_out(c, c->xint, lambda, 0);
     return rc;
   });
 }
@@ -752,8 +787,9 @@ int st_sensitivity(st_ctx_t* c, const double* rho, const double* T, const double
     }
     OpDesc op = c->lv[0].op;
     op.rho = r;
-    const double* Td = in_ptr(c, T, c->N, 1);
-    const double* Ld = in_ptr(c, lambda, c->N, 2);
+    op.g = c->gd0;  // T, lambda in the caller's dense layout
+    const double* Td = in_ptr(c, T, c->Nd, 1);
+    const double* Ld = in_ptr(c, lambda, c->Nd, 2);
     bool staged = false;
     double* dj = out_ptr(c, dJ, c->ndesign, 3, false, &staged);
     launch_sensitivity(op, Td, Ld, dj, c->stream);
@@ -763,6 +799,21 @@ int st_sensitivity(st_ctx_t* c, const double* rho, const double* T, const double
     else CK(cudaStreamSynchronize(c->stream));
     return ST_OK;
   });
+}
+
+// eliminated operator on an arbitrary input: the level kernels assume x = 0 at constrained
+// nodes (true for every vector of the solver), so mask first and restore the identity rows
+void masked_level_apply(st_ctx* c, int l, const double* x, double* xm, double* y, bool trans, bool bc) {
+  const Geom& g = c->lv[l].g;
+  if (bc) {
+    launch_mask_free(g, x, xm, c->stream);
+    op_launch(c, l, MODE_APPLY, trans, true, xm, nullptr, y);
+    launch_copy_cons(g, x, y, c->stream);
+    L(c, 2);
+  } else {
+    op_launch(c, l, MODE_APPLY, trans, false, x, nullptr, y);
+  }
+  check_launch();
 }
 
 int st_apply(st_ctx_t* c, const double* rho, const double* x, double* y, int transpose, int bc) {
@@ -775,13 +826,9 @@ int st_apply(st_ctx_t* c, const double* rho, const double* x, double* y, int tra
       r = c->rho_stage;
     }
     c->lv[0].op.rho = r;
-    const double* xd = in_ptr(c, x, c->N, 1);
-    bool staged = false;
-    double* yd = out_ptr(c, y, c->N, 2, false, &staged);
-    op_launch(c, 0, MODE_APPLY, transpose != 0, bc != 0, xd, nullptr, yd);
-    check_launch();
-    if (staged) copy_back(c, y, yd, c->N);
-    else CK(cudaStreamSynchronize(c->stream));
+    pack_in(c, x, c->tmpN, 1);
+    masked_level_apply(c, 0, c->tmpN, c->tmpN2, c->lv[0].t, transpose != 0, bc != 0);
+    unpack_out(c, c->lv[0].t, y, 2);
     return ST_OK;
   });
 }
@@ -792,13 +839,21 @@ int st_level_apply(st_ctx_t* c, const double* rho, int level, const double* x, d
     if (level < 0 || level >= (int)c->lv.size()) throw StErr{ST_E_INVALID_ARG, "level out of range"};
     CK(cudaSetDevice(c->device));
     prepare(c, rho);
-    const long long n = c->lv[level].g.N;
-    const double* xd = in_ptr(c, x, n, 1);
+    Level& Lv = c->lv[level];
+    const Geom gd = dense_of(Lv.g);
+    const long long nd = nodes_of(Lv.g);
+    double* xi = level == 0 ? c->tmpN : Lv.x;
+    double* xm = level == 0 ? c->tmpN2 : Lv.b;
+    const double* xd = in_ptr(c, x, nd, 1);
+    launch_relayout(gd, xd, Lv.g, xi, c->stream);
+    L(c);
+    masked_level_apply(c, level, xi, xm, Lv.t, transpose != 0, true);
     bool staged = false;
-    double* yd = out_ptr(c, y, n, 2, false, &staged);
-    op_launch(c, level, MODE_APPLY, transpose != 0, true, xd, nullptr, yd);
+    double* yd = out_ptr(c, y, nd, 2, false, &staged);
+    launch_relayout(Lv.g, Lv.t, gd, yd, c->stream);
+    L(c);
     check_launch();
-    if (staged) copy_back(c, y, yd, n);
+    if (staged) copy_back(c, y, yd, nd);
     else CK(cudaStreamSynchronize(c->stream));
     return ST_OK;
   });
@@ -809,27 +864,18 @@ int st_rhs(st_ctx_t* c, const double* rho, double* f, double* b) {
     if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
     CK(cudaSetDevice(c->device));
     prepare(c, rho);
-    if (f) {
-      if (is_device_ptr(f)) CK(cudaMemcpyAsync(f, c->f, c->N * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-      else CK(cudaMemcpyAsync(f, c->f, c->N * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    }
-    if (b) {
-      if (is_device_ptr(b)) CK(cudaMemcpyAsync(b, c->b, c->N * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-      else CK(cudaMemcpyAsync(b, c->b, c->N * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    }
+    if (f) unpack_out(c, c->f, f, 2);
+    if (b) unpack_out(c, c->b, b, 2);
     CK(cudaStreamSynchronize(c->stream));
     return ST_OK;
   });
 }
 
-int st_bench_op(st_ctx_t* c, const double* rho, int level, int mode, int transpose, const double* x,
-                const double* b, double* y, int reps) {
+int st_bench_op(st_ctx_t* c, const double* rho, int level, int mode, int transpose, int reps) {
   return guarded([&]() -> int {
     if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
     if (level < 0 || level >= (int)c->lv.size() || c->lv[level].dense) throw StErr{ST_E_INVALID_ARG, "level"};
     if (mode < 0 || mode > 3 || reps < 0) throw StErr{ST_E_INVALID_ARG, "mode/reps"};
-    if (!is_device_ptr(y) || (mode != 3 && !is_device_ptr(x)) || (mode != 0 && !is_device_ptr(b)))
-      throw StErr{ST_E_INVALID_ARG, "st_bench_op takes device pointers"};
     CK(cudaSetDevice(c->device));
     if (level == 0) {
       if (!is_device_ptr(rho)) throw StErr{ST_E_INVALID_ARG, "rho must be a device pointer"};
@@ -837,7 +883,10 @@ int st_bench_op(st_ctx_t* c, const double* rho, int level, int mode, int transpo
     } else {
       prepare(c, rho);
     }
-    for (int r = 0; r < reps; ++r) op_launch(c, level, mode, transpose != 0, true, x, b, y);
+    Level& Lv = c->lv[level];
+    double* x = level == 0 ? c->tmpN : Lv.x;
+    double* b = level == 0 ? c->tmpN2 : Lv.b;
+    for (int r = 0; r < reps; ++r) op_launch(c, level, mode, transpose != 0, true, x, b, Lv.t);
     check_launch();
     return ST_OK;
   });
@@ -858,12 +907,12 @@ int st_get_hierarchy(const st_ctx_t* c, st_hierarchy_t* h) {
     h->nt[l] = c->lv[l].g.nt;
     h->kind[l] = c->lv[l].kind;
     h->form[l] = c->lv[l].dense ? FORM_DENSE : c->lv[l].op.form;
-    h->nodes[l] = c->lv[l].g.N;
+    h->nodes[l] = nodes_of(c->lv[l].g);
   }
   return ST_OK;
 }
 
-int64_t st_num_nodes(const st_ctx_t* c) { return c ? c->N : -1; }
+int64_t st_num_nodes(const st_ctx_t* c) { return c ? c->Nd : -1; }
 int64_t st_num_design(const st_ctx_t* c) { return c ? c->ndesign : -1; }
 int64_t st_kernel_launches(const st_ctx_t* c) { return c ? c->launches : -1; }
 

@@ -20,12 +20,15 @@ enum Form { FORM_RHO = 0, FORM_MK = 1, FORM_B4 = 2, FORM_DENSE = 3 };
 enum Kind { KIND_FINE = 0, KIND_SPACE = 1, KIND_TIME = 2, KIND_FULL = 3 };
 enum Mode { MODE_APPLY = 0, MODE_RESID = 1, MODE_JAC = 2, MODE_JAC0 = 3 };
 
-// Level geometry: n^sd x nt elements, (n+1)^sd (nt+1) nodes.
+// Level geometry: n^sd x nt elements, (n+1)^sd (nt+1) nodes. Storage: x1 rows of pitch pr
+// (pr = nn for the caller's dense layout; internal vectors use an even pitch so that every
+// row and plane starts 16-byte aligned — TMA tiles); pad entries are kept at zero.
 struct Geom {
   int sd;
   int n, nn, nt;
-  long long P;   // nodes per time plane
-  long long N;   // all nodes
+  int pr;        // row pitch (elements) of the x1 rows
+  long long P;   // stored entries per time plane (pr * nn^(sd-1))
+  long long N;   // stored entries (P * (nt+1))
   int plo, phi;  // sink patch: transverse node range at x1 = 0 (plo > phi: none)
   double dx, dt;
 };
@@ -102,9 +105,18 @@ template <int SD> __device__ __forceinline__ bool is_patch(const Geom& g, const 
 }
 
 template <int SD> __device__ __forceinline__ long long pidx(const Geom& g, const int* c) {
-  long long r = c[0] + (long long)g.nn * c[1];
-  if (SD == 3) r += (long long)g.nn * g.nn * c[2];
+  long long r = c[0] + (long long)g.pr * c[1];
+  if (SD == 3) r += (long long)g.pr * g.nn * c[2];
   return r;
+}
+
+// decode an in-plane storage offset into node coordinates; false for pad entries
+template <int SD> __device__ __forceinline__ bool pdecode(const Geom& g, long long pn, int* c) {
+  c[0] = (int)(pn % g.pr);
+  long long t = pn / g.pr;
+  c[1] = (int)(t % g.nn);
+  c[2] = (SD == 3) ? (int)(t / g.nn) : 0;
+  return c[0] < g.nn;
 }
 
 }  // namespace st

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(NTH, CUNI ? ST_CUNI_MINB : 3) op2d_kernel(OpDe
   const int p1 = min(p0 + chunk, g.nt + 1);
   const int qs = max(p0 - 1, 0), qe = min(p1, g.nt);
   const int i = x0 + tx;
-  const int n = g.n, nn = g.nn;
+  const int n = g.n, nn = g.nn, pr = g.pr;
   const long long P = g.P;
   const double sm = (SRC == 0) ? g.dx * g.dx * (1.0 / 36.0) * (CUNI ? op.m.Cins : 1.0) : 1.0;
   const double sk = (SRC == 0) ? (1.0 / 6.0) : 1.0;
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(NTH, CUNI ? ST_CUNI_MINB : 3) op2d_kernel(OpDe
     int ly = e / HX, lx = e - ly * HX;
     int gi = x0 - 1 + lx, gj = y0 - 1 + ly;
     bool v = (e < PT) && (gi >= 0 && gi <= n && gj >= 0 && gj <= n);
-    xoff[k] = v ? gj * nn + gi : 0;
+    xoff[k] = v ? gj * pr + gi : 0;
     xsm[k] = e < PT ? e : 0;
     if (v) xval |= 1u << k;
     if (v && gi == 0 && gj >= g.plo && gj <= g.phi) xpatch |= 1u << k;
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(NTH, CUNI ? ST_CUNI_MINB : 3) op2d_kernel(OpDe
     int ly = e / TX, lx = e - ly * TX;
     int gi = x0 + lx, gj = y0 + ly;
     bool v = (e < BT) && gi <= n && gj <= n;
-    boff[k] = v ? gj * nn + gi : 0;
+    boff[k] = v ? gj * pr + gi : 0;
     if (v) bval |= 1u << k;
   }
   int roff[RPT];
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(NTH, CUNI ? ST_CUNI_MINB : 3) op2d_kernel(OpDe
         wK_from(ke[0], ke[1], ke[2], ke[3], wK[r]);
       } else {
         // stored symmetric stencils: own forward coefs (k >= 4) + neighbours' mirrored ones
-        const long long pn = act[r] ? (long long)jr[r] * nn + i : 0;
+        const long long pn = act[r] ? (long long)jr[r] * pr + i : 0;
         const double* Mb = op.st;
         const double* Kb = op.st + 5 * P;
 #pragma unroll
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(NTH, CUNI ? ST_CUNI_MINB : 3) op2d_kernel(OpDe
           } else {
             int ni = i + dx, nj = jr[r] + dy;
             bool v = act[r] && ni >= 0 && ni <= n && nj >= 0 && nj <= n;
-            long long q = v ? (long long)nj * nn + ni : 0;
+            long long q = v ? (long long)nj * pr + ni : 0;
             wM[r][k] = v ? __ldg(Mb + (8 - k - 4) * P + q) : 0.0;
             wK[r][k] = v ? __ldg(Kb + (8 - k - 4) * P + q) : 0.0;
           }
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(NTH, CUNI ? ST_CUNI_MINB : 3) op2d_kernel(OpDe
   int cur = qs % NB;
   int prv = (cur + NB - 1) % NB;
   int nxt = (cur + NB - 2) % NB;
-  const int nodeoff0 = jr[0] * nn + i;
+  const int nodeoff0 = jr[0] * pr + i;
   double* yrow = y + (long long)(qs - 1) * P + nodeoff0;   // row q-1 of the current iteration
 
   double Mprev[RY], Kprev[RY], carry[RY], dcarry[RY];
@@ -278,9 +278,9 @@ __global__ void __launch_bounds__(NTH, CUNI ? ST_CUNI_MINB : 3) op2d_kernel(OpDe
                            MASK && i == 0 && jr[1] >= g.plo && jr[1] <= g.phi};
   auto out_row = [&](int p, int slot, int r, double Ax, double od) {
     if (p < p0 || p >= p1 || !act[r]) return;
-    const long long gi = (long long)p * P + nodeoff0 + r * nn;
+    const long long gi = (long long)p * P + nodeoff0 + r * pr;
     const bool cons = MASK && (p == 0 || patchr[r]);
-    double* yo = yrow + r * nn;
+    double* yo = yrow + r * pr;
     const double bv = NBV ? bs[slot][(ty * RY + r) * TX + tx] : 0.0;
     double o;
     if (MODE == MODE_APPLY) {

@@ -44,6 +44,8 @@ void launch_checksum(const double* a, long long n, double* out, RedWs ws, cudaSt
 // misc.cu
 void launch_source(const Geom& g, int kind, double qscale, double a, double w, double tau, double* f, cudaStream_t s);
 void launch_mask_free(const Geom& g, const double* in, double* out, cudaStream_t s);       // out = m_f .* in
+void launch_copy_cons(const Geom& g, const double* src, double* dst, cudaStream_t s);     // dst_c = src_c
+void launch_relayout(const Geom& gs, const double* src, const Geom& gd, double* dst, cudaStream_t s);
 void launch_set_bc_values(const Geom& g, double T0, double* x, cudaStream_t s);          // x_c = xD
 void launch_rhs_combine(const Geom& g, const double* f, const double* KxD, double T0, double* b, cudaStream_t s);
 void launch_xd(const Geom& g, double T0, double* x, cudaStream_t s);                      // x = xD (0 off plane 0)

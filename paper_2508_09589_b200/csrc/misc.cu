@@ -14,13 +14,10 @@ __global__ void source_kernel(Geom g, int kind, double qscale, double a, double 
   if (idx >= g.N) return;
   int p = (int)(idx / g.P);
   long long pn = idx % g.P;
+  int cc[3];
+  if (!pdecode<SD>(g, pn, cc)) { f[idx] = 0.0; return; }
   double sx = 1.0;
-  long long t = pn;
-  for (int d = 0; d < SD; ++d) {
-    int c = (int)(t % g.nn);
-    t /= g.nn;
-    sx *= 0.5 * g.dx * ((c == 0 || c == g.n) ? 1.0 : 2.0);
-  }
+  for (int d = 0; d < SD; ++d) sx *= 0.5 * g.dx * ((cc[d] == 0 || cc[d] == g.n) ? 1.0 : 2.0);
   const double s = 0.5 / sqrt(3.0);
   double ft = 0.0;
   for (int side = 0; side < 2; ++side) {
@@ -44,31 +41,31 @@ void launch_source(const Geom& g, int kind, double qscale, double a, double w, d
 }
 
 // ---------------------------------------------------------------------------------------
-template <int SD> __device__ __forceinline__ void node_of(const Geom& g, long long idx, int* c, int& p) {
+// node of storage index idx; false for pad entries
+template <int SD> __device__ __forceinline__ bool node_of(const Geom& g, long long idx, int* c, int& p) {
   p = (int)(idx / g.P);
-  long long t = idx % g.P;
-  for (int d = 0; d < SD; ++d) { c[d] = (int)(t % g.nn); t /= g.nn; }
+  return pdecode<SD>(g, idx % g.P, c);
 }
 
 template <int SD> __global__ void mask_free_kernel(Geom g, const double* __restrict__ in, double* __restrict__ out) {
   long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= g.N) return;
   int c[3] = {0, 0, 0}, p;
-  node_of<SD>(g, idx, c, p);
+  if (!node_of<SD>(g, idx, c, p)) { out[idx] = 0.0; return; }
   out[idx] = is_cons<SD>(g, c, p) ? 0.0 : in[idx];
 }
 template <int SD> __global__ void set_bc_kernel(Geom g, double T0, double* __restrict__ x) {
   long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= g.N) return;
   int c[3] = {0, 0, 0}, p;
-  node_of<SD>(g, idx, c, p);
+  if (!node_of<SD>(g, idx, c, p)) return;
   if (is_cons<SD>(g, c, p)) x[idx] = (p == 0 && !is_patch<SD>(g, c)) ? T0 : 0.0;
 }
 template <int SD> __global__ void xd_kernel(Geom g, double T0, double* __restrict__ x) {
   long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= g.N) return;
   int c[3] = {0, 0, 0}, p;
-  node_of<SD>(g, idx, c, p);
+  if (!node_of<SD>(g, idx, c, p)) { x[idx] = 0.0; return; }
   x[idx] = (p == 0 && !is_patch<SD>(g, c)) ? T0 : 0.0;
 }
 template <int SD>
@@ -77,9 +74,34 @@ __global__ void rhs_kernel(Geom g, const double* __restrict__ f, const double* _
   long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= g.N) return;
   int c[3] = {0, 0, 0}, p;
-  node_of<SD>(g, idx, c, p);
+  if (!node_of<SD>(g, idx, c, p)) { b[idx] = 0.0; return; }
   if (is_cons<SD>(g, c, p)) b[idx] = (p == 0 && !is_patch<SD>(g, c)) ? T0 : 0.0;
   else b[idx] = f[idx] - (KxD ? KxD[idx] : 0.0);
+}
+
+// relayout between two storage geometries of the same grid (dense caller layout <-> padded
+// internal layout); iterates over the source storage, skips its pads
+template <int SD>
+__global__ void relayout_kernel(Geom gs, const double* __restrict__ src, Geom gd, double* __restrict__ dst) {
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= gs.N) return;
+  int c[3] = {0, 0, 0}, p;
+  if (!node_of<SD>(gs, idx, c, p)) return;
+  dst[(long long)p * gd.P + pidx<SD>(gd, c)] = src[idx];
+}
+// dst_c = src_c at constrained nodes (identity rows of the eliminated operator)
+template <int SD> __global__ void copy_cons_kernel(Geom g, const double* __restrict__ src, double* __restrict__ dst) {
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= g.N) return;
+  int c[3] = {0, 0, 0}, p;
+  if (!node_of<SD>(g, idx, c, p)) return;
+  if (is_cons<SD>(g, c, p)) dst[idx] = src[idx];
+}
+
+void launch_relayout(const Geom& gs, const double* src, const Geom& gd, double* dst, cudaStream_t s) {
+  unsigned grd = (unsigned)((gs.N + 255) / 256);
+  if (gs.sd == 2) relayout_kernel<2><<<grd, 256, 0, s>>>(gs, src, gd, dst);
+  else relayout_kernel<3><<<grd, 256, 0, s>>>(gs, src, gd, dst);
 }
 
 #define EW_LAUNCH(K, ...)                                                   \
@@ -90,6 +112,7 @@ __global__ void rhs_kernel(Geom g, const double* __restrict__ f, const double* _
   } while (0)
 
 void launch_mask_free(const Geom& g, const double* in, double* out, cudaStream_t s) { EW_LAUNCH(mask_free_kernel, in, out); }
+void launch_copy_cons(const Geom& g, const double* src, double* dst, cudaStream_t s) { EW_LAUNCH(copy_cons_kernel, src, dst); }
 void launch_set_bc_values(const Geom& g, double T0, double* x, cudaStream_t s) { EW_LAUNCH(set_bc_kernel, T0, x); }
 void launch_xd(const Geom& g, double T0, double* x, cudaStream_t s) { EW_LAUNCH(xd_kernel, T0, x); }  // x = xD
 void launch_rhs_combine(const Geom& g, const double* f, const double* KxD, double T0, double* b, cudaStream_t s) {

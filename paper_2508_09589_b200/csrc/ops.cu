@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(128) op_kernel(OpDesc op, const double* __rest
   c[0] = i0;
   c[1] = (SD == 2) ? r : r % g.nn;
   c[2] = (SD == 2) ? 0 : r / g.nn;
-  const long long pn = i0 + (long long)g.nn * r;
+  const long long pn = i0 + (long long)g.pr * r;
   const int p0 = blockIdx.z * chunk;
   const int p1 = min(p0 + chunk, g.nt + 1);
   if (p0 > g.nt) return;
@@ -421,10 +421,7 @@ __global__ void rap_space_kernel(OpDesc fop, Geom gc, int nl, double* __restrict
   int s = (int)((idx / gc.P) % NS);
   int tau = (int)(idx / (gc.P * NS));
   int C[3] = {0, 0, 0};
-  {
-    long long t = pc;
-    for (int d = 0; d < SD; ++d) { C[d] = (int)(t % gc.nn); t /= gc.nn; }
-  }
+  if (!pdecode<SD>(gc, pc, C)) return;
   double acc[NC];
 #pragma unroll
   for (int q = 0; q < NC; ++q) acc[q] = 0.0;
@@ -488,10 +485,7 @@ __global__ void rap_time_kernel(OpDesc fop, int nlc, double* __restrict__ out) {
   long long pn = idx % g.P;
   int T = (int)(idx / g.P);
   int c[3] = {0, 0, 0};
-  {
-    long long t = pn;
-    for (int d = 0; d < SD; ++d) { c[d] = (int)(t % g.nn); t /= g.nn; }
-  }
+  if (!pdecode<SD>(g, pn, c)) return;
   const double W[2][2][2] = {{{1.0, 0.0}, {0.5, 0.5}}, {{0.5, 0.5}, {0.0, 1.0}}};
   double* o = out + (long long)T * 5 * NC * g.P;
   for (int q = 0; q < NC; ++q) {
@@ -527,8 +521,7 @@ __global__ void rho_to_mk_kernel(OpDesc fop, int tau, double* __restrict__ out) 
   long long pn = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (pn >= g.P) return;
   int c[3] = {0, 0, 0};
-  long long t = pn;
-  for (int d = 0; d < SD; ++d) { c[d] = (int)(t % g.nn); t /= g.nn; }
+  if (!pdecode<SD>(g, pn, c)) return;
   double ce[SG<SD>::NE], ke[SG<SD>::NE];
   elem_ck<SD>(fop, c, tau, ce, ke);
   for (int q = 0; q < NC; ++q) {
@@ -583,10 +576,8 @@ __global__ void dense_assemble_kernel(OpDesc op, double* __restrict__ A) {
   int p = (int)(row / g.P);
   long long pn = row % g.P;
   int c[3] = {0, 0, 0};
-  long long t = pn;
-  for (int d = 0; d < SD; ++d) { c[d] = (int)(t % g.nn); t /= g.nn; }
   double* Ar = A + row * g.N;
-  if (is_cons<SD>(g, c, p)) { Ar[row] = 1.0; return; }
+  if (!pdecode<SD>(g, pn, c) || is_cons<SD>(g, c, p)) { Ar[row] = 1.0; return; }
   // layer p-1 (top rows: S^{tb} -> plane p-1, S^{tt} -> plane p); layer p (bottom rows)
   for (int side = 0; side < 2; ++side) {
     int tau = side == 0 ? p - 1 : p;

@@ -15,10 +15,7 @@ __global__ void restrict_kernel(Geom gf, Geom gc, const double* __restrict__ rf,
   int P = (int)(idx / gc.P);
   long long pc = idx % gc.P;
   int C[3] = {0, 0, 0};
-  long long t = pc;
-#pragma unroll
-  for (int d = 0; d < SD; ++d) { C[d] = (int)(t % gc.nn); t /= gc.nn; }
-  if (is_cons<SD>(gc, C, P)) { rc[idx] = 0.0; return; }
+  if (!pdecode<SD>(gc, pc, C) || is_cons<SD>(gc, C, P)) { rc[idx] = 0.0; return; }
   constexpr int NS = SP ? SG<SD>::NOFF : 1;
   double acc = 0.0;
 #pragma unroll
@@ -52,10 +49,7 @@ __global__ void prolong_kernel(Geom gf, Geom gc, const double* __restrict__ ec, 
   int p = (int)(idx / gf.P);
   long long pf = idx % gf.P;
   int c[3] = {0, 0, 0};
-  long long t = pf;
-#pragma unroll
-  for (int d = 0; d < SD; ++d) { c[d] = (int)(t % gf.nn); t /= gf.nn; }
-  if (is_cons<SD>(gf, c, p)) return;
+  if (!pdecode<SD>(gf, pf, c) || is_cons<SD>(gf, c, p)) return;
   // time part
   int P0 = TM ? (p >> 1) : p;
   int nP = (TM && (p & 1)) ? 2 : 1;

@@ -89,8 +89,7 @@ def load_library(path: str = LIB_PATH):
     lib.st_apply.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]
     lib.st_rhs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.st_level_apply.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
-    lib.st_bench_op.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
-                                C.c_void_p, C.c_int]
+    lib.st_bench_op.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
     lib.st_get_stats.argtypes = [C.c_void_p, P(Stats)]
     lib.st_get_hierarchy.argtypes = [C.c_void_p, P(Hierarchy)]
     for name in ("st_num_nodes", "st_num_design", "st_kernel_launches"):
@@ -173,10 +172,10 @@ class Solver:
     def level_apply(self, rho, level, x, y, transpose=False):
         return self._check(self.lib.st_level_apply(self.ctx, _ptr(rho), level, _ptr(x), _ptr(y), int(transpose)))
 
-    def bench_op(self, rho, level, mode, x, b, y, reps, transpose=False):
-        """Enqueue `reps` launches of the level operator kernel without synchronising."""
-        return self._check(self.lib.st_bench_op(self.ctx, _ptr(rho), level, mode, int(transpose), _ptr(x), _ptr(b),
-                                                _ptr(y), reps))
+    def bench_op(self, rho, level, mode, reps, transpose=False):
+        """Enqueue `reps` launches of the level operator kernel (internal work vectors) without
+        synchronising."""
+        return self._check(self.lib.st_bench_op(self.ctx, _ptr(rho), level, mode, int(transpose), reps))
 
     def rhs(self, rho, f=None, b=None):
         return self._check(self.lib.st_rhs(self.ctx, _ptr(rho), _ptr(f), _ptr(b)))

@@ -16,8 +16,8 @@ H = s.hierarchy()
 N = H[level]["nodes"]
 x = torch.rand(N, dtype=torch.float64, device=dev); b = torch.rand_like(x); y = torch.empty_like(x)
 with torch.cuda.stream(st):
-    s.bench_op(rho, level, mode, x, b, y, 3)
+    s.bench_op(rho, level, mode, 3)
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(st); s.bench_op(rho, level, mode, x, b, y, 10); e1.record(st)
+    e0.record(st); s.bench_op(rho, level, mode, 10); e1.record(st)
 torch.cuda.synchronize()
 print("us per launch", e0.elapsed_time(e1) / 10 * 1e3, "nodes", N)
