@@ -61,6 +61,8 @@ struct st_ctx {
   MatsDev md{};
   std::vector<Level> lv;
   long long N = 0, Nd = 0, ndesign = 0, ld = 0;   // N: internal (padded) storage, Nd: nodes
+  long long guard = 0;                              // zeroed front guard of internal vectors
+  std::vector<double*> vallocs;                     // guarded allocations (raw bases)
   Geom gd0{};                                      // level-0 geometry in the caller's dense layout
   double *f = nullptr, *b = nullptr, *tmpN = nullptr, *tmpN2 = nullptr, *xint = nullptr;
   double *V = nullptr, *Z = nullptr;
@@ -275,17 +277,28 @@ void setup_forms(st_ctx* c) {
   }
 }
 
+// internal nodal vector: zeroed, with a zeroed front guard of c->guard entries so that the
+// TMA x-tile maps (based pr + 2 entries before the data)
+// only ever see non-negative box coordinates and finite data
+double* vec_alloc(st_ctx* c, long long count) {
+  double* base = nullptr;
+  dzalloc(&base, (size_t)(count + 2 * c->guard));
+  c->vallocs.push_back(base);
+  return base + c->guard;
+}
+
 void allocate(st_ctx* c) {
   const long long N = c->N;
   const int m = c->opt.restart;
-  c->ld = (N + 31) / 32 * 32;
-  dzalloc(&c->f, N);
-  dzalloc(&c->b, N);
-  dzalloc(&c->tmpN, N);
-  dzalloc(&c->tmpN2, N);
-  dzalloc(&c->xint, N);
-  dzalloc(&c->V, (size_t)(m + 1) * c->ld);
-  dzalloc(&c->Z, (size_t)m * c->ld);
+  c->guard = (c->lv[0].g.pr + 2 + 31) / 32 * 32;
+  c->ld = (N + c->guard + 31) / 32 * 32;   // vector j's guard = tail of slot j-1 (never written)
+  c->f = vec_alloc(c, N);
+  c->b = vec_alloc(c, N);
+  c->tmpN = vec_alloc(c, N);
+  c->tmpN2 = vec_alloc(c, N);
+  c->xint = vec_alloc(c, N);
+  c->V = vec_alloc(c, (m + 1) * c->ld);
+  c->Z = vec_alloc(c, m * c->ld);
   dalloc(&c->ws.partial, (size_t)kRedBlocks * 16);
   dalloc(&c->ws.counter, 1);
   CK(cudaMemsetAsync(c->ws.counter, 0, sizeof(unsigned), c->stream));
@@ -295,13 +308,13 @@ void allocate(st_ctx* c) {
     Level& Lv = c->lv[l];
     const long long n = Lv.g.N;
     if (l == 0) {
-      dzalloc(&Lv.r, n);
-      dzalloc(&Lv.t, n);
+      Lv.r = vec_alloc(c, n);
+      Lv.t = vec_alloc(c, n);
     } else {
-      dzalloc(&Lv.x, n);
-      dzalloc(&Lv.b, n);
-      dzalloc(&Lv.r, n);
-      dzalloc(&Lv.t, n);
+      Lv.x = vec_alloc(c, n);
+      Lv.b = vec_alloc(c, n);
+      Lv.r = vec_alloc(c, n);
+      Lv.t = vec_alloc(c, n);
       if (Lv.st_owned) {
         dalloc(&Lv.st, Lv.st_elems);
         Lv.op.st = Lv.st;
@@ -616,11 +629,10 @@ void free_ctx(st_ctx* c) {
   cudaSetDevice(c->device);
   for (auto& Lv : c->lv) {
     if (Lv.st_owned && Lv.st) cudaFree(Lv.st);
-    cudaFree(Lv.x); cudaFree(Lv.b); cudaFree(Lv.r); cudaFree(Lv.t);
     cudaFree(Lv.A); cudaFree(Lv.Ainv); cudaFree(Lv.info);
   }
-  cudaFree(c->f); cudaFree(c->b); cudaFree(c->tmpN); cudaFree(c->tmpN2); cudaFree(c->xint);
-  cudaFree(c->V); cudaFree(c->Z); cudaFree(c->ws.partial); cudaFree(c->ws.counter);
+  for (double* p : c->vallocs) cudaFree(p);
+  cudaFree(c->ws.partial); cudaFree(c->ws.counter);
   cudaFree(c->dsmall);
   if (c->hsmall) cudaFreeHost(c->hsmall);
   cudaFree(c->rho_stage);
@@ -700,6 +712,7 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       if (c->opt.nu_pre < 1 || c->opt.nu_post < 0) throw StErr{ST_E_INVALID_ARG, "nu_pre >= 1, nu_post >= 0"};
       if (c->opt.coarse_max_nodes < 8) c->opt.coarse_max_nodes = 8;
       if (const char* e = getenv("ST_NO_FAST")) g_use_fast = (e[0] == '0');
+      if (const char* e = getenv("ST_FAST_KIND")) g_fast_kind = atoi(e);
       CK(cudaGetDevice(&c->device));
       if (dist && dist->device >= 0) {
         c->device = dist->device;

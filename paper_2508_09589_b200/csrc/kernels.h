@@ -11,7 +11,11 @@ void launch_op(const OpDesc& op, int mode, bool trans, bool mask, const double* 
 // fast2d.cu: specialised (2+1)D kernels; false if the operator form is not covered
 bool launch_op_fast2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                       double omega, cudaStream_t s);
+// tma2d.cu: TMA-streamed (2+1)D kernel (fine level, time-constant MK levels)
+bool launch_op_tma2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
+                     double omega, cudaStream_t s);
 extern bool g_use_fast;
+extern int g_fast_kind;  // 0: TMA, 1: cp.async (fast2d)
 void launch_rap_space(const OpDesc& fop, const Geom& gc, int nl, int ns, double* out, cudaStream_t s);
 void launch_rap_time(const OpDesc& fop, int nlc, double* out, cudaStream_t s);
 void launch_rho_to_mk(const OpDesc& fop, int tau, double* out, cudaStream_t s);

@@ -335,9 +335,11 @@ static void launch_f(const OpDesc& op, int mode, bool trans, bool mask, const do
 }
 
 bool g_use_fast = true;
+int g_fast_kind = 0;
 
 void launch_op(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                double omega, cudaStream_t s) {
+  if (g_use_fast && g_fast_kind == 0 && launch_op_tma2d(op, mode, trans, mask, x, b, y, omega, s)) return;
   if (g_use_fast && launch_op_fast2d(op, mode, trans, mask, x, b, y, omega, s)) return;
   if (op.g.sd == 2) {
     if (op.form == FORM_RHO) launch_f<2, FORM_RHO>(op, mode, trans, mask, x, b, y, omega, s);
