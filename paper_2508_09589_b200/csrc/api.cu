@@ -77,6 +77,8 @@ struct st_ctx {
   st_stats_t stats{};
   long long launches = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  bool fast = true;     // specialised (2+1)D kernels
+  int fast_kind = 0;    // 0: TMA ring, 1: cp.async ring
 };
 
 namespace {
@@ -241,6 +243,10 @@ void setup_forms(st_ctx* c) {
     }
     const Level& Pv = c->lv[l - 1];
     const OpDesc& po = Pv.op;
+    // uniform capacity: every time-constant Galerkin level keeps C_ins x the Q1 mass of its own
+    // grid (nested spaces: P^T M_h P = M_H), applied separably by the lean kernel
+    op.msep = 0;
+    op.msc = 0.0;
     if (Lv.kind == KIND_FULL) throw StErr{ST_E_UNSUPPORTED, "full space-time coarsening not implemented"};
     if (Lv.kind == KIND_SPACE) {
       op.nl = po.nl;
@@ -274,6 +280,10 @@ void setup_forms(st_ctx* c) {
         Lv.st_owned = true;
       }
     }
+    if (op.form == FORM_MK && op.nl == 1 && c->md.dC == 0.0) {
+      op.msep = 1;
+      op.msc = c->md.Cins * Lv.g.dx * Lv.g.dx / 36.0;
+    }
   }
 }
 
@@ -299,7 +309,7 @@ void allocate(st_ctx* c) {
   c->xint = vec_alloc(c, N);
   c->V = vec_alloc(c, (m + 1) * c->ld);
   c->Z = vec_alloc(c, m * c->ld);
-  dalloc(&c->ws.partial, (size_t)kRedBlocks * 16);
+  dalloc(&c->ws.partial, (size_t)kRedBlocks * kMaxDots);
   dalloc(&c->ws.counter, 1);
   CK(cudaMemsetAsync(c->ws.counter, 0, sizeof(unsigned), c->stream));
   dalloc(&c->dsmall, 512);
@@ -333,6 +343,8 @@ void allocate(st_ctx* c) {
 }
 
 void op_launch(st_ctx* c, int l, int mode, bool trans, bool mask, const double* x, const double* b, double* y) {
+  g_use_fast = c->fast;
+  g_fast_kind = c->fast_kind;
   launch_op(c->lv[l].op, mode, trans, mask, x, b, y, c->opt.omega, c->stream);
   L(c);
 }
@@ -452,16 +464,20 @@ void sync_small(st_ctx* c, int off, int n) {
 }
 
 // FGMRES(m), right preconditioned by one V-cycle (Saad 1993). Classical
-// Gram-Schmidt with one conditional re-orthogonalisation (DGKS). Convergence on the TRUE
-// relative residual ||b - A x|| / ||b|| <= rtol (R-14).
+// Gram-Schmidt (fused multi-dot + fused multi-AXPY) with one conditional re-orthogonalisation
+// (DGKS). Convergence on the TRUE relative residual ||b - A x|| / ||b|| <= rtol (R-14).
+// The Arnoldi vectors are stored unnormalised, v_i = sg_i V_i: the V-cycle and the operator are
+// linear, so z_j = sg_j M V_j and A z_j = sg_j A (M V_j), and every scale is folded into the
+// host-side Hessenberg / the device-side AXPY weights (no separate scaling pass over memory).
 int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
   const long long N = c->N;
   const int m = c->opt.restart;
   const double rtol = c->opt.rtol;
   const long long ld = c->ld;
-  double* dh = c->dsmall;        // [0..63] h, [64..127] reorth h, [128..191] y
+  double* dh = c->dsmall;        // [0..63] g, [64..127] reorth g, [128..191] y, [256..319] sg^2
   double* hh = c->hsmall;
-  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), gv(m + 1), y(m);
+  double* ds2 = dh + 256;
+  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), gv(m + 1), y(m), sg(m + 1);
   CK(cudaEventRecord(c->e0, c->stream));
   // ||b||
   launch_mdot(b, nullptr, 0, 0, N, dh + 200, c->ws, c->stream);
@@ -486,8 +502,9 @@ int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
     if (!std::isfinite(beta)) { status = ST_E_BREAKDOWN; break; }
     if (relres <= rtol) { conv = true; break; }
     if (its >= c->opt.maxit) { status = ST_E_NOT_CONVERGED; break; }
-    launch_scale(c->V, c->V, 1.0 / beta, N, c->stream);
-    L(c);
+    sg[0] = 1.0 / beta;
+    hh[256] = sg[0] * sg[0];
+    CK(cudaMemcpyAsync(ds2, hh + 256, sizeof(double), cudaMemcpyHostToDevice, c->stream));
     std::fill(gv.begin(), gv.end(), 0.0);
     gv[0] = beta;
     int jend = 0;
@@ -495,34 +512,35 @@ int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
       double* vj = c->V + (long long)j * ld;
       double* zj = c->Z + (long long)j * ld;
       double* w = c->V + (long long)(j + 1) * ld;
-      vcycle(c, 0, trans, vj, zj);
-      op_launch(c, 0, MODE_APPLY, trans, true, zj, nullptr, w);
-      launch_mdot(w, c->V, ld, j + 1, N, dh, c->ws, c->stream);
-      launch_maxpy_norm(w, c->V, ld, j + 1, dh, N, dh + 196, c->ws, c->stream);
-      L(c, (j + 8) / 8 + 1);
+      vcycle(c, 0, trans, vj, zj);                                       // Z_j = M V_j
+      op_launch(c, 0, MODE_APPLY, trans, true, zj, nullptr, w);         // W = A Z_j
+      launch_mdot(w, c->V, ld, j + 1, N, dh, c->ws, c->stream);          // g_i = V_i . W, ||W||^2
+      launch_maxpy_norm(w, c->V, ld, j + 1, dh, ds2, N, dh + 196, c->ws, c->stream);  // W -= sum sg_i^2 g_i V_i
+      L(c, (j + 16) / 16 + 1);
       check_launch();
       CK(cudaMemcpyAsync(hh, dh, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaMemcpyAsync(hh + 196, dh + 196, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       double* hcol = &H[(size_t)j * (m + 1)];
-      for (int i = 0; i <= j; ++i) hcol[i] = hh[i];
+      for (int i = 0; i <= j; ++i) hcol[i] = sg[i] * sg[j] * hh[i];  // h_ij = v_i . (A z_j)
       double ww = hh[j + 1], w2 = hh[196];
       if (w2 < 0.5 * ww) {  // DGKS re-orthogonalisation
         launch_mdot(w, c->V, ld, j + 1, N, dh + 64, c->ws, c->stream);
-        launch_maxpy_norm(w, c->V, ld, j + 1, dh + 64, N, dh + 196, c->ws, c->stream);
-        L(c, (j + 8) / 8 + 1);
+        launch_maxpy_norm(w, c->V, ld, j + 1, dh + 64, ds2, N, dh + 196, c->ws, c->stream);
+        L(c, (j + 16) / 16 + 1);
         CK(cudaMemcpyAsync(hh + 64, dh + 64, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(hh + 196, dh + 196, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
-        for (int i = 0; i <= j; ++i) hcol[i] += hh[64 + i];
+        for (int i = 0; i <= j; ++i) hcol[i] += sg[i] * sg[j] * hh[64 + i];
         w2 = hh[196];
       }
-      const double hn = std::sqrt(std::max(w2, 0.0));
+      const double hn = sg[j] * std::sqrt(std::max(w2, 0.0));  // ||A z_j - V h||
       hcol[j + 1] = hn;
       ++its;
       if (hn > 0.0) {
-        launch_scale(w, w, 1.0 / hn, N, c->stream);
-        L(c);
+        sg[j + 1] = sg[j] / hn;
+        hh[257 + j] = sg[j + 1] * sg[j + 1];
+        CK(cudaMemcpyAsync(ds2 + j + 1, hh + 257 + j, sizeof(double), cudaMemcpyHostToDevice, c->stream));
       }
       // Givens rotations
       for (int i = 0; i < j; ++i) {
@@ -543,13 +561,13 @@ int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
       if (std::fabs(gv[j + 1]) <= rtol * bnorm || hn == 0.0 || its >= c->opt.maxit) break;
     }
     if (status == ST_E_BREAKDOWN && jend == 0) break;
-    // back substitution H y = g, x += Z y
+    // back substitution H y = g, x += sum_i y_i z_i = sum_i (y_i sg_i) Z_i
     for (int i = jend - 1; i >= 0; --i) {
       double s = gv[i];
       for (int k = i + 1; k < jend; ++k) s -= H[(size_t)k * (m + 1) + i] * y[k];
       y[i] = s / H[(size_t)i * (m + 1) + i];
     }
-    for (int i = 0; i < jend; ++i) hh[128 + i] = y[i];
+    for (int i = 0; i < jend; ++i) hh[128 + i] = y[i] * sg[i];
     CK(cudaMemcpyAsync(dh + 128, hh + 128, jend * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     launch_lincomb(x, c->Z, ld, jend, dh + 128, N, c->stream);
     L(c);
@@ -711,8 +729,12 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       if (c->opt.restart < 1 || c->opt.restart > 60) throw StErr{ST_E_INVALID_ARG, "restart must be in [1, 60]"};
       if (c->opt.nu_pre < 1 || c->opt.nu_post < 0) throw StErr{ST_E_INVALID_ARG, "nu_pre >= 1, nu_post >= 0"};
       if (c->opt.coarse_max_nodes < 8) c->opt.coarse_max_nodes = 8;
-      if (const char* e = getenv("ST_NO_FAST")) g_use_fast = (e[0] == '0');
-      if (const char* e = getenv("ST_FAST_KIND")) g_fast_kind = atoi(e);
+      {  // kernel family (test / bench hook): ST_NO_FAST=1 -> generic kernels; ST_FAST_KIND=1 -> cp.async
+        const char* e = getenv("ST_NO_FAST");
+        c->fast = !(e && e[0] == '1');
+        e = getenv("ST_FAST_KIND");
+        c->fast_kind = e ? atoi(e) : 0;
+      }
       CK(cudaGetDevice(&c->device));
       if (dist && dist->device >= 0) {
         c->device = dist->device;

@@ -31,6 +31,7 @@ struct Geom {
   long long N;   // stored entries (P * (nt+1))
   int plo, phi;  // sink patch: transverse node range at x1 = 0 (plo > phi: none)
   double dx, dt;
+  int pg0;       // global index of local plane 0 (time slabs); 0 on one GPU
 };
 
 struct MatsDev {
@@ -48,6 +49,8 @@ struct OpDesc {
   int rho_tc;             // rho time-constant
   MatsDev m;
   const double* st;       // MK: [nl][2][NC][P]; B4: [nl][5][NC][P] = M, Kbb, Kbt, Ktb, Ktt
+  int msep;               // MK: the stored M equals msc x (Q1 mass pattern of this grid), i.e. the
+  double msc;             //     separable [1,4,1] (x) [1,4,1] stencil (uniform capacity; nested spaces)
 };
 
 template <int SD> struct SG {
@@ -91,7 +94,7 @@ __device__ __forceinline__ double dpowp(double r, double p) {  // d/dr r^p
 
 // constrained node test (R-2, R-4): t = 0 plane, or sink patch at x1 = 0
 template <int SD> __device__ __forceinline__ bool is_cons(const Geom& g, const int* c, int p) {
-  if (p == 0) return true;
+  if (p + g.pg0 == 0) return true;  // initial-condition plane (global t = 0)
   if (c[0] != 0) return false;
   bool in = (c[1] >= g.plo && c[1] <= g.phi);
   if (SD == 3) in = in && (c[2] >= g.plo && c[2] <= g.phi);

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(NTH, CUNI ? ST_CUNI_MINB : 3) op2d_kernel(OpDe
     if (NX) {
       double* dst = xs[slot];
       const double* src = xq;
-      unsigned vm = xval & (MASK ? (q == 0 ? 0u : ~xpatch) : ~0u);
+      unsigned vm = xval & (MASK ? (q + g.pg0 == 0 ? 0u : ~xpatch) : ~0u);
 #pragma unroll
       for (int k = 0; k < XPT; ++k)
         if (k < XPT - 1 || tid + k * NTH < PT) cp_async8(&dst[xsm[k]], src + xoff[k], (vm >> k) & 1u);
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(NTH, CUNI ? ST_CUNI_MINB : 3) op2d_kernel(OpDe
   auto out_row = [&](int p, int slot, int r, double Ax, double od) {
     if (p < p0 || p >= p1 || !act[r]) return;
     const long long gi = (long long)p * P + nodeoff0 + r * pr;
-    const bool cons = MASK && (p == 0 || patchr[r]);
+    const bool cons = MASK && (p + g.pg0 == 0 || patchr[r]);
     double* yo = yrow + r * pr;
     const double bv = NBV ? bs[slot][(ty * RY + r) * TX + tx] : 0.0;
     double o;

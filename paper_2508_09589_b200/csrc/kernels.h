@@ -14,6 +14,9 @@ bool launch_op_fast2d(const OpDesc& op, int mode, bool trans, bool mask, const d
 // tma2d.cu: TMA-streamed (2+1)D kernel (fine level, time-constant MK levels)
 bool launch_op_tma2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                      double omega, cudaStream_t s);
+// tc2d.cu: lean TMA kernel for time-constant levels (fine from rho, stored MK), masked modes
+bool launch_op_tc2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
+                    double omega, cudaStream_t s);
 extern bool g_use_fast;
 extern int g_fast_kind;  // 0: TMA, 1: cp.async (fast2d)
 void launch_rap_space(const OpDesc& fop, const Geom& gc, int nl, int ns, double* out, cudaStream_t s);
@@ -31,13 +34,13 @@ struct RedWs {
   unsigned int* counter;
 };
 constexpr int kRedBlocks = 148 * 6;
-constexpr int kMaxDots = 9;
-// out[0..k-1] = V_j . w (j < k), out[k] = w . w ; k <= 8
+constexpr int kMaxDots = 17;
+// out[0..k-1] = V_j . w (j < k), out[k] = w . w
 void launch_mdot(const double* w, const double* V, long long ldv, int k, long long n, double* out, RedWs ws,
                  cudaStream_t s);
-// w -= sum_j h[j] V_j (h on device); out[0] = ||w||^2 after
-void launch_maxpy_norm(double* w, const double* V, long long ldv, int k, const double* h, long long n,
-                       double* out, RedWs ws, cudaStream_t s);
+// w -= sum_j h[j] s2[j] V_j (h, s2 on device; s2 = null: 1); out[0] = ||w||^2 after
+void launch_maxpy_norm(double* w, const double* V, long long ldv, int k, const double* h, const double* s2,
+                       long long n, double* out, RedWs ws, cudaStream_t s);
 // x += sum_j y[j] Z_j (y on device)
 void launch_lincomb(double* x, const double* Z, long long ldz, int k, const double* y, long long n, cudaStream_t s);
 // v = w / sqrt(nrm2[0]) (nrm2 on device) or v = alpha * w

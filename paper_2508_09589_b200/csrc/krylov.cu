@@ -86,9 +86,10 @@ __global__ void __launch_bounds__(kRedThreads) mdot_kernel(const double* __restr
 
 __global__ void __launch_bounds__(kRedThreads) maxpy_norm_kernel(double* __restrict__ w, const double* __restrict__ V,
                                                                  long long ldv, int k, const double* __restrict__ h,
-                                                                 long long n, double* out, RedWs ws) {
+                                                                 const double* __restrict__ s2, long long n, double* out,
+                                                                 RedWs ws) {
   __shared__ double hs[128];
-  for (int j = threadIdx.x; j < k; j += blockDim.x) hs[j] = h[j];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) hs[j] = s2 ? h[j] * s2[j] : h[j];
   __syncthreads();
   double acc[1] = {0.0};
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -177,12 +178,12 @@ static unsigned red_blocks(long long n) {
 
 void launch_mdot(const double* w, const double* V, long long ldv, int k, long long n, double* out, RedWs ws,
                  cudaStream_t s) {
-  // k dots + ||w||^2 in chunks of <= 8 vectors; the norm rides on the last chunk
+  // k dots + ||w||^2 in chunks of <= 16 vectors; the norm rides on the last chunk
   unsigned g = red_blocks(n);
   int done = 0;
   do {
     int J = k - done;
-    if (J > 8) J = 8;
+    if (J > 16) J = 16;
     bool nrm = (done + J == k);
     const double* Vj = V + (long long)done * ldv;
     double* o = out + done;
@@ -194,15 +195,16 @@ void launch_mdot(const double* w, const double* V, long long ldv, int k, long lo
     switch (J) {
       case 0: mdot_kernel<0, true><<<g, kRedThreads, 0, s>>>(w, Vj, ldv, n, o, ws); break;
       MD(1) MD(2) MD(3) MD(4) MD(5) MD(6) MD(7) MD(8)
+      MD(9) MD(10) MD(11) MD(12) MD(13) MD(14) MD(15) MD(16)
     }
 #undef MD
     done += J;
   } while (done < k);
 }
 
-void launch_maxpy_norm(double* w, const double* V, long long ldv, int k, const double* h, long long n, double* out,
-                       RedWs ws, cudaStream_t s) {
-  maxpy_norm_kernel<<<red_blocks(n), kRedThreads, 0, s>>>(w, V, ldv, k, h, n, out, ws);
+void launch_maxpy_norm(double* w, const double* V, long long ldv, int k, const double* h, const double* s2,
+                       long long n, double* out, RedWs ws, cudaStream_t s) {
+  maxpy_norm_kernel<<<red_blocks(n), kRedThreads, 0, s>>>(w, V, ldv, k, h, s2, n, out, ws);
 }
 
 static unsigned ew_blocks(long long n) {

@@ -25,7 +25,7 @@ __global__ void source_kernel(Geom g, int kind, double qscale, double a, double 
     if (l < 0 || l >= g.nt) continue;
     for (int gp = 0; gp < 2; ++gp) {
       double sg = gp == 0 ? -s : s;
-      double tt = (l + 0.5 + sg) * g.dt;
+      double tt = (l + g.pg0 + 0.5 + sg) * g.dt;  // global time of the Gauss point
       double N = side == 0 ? (0.5 + sg) : (0.5 - sg);
       double Q = qscale * ((kind == 1) ? (1.0 + a * sin(w * tau * tt)) : 1.0);
       ft += 0.5 * g.dt * N * Q;
@@ -59,14 +59,14 @@ template <int SD> __global__ void set_bc_kernel(Geom g, double T0, double* __res
   if (idx >= g.N) return;
   int c[3] = {0, 0, 0}, p;
   if (!node_of<SD>(g, idx, c, p)) return;
-  if (is_cons<SD>(g, c, p)) x[idx] = (p == 0 && !is_patch<SD>(g, c)) ? T0 : 0.0;
+  if (is_cons<SD>(g, c, p)) x[idx] = (p + g.pg0 == 0 && !is_patch<SD>(g, c)) ? T0 : 0.0;
 }
 template <int SD> __global__ void xd_kernel(Geom g, double T0, double* __restrict__ x) {
   long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= g.N) return;
   int c[3] = {0, 0, 0}, p;
   if (!node_of<SD>(g, idx, c, p)) { x[idx] = 0.0; return; }
-  x[idx] = (p == 0 && !is_patch<SD>(g, c)) ? T0 : 0.0;
+  x[idx] = (p + g.pg0 == 0 && !is_patch<SD>(g, c)) ? T0 : 0.0;
 }
 template <int SD>
 __global__ void rhs_kernel(Geom g, const double* __restrict__ f, const double* __restrict__ KxD, double T0,
@@ -75,7 +75,7 @@ __global__ void rhs_kernel(Geom g, const double* __restrict__ f, const double* _
   if (idx >= g.N) return;
   int c[3] = {0, 0, 0}, p;
   if (!node_of<SD>(g, idx, c, p)) { b[idx] = 0.0; return; }
-  if (is_cons<SD>(g, c, p)) b[idx] = (p == 0 && !is_patch<SD>(g, c)) ? T0 : 0.0;
+  if (is_cons<SD>(g, c, p)) b[idx] = (p + g.pg0 == 0 && !is_patch<SD>(g, c)) ? T0 : 0.0;
   else b[idx] = f[idx] - (KxD ? KxD[idx] : 0.0);
 }
 

@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(128) op_kernel(OpDesc op, const double* __rest
       layer_eval<SD, FORM, TRANS, NEEDX, NEEDD>(op, c, pn, p, xb, xt, bot, top, dbot, dtop);
     }
     const long long gi = (long long)p * g.P + pn;
-    const bool cons = MASK && (p == 0 || patch);
+    const bool cons = MASK && (p + g.pg0 == 0 || patch);
     double Ax = carry + bot;
     double D = dcarry + dbot;
     if (cons) {
@@ -339,7 +339,8 @@ int g_fast_kind = 0;
 
 void launch_op(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                double omega, cudaStream_t s) {
-  if (g_use_fast && g_fast_kind == 0 && launch_op_tma2d(op, mode, trans, mask, x, b, y, omega, s)) return;
+  if (g_use_fast && g_fast_kind == 0 && launch_op_tc2d(op, mode, trans, mask, x, b, y, omega, s)) return;
+  if (g_use_fast && (g_fast_kind == 0 || g_fast_kind == 2) && launch_op_tma2d(op, mode, trans, mask, x, b, y, omega, s)) return;
   if (g_use_fast && launch_op_fast2d(op, mode, trans, mask, x, b, y, omega, s)) return;
   if (op.g.sd == 2) {
     if (op.form == FORM_RHO) launch_f<2, FORM_RHO>(op, mode, trans, mask, x, b, y, omega, s);
