@@ -9,7 +9,10 @@ solve to true-residual rtol 1e-8 from T = 0, adjoint solve of the time-integrate
 compliance (dJ/dT = f), element sensitivities. Workload at N = 1: BASELINE config 2
 (configs[1]): (2+1)D 256^2 x 256 elements, 16,974,593 space-time DOFs, time-constant smooth
 design. value = 2 N_n (forward + adjoint DOFs solved) per step time, summed over ranks.
-For N > 1 each rank solves its own replica (time-slab partitioning is not in this build).
+For N > 1 the space-time grid is split into N time slabs (one per GPU, NCCL over NVLink:
+halo planes, Krylov sums, agglomerated coarse levels) and the time extent
+grows with N (weak scaling in time, as BASELINE config 5): 256^2 x 256N elements, tau = N, the
+config-2 design; every rank holds a config-2-sized slab.
 Inputs are resident in HBM before the timed region; L2 is flushed (256 MB write) between
 steps. `e2e` repeats the step through the C ABI with pinned HOST buffers (copies inside).
 `--impl reference` times the CPU oracle (oracle/, SuperLU direct) on a bounded replica.
@@ -41,6 +44,9 @@ WORKLOADS = {
             nt=128, mats=CFG4_MATS, tc=True, design="smooth_tc", source=("uniform", 1.0, 0.0, 0.0), tau=1.0),
     5: dict(name="config5 (per GPU): (2+1)D 512^2x512, space-time design", sdim=2, n=512, nt=512, mats=CFG1_MATS,
             tc=False, design="const", source=("uniform", 1.0, 0.0, 0.0), tau=1.0),
+    3: dict(name="config3-shaped (1/8 of config 3 on one GPU): (2+1)D 512^2x512, an independent smooth field per "
+                 "time layer, Q(t) = 1 + sin(2 pi t)", sdim=2, n=512, nt=512, mats=CFG1_MATS, tc=False,
+            design="smooth_layers", source=("sin", 1.0, 1.0, 6.283185307179586), tau=1.0),
 }
 METRIC = "space-time DOFs solved/sec (FGMRES+MG to rtol 1e-8) & operator GB/s vs HBM peak"
 
@@ -165,15 +171,27 @@ def run_cuda(args):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     stream = torch.cuda.Stream(device=dev)
-    wl = WORKLOADS[args.config]
+    wl = dict(WORKLOADS[args.config])
+    nccl_comm = None
+    if world > 1:  # time slabs over NCCL: the time extent grows with the GPU count
+        wl["nt"] = wl["nt"] * world
+        wl["tau"] = wl["tau"] * world
+        wl["name"] = wl["name"] + f" extended in time to nt={wl['nt']}, tau={wl['tau']:g} (time slabs)"
+        obj = [S.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_comm = S.nccl_comm_init(obj[0], rank, world)
     solver = S.Solver(wl["sdim"], wl["n"], wl["nt"], mats=wl["mats"], source=wl["source"], tau=wl["tau"],
-                      time_constant=wl["tc"], stream=stream.cuda_stream, device=local, rtol=args.rtol, maxit=1000)
-    N = solver.n_nodes
+                      time_constant=wl["tc"], stream=stream.cuda_stream, device=local, rtol=args.rtol, maxit=1000,
+                      rank=rank, size=world, nccl_comm=nccl_comm)
+    N = solver.n_nodes            # this rank's owned nodes
     nd = solver.n_design
+    N_global = (wl["n"] + 1) ** wl["sdim"] * (wl["nt"] + 1)
     nsteps = args.warmup + args.steps
-    rhos = [torch.as_tensor(I.design_for(wl["sdim"], wl["n"], wl["nt"], wl["design"] if wl["design"] != "const"
-                                         else "smooth_layers", seed=1000 * rank + s), device=dev).contiguous()
-            for s in range(nsteps)] if wl["design"] != "const" else \
+    # time-constant designs are replicated on every rank (same seed); the config-5 design is uniform
+    lay = solver.layout()
+    sl = slice(None) if wl["tc"] else slice(lay["layer0"], lay["layer0"] + lay["rho_layers"])  # this rank's layers
+    rhos = [torch.as_tensor(np.ascontiguousarray(I.design_for(wl["sdim"], wl["n"], wl["nt"], wl["design"], seed=s)[sl]),
+                            device=dev) for s in range(nsteps)] if wl["design"] != "const" else \
         [torch.full((nd,), 0.4 + 0.01 * s, dtype=torch.float64, device=dev) for s in range(nsteps)]
     T = torch.zeros(N, dtype=torch.float64, device=dev)
     lam = torch.zeros_like(T)
@@ -224,7 +242,7 @@ def run_cuda(args):
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = 2.0 * N * world / (ms / 1e3)
+    value = 2.0 * N_global / (ms / 1e3)
 
     # ---- dominant kernel: fine-level damped-Jacobi sweep (live CUDA-event timing) ---------
     reps = 20
@@ -275,7 +293,7 @@ def run_cuda(args):
             ems = float(t.item())
         h2d = 3 * 8 * nd + 8 * N * 5          # rho x3; T in (solve, sens); g; lambda in (adjoint, sens)
         d2h = 8 * N * 2 + 8 * nd              # T, lambda, dJ
-        e2e = {"value": 2.0 * N * world / (ems / 1e3), "unit": "DOF/s", "ms_per_step": ems,
+        e2e = {"value": 2.0 * N_global / (ems / 1e3), "unit": "DOF/s", "ms_per_step": ems,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only) ----------------------------------------------
@@ -297,11 +315,14 @@ def run_cuda(args):
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded smooth random designs, st_inputs)",
-        "config": {"workload": wl["name"], "dofs": N, "design_vars": nd, "rtol": args.rtol,
-                   "step": "rho setup + forward solve + adjoint solve + sensitivities",
-                   "parallelism": "replicas" if world > 1 else "1 GPU", "l2": "flushed (256 MB write) between steps"},
+        "config": {"workload": wl["name"], "dofs": N_global, "dofs_per_rank": N, "design_vars": nd,
+                   "rtol": args.rtol, "step": "rho setup + forward solve + adjoint solve + sensitivities",
+                   "parallelism": f"{world} time slabs (NCCL)" if world > 1 else "1 GPU",
+                   "l2": "flushed (256 MB write) between steps"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "fine-level damped-Jacobi sweep (op2d_kernel, time-constant rho)",
+                     "traffic": traffic, "kernel": "fine-level damped-Jacobi sweep (" + ("tc2d_kernel, time-constant rho" if wl["tc"] and wl["sdim"] == 2
+                                                              else "tma2d_kernel, space-time rho" if wl["sdim"] == 2
+                                                              else "op_kernel<3>, (3+1)D") + ")",
                      "bytes_per_launch": alg_bytes, "us_per_launch": t_sweep * 1e6,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,

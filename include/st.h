@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define ST_ABI_VERSION 1
+#define ST_ABI_VERSION 2
 
 enum {
   ST_OK = 0,
@@ -94,12 +94,57 @@ typedef struct {
   int64_t coarse_max_nodes; /* stop coarsening at <= this many nodes (R-19)     */
   int32_t max_levels;       /* 0 = unlimited                                             */
   int32_t full_coarsening;  /* 1 = coarsen space and time together    */
-  int32_t use_graphs;       /* capture the V-cycle in a CUDA graph                        */
+  int32_t use_graphs;       /* 1 (default): the small replicated levels of the V-cycle (< 2^19
+                               nodes) run as one CUDA graph launch per cycle                */
   int32_t verbose;
+  int64_t agg_nodes;        /* time slabs: agglomerate a level once it has fewer than this
+                               many nodes per rank (default 16384)                          */
 } st_options_t;
 
-/* Distribution (time slabs). NULL or size == 1 => one GPU. */
-typedef struct { void* nccl_comm; int32_t rank, size; void* cuda_stream; int32_t device; } st_dist_t;
+/* Distribution over time slabs. NULL or size == 1 => one GPU.
+ * Rank r owns element layers [r nt/G, (r+1) nt/G) and node planes (r nt/G, (r+1) nt/G]
+ * (rank 0 also plane 0); nt must be divisible by G. Every level of the multigrid hierarchy whose
+ * time extent still divides into G slabs stays distributed; the coarser levels are gathered
+ * onto every rank and solved redundantly (agglomeration).
+ * Transports: ST_COMM_NCCL — nccl_comm is an ncclComm_t of `size` ranks (one GPU each; see
+ * st_nccl_unique_id / st_nccl_comm_init); halo planes with grouped ncclSend/ncclRecv, Krylov
+ * sums with ncclAllReduce, agglomeration with ncclAllGather, all on cuda_stream.
+ * ST_COMM_HOST — the caller's host callbacks (below) move pinned host buffers; any number of
+ * ranks may share one GPU (used by the tests). Callbacks return 0 on success. */
+enum { ST_COMM_NONE = 0, ST_COMM_NCCL = 1, ST_COMM_HOST = 2 };
+#define ST_NCCL_ID_BYTES 128
+typedef struct {
+  void* user;
+  /* exchange `count` doubles with `peer`: send `send`, receive into `recv` (host memory) */
+  int (*sendrecv)(void* user, int32_t peer, const double* send, double* recv, int64_t count);
+  /* in-place elementwise sum over all ranks of `count` doubles (host memory) */
+  int (*allreduce_sum)(void* user, double* buf, int64_t count);
+  /* recv[size * count] = concatenation over ranks (in rank order) of send[count] */
+  int (*allgather)(void* user, const double* send, double* recv, int64_t count);
+} st_host_comm_t;
+typedef struct {
+  void* nccl_comm;
+  int32_t rank, size;
+  void* cuda_stream;
+  int32_t device;
+  int32_t transport;          /* ST_COMM_* (size > 1)                                        */
+  st_host_comm_t host;        /* ST_COMM_HOST                                                 */
+} st_dist_t;
+
+/* Local slab of this rank (caller vector layout). T, lambda, dJdT: the owned node planes
+ * [plane0, plane0 + n_planes), dense, x1 fastest. rho (space-time design): element layers
+ * [layer0, layer0 + rho_layers) = the owned layers plus, except on the last rank, the first
+ * layer of the next slab (its ghost); dJ: the owned layers [layer0, layer0 + n_layers).
+ * Time-constant design: rho and dJ are the full spatial field on every rank (dJ summed over
+ * all ranks' layers). */
+typedef struct {
+  int32_t rank, size;
+  int64_t plane0, n_planes;
+  int64_t layer0, n_layers, rho_layers;
+  int64_t nodes_local;        /* n_planes (n+1)^sdim                                         */
+  int64_t design_local;       /* entries of rho this rank passes                             */
+  int32_t n_levels, n_dist_levels;
+} st_layout_t;
 
 typedef struct st_ctx st_ctx_t;
 
@@ -120,8 +165,8 @@ typedef struct {
   int64_t nodes[32];
 } st_hierarchy_t;
 
-/* Fill `o` with the library defaults (rtol 1e-8, restart 30, Jacobi nu 2/2 omega 0.6,
- * lambda_crit 0.5, coarse_max_nodes 400). */
+/* Fill `o` with the library defaults (rtol 1e-8, restart 16, Jacobi nu 3/3 omega 0.75,
+ * lambda_crit 0.5, coarse_max_nodes 400, agg_nodes 16384). */
 void st_default_options(st_options_t* o);
 
 /* Validate, run Algorithm 1, allocate all workspaces, assemble f on the device.
@@ -165,6 +210,29 @@ int st_level_apply(st_ctx_t* ctx, const double* rho, int level, const double* x,
 int st_bench_op(st_ctx_t* ctx, const double* rho, int level, int mode, int transpose, int reps);
 
 int st_get_stats(const st_ctx_t* ctx, st_stats_t* s);
+int st_local_layout(const st_ctx_t* ctx, st_layout_t* layout);
+
+/* Host-only planning (no device call): the Algorithm-1 hierarchy and this rank's slab of every
+ * level for a given rank / size, exactly as st_setup would build them. */
+typedef struct {
+  int32_t n_levels, n_dist_levels;
+  int64_t n[32], nt[32];            /* global elements per level                              */
+  int32_t kind[32];                 /* 0 fine, 1 space, 2 time                                */
+  int32_t dist[32];                 /* 1: time slab, 0: replicated on every rank              */
+  int64_t layer0[32], n_layers[32]; /* owned element layers of a slab level (replicated: all) */
+  int64_t local_layers[32];         /* layers held locally (owned + ghost layer)              */
+  int64_t plane0, n_planes;         /* owned fine node planes (the caller's vector layout)    */
+} st_plan_t;
+int st_plan(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* bcs, const st_options_t* opts,
+            int32_t rank, int32_t size, st_plan_t* plan);
+/* sizeof of the ABI structs (binding self-check): grid, materials, bcs, source, options, dist,
+ * stats, hierarchy, layout, plan */
+int st_struct_sizes(int64_t out[10]);
+/* NCCL helpers (libnccl.so.2 is opened at run time): a unique id on one rank, broadcast by
+ * the caller, then one communicator per rank. Return ST_OK or ST_E_NCCL. */
+int st_nccl_unique_id(char id[ST_NCCL_ID_BYTES]);
+int st_nccl_comm_init(const char id[ST_NCCL_ID_BYTES], int32_t rank, int32_t size, void** comm);
+int st_nccl_comm_destroy(void* comm);
 int st_get_hierarchy(const st_ctx_t* ctx, st_hierarchy_t* h);
 int64_t st_num_nodes(const st_ctx_t* ctx);
 int64_t st_num_design(const st_ctx_t* ctx);

@@ -20,7 +20,7 @@ __all__ = [
     "Mesh", "Materials", "BCs", "Source", "Problem",
     "element_matrices", "element_parts", "connectivity", "simp",
     "assemble_K", "source_vector", "dirichlet", "apply_dirichlet",
-    "pnorm_objective", "diffusion_timescale",
+    "pnorm_objective", "diffusion_timescale", "row_apply", "sensitivity_elements",
 ]
 
 
@@ -447,3 +447,86 @@ class Problem:
             dJ = dJ.reshape(self.mesh.nt, -1).sum(axis=0)
             return dJ.reshape((self.mesh.n,) * self.mesh.sdim)
         return dJ.reshape((self.mesh.nt,) + (self.mesh.n,) * self.mesh.sdim)
+
+
+# --------------------------------------------------------------------------------------
+# Sampled evaluation for full-size certification (R-21): the same element matrices,
+# summed element by element for a few rows / elements only (no global assembly).
+# --------------------------------------------------------------------------------------
+def _node_coords(mesh: Mesh, node):
+    nn = mesh.n + 1
+    c = []
+    for _ in range(mesh.sdim):
+        c.append(node % nn)
+        node //= nn
+    c.append(node)  # time plane
+    return c
+
+
+def row_apply(prob: "Problem", rho, x, nodes, transpose=False):
+    """(K_bc x)[nodes] (or (K_bc^T x)[nodes]) for the eliminated all-at-once matrix
+    (R-1), summing A_e = C_e G + k~_e Kx (element_matrices, quadrature) over
+    the elements adjacent to each node. x is the full nodal vector."""
+    mesh = prob.mesh
+    C, k, _, _, tc = prob.coefficients(rho)
+    G, Kx = element_matrices(mesh.sdim, mesh.dx, mesh.dt)
+    cons, _ = prob.constraints()
+    nd = mesh.sdim + 1
+    nloc = 2 ** nd
+    nn = mesh.n + 1
+    strides = [nn ** d for d in range(mesh.sdim)] + [nn ** mesh.sdim]
+    ecount = [mesh.n] * mesh.sdim + [mesh.nt]
+    x = np.asarray(x)
+    out = np.zeros(len(nodes))
+    for s, node in enumerate(nodes):
+        node = int(node)
+        if cons[node]:
+            out[s] = x[node]
+            continue
+        cc = _node_coords(mesh, node)
+        acc = 0.0
+        for a in range(nloc):  # the node is local corner a of the element at cc - bits(a)
+            e = [cc[d] - ((a >> d) & 1) for d in range(nd)]
+            if any(e[d] < 0 or e[d] >= ecount[d] for d in range(nd)):
+                continue
+            eidx = 0
+            mul = 1
+            for d in range(nd):
+                eidx += e[d] * mul
+                mul *= mesh.n if d < mesh.sdim else 1
+            Ae = C[eidx] * G + k[eidx] * Kx
+            for b in range(nloc):
+                gb = sum((e[d] + ((b >> d) & 1)) * strides[d] for d in range(nd))
+                if cons[gb]:
+                    continue
+                acc += (Ae[b, a] if transpose else Ae[a, b]) * x[gb]
+        out[s] = acc
+    return out
+
+
+def sensitivity_elements(prob: "Problem", rho, T, lam, elems):
+    """dphi/drho_e (R-9) of the space-time elements `elems` (index
+    e1 + n (e2 + ... + n tau)), full T and lambda = 0 on constrained nodes."""
+    mesh = prob.mesh
+    _, _, dC, dk, _ = prob.coefficients(rho)
+    G, Kx = element_matrices(mesh.sdim, mesh.dx, mesh.dt)
+    cons, _ = prob.constraints()
+    nd = mesh.sdim + 1
+    nloc = 2 ** nd
+    nn = mesh.n + 1
+    strides = [nn ** d for d in range(mesh.sdim)] + [nn ** mesh.sdim]
+    T = np.asarray(T)
+    lam = np.where(cons, 0.0, np.asarray(lam))
+    out = np.zeros(len(elems))
+    for s, e in enumerate(elems):
+        e = int(e)
+        ec = []
+        r = e
+        for d in range(mesh.sdim):
+            ec.append(r % mesh.n)
+            r //= mesh.n
+        ec.append(r)
+        idx = [sum((ec[d] + ((a >> d) & 1)) * strides[d] for d in range(nd)) for a in range(nloc)]
+        Te, Le = T[idx], lam[idx]
+        out[s] = -(dC[e] * (Le @ G @ Te) + dk[e] * (Le @ Kx @ Te))
+    return out

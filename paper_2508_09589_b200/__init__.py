@@ -5,6 +5,7 @@ include/st.h; `paper_2508_09589_b200.st` is a thin ctypes binding (argument mars
 only). There is no CPU fallback: importing the binding without the built library raises.
 """
 from .st import (  # noqa: F401
-    Grid, Materials, BCs, Source, Options, Solver, StError, load_library,
-    ST_TIME_CONSTANT, ST_SPACE_TIME, ST_SRC_UNIFORM, ST_SRC_SIN,
+    Grid, Materials, BCs, Source, Options, Solver, StError, load_library, TorchHostComm,
+    nccl_unique_id, nccl_comm_init,
+    ST_TIME_CONSTANT, ST_SPACE_TIME, ST_SRC_UNIFORM, ST_SRC_SIN, ST_COMM_NONE, ST_COMM_NCCL, ST_COMM_HOST,
 )

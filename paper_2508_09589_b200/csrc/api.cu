@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "st.h"
+#include "comm.h"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -34,7 +35,7 @@ struct StErr {
   } while (0)
 
 struct Level {
-  Geom g{};
+  Geom g{};              // local geometry: a time slab (dist) or the whole level (replicated)
   int kind = KIND_FINE;
   OpDesc op{};
   double* st = nullptr;  // owned stencil storage (null if shared / RHO)
@@ -44,6 +45,15 @@ struct Level {
   bool dense = false;
   double *A = nullptr, *Ainv = nullptr;
   int* info = nullptr;
+  // time slabs
+  int ntg = 0;           // global element layers of the level
+  bool dist = false;     // distributed in time slabs (else replicated on every rank)
+  int nloc = 0, a = 0;   // dist: owned element layers [a, a + nloc) = node planes (a, a + nloc]
+  bool gather_in = false;  // first replicated level below a distributed one
+  Geom gs{};             // gather_in: this level in slab form (restriction / stencils before gather)
+  double* bpart = nullptr;
+  double* stpart = nullptr;
+  long long stpart_elems = 0;
 };
 }  // namespace
 
@@ -79,6 +89,18 @@ struct st_ctx {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   bool fast = true;     // specialised (2+1)D kernels
   int fast_kind = 0;    // 0: TMA ring, 1: cp.async ring
+  // time slabs: rank, owned fine planes [o0, o0 + nown) of the local vector (o0 = 0 on rank 0,
+  // else 1: local plane 0 is the ghost copy of the previous rank's last plane)
+  Comm comm;
+  int o0 = 0, nown = 0;
+  long long voff = 0, Nown = 0;   // owned range of an internal fine vector (offset, count)
+  int n_dist = 0;                 // distributed levels
+  // CUDA graphs of the small-level part of the V-cycle (levels >= gl0, replicated and fixed
+  // buffers): one per direction, captured after one eager run, valid for the context lifetime
+  int gl0 = -1;
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  long long gkernels[2] = {0, 0};
+  int geager[2] = {0, 0};
 };
 
 namespace {
@@ -99,8 +121,10 @@ void dzalloc(double** p, size_t count) {
   CK(cudaMemset(*p, 0, std::max<size_t>(count, 1) * sizeof(double)));
 }
 
-// pad = true: internal layout with an even x1 row pitch (16-byte aligned rows and planes)
-Geom make_geom(int sd, int n, int nt, int plo, int phi, bool pad = true) {
+// pad = true: internal layout with an even x1 row pitch (16-byte aligned rows and planes).
+// nt: local element layers; ntg (> 0): global layers of the level (dt = 1/ntg), pg0: global
+// index of local plane 0.
+Geom make_geom(int sd, int n, int nt, int plo, int phi, bool pad = true, int ntg = 0, int pg0 = 0) {
   Geom g{};
   g.sd = sd;
   g.n = n;
@@ -113,7 +137,8 @@ Geom make_geom(int sd, int n, int nt, int plo, int phi, bool pad = true) {
   g.plo = plo;
   g.phi = phi;
   g.dx = 1.0 / n;
-  g.dt = 1.0 / nt;
+  g.dt = 1.0 / (ntg > 0 ? ntg : nt);
+  g.pg0 = pg0;
   return g;
 }
 
@@ -123,7 +148,9 @@ long long nodes_of(const Geom& g) {
   for (int d = 0; d < g.sd; ++d) v *= g.nn;
   return v;
 }
-Geom dense_of(const Geom& g) { return make_geom(g.sd, g.n, g.nt, g.plo, g.phi, false); }
+Geom dense_of(const Geom& g) {
+  return make_geom(g.sd, g.n, g.nt, g.plo, g.phi, false, (int)std::lround(1.0 / g.dt), g.pg0);
+}
 
 // E' = W0^T E W0 + W1^T E W1 (linear-in-time prolongation, two fine layers per coarse layer)
 void time_coarsen_factor(const double E[2][2], double out[2][2]) {
@@ -223,6 +250,42 @@ void build_hierarchy(st_ctx* c) {
   if (c->lv.back().g.N > 8192)
     throw StErr{ST_E_DIVISIBILITY, "coarsest level too large for the dense solve (" +
                                        std::to_string(c->lv.back().g.N) + " nodes): grid not divisible enough"};
+  for (auto& Lv : c->lv) Lv.ntg = Lv.g.nt;
+}
+
+// Time slabs: the leading levels whose time extent splits into G equal
+// slabs (and that still have >= agg_nodes nodes per rank) are distributed; the next level is
+// gathered onto every rank (it must split too: it is produced in slab form, then gathered) and
+// every coarser level, including the dense coarsest one, is replicated.
+void assign_slabs(st_ctx* c) {
+  const int G = c->comm.size, r = c->comm.rank;
+  const int nl = (int)c->lv.size();
+  int nd = 0;
+  if (G > 1) {
+    auto splits = [&](int l) { return c->lv[l].ntg % G == 0 && c->lv[l].ntg / G >= 1; };
+    auto big = [&](int l) { return nodes_of(c->lv[l].g) / G >= c->opt.agg_nodes; };
+    nd = 1;  // the fine level is always distributed (validated in st_setup)
+    while (nd < nl - 1 && splits(nd) && big(nd)) ++nd;
+    // the first replicated level must split too (slab-form restriction before the gather)
+    while (nd > 1 && nd < nl && !splits(nd)) --nd;
+    if (nd < nl && !splits(nd)) throw StErr{ST_E_DIVISIBILITY, "time slabs: level 1 does not split over the ranks"};
+  }
+  c->n_dist = nd;
+  for (int l = 0; l < nl; ++l) {
+    Level& Lv = c->lv[l];
+    const Geom g = Lv.g;  // global geometry
+    if (l < nd) {
+      Lv.dist = true;
+      Lv.nloc = Lv.ntg / G;
+      Lv.a = r * Lv.nloc;
+      const int ntl = Lv.nloc + (r < G - 1 ? 1 : 0);  // + ghost layer (except the last rank)
+      Lv.g = make_geom(g.sd, g.n, ntl, g.plo, g.phi, true, Lv.ntg, Lv.a);
+    } else if (l == nd && nd > 0) {
+      Lv.gather_in = true;
+      const int nlc = Lv.ntg / G, ac = r * nlc;
+      Lv.gs = make_geom(g.sd, g.n, nlc + (r < G - 1 ? 1 : 0), g.plo, g.phi, true, Lv.ntg, ac);
+    }
+  }
 }
 
 void setup_forms(st_ctx* c) {
@@ -235,6 +298,7 @@ void setup_forms(st_ctx* c) {
     if (l == 0) {
       op.form = FORM_RHO;
       op.nl = c->tc ? 1 : Lv.g.nt;
+      op.tvl = c->tc ? 0 : 1;
       op.rho_tc = c->tc ? 1 : 0;
       op.U[0][0] = 0.0; op.U[0][1] = 0.0; op.U[1][0] = -1.0; op.U[1][1] = 1.0;
       double s = Lv.g.dt / 6.0;
@@ -247,40 +311,41 @@ void setup_forms(st_ctx* c) {
     // grid (nested spaces: P^T M_h P = M_H), applied separably by the lean kernel
     op.msep = 0;
     op.msc = 0.0;
+    // stored layers: 1 (time-constant design) or every local layer of the level
+    const bool tv = po.tvl != 0;  // explicit: a slab of a time-varying level may hold one layer
+    op.tvl = tv ? 1 : 0;
     if (Lv.kind == KIND_FULL) throw StErr{ST_E_UNSUPPORTED, "full space-time coarsening not implemented"};
+    int ns = 2;
     if (Lv.kind == KIND_SPACE) {
-      op.nl = po.nl;
+      op.nl = tv ? Lv.g.nt : 1;
+      memcpy(op.U, po.U, sizeof(op.U));
       if (po.form == FORM_RHO || po.form == FORM_MK) {
         op.form = FORM_MK;
-        memcpy(op.U, po.U, sizeof(op.U));
         memcpy(op.Tm, po.Tm, sizeof(op.Tm));
-        Lv.st_elems = (long long)op.nl * 2 * NC * Lv.g.P;
+        ns = 2;
       } else {
         op.form = FORM_B4;
-        memcpy(op.U, po.U, sizeof(op.U));
-        Lv.st_elems = (long long)op.nl * 5 * NC * Lv.g.P;
+        ns = 5;
       }
       Lv.st_owned = true;
     } else {  // KIND_TIME: Galerkin conduction, re-stabilised (upwind) capacity in time
       op.U[0][0] = 0.0; op.U[0][1] = 0.0; op.U[1][0] = -1.0; op.U[1][1] = 1.0;
-      if (po.nl == 1) {
+      if (!tv) {
         op.form = FORM_MK;
         op.nl = 1;
         time_coarsen_factor(po.Tm, op.Tm);
-        if (po.form == FORM_RHO) {
-          Lv.st_elems = 2LL * NC * Lv.g.P;
-          Lv.st_owned = true;
-        } else {
-          Lv.st_owned = false;  // same spatial stencils as the finer level
-        }
+        Lv.st_owned = (po.form == FORM_RHO);  // else: the same spatial stencils as the finer level
+        ns = 2;
       } else {
         op.form = FORM_B4;
-        op.nl = po.nl / 2;
-        Lv.st_elems = (long long)op.nl * 5 * NC * Lv.g.P;
+        op.nl = Lv.g.nt;
         Lv.st_owned = true;
+        ns = 5;
       }
     }
-    if (op.form == FORM_MK && op.nl == 1 && c->md.dC == 0.0) {
+    Lv.st_elems = Lv.st_owned ? (long long)op.nl * ns * NC * Lv.g.P : 0;
+    if (Lv.gather_in && tv) Lv.stpart_elems = (long long)Lv.gs.nt * ns * NC * Lv.gs.P;
+    if (op.form == FORM_MK && !tv && c->md.dC == 0.0) {
       op.msep = 1;
       op.msc = c->md.Cins * Lv.g.dx * Lv.g.dx / 36.0;
     }
@@ -331,6 +396,10 @@ void allocate(st_ctx* c) {
       } else {
         Lv.op.st = c->lv[l - 1].op.st;  // resolved again after build (shared)
       }
+      if (Lv.gather_in) {
+        Lv.bpart = vec_alloc(c, Lv.gs.N);
+        if (Lv.stpart_elems > 0) dalloc(&Lv.stpart, Lv.stpart_elems);
+      }
     }
   }
   Level& Lc = c->lv.back();
@@ -340,6 +409,14 @@ void allocate(st_ctx* c) {
   dalloc(&Lc.info, 1);
   CK(cudaEventCreate(&c->e0));
   CK(cudaEventCreate(&c->e1));
+  c->gl0 = -1;
+  for (size_t l = 1; l + 1 < c->lv.size(); ++l) {
+    const Level& Lv = c->lv[l];
+    if (!Lv.dist && nodes_of(Lv.g) < (1LL << 19)) {
+      c->gl0 = (int)l;
+      break;
+    }
+  }
 }
 
 void op_launch(st_ctx* c, int l, int mode, bool trans, bool mask, const double* x, const double* b, double* y) {
@@ -347,6 +424,32 @@ void op_launch(st_ctx* c, int l, int mode, bool trans, bool mask, const double* 
   g_fast_kind = c->fast_kind;
   launch_op(c->lv[l].op, mode, trans, mask, x, b, y, c->opt.omega, c->stream);
   L(c);
+}
+
+// ---- time-slab communication -------------------------------------------
+template <class F> void comm_call(F&& f) {
+  try {
+    f();
+  } catch (const CommError& e) {
+    throw StErr{ST_E_NCCL, e.msg};
+  }
+}
+// refresh the two ghost planes of a vector of distributed level l
+void halo(st_ctx* c, int l, double* v) {
+  const Level& Lv = c->lv[l];
+  if (!Lv.dist || c->comm.size <= 1) return;
+  const long long P = Lv.g.P;
+  comm_call([&] { comm_halo(c->comm, v + P, v, v + (long long)Lv.nloc * P, v + (long long)(Lv.nloc + 1) * P, P, c->stream); });
+}
+void allreduce(st_ctx* c, double* d, long long n) {
+  if (c->comm.size <= 1) return;
+  comm_call([&] { comm_allreduce(c->comm, d, n, c->stream); });
+}
+// owned planes 1..nlc of a slab-form vector of level Nx -> planes 1..ntg of its replicated copy
+void gather_planes(st_ctx* c, const Level& Nx, const double* part, double* full) {
+  const int nlc = Nx.ntg / c->comm.size;
+  const long long P = Nx.g.P;
+  comm_call([&] { comm_allgather(c->comm, part + P, full + P, (long long)nlc * P, c->stream); });
 }
 
 // rho -> level-0 operator pointer; returns true if rho changed since the last full setup
@@ -359,6 +462,7 @@ bool bind_rho(st_ctx* c, const double* rho_in) {
   c->lv[0].op.rho = rho;
   launch_checksum(rho, c->ndesign, c->dsmall + 500, c->ws, c->stream);
   L(c);
+  allreduce(c, c->dsmall + 500, 2);  // one decision on every rank
   CK(cudaMemcpyAsync(c->hsmall + 500, c->dsmall + 500, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   bool changed = !(c->have_ops && c->hsmall[500] == c->rho_ck[0] && c->hsmall[501] == c->rho_ck[1]);
@@ -371,20 +475,41 @@ bool bind_rho(st_ctx* c, const double* rho_in) {
 // eliminated right-hand side b.
 void build_ops(st_ctx* c) {
   CK(cudaEventRecord(c->e0, c->stream));
+  const int NC = nc_of(c->sd);
   for (size_t l = 1; l < c->lv.size(); ++l) {
     Level& Lv = c->lv[l];
     const Level& Pv = c->lv[l - 1];
+    const int ns = Lv.op.form == FORM_B4 ? 5 : 2;
+    const bool tv = Lv.op.tvl != 0;
+    const long long layer = (long long)ns * NC * Lv.g.P;  // stencil doubles per layer
     if (Lv.kind == KIND_SPACE) {
-      launch_rap_space(Pv.op, Lv.g, Lv.op.nl, Lv.op.form == FORM_MK ? 2 : 5, Lv.st, c->stream);
-      L(c);
+      if (Lv.gather_in && tv) {  // slab form, then gather the owned layers
+        launch_rap_space(Pv.op, Lv.gs, Lv.gs.nt, ns, Lv.stpart, c->stream);
+        L(c);
+        comm_call([&] { comm_allgather(c->comm, Lv.stpart, Lv.st, (long long)(Lv.ntg / c->comm.size) * layer, c->stream); });
+      } else {
+        launch_rap_space(Pv.op, Lv.g, Lv.op.nl, ns, Lv.st, c->stream);
+        L(c);
+      }
     } else if (Lv.kind == KIND_TIME) {
-      if (Pv.op.nl == 1) {
+      if (!tv) {
         if (Pv.op.form == FORM_RHO) {
           launch_rho_to_mk(Pv.op, 0, Lv.st, c->stream);
           L(c);
         } else {
           Lv.op.st = Pv.op.st;
         }
+      } else if (Lv.gather_in) {
+        const int nlc = Lv.ntg / c->comm.size;
+        launch_rap_time(Pv.op, nlc, Lv.stpart, c->stream);
+        L(c);
+        comm_call([&] { comm_allgather(c->comm, Lv.stpart, Lv.st, (long long)nlc * layer, c->stream); });
+      } else if (Lv.dist) {
+        // owned coarse layers from owned fine layer pairs; the ghost layer (first layer of the
+        // next slab) comes from the next rank
+        launch_rap_time(Pv.op, Lv.nloc, Lv.st, c->stream);
+        L(c);
+        comm_call([&] { comm_shift_down(c->comm, Lv.st, Lv.st + (long long)Lv.nloc * layer, layer, c->stream); });
       } else {
         launch_rap_time(Pv.op, Lv.op.nl, Lv.st, c->stream);
         L(c);
@@ -429,7 +554,33 @@ void prepare(st_ctx* c, const double* rho) {
 // ---------------------------------------------------------------------------------------
 // V-cycle: damped-Jacobi pre-smoothing from zero, residual,
 // restriction, recursion, prolongation + correction, post-smoothing; coarsest: exact.
-void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x) {
+void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_graph = false);
+
+// levels >= gl0 as one CUDA graph launch (launch latency dominates there)
+bool vcycle_graph(st_ctx* c, int l, bool trans, const double* b, double* x) {
+  if (!c->opt.use_graphs || l != c->gl0 || c->gl0 < 0) return false;
+  Level& Lv = c->lv[l];
+  if (b != Lv.b || x != Lv.x) return false;
+  const int d = trans ? 1 : 0;
+  if (!c->gexec[d]) {
+    if (c->geager[d]++ < 1) return false;  // first run eager: kernel attributes / occupancy cached
+    cudaGraph_t graph = nullptr;
+    const long long l0 = c->launches;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+    vcycle(c, l, trans, b, x, true);
+    CK(cudaStreamEndCapture(c->stream, &graph));
+    c->gkernels[d] = c->launches - l0;
+    c->launches = l0;
+    CK(cudaGraphInstantiate(&c->gexec[d], graph, 0));
+    cudaGraphDestroy(graph);
+  }
+  CK(cudaGraphLaunch(c->gexec[d], c->stream));
+  L(c, c->gkernels[d]);
+  return true;
+}
+
+void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_graph) {
+  if (!in_graph && vcycle_graph(c, l, trans, b, x)) return;
   Level& Lv = c->lv[l];
   if (Lv.dense) {
     launch_dense_solve(Lv.Ainv, (int)Lv.g.N, trans, b, x, c->stream);
@@ -442,18 +593,29 @@ void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x) {
   double* cur = (total % 2 == 1) ? x : Lv.t;
   double* oth = (cur == x) ? Lv.t : x;
   op_launch(c, l, MODE_JAC0, trans, true, nullptr, b, cur);
+  halo(c, l, cur);
   for (int s = 1; s < npre; ++s) {
     op_launch(c, l, MODE_JAC, trans, true, cur, b, oth);
+    halo(c, l, oth);
     std::swap(cur, oth);
   }
   op_launch(c, l, MODE_RESID, trans, true, cur, b, Lv.r);
-  launch_restrict(Lv.g, Nx.g, Nx.kind, Lv.r, Nx.b, c->stream);
-  L(c);
-  vcycle(c, l + 1, trans, Nx.b, Nx.x);
+  if (Nx.kind == KIND_TIME) halo(c, l, Lv.r);  // time restriction reads the next slab's first plane
+  if (Nx.gather_in) {  // agglomeration: restrict in slab form, gather onto every rank
+    launch_restrict(Lv.g, Nx.gs, Nx.kind, Lv.r, Nx.bpart, c->stream);
+    L(c);
+    gather_planes(c, Nx, Nx.bpart, Nx.b);
+  } else {
+    launch_restrict(Lv.g, Nx.g, Nx.kind, Lv.r, Nx.b, c->stream);
+    L(c);
+  }
+  vcycle(c, l + 1, trans, Nx.b, Nx.x, in_graph);
   launch_prolong_add(Lv.g, Nx.g, Nx.kind, Nx.x, cur, c->stream);
   L(c);
+  if (npost == 0) halo(c, l, cur);
   for (int s = 0; s < npost; ++s) {
     op_launch(c, l, MODE_JAC, trans, true, cur, b, oth);
+    halo(c, l, oth);
     std::swap(cur, oth);
   }
 }
@@ -470,7 +632,8 @@ void sync_small(st_ctx* c, int off, int n) {
 // linear, so z_j = sg_j M V_j and A z_j = sg_j A (M V_j), and every scale is folded into the
 // host-side Hessenberg / the device-side AXPY weights (no separate scaling pass over memory).
 int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
-  const long long N = c->N;
+  const long long N = c->Nown;      // inner products and updates over this rank's owned planes
+  const long long vo = c->voff;
   const int m = c->opt.restart;
   const double rtol = c->opt.rtol;
   const long long ld = c->ld;
@@ -480,22 +643,24 @@ int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
   std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), gv(m + 1), y(m), sg(m + 1);
   CK(cudaEventRecord(c->e0, c->stream));
   // ||b||
-  launch_mdot(b, nullptr, 0, 0, N, dh + 200, c->ws, c->stream);
+  launch_mdot(b + vo, nullptr, 0, 0, N, dh + 200, c->ws, c->stream);
   L(c);
+  allreduce(c, dh + 200, 1);
   sync_small(c, 200, 1);
   const double bnorm = std::sqrt(hh[200]);
   int its = 0, restarts = 0, status = ST_OK;
   double relres = 0.0;
   bool conv = false;
   if (bnorm == 0.0) {
-    CK(cudaMemsetAsync(x, 0, N * sizeof(double), c->stream));
+    CK(cudaMemsetAsync(x, 0, c->N * sizeof(double), c->stream));
     conv = true;
   }
   while (!conv) {
     // true residual r = b - A x into V_0
     op_launch(c, 0, MODE_RESID, trans, true, x, b, c->V);
-    launch_mdot(c->V, nullptr, 0, 0, N, dh + 200, c->ws, c->stream);
+    launch_mdot(c->V + vo, nullptr, 0, 0, N, dh + 200, c->ws, c->stream);
     L(c);
+    allreduce(c, dh + 200, 1);
     sync_small(c, 200, 1);
     const double beta = std::sqrt(hh[200]);
     relres = beta / bnorm;
@@ -514,8 +679,10 @@ int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
       double* w = c->V + (long long)(j + 1) * ld;
       vcycle(c, 0, trans, vj, zj);                                       // Z_j = M V_j
       op_launch(c, 0, MODE_APPLY, trans, true, zj, nullptr, w);         // W = A Z_j
-      launch_mdot(w, c->V, ld, j + 1, N, dh, c->ws, c->stream);          // g_i = V_i . W, ||W||^2
-      launch_maxpy_norm(w, c->V, ld, j + 1, dh, ds2, N, dh + 196, c->ws, c->stream);  // W -= sum sg_i^2 g_i V_i
+      launch_mdot(w + vo, c->V + vo, ld, j + 1, N, dh, c->ws, c->stream);  // g_i = V_i . W, ||W||^2
+      allreduce(c, dh, j + 2);
+      launch_maxpy_norm(w + vo, c->V + vo, ld, j + 1, dh, ds2, N, dh + 196, c->ws, c->stream);  // W -= sum sg_i^2 g_i V_i
+      allreduce(c, dh + 196, 1);
       L(c, (j + 16) / 16 + 1);
       check_launch();
       CK(cudaMemcpyAsync(hh, dh, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -525,8 +692,10 @@ int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
       for (int i = 0; i <= j; ++i) hcol[i] = sg[i] * sg[j] * hh[i];  // h_ij = v_i . (A z_j)
       double ww = hh[j + 1], w2 = hh[196];
       if (w2 < 0.5 * ww) {  // DGKS re-orthogonalisation
-        launch_mdot(w, c->V, ld, j + 1, N, dh + 64, c->ws, c->stream);
-        launch_maxpy_norm(w, c->V, ld, j + 1, dh + 64, ds2, N, dh + 196, c->ws, c->stream);
+        launch_mdot(w + vo, c->V + vo, ld, j + 1, N, dh + 64, c->ws, c->stream);
+        allreduce(c, dh + 64, j + 1);
+        launch_maxpy_norm(w + vo, c->V + vo, ld, j + 1, dh + 64, ds2, N, dh + 196, c->ws, c->stream);
+        allreduce(c, dh + 196, 1);
         L(c, (j + 16) / 16 + 1);
         CK(cudaMemcpyAsync(hh + 64, dh + 64, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(hh + 196, dh + 196, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -569,9 +738,10 @@ int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
     }
     for (int i = 0; i < jend; ++i) hh[128 + i] = y[i] * sg[i];
     CK(cudaMemcpyAsync(dh + 128, hh + 128, jend * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    launch_lincomb(x, c->Z, ld, jend, dh + 128, N, c->stream);
+    launch_lincomb(x + vo, c->Z + vo, ld, jend, dh + 128, N, c->stream);
     L(c);
     check_launch();
+    halo(c, 0, x);
     ++restarts;
     if (status == ST_E_BREAKDOWN) status = ST_OK;  // lucky/hard breakdown: re-check true residual
   }
@@ -606,22 +776,33 @@ void copy_back(st_ctx* c, double* host, const double* dev, long long n) {
   CK(cudaStreamSynchronize(c->stream));
 }
 
-// caller vector (dense layout, host or device) -> internal padded vector
-void pack_in(st_ctx* c, const double* user, double* internal, int slot) {
+// owned planes of an internal fine vector, as a geometry starting at plane o0
+Geom owned_geom(const st_ctx* c) {
+  Geom g = c->lv[0].g;
+  g.nt = c->nown - 1;
+  g.N = g.P * c->nown;
+  g.pg0 += c->o0;
+  return g;
+}
+// caller vector (dense layout of the owned planes, host or device) -> internal padded vector;
+// ghost = true refreshes the ghost planes (vectors read through the stencil)
+void pack_in(st_ctx* c, const double* user, double* internal, int slot, bool ghost = false) {
   const double* d = in_ptr(c, user, c->Nd, slot);
-  launch_relayout(c->gd0, d, c->lv[0].g, internal, c->stream);
+  launch_relayout(c->gd0, d, c->lv[0].g, internal + c->voff, c->stream);
   L(c);
+  if (ghost) halo(c, 0, internal);
 }
 // internal padded vector -> caller vector (dense layout, host or device); synchronises
 void unpack_out(st_ctx* c, const double* internal, double* user, int slot) {
   if (!user) throw StErr{ST_E_INVALID_ARG, "null pointer"};
+  const Geom go = owned_geom(c);
   if (is_device_ptr(user)) {
-    launch_relayout(c->lv[0].g, internal, c->gd0, user, c->stream);
+    launch_relayout(go, internal + c->voff, c->gd0, user, c->stream);
     L(c);
     CK(cudaStreamSynchronize(c->stream));
   } else {
     double* d = stage(c, slot, c->Nd);
-    launch_relayout(c->lv[0].g, internal, c->gd0, d, c->stream);
+    launch_relayout(go, internal + c->voff, c->gd0, d, c->stream);
     L(c);
     copy_back(c, user, d, c->Nd);
   }
@@ -654,7 +835,11 @@ void free_ctx(st_ctx* c) {
   cudaFree(c->dsmall);
   if (c->hsmall) cudaFreeHost(c->hsmall);
   cudaFree(c->rho_stage);
+  comm_release(c->comm);
+  for (auto& Lv : c->lv) cudaFree(Lv.stpart);
   for (int i = 0; i < 4; ++i) cudaFree(c->io_stage[i]);
+  for (int d = 0; d < 2; ++d)
+    if (c->gexec[d]) cudaGraphExecDestroy(c->gexec[d]);
   if (c->e0) cudaEventDestroy(c->e0);
   if (c->e1) cudaEventDestroy(c->e1);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -674,17 +859,18 @@ void st_default_options(st_options_t* o) {
   o->design_mode = ST_SPACE_TIME;
   o->rtol = 1e-8;
   o->maxit = 500;
-  o->restart = 30;
+  o->restart = 16;
   o->smoother = ST_SMOOTH_JACOBI;
-  o->nu_pre = 2;
-  o->nu_post = 2;
-  o->omega = 0.6;
+  o->nu_pre = 3;   // measured sweep on config 2 / a config-3-like grid
+  o->nu_post = 3;
+  o->omega = 0.75;
   o->lambda_crit = 0.5;
   o->coarse_max_nodes = 400;
   o->max_levels = 0;
   o->full_coarsening = 0;
-  o->use_graphs = 0;
+  o->use_graphs = 1;
   o->verbose = 0;
+  o->agg_nodes = 16384;
 }
 
 const char* st_strerror(int code) {
@@ -717,7 +903,16 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       throw StErr{ST_E_INVALID_ARG, "material constants must be > 0"};
     if (bcs->has_patch && bcs->face != 0) throw StErr{ST_E_UNSUPPORTED, "only face 0 (x1 = 0) supported"};
     if (src->kind != ST_SRC_UNIFORM && src->kind != ST_SRC_SIN) throw StErr{ST_E_UNSUPPORTED, "source kind"};
-    if (dist && dist->size > 1) throw StErr{ST_E_UNSUPPORTED, "multi-GPU time slabs: not in this build"};
+    if (dist && dist->size > 1) {
+      if (dist->rank < 0 || dist->rank >= dist->size) throw StErr{ST_E_INVALID_ARG, "rank out of range"};
+      if (grid->nt % dist->size != 0) throw StErr{ST_E_DIVISIBILITY, "time slabs: nt must be divisible by the rank count"};
+      if (dist->transport == ST_COMM_NCCL && !dist->nccl_comm) throw StErr{ST_E_INVALID_ARG, "NCCL transport needs nccl_comm"};
+      if (dist->transport == ST_COMM_HOST &&
+          (!dist->host.sendrecv || !dist->host.allreduce_sum || !dist->host.allgather))
+        throw StErr{ST_E_INVALID_ARG, "host transport needs sendrecv, allreduce_sum and allgather"};
+      if (dist->transport != ST_COMM_NCCL && dist->transport != ST_COMM_HOST)
+        throw StErr{ST_E_INVALID_ARG, "size > 1 needs a transport (ST_COMM_NCCL or ST_COMM_HOST)"};
+    }
     st_ctx* c = new st_ctx();
     try {
       c->grid = *grid;
@@ -748,6 +943,14 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       }
       c->sd = grid->sdim;
       c->tc = (c->opt.design_mode == ST_TIME_CONSTANT);
+      if (c->opt.agg_nodes <= 0) c->opt.agg_nodes = 16384;
+      if (dist && dist->size > 1) {
+        c->comm.rank = dist->rank;
+        c->comm.size = dist->size;
+        c->comm.kind = dist->transport;
+        c->comm.nccl = dist->nccl_comm;
+        c->comm.host = dist->host;
+      }
       const double scale = grid->tau / (grid->L * grid->L);
       c->md.Cins = mats->C_ins;
       c->md.dC = mats->C_con - mats->C_ins;
@@ -756,13 +959,19 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       c->md.dk = (mats->k_con - mats->k_ins) * scale;
       c->md.pk = mats->p_k;
       build_hierarchy(c);
+      assign_slabs(c);
       setup_forms(c);
-      c->N = c->lv[0].g.N;
-      c->Nd = nodes_of(c->lv[0].g);
-      c->gd0 = dense_of(c->lv[0].g);
+      const Level& L0 = c->lv[0];
+      c->N = L0.g.N;
+      c->o0 = (L0.dist && c->comm.rank > 0) ? 1 : 0;
+      c->nown = L0.dist ? L0.nloc + (c->comm.rank == 0 ? 1 : 0) : L0.g.nt + 1;
+      c->voff = (long long)c->o0 * L0.g.P;
+      c->Nown = (long long)c->nown * L0.g.P;
+      c->gd0 = make_geom(c->sd, L0.g.n, c->nown - 1, L0.g.plo, L0.g.phi, false, L0.ntg, L0.g.pg0 + c->o0);
+      c->Nd = nodes_of(c->gd0);
       long long nsp = 1;
       for (int d = 0; d < c->sd; ++d) nsp *= grid->n;
-      c->ndesign = c->tc ? nsp : nsp * grid->nt;
+      c->ndesign = c->tc ? nsp : nsp * L0.g.nt;   // space-time: owned layers + the ghost layer
       allocate(c);
       dalloc(&c->rho_stage, c->ndesign);
       // source vector f: Q~ = Q tau
@@ -789,6 +998,7 @@ int st_solve(st_ctx_t* c, const double* rho, double* T) {
     pack_in(c, T, c->xint, 0);
     launch_set_bc_values(c->lv[0].g, c->bcs.T0, c->xint, c->stream);  // x_c = xD
     L(c, 2);
+    halo(c, 0, c->xint);
     int rc = fgmres(c, false, c->b, c->xint);
     unpack_out(c, c->xint, T, 0);
     return rc;
@@ -805,6 +1015,7 @@ int st_adjoint(st_ctx_t* c, const double* rho, const double* dJdT, double* lambd
     pack_in(c, lambda, c->xint, 0);
     launch_set_bc_values(c->lv[0].g, 0.0, c->xint, c->stream);  // lambda_c = 0
     L(c, 4);
+    halo(c, 0, c->xint);
     int rc = fgmres(c, true, c->tmpN2, c->xint);
     unpack_out(c, c->xint, lambda, 0);
     return rc;
@@ -820,17 +1031,23 @@ int st_sensitivity(st_ctx_t* c, const double* rho, const double* T, const double
       CK(cudaMemcpyAsync(c->rho_stage, rho, c->ndesign * sizeof(double), cudaMemcpyHostToDevice, c->stream));
       r = c->rho_stage;
     }
-    OpDesc op = c->lv[0].op;
+    // T and lambda into internal slab vectors with ghost planes (element layers of this rank)
+    pack_in(c, T, c->tmpN, 1, true);
+    pack_in(c, lambda, c->tmpN2, 2, true);
+    const Level& L0 = c->lv[0];
+    OpDesc op = L0.op;
     op.rho = r;
-    op.g = c->gd0;  // T, lambda in the caller's dense layout
-    const double* Td = in_ptr(c, T, c->Nd, 1);
-    const double* Ld = in_ptr(c, lambda, c->Nd, 2);
+    op.g.nt = L0.dist ? L0.nloc : L0.g.nt;  // owned element layers
+    long long nsp = 1;
+    for (int d = 0; d < c->sd; ++d) nsp *= c->grid.n;
+    const long long ndj = c->tc ? nsp : nsp * op.g.nt;
     bool staged = false;
-    double* dj = out_ptr(c, dJ, c->ndesign, 3, false, &staged);
-    launch_sensitivity(op, Td, Ld, dj, c->stream);
+    double* dj = out_ptr(c, dJ, ndj, 3, false, &staged);
+    launch_sensitivity(op, c->tmpN, c->tmpN2, dj, c->stream);
     L(c);
     check_launch();
-    if (staged) copy_back(c, dJ, dj, c->ndesign);
+    if (c->tc) allreduce(c, dj, ndj);  // time-constant design: sum through time over all slabs
+    if (staged) copy_back(c, dJ, dj, ndj);
     else CK(cudaStreamSynchronize(c->stream));
     return ST_OK;
   });
@@ -861,7 +1078,7 @@ int st_apply(st_ctx_t* c, const double* rho, const double* x, double* y, int tra
       r = c->rho_stage;
     }
     c->lv[0].op.rho = r;
-    pack_in(c, x, c->tmpN, 1);
+    pack_in(c, x, c->tmpN, 1, true);
     masked_level_apply(c, 0, c->tmpN, c->tmpN2, c->lv[0].t, transpose != 0, bc != 0);
     unpack_out(c, c->lv[0].t, y, 2);
     return ST_OK;
@@ -872,6 +1089,7 @@ int st_level_apply(st_ctx_t* c, const double* rho, int level, const double* x, d
   return guarded([&]() -> int {
     if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
     if (level < 0 || level >= (int)c->lv.size()) throw StErr{ST_E_INVALID_ARG, "level out of range"};
+    if (c->comm.size > 1) throw StErr{ST_E_UNSUPPORTED, "st_level_apply: single-rank contexts only"};
     CK(cudaSetDevice(c->device));
     prepare(c, rho);
     Level& Lv = c->lv[level];
@@ -938,14 +1156,107 @@ int st_get_hierarchy(const st_ctx_t* c, st_hierarchy_t* h) {
   memset(h, 0, sizeof(*h));
   h->n_levels = (int)std::min<size_t>(c->lv.size(), 32);
   for (int l = 0; l < h->n_levels; ++l) {
-    h->n[l] = c->lv[l].g.n;
-    h->nt[l] = c->lv[l].g.nt;
-    h->kind[l] = c->lv[l].kind;
-    h->form[l] = c->lv[l].dense ? FORM_DENSE : c->lv[l].op.form;
-    h->nodes[l] = nodes_of(c->lv[l].g);
+    const Level& Lv = c->lv[l];
+    h->n[l] = Lv.g.n;
+    h->nt[l] = Lv.ntg;  // global extent (a rank holds a slab of distributed levels)
+    h->kind[l] = Lv.kind;
+    h->form[l] = Lv.dense ? FORM_DENSE : Lv.op.form;
+    long long v = Lv.ntg + 1;
+    for (int d = 0; d < Lv.g.sd; ++d) v *= Lv.g.nn;
+    h->nodes[l] = v;
   }
   return ST_OK;
 }
+
+int st_local_layout(const st_ctx_t* c, st_layout_t* o) {
+  if (!c || !o) return ST_E_INVALID_ARG;
+  memset(o, 0, sizeof(*o));
+  const Level& L0 = c->lv[0];
+  o->rank = c->comm.rank;
+  o->size = c->comm.size;
+  o->plane0 = L0.g.pg0 + c->o0;
+  o->n_planes = c->nown;
+  o->layer0 = L0.g.pg0;
+  o->n_layers = L0.dist ? L0.nloc : L0.g.nt;
+  o->rho_layers = c->tc ? 0 : L0.g.nt;
+  o->nodes_local = c->Nd;
+  o->design_local = c->ndesign;
+  o->n_levels = (int)c->lv.size();
+  o->n_dist_levels = c->n_dist;
+  return ST_OK;
+}
+
+int st_plan(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* bcs, const st_options_t* opts,
+            int32_t rank, int32_t size, st_plan_t* plan) {
+  return guarded([&]() -> int {
+    if (!grid || !mats || !bcs || !plan) throw StErr{ST_E_INVALID_ARG, "null argument"};
+    if (grid->sdim != 2 && grid->sdim != 3) throw StErr{ST_E_INVALID_ARG, "sdim must be 2 or 3"};
+    if (grid->n < 2 || grid->nt < 2) throw StErr{ST_E_INVALID_ARG, "n and nt must be >= 2"};
+    if (size < 1 || rank < 0 || rank >= size) throw StErr{ST_E_INVALID_ARG, "rank / size"};
+    if (grid->nt % size != 0) throw StErr{ST_E_DIVISIBILITY, "time slabs: nt must be divisible by the rank count"};
+    st_ctx c;  // host-only: no device call below
+    c.grid = *grid;
+    c.mats = *mats;
+    c.bcs = *bcs;
+    if (opts) c.opt = *opts;
+    else st_default_options(&c.opt);
+    if (c.opt.coarse_max_nodes < 8) c.opt.coarse_max_nodes = 8;
+    if (c.opt.agg_nodes <= 0) c.opt.agg_nodes = 16384;
+    c.sd = grid->sdim;
+    c.comm.rank = rank;
+    c.comm.size = size;
+    build_hierarchy(&c);
+    assign_slabs(&c);
+    memset(plan, 0, sizeof(*plan));
+    plan->n_levels = (int)std::min<size_t>(c.lv.size(), 32);
+    plan->n_dist_levels = c.n_dist;
+    for (int l = 0; l < plan->n_levels; ++l) {
+      const Level& Lv = c.lv[l];
+      plan->n[l] = Lv.g.n;
+      plan->nt[l] = Lv.ntg;
+      plan->kind[l] = Lv.kind;
+      plan->dist[l] = Lv.dist ? 1 : 0;
+      plan->layer0[l] = Lv.dist ? Lv.a : 0;
+      plan->n_layers[l] = Lv.dist ? Lv.nloc : Lv.ntg;
+      plan->local_layers[l] = Lv.g.nt;
+    }
+    const Level& L0 = c.lv[0];
+    const int o0 = (L0.dist && rank > 0) ? 1 : 0;
+    plan->plane0 = L0.g.pg0 + o0;
+    plan->n_planes = L0.dist ? L0.nloc + (rank == 0 ? 1 : 0) : L0.g.nt + 1;
+    c.lv.clear();
+    return ST_OK;
+  });
+}
+
+int st_struct_sizes(int64_t out[10]) {
+  if (!out) return ST_E_INVALID_ARG;
+  out[0] = sizeof(st_grid_t); out[1] = sizeof(st_materials_t); out[2] = sizeof(st_bcs_t);
+  out[3] = sizeof(st_source_t); out[4] = sizeof(st_options_t); out[5] = sizeof(st_dist_t);
+  out[6] = sizeof(st_stats_t); out[7] = sizeof(st_hierarchy_t); out[8] = sizeof(st_layout_t);
+  out[9] = sizeof(st_plan_t);
+  return ST_OK;
+}
+
+int st_nccl_unique_id(char id[ST_NCCL_ID_BYTES]) {
+  if (!id) return ST_E_INVALID_ARG;
+  if (nccl_unique_id(id) != 0) {
+    g_last_error = "libnccl.so.2 not available or ncclGetUniqueId failed";
+    return ST_E_NCCL;
+  }
+  return ST_OK;
+}
+
+int st_nccl_comm_init(const char id[ST_NCCL_ID_BYTES], int32_t rank, int32_t size, void** comm) {
+  if (!id || !comm || size < 1 || rank < 0 || rank >= size) return ST_E_INVALID_ARG;
+  if (nccl_comm_init(id, rank, size, comm) != 0) {
+    g_last_error = "ncclCommInitRank failed";
+    return ST_E_NCCL;
+  }
+  return ST_OK;
+}
+
+int st_nccl_comm_destroy(void* comm) { return nccl_comm_destroy(comm) == 0 ? ST_OK : ST_E_NCCL; }
 
 int64_t st_num_nodes(const st_ctx_t* c) { return c ? c->Nd : -1; }
 int64_t st_num_design(const st_ctx_t* c) { return c ? c->ndesign : -1; }

@@ -43,7 +43,8 @@ struct MatsDev {
 struct OpDesc {
   Geom g;
   int form;
-  int nl;                 // stored layers: 1 (time-constant) or nt
+  int nl;                 // stored layers: 1 (time-constant) or the (local) layer count
+  int tvl;                // per-layer (time-varying) storage; a slab may hold a single layer
   double U[2][2], Tm[2][2];
   const double* rho;      // FORM_RHO
   int rho_tc;             // rho time-constant

@@ -475,7 +475,7 @@ bool launch_op_fast2d(const OpDesc& op, int mode, bool trans, bool mask, const d
     else l2d_modes<false, 0, false>(op, mode, trans, mask, x, b, y, omega, s);
     return true;
   }
-  if (op.form == FORM_MK && op.nl == 1) {
+  if (op.form == FORM_MK && !op.tvl) {
     l2d_modes<true, 1, false>(op, mode, trans, mask, x, b, y, omega, s);
     return true;
   }

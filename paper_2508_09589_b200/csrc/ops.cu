@@ -166,7 +166,7 @@ __device__ __forceinline__ void layer_eval(const OpDesc& op, const int* c, long 
       dtop = op.U[1][1] * Mc + op.Tm[1][1] * Kc;
     }
   } else if (FORM == FORM_MK) {
-    const double* Mbase = op.st + (long long)(op.nl == 1 ? 0 : tau) * 2 * NC * g.P;
+    const double* Mbase = op.st + (long long)(op.tvl ? tau : 0) * 2 * NC * g.P;
     const double* Kbase = Mbase + (long long)NC * g.P;
     if (NEEDX) {
       double Mb = st_apply<SD>(g, Mbase, c, pn, xb), Mt = st_apply<SD>(g, Mbase, c, pn, xt);
@@ -179,7 +179,7 @@ __device__ __forceinline__ void layer_eval(const OpDesc& op, const int* c, long 
       dtop = op.U[1][1] * Mc + op.Tm[1][1] * Kc;
     }
   } else {  // FORM_B4: [M, Kbb, Kbt, Ktb, Ktt], S^{ab} = U[a][b] M + K^{ab}
-    const double* base = op.st + (long long)(op.nl == 1 ? 0 : tau) * 5 * NC * g.P;
+    const double* base = op.st + (long long)(op.tvl ? tau : 0) * 5 * NC * g.P;
     const double* Mst = base;
     const double* Kbb = base + (long long)NC * g.P;
     const double* Kbt = base + 2LL * NC * g.P;
@@ -365,9 +365,9 @@ __device__ double mpart_weight(const OpDesc& op, const int* c, long long pn, int
     elem_ck<SD>(op, c, tau, ce, ke);
     return rho_weight<SD>(ce, ke, k, 0, g.dx);
   } else if (FORM == FORM_MK) {
-    return st_weight<SD>(g, op.st + (long long)(op.nl == 1 ? 0 : tau) * 2 * NC * g.P, c, pn, k);
+    return st_weight<SD>(g, op.st + (long long)(op.tvl ? tau : 0) * 2 * NC * g.P, c, pn, k);
   } else {
-    return st_weight<SD>(g, op.st + (long long)(op.nl == 1 ? 0 : tau) * 5 * NC * g.P, c, pn, k);
+    return st_weight<SD>(g, op.st + (long long)(op.tvl ? tau : 0) * 5 * NC * g.P, c, pn, k);
   }
 }
 
@@ -380,10 +380,10 @@ __device__ double kblock_weight(const OpDesc& op, const int* c, long long pn, in
     elem_ck<SD>(op, c, tau, ce, ke);
     return op.Tm[a][bb] * rho_weight<SD>(ce, ke, k, 1, g.dx);
   } else if (FORM == FORM_MK) {
-    const double* Kb = op.st + (long long)(op.nl == 1 ? 0 : tau) * 2 * NC * g.P + (long long)NC * g.P;
+    const double* Kb = op.st + (long long)(op.tvl ? tau : 0) * 2 * NC * g.P + (long long)NC * g.P;
     return op.Tm[a][bb] * st_weight<SD>(g, Kb, c, pn, k);
   } else {
-    const double* Kb = op.st + (long long)(op.nl == 1 ? 0 : tau) * 5 * NC * g.P + (long long)(1 + 2 * a + bb) * NC * g.P;
+    const double* Kb = op.st + (long long)(op.tvl ? tau : 0) * 5 * NC * g.P + (long long)(1 + 2 * a + bb) * NC * g.P;
     return st_weight<SD>(g, Kb, c, pn, k);
   }
 }
@@ -403,7 +403,7 @@ __device__ double mk_weight(const OpDesc& op, const int* c, long long pn, int ta
     elem_ck<SD>(op, c, tau, ce, ke);
     return rho_weight<SD>(ce, ke, k, s, g.dx);
   } else {
-    const double* base = op.st + (long long)(op.nl == 1 ? 0 : tau) * 2 * NC * g.P + (long long)s * NC * g.P;
+    const double* base = op.st + (long long)(op.tvl ? tau : 0) * 2 * NC * g.P + (long long)s * NC * g.P;
     return st_weight<SD>(g, base, c, pn, k);
   }
 }
@@ -496,7 +496,7 @@ __global__ void rap_time_kernel(OpDesc fop, int nlc, double* __restrict__ out) {
     double macc = 0.0;
     for (int f = 0; f < 2; ++f) {
       int tau = 2 * T + f;
-      if ((FFORM == FORM_RHO && fop.rho_tc) || (FFORM != FORM_RHO && fop.nl == 1)) tau = 0;
+      if ((FFORM == FORM_RHO && fop.rho_tc) || (FFORM != FORM_RHO && !fop.tvl)) tau = 0;
       macc += 0.5 * mpart_weight<SD, FFORM>(fop, c, pn, tau, q + CEN);
       double s[2][2];
       for (int a = 0; a < 2; ++a)

@@ -390,7 +390,7 @@ bool launch_op_tc2d(const OpDesc& op, int mode, bool trans, bool mask, const dou
                     double omega, cudaStream_t s) {
   const Geom& g = op.g;
   if (g.sd != 2 || !mask) return false;
-  const bool rho_tc = (op.form == FORM_RHO && op.rho_tc), mk_tc = (op.form == FORM_MK && op.nl == 1);
+  const bool rho_tc = (op.form == FORM_RHO && op.rho_tc), mk_tc = (op.form == FORM_MK && !op.tvl);
   if (!rho_tc && !mk_tc) return false;
   // the lean kernel hard-wires the upwind capacity factor and a symmetric conduction factor
   if (op.U[0][0] != 0.0 || op.U[0][1] != 0.0 || op.U[1][0] != -1.0 || op.U[1][1] != 1.0) return false;

@@ -497,7 +497,7 @@ bool launch_op_tma2d(const OpDesc& op, int mode, bool trans, bool mask, const do
   const Geom& g = op.g;
   if (g.sd != 2) return false;
   const bool rho_tc = (op.form == FORM_RHO && op.rho_tc), rho_tv = (op.form == FORM_RHO && !op.rho_tc);
-  const bool mk_tc = (op.form == FORM_MK && op.nl == 1);
+  const bool mk_tc = (op.form == FORM_MK && !op.tvl);
   if (!rho_tc && !rho_tv && !mk_tc) return false;
   CUtensorMap mx{}, mb{};
   const unsigned long long nn = g.nn, s1 = (unsigned long long)g.pr * 8, s2 = (unsigned long long)g.P * 8;

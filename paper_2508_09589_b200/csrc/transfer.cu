@@ -2,7 +2,9 @@
 // Prolongation P: linear interpolation along each coarsened direction (space: bi/trilinear,
 // weights 1 and 1/2; time: 1 and 1/2 — non-causal). Restriction = P^T.
 // Dirichlet masks: restriction output zero at coarse
-// constrained nodes; prolongation never updates fine constrained nodes.
+// constrained nodes; prolongation never updates fine constrained nodes. Planes are mapped in
+// global numbering (Geom::pg0), so a time slab can restrict into / prolong from a coarse slab
+// or a replicated (agglomerated) coarse level.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -17,10 +19,11 @@ __global__ void restrict_kernel(Geom gf, Geom gc, const double* __restrict__ rf,
   int C[3] = {0, 0, 0};
   if (!pdecode<SD>(gc, pc, C) || is_cons<SD>(gc, C, P)) { rc[idx] = 0.0; return; }
   constexpr int NS = SP ? SG<SD>::NOFF : 1;
+  const int Pg = P + gc.pg0;  // global coarse plane; fine planes in global numbering, then local
   double acc = 0.0;
 #pragma unroll
   for (int at = (TM ? -1 : 0); at <= (TM ? 1 : 0); ++at) {
-    int q = TM ? 2 * P + at : P;
+    int q = (TM ? 2 * Pg + at : Pg) - gf.pg0;
     if (q < 0 || q > gf.nt) continue;
     double wt = (at == 0) ? 1.0 : 0.5;
     const double* rp = rf + (long long)q * gf.P;
@@ -50,12 +53,14 @@ __global__ void prolong_kernel(Geom gf, Geom gc, const double* __restrict__ ec, 
   long long pf = idx % gf.P;
   int c[3] = {0, 0, 0};
   if (!pdecode<SD>(gf, pf, c) || is_cons<SD>(gf, c, p)) return;
-  // time part
-  int P0 = TM ? (p >> 1) : p;
-  int nP = (TM && (p & 1)) ? 2 : 1;
+  // time part (global plane numbering on both grids)
+  const int pg = p + gf.pg0;
+  int P0 = (TM ? (pg >> 1) : pg) - gc.pg0;
+  int nP = (TM && (pg & 1)) ? 2 : 1;
   double acc = 0.0;
   for (int it = 0; it < nP; ++it) {
     int Pq = P0 + it;
+    if (Pq < 0 || Pq > gc.nt) continue;  // only ghost rows of a slab can reach past the coarse slab
     double wt = (nP == 2) ? 0.5 : 1.0;
     const double* ep = ec + (long long)Pq * gc.P;
     // space part: corners of the coarse cell

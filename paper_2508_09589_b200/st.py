@@ -38,12 +38,41 @@ class Options(C.Structure):
     _fields_ = [("design_mode", C.c_int32), ("rtol", C.c_double), ("maxit", C.c_int32), ("restart", C.c_int32),
                 ("smoother", C.c_int32), ("nu_pre", C.c_int32), ("nu_post", C.c_int32), ("omega", C.c_double),
                 ("lambda_crit", C.c_double), ("coarse_max_nodes", C.c_int64), ("max_levels", C.c_int32),
-                ("full_coarsening", C.c_int32), ("use_graphs", C.c_int32), ("verbose", C.c_int32)]
+                ("full_coarsening", C.c_int32), ("use_graphs", C.c_int32), ("verbose", C.c_int32),
+                ("agg_nodes", C.c_int64)]
+
+
+ST_COMM_NONE, ST_COMM_NCCL, ST_COMM_HOST = 0, 1, 2
+ST_NCCL_ID_BYTES = 128
+_DP = C.POINTER(C.c_double)
+CB_SENDRECV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, _DP, _DP, C.c_int64)
+CB_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, _DP, C.c_int64)
+CB_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, _DP, _DP, C.c_int64)
+
+
+class HostComm(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("sendrecv", CB_SENDRECV), ("allreduce_sum", CB_ALLREDUCE),
+                ("allgather", CB_ALLGATHER)]
 
 
 class Dist(C.Structure):
     _fields_ = [("nccl_comm", C.c_void_p), ("rank", C.c_int32), ("size", C.c_int32),
-                ("cuda_stream", C.c_void_p), ("device", C.c_int32)]
+                ("cuda_stream", C.c_void_p), ("device", C.c_int32), ("transport", C.c_int32),
+                ("host", HostComm)]
+
+
+class Plan(C.Structure):
+    _fields_ = [("n_levels", C.c_int32), ("n_dist_levels", C.c_int32), ("n", C.c_int64 * 32), ("nt", C.c_int64 * 32),
+                ("kind", C.c_int32 * 32), ("dist", C.c_int32 * 32), ("layer0", C.c_int64 * 32),
+                ("n_layers", C.c_int64 * 32), ("local_layers", C.c_int64 * 32), ("plane0", C.c_int64),
+                ("n_planes", C.c_int64)]
+
+
+class Layout(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("size", C.c_int32), ("plane0", C.c_int64), ("n_planes", C.c_int64),
+                ("layer0", C.c_int64), ("n_layers", C.c_int64), ("rho_layers", C.c_int64),
+                ("nodes_local", C.c_int64), ("design_local", C.c_int64), ("n_levels", C.c_int32),
+                ("n_dist_levels", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -59,6 +88,8 @@ class Hierarchy(C.Structure):
 
 EXPORTS = ["st_abi_version", "st_default_options", "st_setup", "st_destroy", "st_solve", "st_adjoint",
            "st_sensitivity", "st_apply", "st_rhs", "st_level_apply", "st_bench_op", "st_get_stats", "st_get_hierarchy",
+           "st_local_layout", "st_nccl_unique_id", "st_nccl_comm_init", "st_nccl_comm_destroy", "st_plan",
+           "st_struct_sizes",
            "st_num_nodes", "st_num_design", "st_kernel_launches", "st_strerror", "st_last_error"]
 
 _lib = None
@@ -92,6 +123,12 @@ def load_library(path: str = LIB_PATH):
     lib.st_bench_op.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
     lib.st_get_stats.argtypes = [C.c_void_p, P(Stats)]
     lib.st_get_hierarchy.argtypes = [C.c_void_p, P(Hierarchy)]
+    lib.st_local_layout.argtypes = [C.c_void_p, P(Layout)]
+    lib.st_nccl_unique_id.argtypes = [C.c_char_p]
+    lib.st_nccl_comm_init.argtypes = [C.c_char_p, C.c_int32, C.c_int32, P(C.c_void_p)]
+    lib.st_nccl_comm_destroy.argtypes = [C.c_void_p]
+    lib.st_plan.argtypes = [P(Grid), P(Materials), P(BCs), P(Options), C.c_int32, C.c_int32, P(Plan)]
+    lib.st_struct_sizes.argtypes = [P(C.c_int64)]
     for name in ("st_num_nodes", "st_num_design", "st_kernel_launches"):
         getattr(lib, name).argtypes = [C.c_void_p]
         getattr(lib, name).restype = C.c_int64
@@ -117,12 +154,99 @@ def _ptr(a):
     return a.ctypes.data
 
 
+class TorchHostComm:
+    """ST_COMM_HOST transport implemented with torch.distributed on host tensors (e.g. a gloo
+    group). Marshalling only: the library stages device planes through pinned host buffers and
+    calls these functions; any number of ranks may share one GPU."""
+
+    def __init__(self, group=None):
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        self.np, self.torch, self.dist, self.group = np, torch, dist, group
+        self.size = dist.get_world_size(group)
+        self._cbs = (CB_SENDRECV(self._sendrecv), CB_ALLREDUCE(self._allreduce), CB_ALLGATHER(self._allgather))
+        self.struct = HostComm(None, *self._cbs)
+
+    def _t(self, ptr, n):
+        return self.torch.from_numpy(self.np.ctypeslib.as_array(ptr, (int(n),)))
+
+    def _sendrecv(self, user, peer, send, recv, count):
+        try:
+            s, r = self._t(send, count).clone(), self._t(recv, count)
+            reqs = [self.dist.isend(s, int(peer), group=self.group), self.dist.irecv(r, int(peer), group=self.group)]
+            for q in reqs:
+                q.wait()
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    def _allreduce(self, user, buf, count):
+        try:
+            self.dist.all_reduce(self._t(buf, count), group=self.group)
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    def _allgather(self, user, send, recv, count):
+        try:
+            parts = [self.torch.empty(int(count), dtype=self.torch.float64) for _ in range(self.size)]
+            self.dist.all_gather(parts, self._t(send, count).clone(), group=self.group)
+            self._t(recv, count * self.size).copy_(self.torch.cat(parts))
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+
+STRUCTS = [Grid, Materials, BCs, Source, Options, Dist, Stats, Hierarchy, Layout, Plan]
+
+
+def plan(sdim, n, nt, rank=0, size=1, mats=(1.0, 1.0, 1.0, 1e-3, 1.0, 3.0), tau=1.0, L=1.0, has_patch=True,
+         **opts):
+    """Host-only st_plan: the hierarchy and this rank's slab of every level (no GPU needed)."""
+    lib = load_library()
+    o = Options()
+    lib.st_default_options(C.byref(o))
+    for k, v in opts.items():
+        setattr(o, k, v)
+    p = Plan()
+    rc = lib.st_plan(C.byref(Grid(sdim, n, nt, L, tau)), C.byref(Materials(*mats)),
+                     C.byref(BCs(0.0, 1 if has_patch else 0, 0, 0.5, 0.05)), C.byref(o), rank, size, C.byref(p))
+    if rc != ST_OK:
+        raise StError(rc, lib.st_last_error().decode())
+    kinds = ["fine", "space", "time", "full"]
+    levels = [dict(n=p.n[i], nt=p.nt[i], kind=kinds[p.kind[i]], dist=bool(p.dist[i]), layer0=p.layer0[i],
+                   n_layers=p.n_layers[i], local_layers=p.local_layers[i]) for i in range(p.n_levels)]
+    return dict(levels=levels, n_dist=p.n_dist_levels, plane0=p.plane0, n_planes=p.n_planes)
+
+
+def nccl_unique_id():
+    lib = load_library()
+    buf = C.create_string_buffer(ST_NCCL_ID_BYTES)
+    if lib.st_nccl_unique_id(buf) != ST_OK:
+        raise StError(-7, lib.st_last_error().decode())
+    return buf.raw
+
+
+def nccl_comm_init(uid: bytes, rank: int, size: int):
+    lib = load_library()
+    comm = C.c_void_p()
+    if lib.st_nccl_comm_init(uid, rank, size, C.byref(comm)) != ST_OK:
+        raise StError(-7, lib.st_last_error().decode())
+    return comm
+
+
 class Solver:
-    """One space-time problem on one GPU: st_setup at construction, st_destroy on close()."""
+    """One space-time problem: st_setup at construction, st_destroy on close().
+
+    Time slabs: pass rank/size and either host_comm (a TorchHostComm; ranks may share a GPU)
+    or nccl_comm (from nccl_unique_id / nccl_comm_init; one GPU per rank). Vectors are then
+    this rank's owned planes (see layout())."""
 
     def __init__(self, sdim, n, nt, mats=(1.0, 1.0, 1.0, 1e-3, 1.0, 3.0), T0=0.0, has_patch=True,
                  center=0.5, halfwidth=0.05, source=("uniform", 1.0, 0.0, 0.0), L=1.0, tau=1.0,
-                 time_constant=False, stream=None, device=None, **opts):
+                 time_constant=False, stream=None, device=None, rank=0, size=1, host_comm=None,
+                 nccl_comm=None, **opts):
         self.lib = load_library()
         self.grid = Grid(sdim, n, nt, L, tau)
         self.mats = Materials(*mats)
@@ -137,7 +261,14 @@ class Solver:
                 raise TypeError(f"unknown option {k}")
             setattr(o, k, v)
         self.opts = o
-        d = Dist(None, 0, 1, stream if stream is not None else None, -1 if device is None else device)
+        transport = ST_COMM_NONE
+        if size > 1:
+            transport = ST_COMM_NCCL if nccl_comm is not None else ST_COMM_HOST
+            if transport == ST_COMM_HOST and host_comm is None:
+                raise ValueError("size > 1 needs host_comm or nccl_comm")
+        self._host_comm = host_comm  # keeps the callbacks alive
+        d = Dist(nccl_comm, rank, size, stream if stream is not None else None, -1 if device is None else device,
+                 transport, host_comm.struct if host_comm is not None else HostComm())
         h = C.c_void_p()
         self._check(self.lib.st_setup(C.byref(self.grid), C.byref(self.mats), C.byref(self.bcs),
                                       C.byref(self.src), C.byref(o), C.byref(d), C.byref(h)))
@@ -192,6 +323,11 @@ class Solver:
         forms = ["rho", "mk", "b4", "dense"]
         return [dict(n=h.n[i], nt=h.nt[i], kind=kinds[h.kind[i]], form=forms[h.form[i]], nodes=h.nodes[i])
                 for i in range(h.n_levels)]
+
+    def layout(self):
+        lay = Layout()
+        self.lib.st_local_layout(self.ctx, C.byref(lay))
+        return {k: getattr(lay, k) for k, _ in Layout._fields_}
 
     def kernel_launches(self):
         return self.lib.st_kernel_launches(self.ctx)

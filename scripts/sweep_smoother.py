@@ -13,9 +13,8 @@ else:
     sdim, n, nt, tc, design, src = 2, 256, 256, False, "smooth_layers", ("sin", 1.0, 1.0, 6.283185307179586)
 rho = torch.as_tensor(I.design_for(sdim, n, nt, design, 0), device=dev).contiguous()
 res = []
-for nu, om, cmax, m in [(2, 0.6, 400, 30), (1, 0.6, 400, 30), (3, 0.6, 400, 30), (4, 0.6, 400, 30), (2, 0.5, 400, 30),
-                         (2, 0.7, 400, 30), (2, 0.8, 400, 30), (3, 0.7, 400, 30), (2, 0.6, 1200, 30), (2, 0.6, 400, 12),
-                         (2, 0.6, 400, 20), (3, 0.8, 400, 30), (2, 0.9, 400, 30)]:
+for nu, om, cmax, m in [(2, 0.6, 400, 30), (3, 0.7, 400, 30), (3, 0.8, 400, 30), (4, 0.7, 400, 30), (4, 0.8, 400, 30),
+                         (3, 0.75, 400, 16), (4, 0.75, 400, 16), (3, 0.75, 400, 12), (5, 0.75, 400, 30), (6, 0.75, 400, 30)]:
     s = S.Solver(sdim, n, nt, time_constant=tc, source=src, stream=stream.cuda_stream, rtol=1e-8, maxit=300,
                  nu_pre=nu, nu_post=nu, omega=om, coarse_max_nodes=cmax, restart=m)
     T = torch.zeros(s.n_nodes, dtype=torch.float64, device=dev)

@@ -35,8 +35,8 @@ def test_default_options_and_errors():
     lib = st.load_library()
     o = st.Options()
     lib.st_default_options(ctypes.byref(o))
-    assert o.rtol == 1e-8 and o.lambda_crit == 0.5 and o.restart == 30
-    assert lib.st_abi_version() == 1
+    assert o.rtol == 1e-8 and o.lambda_crit == 0.5 and o.restart == 16 and o.nu_pre == 3
+    assert lib.st_abi_version() == 2
     assert lib.st_strerror(-2).decode().startswith("grid not divisible")
 
 
@@ -64,3 +64,33 @@ def test_cubin_is_sm100a():
         pytest.skip("cuobjdump not available")
     out = subprocess.run([tool, "--list-elf", path], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_struct_layouts_match_binding():
+    """The ctypes mirrors of every ABI struct have the C sizes (catches a field added on one side)."""
+    from paper_2508_09589_b200 import st
+    lib = st.load_library()
+    out = (ctypes.c_int64 * 10)()
+    assert lib.st_struct_sizes(out) == 0
+    for cls, size in zip(st.STRUCTS, out):
+        assert ctypes.sizeof(cls) == size, (cls.__name__, ctypes.sizeof(cls), size)
+
+
+def test_setup_validates_distribution_without_gpu():
+    """Time slabs: nt not divisible by the rank count -> ST_E_DIVISIBILITY; no transport -> invalid."""
+    from paper_2508_09589_b200 import st
+    lib = st.load_library()
+    g = st.Grid(2, 16, 18, 1.0, 1.0)
+    m = st.Materials(1, 1, 1, 1e-3, 1, 3)
+    b = st.BCs(0.0, 1, 0, 0.5, 0.05)
+    s = st.Source(0, 1.0, 0.0, 0.0)
+    h = ctypes.c_void_p()
+    d = st.Dist(None, 0, 4, None, -1, st.ST_COMM_HOST, st.HostComm())
+    assert lib.st_setup(ctypes.byref(g), ctypes.byref(m), ctypes.byref(b), ctypes.byref(s), None,
+                        ctypes.byref(d), ctypes.byref(h)) == -2
+    g = st.Grid(2, 16, 16, 1.0, 1.0)
+    assert lib.st_setup(ctypes.byref(g), ctypes.byref(m), ctypes.byref(b), ctypes.byref(s), None,
+                        ctypes.byref(d), ctypes.byref(h)) == -1  # host transport without callbacks
+    d = st.Dist(None, 0, 4, None, -1, st.ST_COMM_NONE, st.HostComm())
+    assert lib.st_setup(ctypes.byref(g), ctypes.byref(m), ctypes.byref(b), ctypes.byref(s), None,
+                        ctypes.byref(d), ctypes.byref(h)) == -1

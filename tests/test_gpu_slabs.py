@@ -1,0 +1,138 @@
+"""Time slabs on one GPU: G ranks, each a process with its own slab of the
+space-time grid on cuda:0, exchanging halo planes, Krylov sums and agglomerated coarse levels
+through the host-callback transport (torch.distributed gloo). The kernels never wait on each
+other: every exchange is a host call. Results are compared with the oracle's direct solution
+(north_star tolerances) and with the single-rank iteration count (partition invariance)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle as O
+import st_inputs as I
+from gpu_util import CFG1_MATS, CFG4_MATS, rel
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, size, port, case, q):
+    try:
+        import torch
+        import torch.distributed as dist
+        import paper_2508_09589_b200 as S
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import datetime
+        dist.init_process_group("gloo", rank=rank, world_size=size, timeout=datetime.timedelta(seconds=180))
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda:0")
+        sdim, n, nt, mats, T0, src, tau, design, tc, agg = case
+        hc = S.TorchHostComm() if size > 1 else None
+        solver = S.Solver(sdim, n, nt, mats=mats, T0=T0, source=src, tau=tau, time_constant=tc, rank=rank,
+                          size=size, host_comm=hc, rtol=1e-10, maxit=400, agg_nodes=agg)
+        lay = solver.layout()
+        rho = I.rho_uniform((n,) * sdim if tc else (nt,) + (n,) * sdim, 0) if design == "uniform" else \
+            I.design_for(sdim, n, nt, design, 0)
+        prob = O.Problem(O.Mesh(sdim, n, nt, tau=tau), O.Materials(*mats), O.BCs(T0=T0), O.Source(*src))
+        P = (n + 1) ** sdim
+        p0, npl = lay["plane0"], lay["n_planes"]
+        if tc:
+            rho_loc = rho
+        else:
+            rho_loc = rho[lay["layer0"]:lay["layer0"] + lay["rho_layers"]]
+        rd = torch.as_tensor(np.ascontiguousarray(rho_loc), device=dev)
+        T = torch.zeros(npl * P, dtype=torch.float64, device=dev)
+        solver.solve(rd, T)
+        st_f = solver.stats()
+        g = prob.compliance_rhs()[p0 * P:(p0 + npl) * P]
+        lam = torch.zeros_like(T)
+        solver.adjoint(rd, torch.as_tensor(g, device=dev), lam)
+        st_a = solver.stats()
+        nd = n ** sdim * (1 if tc else lay["n_layers"])
+        dJ = torch.zeros(nd, dtype=torch.float64, device=dev)
+        solver.sensitivity(rd, T, lam, dJ)
+        torch.cuda.synchronize()
+        out = dict(rank=rank, lay=lay, T=T.cpu().numpy(), lam=lam.cpu().numpy(), dJ=dJ.cpu().numpy(),
+                   its=(st_f["iterations"], st_a["iterations"]), conv=(st_f["converged"], st_a["converged"]))
+        solver.close()
+        if size > 1:
+            dist.barrier()
+        dist.destroy_process_group()
+        q.put(out)
+    except Exception as e:  # noqa: BLE001
+        import traceback
+        q.put(dict(rank=rank, error=traceback.format_exc()))
+
+
+def _run(case, size):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, size, port, case, q)) for r in range(size)]
+    for p in procs:
+        p.start()
+    res = []
+    try:
+        for _ in procs:
+            r = q.get(timeout=400)
+            assert "error" not in r, r["error"]  # report the first failing rank at once
+            res.append(r)
+    finally:
+        for p in procs:
+            p.join(timeout=5)
+            if p.is_alive():
+                p.terminate()
+    return sorted(res, key=lambda r: r["rank"])
+
+
+CASES = {
+    # sdim, n, nt, mats, T0, source, tau, design, time-constant, agg_nodes
+    "cfg1": (2, 16, 16, CFG1_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0), 1.0, "uniform", False, 64),
+    "cfg2-replica": (2, 32, 32, CFG1_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0), 1.0, "smooth_tc", True, 64),
+    "cfg3-replica": (2, 32, 32, CFG1_MATS, 0.0, ("sin", 1.0, 1.0, 2 * np.pi), 1.0, "smooth_layers", False, 64),
+    "cfg4-replica": (3, 6, 12, CFG4_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0), 1.0, "smooth_tc", True, 64),
+    "T0-cfg4mats": (2, 12, 16, CFG4_MATS, 0.7, ("sin", 1.0, 1.0, 2 * np.pi), 1.0, "uniform", False, 64),
+}
+
+
+@pytest.mark.parametrize("size", [2, 4])
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_time_slabs_match_oracle(name, size):
+    case = CASES[name]
+    sdim, n, nt, mats, T0, src, tau, design, tc, agg = case
+    if nt % size:
+        pytest.skip("nt not divisible")
+    res = _run(case, size)
+    T = np.concatenate([r["T"] for r in res])
+    lam = np.concatenate([r["lam"] for r in res])
+    dJ = sum(r["dJ"] for r in res) / size if tc else np.concatenate([r["dJ"] for r in res])
+    if tc:  # every rank returns the same globally summed field
+        for r in res:
+            assert rel(r["dJ"], res[0]["dJ"]) <= 1e-14
+    rho = I.rho_uniform((n,) * sdim if tc else (nt,) + (n,) * sdim, 0) if design == "uniform" else \
+        I.design_for(sdim, n, nt, design, 0)
+    prob = O.Problem(O.Mesh(sdim, n, nt, tau=tau), O.Materials(*mats), O.BCs(T0=T0), O.Source(*src))
+    T_ref, lam_ref = prob.solve_both(rho)
+    dJ_ref = prob.sensitivity(rho, T_ref, lam_ref)
+    assert all(r["conv"] == (1, 1) for r in res)
+    assert rel(T, T_ref) <= 1e-8, rel(T, T_ref)
+    assert rel(lam, lam_ref) <= 1e-8, rel(lam, lam_ref)
+    assert rel(dJ.reshape(dJ_ref.shape), dJ_ref) <= 1e-7, rel(dJ.reshape(dJ_ref.shape), dJ_ref)
+    # partition invariance of the method: the same iteration counts as one rank (+-1: rounding order)
+    ref1 = _run(case, 1)[0]
+    assert abs(res[0]["its"][0] - ref1["its"][0]) <= 1 and abs(res[0]["its"][1] - ref1["its"][1]) <= 1, \
+        (res[0]["its"], ref1["its"])

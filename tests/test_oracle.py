@@ -369,3 +369,25 @@ def test_algorithm1_odd_raises_and_stop_rule():
     lv = O.algorithm1(256, 256, np.sqrt(1e-3), max_nodes=25000)
     assert (lv[-1][0] + 1) ** 2 * (lv[-1][1] + 1) <= 25000
     assert [k for *_, k in lv][:4] == ["fine", "space", "space", "space"]
+
+
+@pytest.mark.parametrize("sdim,n,nt,tc", [(2, 5, 6, False), (3, 3, 4, True), (2, 6, 4, True)])
+def test_sampled_rows_and_elements_equal_assembled(sdim, n, nt, tc):
+    """row_apply / sensitivity_elements (used to certify full-size GPU results, R-21)
+    equal the assembled K_bc, K_bc^T and the vectorised sensitivities on every row / element."""
+    rng = np.random.default_rng(3)
+    mesh = O.Mesh(sdim, n, nt)
+    prob = O.Problem(mesh, O.Materials(0.1, 1.0, 1.0, 1e-4, 1.0, 3.0), O.BCs(T0=0.4), O.Source("sin", 1.0, 1.0, 6.0))
+    rho = rng.uniform(0.1, 1.0, (n,) * sdim if tc else (nt,) + (n,) * sdim)
+    Kbc, _, _, _ = prob.system(rho)
+    x = rng.uniform(-1, 1, mesh.n_nodes)
+    allrows = np.arange(mesh.n_nodes)
+    assert np.allclose(O.row_apply(prob, rho, x, allrows), Kbc @ x, rtol=0, atol=1e-14)
+    assert np.allclose(O.row_apply(prob, rho, x, allrows, transpose=True), Kbc.T @ x, rtol=0, atol=1e-14)
+    T, lam = prob.solve_both(rho)
+    dJ = prob.sensitivity(rho, T, lam)
+    # space-time elements; a time-constant design sums them through time
+    per = O.sensitivity_elements(prob, np.broadcast_to(rho, (nt,) + (n,) * sdim).copy() if tc else rho, T, lam,
+                                 np.arange(mesh.n_elems))
+    ref = per.reshape(nt, -1).sum(axis=0).reshape(dJ.shape) if tc else per.reshape(dJ.shape)
+    assert np.allclose(ref, dJ, rtol=1e-12, atol=1e-15)
