@@ -322,7 +322,7 @@ def run_cuda(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "fine-level damped-Jacobi sweep (" + ("tc2d_kernel, time-constant rho" if wl["tc"] and wl["sdim"] == 2
                                                               else "tma2d_kernel, space-time rho" if wl["sdim"] == 2
-                                                              else "op_kernel<3>, (3+1)D") + ")",
+                                                              else "tc3d_kernel, (3+1)D time-constant rho") + ")",
                      "bytes_per_launch": alg_bytes, "us_per_launch": t_sweep * 1e6,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,

@@ -163,6 +163,8 @@ typedef struct {
   int32_t kind[32];          /* 0 fine, 1 space, 2 time, 3 full                            */
   int32_t form[32];          /* operator storage: 0 matrix-free (rho), 1 MK, 2 block-4, 3 dense */
   int64_t nodes[32];
+  double omega[32];          /* damped-Jacobi weight of the level (last design)                */
+  double lam_max[32];        /* Gershgorin bound on |lambda|_max(D^-1 A)     */
 } st_hierarchy_t;
 
 /* Fill `o` with the library defaults (rtol 1e-8, restart 16, Jacobi nu 3/3 omega 0.75,
@@ -195,6 +197,10 @@ int st_sensitivity(st_ctx_t* ctx, const double* rho, const double* T, const doub
 /* Test hook: y = K x (transpose = 0) or K^T x (1); bc = 1 applies the eliminated
  * operator m_f K m_f + m_c, bc = 0 the unconstrained K. */
 int st_apply(st_ctx_t* ctx, const double* rho, const double* x, double* y, int transpose, int bc);
+
+/* Test hook: z = M b, one multigrid V-cycle (the FGMRES preconditioner) of the
+ * forward (transpose = 0) or adjoint (1) operator; b, z: this rank's owned planes. */
+int st_vcycle(st_ctx_t* ctx, const double* rho, const double* b, double* z, int transpose);
 
 /* Source vector f and the eliminated right-hand side b. */
 int st_rhs(st_ctx_t* ctx, const double* rho, double* f, double* b);

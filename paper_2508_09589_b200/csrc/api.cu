@@ -51,6 +51,8 @@ struct Level {
   int nloc = 0, a = 0;   // dist: owned element layers [a, a + nloc) = node planes (a, a + nloc]
   bool gather_in = false;  // first replicated level below a distributed one
   Geom gs{};             // gather_in: this level in slab form (restriction / stencils before gather)
+  double omega = 0.0;    // damped-Jacobi weight of this level (per design)
+  double lam_max = 0.0;  // power-iteration estimate of |lambda|_max(D^-1 A) of this level
   double* bpart = nullptr;
   double* stpart = nullptr;
   long long stpart_elems = 0;
@@ -365,7 +367,13 @@ double* vec_alloc(st_ctx* c, long long count) {
 void allocate(st_ctx* c) {
   const long long N = c->N;
   const int m = c->opt.restart;
-  c->guard = (c->lv[0].g.pr + 2 + 31) / 32 * 32;
+  // zeroed front guard: the TMA x maps are based one row (2D) / one slice + one row (3D) + 2
+  // entries before the data
+  {
+    const Geom& g0 = c->lv[0].g;
+    const long long need = (c->sd == 3 ? (long long)g0.pr * g0.nn : 0) + g0.pr + 2;
+    c->guard = (need + 31) / 32 * 32;
+  }
   c->ld = (N + c->guard + 31) / 32 * 32;   // vector j's guard = tail of slot j-1 (never written)
   c->f = vec_alloc(c, N);
   c->b = vec_alloc(c, N);
@@ -379,6 +387,7 @@ void allocate(st_ctx* c) {
   CK(cudaMemsetAsync(c->ws.counter, 0, sizeof(unsigned), c->stream));
   dalloc(&c->dsmall, 512);
   CK(cudaMallocHost((void**)&c->hsmall, 512 * sizeof(double)));
+  if ((long long)c->comm.size * (long long)c->lv.size() > 140) throw StErr{ST_E_INVALID_ARG, "too many ranks x levels"};
   for (size_t l = 0; l < c->lv.size(); ++l) {
     Level& Lv = c->lv[l];
     const long long n = Lv.g.N;
@@ -422,7 +431,7 @@ void allocate(st_ctx* c) {
 void op_launch(st_ctx* c, int l, int mode, bool trans, bool mask, const double* x, const double* b, double* y) {
   g_use_fast = c->fast;
   g_fast_kind = c->fast_kind;
-  launch_op(c->lv[l].op, mode, trans, mask, x, b, y, c->opt.omega, c->stream);
+  launch_op(c->lv[l].op, mode, trans, mask, x, b, y, c->lv[l].omega > 0.0 ? c->lv[l].omega : c->opt.omega, c->stream);
   L(c);
 }
 
@@ -471,10 +480,70 @@ bool bind_rho(st_ctx* c, const double* rho_in) {
   return changed;
 }
 
+// owned node planes of a level vector (slab: without ghosts; replicated: all)
+void owned_range(const st_ctx* c, int l, long long* off, long long* cnt) {
+  const Level& Lv = c->lv[l];
+  if (Lv.dist) {
+    const int o0 = c->comm.rank > 0 ? 1 : 0;
+    *off = (long long)o0 * Lv.g.P;
+    *cnt = (long long)(Lv.nloc + (c->comm.rank == 0 ? 1 : 0)) * Lv.g.P;
+  } else {
+    *off = 0;
+    *cnt = Lv.g.N;
+  }
+}
+
+// Per-level Jacobi weight: the capacity term is an upwind difference in time,
+// so on capacity-dominated levels the spectrum of D^-1 A fills a disk through 0 of diameter
+// R = |lambda|_max (R = 2 x mass row-sum / diagonal: 4.5 in 2D, 6.75 in 3D) and damped Jacobi is
+// stable iff omega R / 2 < 1. R is bounded by the row-wise Gershgorin ratio max_i sum_j |A_ij| /
+// |A_ii| (one pass over the level's stencils, every design); omega_l = min(omega_cap, 1.8 / R).
+void estimate_omegas(st_ctx* c) {
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(c->dsmall + 320);
+  const int nl = (int)c->lv.size();
+  CK(cudaMemsetAsync(d, 0, nl * sizeof(double), c->stream));
+  for (int l = 0; l < nl; ++l) {
+    const Level& Lv = c->lv[l];
+    if (Lv.dense) continue;
+    // time-constant: interior row type (plane 1) and the last plane; else every local row
+    // (ghost planes of a slab: row 0 is skipped by pa = 1; the top ghost row is not a real row)
+    const int pa = 1, pb = Lv.g.nt - ((Lv.dist && c->comm.rank < c->comm.size - 1) ? 1 : 0);
+    if (!Lv.op.tvl && !(Lv.op.form == FORM_RHO && !Lv.op.rho_tc)) {
+      launch_gersh(Lv.op, 1, std::min(2, Lv.g.nt), d + l, c->stream);
+      launch_gersh(Lv.op, Lv.g.nt, Lv.g.nt, d + l, c->stream);
+      L(c, 2);
+    } else {
+      launch_gersh(Lv.op, pa, pb, d + l, c->stream);
+      L(c);
+    }
+  }
+  check_launch();
+  // max over ranks: gather every rank's values (the host transport has sums and gathers only)
+  const int G = c->comm.size;
+  double* gat = c->dsmall + 352;  // G * nl doubles (G * nl <= 160)
+  if (G > 1) comm_call([&] { comm_allgather(c->comm, c->dsmall + 320, gat, nl, c->stream); });
+  CK(cudaMemcpyAsync(c->hsmall + 352, G > 1 ? gat : c->dsmall + 320, (size_t)G * nl * sizeof(double),
+                     cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int l = 0; l < nl; ++l) {
+    Level& Lv = c->lv[l];
+    double R = 0.0;
+    for (int r = 0; r < G; ++r) R = std::max(R, c->hsmall[352 + r * nl + l]);
+    Lv.lam_max = R;
+    Lv.omega = (R > 0.0 && std::isfinite(R)) ? std::min(c->opt.omega, 1.8 / R) : c->opt.omega;
+  }
+}
+
 // rho-dependent setup: Galerkin coarse operators, dense coarsest inverse,
 // eliminated right-hand side b.
 void build_ops(st_ctx* c) {
   CK(cudaEventRecord(c->e0, c->stream));
+  // the per-level Jacobi weights are re-estimated per design: drop captured V-cycle graphs
+  for (int d = 0; d < 2; ++d) {
+    if (c->gexec[d]) cudaGraphExecDestroy(c->gexec[d]);
+    c->gexec[d] = nullptr;
+    c->geager[d] = 0;
+  }
   const int NC = nc_of(c->sd);
   for (size_t l = 1; l < c->lv.size(); ++l) {
     Level& Lv = c->lv[l];
@@ -536,6 +605,7 @@ void build_ops(st_ctx* c) {
     L(c);
   }
   check_launch();
+  estimate_omegas(c);
   CK(cudaEventRecord(c->e1, c->stream));
   CK(cudaEventSynchronize(c->e1));
   int info = 0;
@@ -1112,6 +1182,20 @@ int st_level_apply(st_ctx_t* c, const double* rho, int level, const double* x, d
   });
 }
 
+int st_vcycle(st_ctx_t* c, const double* rho, const double* b, double* z, int transpose) {
+  return guarded([&]() -> int {
+    if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
+    CK(cudaSetDevice(c->device));
+    prepare(c, rho);
+    pack_in(c, b, c->tmpN2, 1);
+    launch_mask_free(c->lv[0].g, c->tmpN2, c->tmpN2, c->stream);  // the solver's vectors vanish there
+    L(c);
+    vcycle(c, 0, transpose != 0, c->tmpN2, c->tmpN);
+    unpack_out(c, c->tmpN, z, 2);
+    return ST_OK;
+  });
+}
+
 int st_rhs(st_ctx_t* c, const double* rho, double* f, double* b) {
   return guarded([&]() -> int {
     if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
@@ -1164,6 +1248,8 @@ int st_get_hierarchy(const st_ctx_t* c, st_hierarchy_t* h) {
     long long v = Lv.ntg + 1;
     for (int d = 0; d < Lv.g.sd; ++d) v *= Lv.g.nn;
     h->nodes[l] = v;
+    h->omega[l] = Lv.omega;
+    h->lam_max[l] = Lv.lam_max;
   }
   return ST_OK;
 }

@@ -17,12 +17,20 @@ bool launch_op_tma2d(const OpDesc& op, int mode, bool trans, bool mask, const do
 // tc2d.cu: lean TMA kernel for time-constant levels (fine from rho, stored MK), masked modes
 bool launch_op_tc2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                     double omega, cudaStream_t s);
+// tc3d.cu: (3+1)D TMA kernel for time-constant levels (fine from rho, stored MK), masked modes
+bool launch_op_tc3d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
+                    double omega, cudaStream_t s);
+// tv2d.cu: fine level of a space-time design with uniform capacity (configs 1, 3, 5), masked modes
+bool launch_op_tv2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
+                    double omega, cudaStream_t s);
 extern bool g_use_fast;
 extern int g_fast_kind;  // 0: TMA, 1: cp.async (fast2d)
 void launch_rap_space(const OpDesc& fop, const Geom& gc, int nl, int ns, double* out, cudaStream_t s);
 void launch_rap_time(const OpDesc& fop, int nlc, double* out, cudaStream_t s);
 void launch_rho_to_mk(const OpDesc& fop, int tau, double* out, cudaStream_t s);
 void launch_dense_assemble(const OpDesc& op, double* A, cudaStream_t s);
+// max over rows of local planes [pa, pb] of sum_j |A_ij| / |A_ii| (bits of a positive double, atomicMax)
+void launch_gersh(const OpDesc& op, int pa, int pb, unsigned long long* out, cudaStream_t s);
 
 // transfer.cu — restriction r_c = m_f^c P^T r_f, prolongation x_f += m_f P e_c
 void launch_restrict(const Geom& gf, const Geom& gc, int kind, const double* rf, double* rc, cudaStream_t s);
@@ -55,7 +63,8 @@ void launch_copy_cons(const Geom& g, const double* src, double* dst, cudaStream_
 void launch_relayout(const Geom& gs, const double* src, const Geom& gd, double* dst, cudaStream_t s);
 void launch_set_bc_values(const Geom& g, double T0, double* x, cudaStream_t s);          // x_c = xD
 void launch_rhs_combine(const Geom& g, const double* f, const double* KxD, double T0, double* b, cudaStream_t s);
-void launch_xd(const Geom& g, double T0, double* x, cudaStream_t s);                      // x = xD (0 off plane 0)
+void launch_xd(const Geom& g, double T0, double* x, cudaStream_t s);
+void launch_hash_vec(const Geom& g, double* v, cudaStream_t s);                            // power-iteration start                      // x = xD (0 off plane 0)
 void launch_sensitivity(const OpDesc& op, const double* T, const double* lam, double* dJ, cudaStream_t s);
 void launch_dense_invert(double* A, double* Ainv, int n, int* info, cudaStream_t s);
 void launch_dense_solve(const double* Ainv, int n, bool trans, const double* b, double* x, cudaStream_t s);

@@ -79,6 +79,24 @@ __global__ void rhs_kernel(Geom g, const double* __restrict__ f, const double* _
   else b[idx] = f[idx] - (KxD ? KxD[idx] : 0.0);
 }
 
+// power-iteration start vector: a fixed hash in (-1/2, 1/2] at free nodes, 0 elsewhere (pads,
+// constrained nodes); global node numbering, so every partition starts from the same vector
+template <int SD> __global__ void hash_vec_kernel(Geom g, double* __restrict__ v) {
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= g.N) return;
+  int c[3] = {0, 0, 0}, p;
+  if (!node_of<SD>(g, idx, c, p) || is_cons<SD>(g, c, p)) { v[idx] = 0.0; return; }
+  long long gid = (long long)(p + g.pg0) * g.P + (idx % g.P);
+  unsigned long long z = (unsigned long long)gid * 0x9E3779B97F4A7C15ull;
+  z ^= z >> 31; z *= 0xBF58476D1CE4E5B9ull; z ^= z >> 27;
+  v[idx] = (double)(z >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+}
+void launch_hash_vec(const Geom& g, double* v, cudaStream_t s) {
+  unsigned grd = (unsigned)((g.N + 255) / 256);
+  if (g.sd == 2) hash_vec_kernel<2><<<grd, 256, 0, s>>>(g, v);
+  else hash_vec_kernel<3><<<grd, 256, 0, s>>>(g, v);
+}
+
 // relayout between two storage geometries of the same grid (dense caller layout <-> padded
 // internal layout); iterates over the source storage, skips its pads
 template <int SD>

@@ -340,6 +340,8 @@ int g_fast_kind = 0;
 void launch_op(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                double omega, cudaStream_t s) {
   if (g_use_fast && g_fast_kind == 0 && launch_op_tc2d(op, mode, trans, mask, x, b, y, omega, s)) return;
+  if (g_use_fast && g_fast_kind == 0 && launch_op_tc3d(op, mode, trans, mask, x, b, y, omega, s)) return;
+  if (g_use_fast && g_fast_kind == 0 && launch_op_tv2d(op, mode, trans, mask, x, b, y, omega, s)) return;
   if (g_use_fast && (g_fast_kind == 0 || g_fast_kind == 2) && launch_op_tma2d(op, mode, trans, mask, x, b, y, omega, s)) return;
   if (g_use_fast && launch_op_fast2d(op, mode, trans, mask, x, b, y, omega, s)) return;
   if (op.g.sd == 2) {
@@ -566,6 +568,75 @@ void launch_rho_to_mk(const OpDesc& fop, int tau, double* out, cudaStream_t s) {
   long long grd = (fop.g.P + blk - 1) / blk;
   if (fop.g.sd == 2) rho_to_mk_kernel<2><<<(unsigned)grd, blk, 0, s>>>(fop, tau, out);
   else rho_to_mk_kernel<3><<<(unsigned)grd, blk, 0, s>>>(fop, tau, out);
+}
+
+// ---------------------------------------------------------------------------------------
+// Row-wise Gershgorin ratio max_i sum_j |A_ij| / |A_ii| of the eliminated level operator
+// (bound on |lambda|_max(D^-1 A) for the per-level Jacobi weight). Rows of local
+// planes [pa, pb]; a time-constant level has only two row types (interior, last plane), so the
+// caller passes pa = 1 and the plane count is irrelevant apart from the last-row test.
+template <int SD, int FORM>
+__global__ void gersh_kernel(OpDesc op, int pa, int pb, unsigned long long* __restrict__ out) {
+  constexpr int NOFF = SG<SD>::NOFF, CEN = SG<SD>::CEN;
+  const Geom& g = op.g;
+  const long long nper = g.P;
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double best = 0.0;
+  if (idx < nper * (pb - pa + 1)) {
+    const int p = pa + (int)(idx / nper);
+    const long long pn = idx % nper;
+    int c[3] = {0, 0, 0};
+    if (pdecode<SD>(g, pn, c) && !is_cons<SD>(g, c, p)) {
+      double diag = 0.0, sum = 0.0;
+      for (int k = 0; k < NOFF; ++k) {
+        int nb[3] = {0, 0, 0};
+        bool ok = true;
+        for (int d = 0; d < SD; ++d) {
+          nb[d] = c[d] + SG<SD>::od(k, d);
+          ok = ok && nb[d] >= 0 && nb[d] < g.nn;
+        }
+        if (!ok) continue;
+        // columns on planes p-1, p, p+1 (eliminated constrained columns are zero)
+        double wlo = 0.0, wmid = 0.0, whi = 0.0;
+        if (p >= 1) {  // layer p-1: top rows
+          wlo = block_weight<SD, FORM>(op, c, pn, p - 1, 1, 0, k);
+          wmid = block_weight<SD, FORM>(op, c, pn, p - 1, 1, 1, k);
+        }
+        if (p < g.nt) {  // layer p: bottom rows
+          wmid += block_weight<SD, FORM>(op, c, pn, p, 0, 0, k);
+          whi = block_weight<SD, FORM>(op, c, pn, p, 0, 1, k);
+        }
+        if (k == CEN) diag = wmid;
+        if (p >= 1 && !is_cons<SD>(g, nb, p - 1)) sum += fabs(wlo);
+        if (!is_cons<SD>(g, nb, p)) sum += fabs(wmid);
+        if (p < g.nt && !is_cons<SD>(g, nb, p + 1)) sum += fabs(whi);
+      }
+      if (diag != 0.0) best = sum / fabs(diag);
+    }
+  }
+  // block max, then one atomic per block (positive doubles order like their bit patterns)
+  for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_down_sync(0xffffffffu, best, o));
+  __shared__ double wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, wm[w]);
+    atomicMax(out, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+void launch_gersh(const OpDesc& op, int pa, int pb, unsigned long long* out, cudaStream_t s) {
+  long long total = op.g.P * (long long)(pb - pa + 1);
+  if (total <= 0) return;
+  unsigned grd = (unsigned)((total + 255) / 256);
+#define GK(SD, F) gersh_kernel<SD, F><<<grd, 256, 0, s>>>(op, pa, pb, out)
+  if (op.g.sd == 2) {
+    if (op.form == FORM_RHO) GK(2, FORM_RHO); else if (op.form == FORM_MK) GK(2, FORM_MK); else GK(2, FORM_B4);
+  } else {
+    if (op.form == FORM_RHO) GK(3, FORM_RHO); else if (op.form == FORM_MK) GK(3, FORM_MK); else GK(3, FORM_B4);
+  }
+#undef GK
 }
 
 // ---------------------------------------------------------------------------------------

@@ -83,11 +83,12 @@ class Stats(C.Structure):
 
 class Hierarchy(C.Structure):
     _fields_ = [("n_levels", C.c_int32), ("n", C.c_int64 * 32), ("nt", C.c_int64 * 32),
-                ("kind", C.c_int32 * 32), ("form", C.c_int32 * 32), ("nodes", C.c_int64 * 32)]
+                ("kind", C.c_int32 * 32), ("form", C.c_int32 * 32), ("nodes", C.c_int64 * 32),
+                ("omega", C.c_double * 32), ("lam_max", C.c_double * 32)]
 
 
 EXPORTS = ["st_abi_version", "st_default_options", "st_setup", "st_destroy", "st_solve", "st_adjoint",
-           "st_sensitivity", "st_apply", "st_rhs", "st_level_apply", "st_bench_op", "st_get_stats", "st_get_hierarchy",
+           "st_sensitivity", "st_apply", "st_vcycle", "st_rhs", "st_level_apply", "st_bench_op", "st_get_stats", "st_get_hierarchy",
            "st_local_layout", "st_nccl_unique_id", "st_nccl_comm_init", "st_nccl_comm_destroy", "st_plan",
            "st_struct_sizes",
            "st_num_nodes", "st_num_design", "st_kernel_launches", "st_strerror", "st_last_error"]
@@ -119,6 +120,7 @@ def load_library(path: str = LIB_PATH):
     lib.st_sensitivity.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.st_apply.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]
     lib.st_rhs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.st_vcycle.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
     lib.st_level_apply.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
     lib.st_bench_op.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
     lib.st_get_stats.argtypes = [C.c_void_p, P(Stats)]
@@ -300,6 +302,10 @@ class Solver:
     def apply(self, rho, x, y, transpose=False, bc=True):
         return self._check(self.lib.st_apply(self.ctx, _ptr(rho), _ptr(x), _ptr(y), int(transpose), int(bc)))
 
+    def vcycle(self, rho, b, z, transpose=False):
+        """z = one V-cycle applied to b (test hook)."""
+        return self._check(self.lib.st_vcycle(self.ctx, _ptr(rho), _ptr(b), _ptr(z), int(transpose)))
+
     def level_apply(self, rho, level, x, y, transpose=False):
         return self._check(self.lib.st_level_apply(self.ctx, _ptr(rho), level, _ptr(x), _ptr(y), int(transpose)))
 
@@ -321,8 +327,8 @@ class Solver:
         self.lib.st_get_hierarchy(self.ctx, C.byref(h))
         kinds = ["fine", "space", "time", "full"]
         forms = ["rho", "mk", "b4", "dense"]
-        return [dict(n=h.n[i], nt=h.nt[i], kind=kinds[h.kind[i]], form=forms[h.form[i]], nodes=h.nodes[i])
-                for i in range(h.n_levels)]
+        return [dict(n=h.n[i], nt=h.nt[i], kind=kinds[h.kind[i]], form=forms[h.form[i]], nodes=h.nodes[i],
+                     omega=h.omega[i], lam_max=h.lam_max[i]) for i in range(h.n_levels)]
 
     def layout(self):
         lay = Layout()

@@ -1,5 +1,6 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
-timeout 1500 python -m pytest tests/test_gpu_slabs.py -q -k "cfg2" > gpurun_out/pytest_slabs.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_slabs.log
+timeout 600 python scripts/debug_conv.py > gpurun_out/debug_conv.log 2>&1
 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 timeout 600 python bench.py --config 4 --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench4.log 2>&1; echo "rc=$?" >> gpurun_out/bench4.log

@@ -36,6 +36,7 @@ OP_CASES = [
     (2, 7, 5, CFG4_MATS, 0.0, "uniform", 4, False),
     (3, 4, 6, CFG4_MATS, 0.2, "uniform", 0, False),
     (3, 6, 12, CFG4_MATS, 0.0, "smooth_tc", 0, True),
+    (3, 10, 8, CFG4_MATS, 0.2, "smooth_tc", 1, True),     # (3+1)D TMA kernel: several 32x4x2 tiles, ragged
 ]
 
 
@@ -148,7 +149,8 @@ def _P1(nf, kind):
     return P
 
 
-@pytest.mark.parametrize("sdim,n,nt,tc", [(2, 16, 16, False), (2, 32, 32, True), (3, 4, 8, False), (2, 8, 32, False)])
+@pytest.mark.parametrize("sdim,n,nt,tc", [(2, 16, 16, False), (2, 32, 32, True), (3, 4, 8, False), (2, 8, 32, False),
+                                            (3, 8, 8, True)])
 def test_coarse_operators(sdim, n, nt, tc):
     """Each coarse level equals, with the Dirichlet masks of its own grid, the operator built
     here independently from assembled matrices: conduction part
@@ -214,13 +216,14 @@ def test_iteration_counts_reasonable():
     solver.close()
 
 
-KERNEL_VARIANTS = {"tma": ("0", "0"), "cpasync": ("0", "1"), "generic": ("1", "0")}  # ST_NO_FAST, ST_FAST_KIND
+KERNEL_VARIANTS = {"tma": ("0", "0"), "cpasync": ("0", "1"), "tma2d": ("0", "2"), "generic": ("1", "0")}  # ST_NO_FAST, ST_FAST_KIND
 
 
 @pytest.mark.parametrize("variant", sorted(KERNEL_VARIANTS))
 @pytest.mark.parametrize("case", [(2, 32, 32, "smooth_tc", True), (2, 16, 16, "uniform", False),
-                                  (2, 40, 7, "uniform", False), (2, 64, 24, "smooth_tc", True)],
-                         ids=lambda c: f"{c[1]}x{c[2]}-{'tc' if c[4] else 'st'}")
+                                  (2, 40, 7, "uniform", False), (2, 64, 24, "smooth_tc", True),
+                                  (3, 8, 6, "smooth_tc", True)],
+                         ids=lambda c: f"{c[0]}d-{c[1]}x{c[2]}-{'tc' if c[4] else 'st'}")
 def test_operator_parity_all_kernel_variants(variant, case, monkeypatch):
     """Every (2+1)D operator kernel (TMA ring, cp.async ring, generic) gives the oracle's K x and
     K^T x on every level kind it serves; the grids span several 32 x 8 tiles with ragged tails and
@@ -246,4 +249,28 @@ def test_operator_parity_all_kernel_variants(variant, case, monkeypatch):
     solver.solve(dev(rho), T)
     assert solver.stats()["converged"] == 1
     assert rel(host(T), T_ref) <= 1e-8
+    solver.close()
+
+
+@pytest.mark.parametrize("sdim,n,nt,tc,mats", [(2, 12, 10, True, CFG1_MATS), (2, 8, 12, False, CFG4_MATS),
+                                               (3, 4, 6, True, CFG4_MATS)])
+def test_jacobi_weight_bound(sdim, n, nt, tc, mats):
+    """The fine level's Gershgorin ratio equals max_i sum_j |A_ij| / |A_ii| of the
+    oracle's K_bc over free rows, bounds the spectral radius of D^-1 K_bc, and omega = min(cap, 1.8/R)."""
+    solver, prob = make_pair(sdim, n, nt, mats=mats, time_constant=tc)
+    rho = _rho(sdim, n, nt, "uniform", 2, tc)
+    x = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+    solver.apply(dev(rho), x, torch.empty_like(x))      # binds rho
+    solver.rhs(dev(rho), None, None)                    # rho-dependent setup (incl. the weights)
+    H = solver.hierarchy()
+    Kbc, _, cons, _ = prob.system(rho)
+    A = abs(Kbc).tocsr()
+    d = np.abs(Kbc.diagonal())
+    ratio = np.asarray(A.sum(axis=1)).ravel() / d
+    R_ref = ratio[~cons].max()
+    assert abs(H[0]["lam_max"] - R_ref) <= 1e-12 * R_ref, (H[0]["lam_max"], R_ref)
+    DinvK = (Kbc.toarray() / Kbc.diagonal()[:, None])
+    rho_spec = np.abs(np.linalg.eigvals(DinvK)).max()
+    assert rho_spec <= H[0]["lam_max"] * (1 + 1e-12)
+    assert abs(H[0]["omega"] - min(0.75, 1.8 / R_ref)) <= 1e-14
     solver.close()
