@@ -42,8 +42,10 @@ WORKLOADS = {
             design="uniform", source=("uniform", 1.0, 0.0, 0.0), tau=1.0),
     4: dict(name="config4: (3+1)D 64^3x128, time-constant smooth rho, c=0.1+0.9rho, k_min=1e-4", sdim=3, n=64,
             nt=128, mats=CFG4_MATS, tc=True, design="smooth_tc", source=("uniform", 1.0, 0.0, 0.0), tau=1.0),
-    5: dict(name="config5 (per GPU): (2+1)D 512^2x512, space-time design", sdim=2, n=512, nt=512, mats=CFG1_MATS,
-            tc=False, design="const", source=("uniform", 1.0, 0.0, 0.0), tau=1.0),
+    5: dict(name="config5 (per GPU): (2+1)D 512^2x512, space-time design; a step = one OC design iteration "
+                 "(density filter r=2, forward, adjoint, sensitivities, filter^T, OC volfrac 0.4) from rho=0.4",
+            sdim=2, n=512, nt=512, mats=CFG1_MATS, tc=False, design="const", source=("uniform", 1.0, 0.0, 0.0),
+            tau=1.0),
     3: dict(name="config3-shaped (1/8 of config 3 on one GPU): (2+1)D 512^2x512, an independent smooth field per "
                  "time layer, Q(t) = 1 + sin(2 pi t)", sdim=2, n=512, nt=512, mats=CFG1_MATS, tc=False,
             design="smooth_layers", source=("sin", 1.0, 1.0, 6.283185307179586), tau=1.0),
@@ -202,18 +204,38 @@ def run_cuda(args):
         solver.rhs(rhos[0], f, None)
     its = []
 
+    design = args.config == 5  # a step is one config-5 design iteration (R-13)
+    if design:
+        rho_d = torch.full((solver.layout()["n_layers"] * wl["n"] ** wl["sdim"],), 0.4, dtype=torch.float64, device=dev)
+        rt = torch.empty(nd, dtype=torch.float64, device=dev)
+        dJt = torch.empty_like(rho_d)
+        dJd = torch.empty_like(rho_d)
+        rnew = torch.empty_like(rho_d)
+
     def step(i):
-        solver.solve(rhos[i], T)
-        a = solver.stats()
-        solver.adjoint(rhos[i], f, lam)
-        b = solver.stats()
-        solver.sensitivity(rhos[i], T, lam, dJ)
+        if design:  # filter -> solve -> adjoint -> sensitivities -> F^T -> OC (warm starts kept)
+            solver.filter(rho_d, rt)
+            solver.solve(rt, T)
+            a = solver.stats()
+            solver.adjoint(rt, f, lam)
+            b = solver.stats()
+            solver.sensitivity(rt, T, lam, dJt)
+            solver.filter(dJt, dJd, transpose=True)
+            solver.oc_update(rho_d, dJd, rnew)
+            rho_d.copy_(rnew)
+        else:
+            solver.solve(rhos[i], T)
+            a = solver.stats()
+            solver.adjoint(rhos[i], f, lam)
+            b = solver.stats()
+            solver.sensitivity(rhos[i], T, lam, dJ)
         its.append((a["iterations"], b["iterations"], a["solve_ms"], b["solve_ms"], b["setup_ms"],
                     a["rel_residual"], b["rel_residual"]))
 
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
-            T.zero_(); lam.zero_()
+            if not design:
+                T.zero_(); lam.zero_()
             step(i)
         its.clear()
         torch.cuda.synchronize()
@@ -225,7 +247,8 @@ def run_cuda(args):
         times = []
         for k in range(args.steps):
             flush.fill_(float(k))                      # L2 flush, outside the timed events
-            T.zero_(); lam.zero_()
+            if not design:                             # design loop: warm start
+                T.zero_(); lam.zero_()
             e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             step(args.warmup + k)

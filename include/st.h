@@ -24,7 +24,9 @@
  *  - Pointers may be DEVICE pointers (current device of the context) or HOST pointers;
  *    the library detects host memory (cudaPointerGetAttributes) and stages it through
  *    device buffers inside the call. Caller owns every vector; the context owns workspaces.
- *  - Every call enqueues on the context's stream and returns after completion.
+ *  - Every call enqueues on the context's stream and returns after completion. Without a
+ *    caller stream the context creates a blocking stream (ordered with the legacy default
+ *    stream, e.g. PyTorch's default stream).
  *  - Dirichlet data (R-1..R-4): T = T0 on the t = 0 node plane (initial
  *    condition); T = 0 on the sink patch of the face x1 = 0 (all t, including t = 0) whose
  *    transverse coordinates lie within halfwidth of center. Symmetric elimination with
@@ -214,6 +216,25 @@ int st_level_apply(st_ctx_t* ctx, const double* rho, int level, const double* x,
  * on the context's internal work vectors and return WITHOUT synchronising (the caller
  * brackets them with events on the context stream). rho: device pointer. */
 int st_bench_op(st_ctx_t* ctx, const double* rho, int level, int mode, int transpose, int reps);
+
+/* ---- Config-5 design loop (driver level: BASELINE config 5, R-13; NOT the paper's
+ * method, which uses a PDE filter, projection and MMA) ---------------------- */
+/* Density filter with hat weights max(0, radius - |index distance|) over the element grid
+ * (x1, x2[, x3], t); a time-constant design is filtered in space. transpose = 0: out = F in,
+ * in = this rank's owned element layers, out = the layers st_solve takes (owned + the next slab's
+ * first layer, filtered); transpose = 1 (chain rule): out = F^T in on the owned layers. */
+int st_filter(st_ctx_t* ctx, const double* in, double* out, int transpose, double radius);
+/* Optimality-criteria update rho_new = clip(rho sqrt(max(0, -dJ) / Lambda), [max(rho_min, rho - move),
+ * min(1, rho + move)]) with Lambda by bisection so that the mean over all elements (all ranks) is
+ * volfrac. rho, dJ, rho_new: owned element layers. Lambda is written to *lambda_out if non-null. */
+int st_oc_update(st_ctx_t* ctx, const double* rho, const double* dJ, double volfrac, double move, double rho_min,
+                 double* rho_new, double* lambda_out);
+/* The paper's objective: phi = (sum_e Tavg_e^P)^(1/P) over all elements (all ranks),
+ * Tavg_e the mean of the element's nodal temperatures (P = 20 in the paper), and, if dphidT is
+ * non-null, its gradient on this rank's owned planes — the adjoint RHS. */
+int st_pnorm(st_ctx_t* ctx, const double* T, double P, double* phi, double* dphidT);
+/* out = x . y over the owned nodes of all ranks (e.g. the compliance f^T T). */
+int st_dot(st_ctx_t* ctx, const double* x, const double* y, double* out);
 
 int st_get_stats(const st_ctx_t* ctx, st_stats_t* s);
 int st_local_layout(const st_ctx_t* ctx, st_layout_t* layout);

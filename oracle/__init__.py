@@ -23,3 +23,4 @@ values (tests/golden/), invariants, brute force and finite differences.
 from .stfem import *  # noqa: F401,F403
 from .hierarchy import algorithm1, d_eff  # noqa: F401
 from .timestep import backward_euler  # noqa: F401
+from .design import density_filter, oc_update, design_loop  # noqa: F401

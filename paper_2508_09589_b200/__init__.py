@@ -9,3 +9,4 @@ from .st import (  # noqa: F401
     nccl_unique_id, nccl_comm_init,
     ST_TIME_CONSTANT, ST_SPACE_TIME, ST_SRC_UNIFORM, ST_SRC_SIN, ST_COMM_NONE, ST_COMM_NCCL, ST_COMM_HOST,
 )
+from .design import design_loop  # noqa: F401,E402

@@ -101,6 +101,10 @@ struct st_ctx {
   // buffers): one per direction, captured after one eager run, valid for the context lifetime
   int gl0 = -1;
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  // fused small-level V-cycle (vsmall.cu): levels >= vs0 in one cluster kernel (-1: off)
+  int vs0 = -1;
+  // config-5 design update buffers (st_filter / st_oc_update), allocated on first use
+  double *fbuf = nullptr, *fw = nullptr;
   long long gkernels[2] = {0, 0};
   int geager[2] = {0, 0};
 };
@@ -347,7 +351,7 @@ void setup_forms(st_ctx* c) {
     }
     Lv.st_elems = Lv.st_owned ? (long long)op.nl * ns * NC * Lv.g.P : 0;
     if (Lv.gather_in && tv) Lv.stpart_elems = (long long)Lv.gs.nt * ns * NC * Lv.gs.P;
-    if (op.form == FORM_MK && !tv && c->md.dC == 0.0) {
+    if (op.form == FORM_MK && c->md.dC == 0.0) {  // time-constant or per-layer (M is C_ins x Q1 mass)
       op.msep = 1;
       op.msc = c->md.Cins * Lv.g.dx * Lv.g.dx / 36.0;
     }
@@ -418,6 +422,23 @@ void allocate(st_ctx* c) {
   dalloc(&Lc.info, 1);
   CK(cudaEventCreate(&c->e0));
   CK(cudaEventCreate(&c->e1));
+  // fused small-level tail: the first level from which every level is replicated and small
+  c->vs0 = -1;
+  {
+    // opt-in (ST_VSMALL=1): measured slower than the graph-launched per-level kernels on config 2
+    // (408 vs 441 MDOF/s with levels <= 4096 nodes fused; profiles/r01), kept for the experiment
+    const char* e = getenv("ST_VSMALL");
+    const int nl = (int)c->lv.size();
+    if (e && e[0] == '1')
+      for (int l = 1; l + 1 < nl; ++l) {
+        bool ok = nl - l <= kMaxSmall;
+        for (int k = l; k < nl && ok; ++k) ok = !c->lv[k].dist && nodes_of(c->lv[k].g) <= 4096;
+        if (ok) {
+          c->vs0 = l;
+          break;
+        }
+      }
+  }
   c->gl0 = -1;
   for (size_t l = 1; l + 1 < c->lv.size(); ++l) {
     const Level& Lv = c->lv[l];
@@ -478,19 +499,6 @@ bool bind_rho(st_ctx* c, const double* rho_in) {
   c->rho_ck[0] = c->hsmall[500];
   c->rho_ck[1] = c->hsmall[501];
   return changed;
-}
-
-// owned node planes of a level vector (slab: without ghosts; replicated: all)
-void owned_range(const st_ctx* c, int l, long long* off, long long* cnt) {
-  const Level& Lv = c->lv[l];
-  if (Lv.dist) {
-    const int o0 = c->comm.rank > 0 ? 1 : 0;
-    *off = (long long)o0 * Lv.g.P;
-    *cnt = (long long)(Lv.nloc + (c->comm.rank == 0 ? 1 : 0)) * Lv.g.P;
-  } else {
-    *off = 0;
-    *cnt = Lv.g.N;
-  }
 }
 
 // Per-level Jacobi weight: the capacity term is an upwind difference in time,
@@ -650,8 +658,28 @@ bool vcycle_graph(st_ctx* c, int l, bool trans, const double* b, double* x) {
 }
 
 void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_graph) {
-  if (!in_graph && vcycle_graph(c, l, trans, b, x)) return;
   Level& Lv = c->lv[l];
+  if (l == c->vs0 && b == Lv.b && x == Lv.x) {  // the small-level tail: one cluster kernel
+    SmallCycle cyc{};
+    cyc.nlev = (int)c->lv.size() - l;
+    cyc.npre = c->opt.nu_pre;
+    cyc.npost = c->opt.nu_post;
+    for (int k = 0; k < cyc.nlev; ++k) {
+      const Level& S = c->lv[l + k];
+      SmallLevel& d = cyc.L[k];
+      d.op = S.op;
+      d.x = S.x; d.b = S.b; d.r = S.r; d.t = S.t;
+      d.kind = S.kind;
+      d.dense = S.dense ? 1 : 0;
+      d.omega = S.omega > 0.0 ? S.omega : c->opt.omega;
+      d.Ainv = S.Ainv;
+    }
+    launch_vsmall(cyc, c->sd, trans, c->stream);
+    L(c);
+    check_launch();
+    return;
+  }
+  if (!in_graph && vcycle_graph(c, l, trans, b, x)) return;
   if (Lv.dense) {
     launch_dense_solve(Lv.Ainv, (int)Lv.g.N, trans, b, x, c->stream);
     L(c);
@@ -906,6 +934,8 @@ void free_ctx(st_ctx* c) {
   if (c->hsmall) cudaFreeHost(c->hsmall);
   cudaFree(c->rho_stage);
   comm_release(c->comm);
+  cudaFree(c->fbuf);
+  cudaFree(c->fw);
   for (auto& Lv : c->lv) cudaFree(Lv.stpart);
   for (int i = 0; i < 4; ++i) cudaFree(c->io_stage[i]);
   for (int d = 0; d < 2; ++d)
@@ -1008,7 +1038,9 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       if (dist && dist->cuda_stream) {
         c->stream = (cudaStream_t)dist->cuda_stream;
       } else {
-        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        // blocking stream: ordered with work the caller enqueues on the legacy default stream
+        // (e.g. PyTorch's default stream), so caller-side fills / copies never race the library
+        CK(cudaStreamCreate(&c->stream));
         c->own_stream = true;
       }
       c->sd = grid->sdim;
@@ -1192,6 +1224,148 @@ int st_vcycle(st_ctx_t* c, const double* rho, const double* b, double* z, int tr
     L(c);
     vcycle(c, 0, transpose != 0, c->tmpN2, c->tmpN);
     unpack_out(c, c->tmpN, z, 2);
+    return ST_OK;
+  });
+}
+
+// ---- config-5 design update (R-13) --------------------------------------------------
+namespace {
+struct DesignShape {
+  long long nsp;    // elements per layer (spatial field)
+  int nloc;         // owned layers (time-constant: 1)
+  int out_layers;   // layers of the filtered field st_solve takes (owned + ghost)
+  long long nglob;  // elements over all ranks
+  bool tv;
+};
+DesignShape design_shape(const st_ctx* c) {
+  DesignShape d{};
+  d.nsp = 1;
+  for (int k = 0; k < c->sd; ++k) d.nsp *= c->grid.n;
+  const Level& L0 = c->lv[0];
+  d.tv = !c->tc;
+  d.nloc = d.tv ? (L0.dist ? L0.nloc : L0.g.nt) : 1;
+  d.out_layers = d.tv ? L0.g.nt : 1;
+  d.nglob = d.tv ? d.nsp * c->grid.nt : d.nsp;
+  return d;
+}
+void ensure_design_bufs(st_ctx* c, const DesignShape& d) {
+  if (!c->fbuf) {
+    dzalloc(&c->fbuf, (size_t)d.nsp * (d.nloc + 2));
+    dzalloc(&c->fw, (size_t)d.nsp * d.nloc);
+  }
+}
+}  // namespace
+
+int st_filter(st_ctx_t* c, const double* in, double* out, int transpose, double radius) {
+  return guarded([&]() -> int {
+    if (!c || !in || !out) throw StErr{ST_E_INVALID_ARG, "null argument"};
+    if (!(radius > 0)) throw StErr{ST_E_INVALID_ARG, "radius must be > 0"};
+    CK(cudaSetDevice(c->device));
+    const DesignShape d = design_shape(c);
+    ensure_design_bufs(c, d);
+    const bool slab = d.tv && c->lv[0].dist;
+    const int lo_ok = slab && c->comm.rank > 0, hi_ok = slab && c->comm.rank < c->comm.size - 1;
+    const int tdir = d.tv ? 1 : 0;
+    const long long nown = d.nsp * d.nloc;
+    const double* src = in_ptr(c, in, nown, 1);
+    if (transpose) launch_filter_w(c->sd, (int)c->grid.n, d.nloc, tdir, lo_ok, hi_ok, radius, c->fw, c->stream);
+    launch_filter_pack(nown, src, transpose ? c->fw : nullptr, c->fbuf + d.nsp, c->stream);
+    L(c, transpose ? 2 : 1);
+    if (slab)
+      comm_call([&] {
+        comm_halo(c->comm, c->fbuf + d.nsp, c->fbuf, c->fbuf + (long long)d.nloc * d.nsp,
+                  c->fbuf + (long long)(d.nloc + 1) * d.nsp, d.nsp, c->stream);
+      });
+    const long long nout = transpose ? nown : d.nsp * d.out_layers;
+    bool staged = false;
+    double* dst = out_ptr(c, out, nout, 3, false, &staged);
+    launch_filter(c->sd, (int)c->grid.n, d.nloc, tdir, lo_ok, hi_ok, radius, c->fbuf, dst, transpose ? 1 : 0,
+                  c->stream);
+    L(c);
+    check_launch();
+    if (!transpose && slab)  // the solver's ghost layer: the next slab's first filtered layer (all ranks take part)
+      comm_call([&] { comm_shift_down(c->comm, dst, dst + (long long)d.nloc * d.nsp, d.nsp, c->stream); });
+    if (staged) copy_back(c, out, dst, nout);
+    else CK(cudaStreamSynchronize(c->stream));
+    return ST_OK;
+  });
+}
+
+int st_oc_update(st_ctx_t* c, const double* rho, const double* dJ, double volfrac, double move, double rho_min,
+                 double* rho_new, double* lambda_out) {
+  return guarded([&]() -> int {
+    if (!c || !rho || !dJ || !rho_new) throw StErr{ST_E_INVALID_ARG, "null argument"};
+    if (!(volfrac > 0 && volfrac <= 1) || !(move > 0) || !(rho_min >= 0 && rho_min < 1))
+      throw StErr{ST_E_INVALID_ARG, "volfrac / move / rho_min"};
+    CK(cudaSetDevice(c->device));
+    const DesignShape d = design_shape(c);
+    const long long nown = d.nsp * d.nloc;
+    const double* r = in_ptr(c, rho, nown, 1);
+    const double* g = in_ptr(c, dJ, nown, 2);
+    const bool slab = d.tv && c->lv[0].dist;
+    double* dsum = c->dsmall + 480;
+    // bisection on Lambda (the oracle runs the same loop, oracle/design.py)
+    double l1 = 0.0, l2 = 1e9;
+    for (int it = 0; it < 200 && (l2 - l1) / (l1 + l2) > 1e-12; ++it) {
+      const double lm = 0.5 * (l1 + l2);
+      launch_oc_sum(r, g, nown, lm, move, rho_min, c->ws.partial, c->ws.counter, dsum, c->stream);
+      L(c);
+      if (slab) allreduce(c, dsum, 1);
+      sync_small(c, 480, 1);
+      if (c->hsmall[480] / (double)d.nglob > volfrac) l1 = lm;
+      else l2 = lm;
+    }
+    const double lam = 0.5 * (l1 + l2);
+    bool staged = false;
+    double* dst = out_ptr(c, rho_new, nown, 3, false, &staged);
+    launch_oc_apply(r, g, nown, lam, move, rho_min, dst, c->stream);
+    L(c);
+    check_launch();
+    if (staged) copy_back(c, rho_new, dst, nown);
+    else CK(cudaStreamSynchronize(c->stream));
+    if (lambda_out) *lambda_out = lam;
+    return ST_OK;
+  });
+}
+
+int st_pnorm(st_ctx_t* c, const double* T, double P, double* phi, double* dphidT) {
+  return guarded([&]() -> int {
+    if (!c || !T || !phi) throw StErr{ST_E_INVALID_ARG, "null argument"};
+    if (!(P >= 1.0)) throw StErr{ST_E_INVALID_ARG, "P must be >= 1"};
+    CK(cudaSetDevice(c->device));
+    pack_in(c, T, c->tmpN, 1, true);  // with ghost planes: elements of the slab boundary planes
+    const Level& L0 = c->lv[0];
+    const int nl = L0.dist ? L0.nloc : L0.g.nt;
+    launch_pnorm_sum(L0.g, nl, c->tmpN, P, c->ws.partial, c->ws.counter, c->dsmall + 486, c->stream);
+    L(c);
+    allreduce(c, c->dsmall + 486, 1);
+    sync_small(c, 486, 1);
+    const double theta = c->hsmall[486];
+    *phi = std::pow(theta, 1.0 / P);
+    if (dphidT) {
+      const double scale = std::pow(theta, (1.0 - P) / P) / (double)(1 << (c->sd + 1));
+      launch_pnorm_grad(L0.g, c->o0, c->nown, L0.ntg, c->tmpN, P, scale, c->tmpN2, c->stream);
+      L(c);
+      check_launch();
+      unpack_out(c, c->tmpN2, dphidT, 2);
+    } else {
+      CK(cudaStreamSynchronize(c->stream));
+    }
+    return ST_OK;
+  });
+}
+
+int st_dot(st_ctx_t* c, const double* x, const double* y, double* out) {
+  return guarded([&]() -> int {
+    if (!c || !x || !y || !out) throw StErr{ST_E_INVALID_ARG, "null argument"};
+    CK(cudaSetDevice(c->device));
+    const double* xd = in_ptr(c, x, c->Nd, 1);
+    const double* yd = in_ptr(c, y, c->Nd, 2);
+    launch_mdot(xd, yd, 0, 1, c->Nd, c->dsmall + 484, c->ws, c->stream);  // x . y and ||x||^2
+    L(c);
+    allreduce(c, c->dsmall + 484, 1);
+    sync_small(c, 484, 1);
+    *out = c->hsmall[484];
     return ST_OK;
   });
 }

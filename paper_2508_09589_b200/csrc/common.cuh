@@ -13,6 +13,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 namespace st {
 
@@ -121,6 +122,45 @@ template <int SD> __device__ __forceinline__ bool pdecode(const Geom& g, long lo
   c[1] = (int)(t % g.nn);
   c[2] = (SD == 3) ? (int)(t / g.nn) : 0;
   return c[0] < g.nn;
+}
+
+// Work list of the persistent stencil kernels: (tile, time plane) items ordered by time chunks of K
+// planes (chunk-major, then tile, then plane), so that all CTAs sweep the same planes together and
+// the halo rows of neighbouring tiles are L2 hits. Decodes item w into a segment
+// (tile, planes [p0, p1)) that stays inside one chunk and one tile and ends at or before wend.
+__device__ __forceinline__ void work_segment(long long w, long long wend, long long tiles, int NP, int K,
+                                             long long* tile, int* p0, int* p1) {
+  const long long csz = tiles * K;
+  const int nch = (NP + K - 1) / K;
+  long long c = w / csz;
+  if (c > nch - 1) c = nch - 1;
+  const long long r = w - c * csz;
+  const int Kc = (c == nch - 1) ? NP - (int)c * K : K;
+  *tile = r / Kc;
+  *p0 = (int)(c * K + r % Kc);
+  const int cend = (int)(c * K) + Kc;
+  const long long rem = wend - w;
+  *p1 = (rem < cend - *p0) ? *p0 + (int)rem : cend;
+}
+
+// planes per chunk: the chunk's x and b planes (2 x K x P doubles) within `mb` MB of L2; mb <= 0:
+// one chunk (tile-major order, the default). Measured (profiles/r01): chunking cuts the (3+1)D
+// kernel's DRAM reads 1.57 -> 1.20 GB per sweep but makes it 5x slower (a segment restart per
+// chunk and tile: pipeline fill + weight rebuild), and (2+1)D traffic is already the algorithmic
+// bytes. ST_CHUNK_MB enables it (experiments).
+inline int chunk_planes(long long P, int NP, int sd) {
+  static int env_mb = -2;
+  if (env_mb == -2) {
+    const char* e = getenv("ST_CHUNK_MB");
+    env_mb = e ? atoi(e) : -1;
+  }
+  const long long mb = env_mb >= 0 ? env_mb : 0;
+  (void)sd;
+  if (mb <= 0) return NP;
+  long long K = mb * 1000000LL / (16LL * P);
+  if (K < 8) K = 8;
+  if (K > NP) K = NP;
+  return (int)K;
 }
 
 }  // namespace st

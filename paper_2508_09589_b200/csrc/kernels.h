@@ -69,4 +69,34 @@ void launch_sensitivity(const OpDesc& op, const double* T, const double* lam, do
 void launch_dense_invert(double* A, double* Ainv, int n, int* info, cudaStream_t s);
 void launch_dense_solve(const double* Ainv, int n, bool trans, const double* b, double* x, cudaStream_t s);
 
+// vsmall.cu — the small-level tail of the V-cycle as one thread-block-cluster kernel
+constexpr int kMaxSmall = 12;
+struct SmallLevel {
+  OpDesc op;                    // replicated level (FORM_MK / FORM_B4), or the dense coarsest
+  double *x, *b, *r, *t;
+  int kind;                     // coarsening kind relative to the finer level
+  int dense;
+  double omega;
+  const double* Ainv;           // dense coarsest inverse
+};
+struct SmallCycle {
+  int nlev, npre, npost;
+  SmallLevel L[kMaxSmall];
+};
+void launch_vsmall(const SmallCycle& cyc, int sd, bool trans, cudaStream_t s);
+
+// design.cu — config-5 design update (density filter, OC)
+void launch_filter(int sd, int n, int nl, int tdir, int lo_ok, int hi_ok, double r, const double* ghosted, double* out,
+                   int mode, cudaStream_t s);
+void launch_filter_w(int sd, int n, int nl, int tdir, int lo_ok, int hi_ok, double r, double* out, cudaStream_t s);
+void launch_filter_pack(long long count, const double* src, const double* W, double* dst, cudaStream_t s);
+void launch_oc_sum(const double* rho, const double* dj, long long n, double lam, double move, double lo,
+                   double* partial, unsigned* counter, double* out, cudaStream_t s);
+void launch_pnorm_sum(const Geom& g, int nl, const double* T, double P, double* partial, unsigned* counter, double* out,
+                      cudaStream_t s);
+void launch_pnorm_grad(const Geom& g, int p0, int np, int ntg, const double* T, double P, double scale, double* out,
+                       cudaStream_t s);
+void launch_oc_apply(const double* rho, const double* dj, long long n, double lam, double move, double lo, double* out,
+                     cudaStream_t s);
+
 }  // namespace st

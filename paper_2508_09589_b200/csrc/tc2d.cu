@@ -32,6 +32,10 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef ST_TC2D_MINB
+#define ST_TC2D_MINB 4  // resident CTAs per SM for the uniform-capacity variants (register cap 128)
+#endif
+
 namespace st {
 namespace tc {
 
@@ -84,9 +88,9 @@ __device__ __forceinline__ double ap9(const double (&w)[9], const double (&nb)[R
 
 // SRC: 0 = fine level from rho (time-constant design), 1 = stored MK stencils (nl = 1)
 template <int SRC, bool CUNI, int MODE, bool TRANS>
-__global__ void __launch_bounds__(NTH, CUNI ? 4 : 3)
+__global__ void __launch_bounds__(NTH, CUNI ? ST_TC2D_MINB : 3)
     tc2d_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, OpDesc op,
-                const double* __restrict__ x, double* __restrict__ y, double omega, long long wtot, int ntx) {
+                const double* __restrict__ x, double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx) {
   constexpr bool NX = (MODE != MODE_JAC0);
   constexpr bool NBV = (MODE != MODE_APPLY);
   constexpr bool ND = (MODE == MODE_JAC || MODE == MODE_JAC0);
@@ -118,9 +122,9 @@ __global__ void __launch_bounds__(NTH, CUNI ? 4 : 3)
   const long long wend = wtot * (blockIdx.x + 1) / gridDim.x;
   unsigned ring = 0u, phase = 0u;
   while (w < wend) {
-    const long long tile = w / NP;
-    const int p0 = (int)(w - tile * NP);
-    const int p1 = (int)((wend - w) < NP - p0 ? p0 + (wend - w) : NP);
+    long long tile;
+    int p0, p1;
+    work_segment(w, wend, wtot / NP, (int)NP, kchunk, &tile, &p0, &p1);
     w += p1 - p0;
     const int x0 = (int)(tile % ntx) * TX, y0 = (int)(tile / ntx) * TY;
     const int qs = max(p0 - 1, 0), qe = min(p1, g.nt);
@@ -362,9 +366,12 @@ void ltc(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, const d
   const long long ntx = (g.nn + TX - 1) / TX, nty = (g.nn + TY - 1) / TY;
   const long long wtot = ntx * nty * (g.nt + 1);
   long long grid = (long long)nsm * resident;
-  if (grid > wtot / 4) grid = wtot / 4;
+  // large levels: >= 4 planes per CTA (one reload plane per segment); small levels: every CTA a
+  // short chain so that the TMA round trips of a level overlap (launch-latency bound there)
+  const long long minw = (wtot >= 16LL * nsm * resident) ? 4 : 1;
+  if (grid > wtot / minw) grid = wtot / minw;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, op, x, y, omega, wtot, (int)ntx);
+  kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, op, x, y, omega, wtot, chunk_planes(g.P, g.nt + 1, g.sd), (int)ntx);
 }
 
 template <int SRC, bool CUNI>

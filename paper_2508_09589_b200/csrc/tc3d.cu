@@ -10,8 +10,9 @@
 // its 6 face-neighbour weights vanish for the trilinear element).
 // Design:
 //   * persistent one-wave grid over the (tile, plane) list, as tc2d;
-//   * CTA = 256 threads = one 32 x 4 x 2 node tile, one node per thread; one elected thread
-//     streams the x tile (36 x 6 x 4 with halo) and the b tile (32 x 4 x 2) of every plane with
+//   * CTA = 256 threads = one 16 x 8 x 2 node tile, one node per thread (16-wide x rows waste
+//     less than 32-wide ones on the 2^k + 1 node lines of the hierarchy); one elected thread
+//     streams the x tile (20 x 10 x 4 with halo) and the b tile (16 x 8 x 2) of every plane with
 //     4-D cp.async.bulk.tensor into a 5-slot mbarrier ring (4 planes in flight);
 //   * 27 + 21 weights per node in registers (fine level; a Galerkin coarse stiffness has 27),
 //     built once per segment (from rho, or from the stored forward coefficients and the
@@ -28,9 +29,9 @@
 namespace st {
 namespace t3 {
 
-constexpr int TX = 32, TY = 4, TZ = 2;                    // node tile 32 x 4 x 2
-constexpr int HX = TX + 4, HY = TY + 2, HZ = TZ + 2;      // x tile 36 x 6 x 4 (col 0 unused)
-constexpr int XS = HX * HY * HZ;                          // 864 doubles (6912 B, 128-B multiple)
+constexpr int TX = 16, TY = 8, TZ = 2;                    // node tile 16 x 8 x 2 (a warp: 16 x 2)
+constexpr int HX = TX + 4, HY = TY + 2, HZ = TZ + 2;      // x tile 20 x 10 x 4 (col 0 unused)
+constexpr int XS = HX * HY * HZ;                          // 800 doubles (6400 B, 128-B multiple)
 constexpr int BS = TX * TY * TZ;                          // 256 doubles
 constexpr int NB = 5;
 constexpr int NTH = TX * TY * TZ;
@@ -74,7 +75,7 @@ template <bool FACE0> __host__ __device__ constexpr int kslot(int k) {
 template <int SRC, int MODE, bool TRANS>
 __global__ void __launch_bounds__(NTH, SRC == 0 ? 2 : 1)
     tc3d_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, OpDesc op,
-                const double* __restrict__ x, double* __restrict__ y, double omega, long long wtot, int ntx,
+                const double* __restrict__ x, double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx,
                 int nty) {
   constexpr bool NX = (MODE != MODE_JAC0);
   constexpr bool NBV = (MODE != MODE_APPLY);
@@ -109,9 +110,9 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 2 : 1)
   const long long wend = wtot * (blockIdx.x + 1) / gridDim.x;
   unsigned ring = 0u, phase = 0u;
   while (w < wend) {
-    const long long tile = w / NP;
-    const int p0 = (int)(w - tile * NP);
-    const int p1 = (int)((wend - w) < NP - p0 ? p0 + (wend - w) : NP);
+    long long tile;
+    int p0, p1;
+    work_segment(w, wend, wtot / NP, (int)NP, kchunk, &tile, &p0, &p1);
     w += p1 - p0;
     const int tyx = (int)(tile % ((long long)ntx * nty));
     const int x0 = (tyx % ntx) * TX, y0 = (tyx / ntx) * TY, z0 = (int)(tile / ((long long)ntx * nty)) * TZ;
@@ -325,9 +326,12 @@ void lt3(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, const d
   const long long ntx = (g.nn + TX - 1) / TX, nty = (g.nn + TY - 1) / TY, ntz = (g.nn + TZ - 1) / TZ;
   const long long wtot = ntx * nty * ntz * (g.nt + 1);
   long long grid = (long long)nsm * resident;
-  if (grid > wtot / 4) grid = wtot / 4;
+  // large levels: >= 4 planes per CTA (one reload plane per segment); small levels: every CTA a
+  // short chain so that the TMA round trips of a level overlap (launch-latency bound there)
+  const long long minw = (wtot >= 16LL * nsm * resident) ? 4 : 1;
+  if (grid > wtot / minw) grid = wtot / minw;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, dim3(TX, TY, TZ), bytes, s>>>(mx, mb, op, x, y, omega, wtot, (int)ntx, (int)nty);
+  kern<<<(unsigned)grid, dim3(TX, TY, TZ), bytes, s>>>(mx, mb, op, x, y, omega, wtot, chunk_planes(g.P, g.nt + 1, g.sd), (int)ntx, (int)nty);
 }
 
 template <int SRC>

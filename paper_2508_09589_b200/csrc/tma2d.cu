@@ -99,7 +99,7 @@ __device__ __forceinline__ void wK_from(double sw, double se, double nw, double 
 template <bool TC, int SRC, bool CUNI, int MODE, bool TRANS, bool MASK>
 __global__ void __launch_bounds__(NTH, (TC && CUNI) ? 4 : 3)
     tma2d_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, OpDesc op,
-                 const double* __restrict__ x, double* __restrict__ y, double omega, long long wtot, int ntx) {
+                 const double* __restrict__ x, double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx) {
   constexpr bool TVR = (!TC) && SRC == 0;
   constexpr bool NX = (MODE != MODE_JAC0);
   constexpr bool NBV = (MODE != MODE_APPLY);
@@ -141,9 +141,9 @@ __global__ void __launch_bounds__(NTH, (TC && CUNI) ? 4 : 3)
   unsigned ring = 0u;   // slot of the first plane of the next segment
   unsigned phase = 0u;  // mbarrier parity bit per slot
   while (w < wend) {
-    const long long tile = w / NP;
-    const int p0 = (int)(w - tile * NP);
-    const int p1 = (int)((wend - w) < NP - p0 ? p0 + (wend - w) : NP);
+    long long tile;
+    int p0, p1;
+    work_segment(w, wend, wtot / NP, (int)NP, kchunk, &tile, &p0, &p1);
     w += p1 - p0;
     const int x0 = (int)(tile % ntx) * TX, y0 = (int)(tile / ntx) * TY;
     const int qs = max(p0 - 1, 0), qe = min(p1, g.nt);
@@ -464,9 +464,12 @@ void lt2(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, const d
   const long long wtot = ntx * nty * (g.nt + 1);
   // one wave; at least ~4 planes per CTA so that small levels do not pay a pipeline fill per plane
   long long grid = (long long)nsm * resident;
-  if (grid > wtot / 4) grid = wtot / 4;
+  // large levels: >= 4 planes per CTA (one reload plane per segment); small levels: every CTA a
+  // short chain so that the TMA round trips of a level overlap (launch-latency bound there)
+  const long long minw = (wtot >= 16LL * nsm * resident) ? 4 : 1;
+  if (grid > wtot / minw) grid = wtot / minw;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, op, x, y, omega, wtot, (int)ntx);
+  kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, op, x, y, omega, wtot, chunk_planes(g.P, g.nt + 1, g.sd), (int)ntx);
 }
 
 template <bool TC, int SRC, bool CUNI>

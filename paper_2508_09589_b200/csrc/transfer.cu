@@ -88,7 +88,56 @@ __global__ void prolong_kernel(Geom gf, Geom gc, const double* __restrict__ ec, 
   xf[idx] += acc;
 }
 
+// (2+1)D space coarsening, the hot transfer pair: thread per (x1 node, x2 row, plane), no 64-bit
+// index arithmetic; rows are read coalesced and the coarse row of the prolongation comes from L1.
+__global__ void __launch_bounds__(128) prolong2s_kernel(Geom gf, Geom gc, const double* __restrict__ ec,
+                                                        double* __restrict__ xf) {
+  const int i = blockIdx.x * 128 + threadIdx.x, j = blockIdx.y, p = blockIdx.z;
+  if (i >= gf.nn) return;
+  int c[3] = {i, j, 0};
+  if (is_cons<2>(gf, c, p)) return;
+  const int Pc = p + gf.pg0 - gc.pg0;
+  if (Pc < 0 || Pc > gc.nt) return;
+  const double* e0 = ec + (long long)Pc * gc.P + (long long)(j >> 1) * gc.pr + (i >> 1);
+  double v;
+  if (!(i & 1) && !(j & 1)) v = __ldg(e0);
+  else if (!(j & 1)) v = 0.5 * (__ldg(e0) + __ldg(e0 + 1));
+  else if (!(i & 1)) v = 0.5 * (__ldg(e0) + __ldg(e0 + gc.pr));
+  else v = 0.25 * ((__ldg(e0) + __ldg(e0 + 1)) + (__ldg(e0 + gc.pr) + __ldg(e0 + gc.pr + 1)));
+  xf[(long long)p * gf.P + (long long)j * gf.pr + i] += v;
+}
+
+__global__ void __launch_bounds__(128) restrict2s_kernel(Geom gf, Geom gc, const double* __restrict__ rf,
+                                                         double* __restrict__ rc) {
+  const int I = blockIdx.x * 128 + threadIdx.x, J = blockIdx.y, Pp = blockIdx.z;
+  if (I >= gc.pr) return;
+  double* out = rc + (long long)Pp * gc.P + (long long)J * gc.pr + I;
+  int C[3] = {I, J, 0};
+  if (I >= gc.nn || is_cons<2>(gc, C, Pp)) { *out = 0.0; return; }
+  const int q = Pp + gc.pg0 - gf.pg0;
+  if (q < 0 || q > gf.nt) { *out = 0.0; return; }
+  const double* rp = rf + (long long)q * gf.P;
+  double acc = 0.0;
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy) {
+    const int fj = 2 * J + dy;
+    if (fj < 0 || fj >= gf.nn) continue;
+    const double wy = dy == 0 ? 1.0 : 0.5;
+    const double* row = rp + (long long)fj * gf.pr;
+    const int fi = 2 * I;
+    double r = __ldg(row + fi);
+    if (fi - 1 >= 0) r += 0.5 * __ldg(row + fi - 1);
+    if (fi + 1 < gf.nn) r += 0.5 * __ldg(row + fi + 1);
+    acc += wy * r;
+  }
+  *out = acc;
+}
+
 void launch_restrict(const Geom& gf, const Geom& gc, int kind, const double* rf, double* rc, cudaStream_t s) {
+  if (gf.sd == 2 && kind == KIND_SPACE && gc.nt + 1 <= 65535) {
+    restrict2s_kernel<<<dim3((gc.pr + 127) / 128, gc.nn, gc.nt + 1), 128, 0, s>>>(gf, gc, rf, rc);
+    return;
+  }
   int blk = 256;
   unsigned grd = (unsigned)((gc.N + blk - 1) / blk);
   bool SPc = (kind == KIND_SPACE || kind == KIND_FULL), TMc = (kind == KIND_TIME || kind == KIND_FULL);
@@ -102,6 +151,10 @@ void launch_restrict(const Geom& gf, const Geom& gc, int kind, const double* rf,
 }
 
 void launch_prolong_add(const Geom& gf, const Geom& gc, int kind, const double* ec, double* xf, cudaStream_t s) {
+  if (gf.sd == 2 && kind == KIND_SPACE && gf.nt + 1 <= 65535) {
+    prolong2s_kernel<<<dim3((gf.nn + 127) / 128, gf.nn, gf.nt + 1), 128, 0, s>>>(gf, gc, ec, xf);
+    return;
+  }
   int blk = 256;
   unsigned grd = (unsigned)((gf.N + blk - 1) / blk);
   bool SPc = (kind == KIND_SPACE || kind == KIND_FULL), TMc = (kind == KIND_TIME || kind == KIND_FULL);

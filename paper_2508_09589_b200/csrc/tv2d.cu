@@ -27,7 +27,8 @@ constexpr int TX = 32, TYT = 4, RY = 2, TY = TYT * RY;   // node tile 32 x 8
 constexpr int HX = TX + 4, HY = TY + 2;                  // x tile 36 x 10 (col 0 unused)
 constexpr int XS = 368, BS = 256;                        // slot sizes (doubles)
 constexpr int EX = TX + 1, EY = TY + 1, ET = EX * EY;    // element tile 33 x 9
-constexpr int RS = 304;                                  // rho slot (doubles)
+constexpr int CXW = TX + 2, CT = CXW * EY;               // stored-coefficient node tile 34 x 9
+constexpr int RS0 = 304, RS1 = 5 * CT + 2;               // per-layer slot: rho tile / 5 K coefficient tiles
 constexpr int NB = 6;
 constexpr int NTH = TX * TYT;
 constexpr unsigned XBYTES = HX * HY * 8, BBYTES = TX * TY * 8;
@@ -78,10 +79,12 @@ __device__ __forceinline__ void wk_from(double sw, double se, double nw, double 
   w[4] = 4.0 * ((sw + se) + (nw + ne));
 }
 
-template <int MODE, bool TRANS>
-__global__ void __launch_bounds__(NTH, 3)
+// SRC: 0 = fine level from rho (per-layer k~ from the element densities); 1 = stored per-layer
+// stiffness of a time-varying Galerkin space level (uniform capacity: the separable mass op.msc)
+template <int SRC, int MODE, bool TRANS>
+__global__ void __launch_bounds__(NTH, SRC == 0 ? 3 : 2)
     tv2d_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, OpDesc op,
-                const double* __restrict__ x, double* __restrict__ y, double omega, long long wtot, int ntx) {
+                const double* __restrict__ x, double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx) {
   constexpr bool NX = (MODE != MODE_JAC0);
   constexpr bool NBV = (MODE != MODE_APPLY);
   constexpr bool ND = (MODE == MODE_JAC || MODE == MODE_JAC0);
@@ -89,8 +92,9 @@ __global__ void __launch_bounds__(NTH, 3)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   double* xs = smem + 16;                    // [NB][XS]
   double* bs = xs + (NX ? NB * XS : 0);      // [NB][BS]
-  double* rs = bs + (NBV ? NB * BS : 0);     // [NB][RS] rho tiles (layer q arrives with plane q)
-  double* kk = rs + NB * RS;                 // [2][ET] k~ of the current / next layer
+  constexpr int RS = SRC == 0 ? RS0 : RS1;
+  double* rs = bs + (NBV ? NB * BS : 0);     // [NB][RS] layer tiles (layer q arrives with plane q)
+  double* kk = rs + NB * RS;                 // [2][ET] k~ of the current / next layer (SRC 0)
 
   const Geom& g = op.g;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
@@ -99,15 +103,16 @@ __global__ void __launch_bounds__(NTH, 3)
   const long long NP = g.nt + 1;
   const int xo = (ty * RY) * HX + tx + 1;
   const int bo = (ty * RY) * TX + tx;
-  constexpr int RPT = (ET + NTH - 1) / NTH;
+  constexpr int TILE = SRC == 0 ? ET : 5 * CT;  // doubles copied per layer
+  constexpr int RPT = (TILE + NTH - 1) / NTH;
 
   if (tid == 0) {
 #pragma unroll
     for (int k = 0; k < NB; ++k) mbar_init(&bar[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  const double sm = g.dx * g.dx * (1.0 / 36.0) * op.m.Cins;
-  const double sk = 1.0 / 6.0;
+  const double sm = SRC == 0 ? g.dx * g.dx * (1.0 / 36.0) * op.m.Cins : op.msc;
+  const double sk = SRC == 0 ? 1.0 / 6.0 : 1.0;
   const double t00 = op.Tm[0][0] * sk, t01 = op.Tm[0][1] * sk, t11 = op.Tm[1][1] * sk;
   const unsigned tx_full = (NX ? XBYTES : 0u) + (NBV ? BBYTES : 0u);
 
@@ -115,9 +120,9 @@ __global__ void __launch_bounds__(NTH, 3)
   const long long wend = wtot * (blockIdx.x + 1) / gridDim.x;
   unsigned ring = 0u, phase = 0u;
   while (w < wend) {
-    const long long tile = w / NP;
-    const int p0 = (int)(w - tile * NP);
-    const int p1 = (int)((wend - w) < NP - p0 ? p0 + (wend - w) : NP);
+    long long tile;
+    int p0, p1;
+    work_segment(w, wend, wtot / NP, (int)NP, kchunk, &tile, &p0, &p1);
     w += p1 - p0;
     const int x0 = (int)(tile % ntx) * TX, y0 = (int)(tile / ntx) * TY;
     const int qs = max(p0 - 1, 0), qe = min(p1, g.nt);
@@ -132,16 +137,26 @@ __global__ void __launch_bounds__(NTH, 3)
       cy[r] = (j == 0 || j == n) ? 2.0 : 4.0;
     }
     const double cx = (i == 0 || i == n) ? 2.0 : 4.0;
-    // this thread's rho copies (33 x 9 element tile from (x0-1, y0-1); zero outside)
-    int roff[RPT];
+    // this thread's per-layer copies: SRC 0 the 33 x 9 element tile of rho from (x0-1, y0-1);
+    // SRC 1 the 34 x 9 node tiles of the 5 forward stiffness coefficients from (x0-1, y0-1); zero outside
+    long long roff[RPT];
     unsigned rval = 0u;
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
       const int e = tid + k * NTH;
-      const int ly = e / EX, lx = e - ly * EX;
-      const int gi = x0 - 1 + lx, gj = y0 - 1 + ly;
-      const bool v = (e < ET) && gi >= 0 && gi < n && gj >= 0 && gj < n;
-      roff[k] = v ? gj * n + gi : 0;
+      bool v;
+      if (SRC == 0) {
+        const int ly = e / EX, lx = e - ly * EX;
+        const int gi = x0 - 1 + lx, gj = y0 - 1 + ly;
+        v = (e < ET) && gi >= 0 && gi < n && gj >= 0 && gj < n;
+        roff[k] = v ? (long long)gj * n + gi : 0;
+      } else {
+        const int a = e / CT, loc = e - a * CT;
+        const int ly = loc / CXW, lx = loc - ly * CXW;
+        const int gi = x0 - 1 + lx, gj = y0 - 1 + ly;
+        v = (e < 5 * CT) && gi >= 0 && gi <= n && gj >= 0 && gj <= n;
+        roff[k] = v ? (long long)a * P + (long long)gj * pr + gi : 0;
+      }
       if (v) rval |= 1u << k;
     }
     __syncthreads();  // barrier init / previous segment fully consumed
@@ -151,11 +166,12 @@ __global__ void __launch_bounds__(NTH, 3)
     auto issue_rho = [&](int q, unsigned slot) {
       if (q < g.nt) {  // layer q exists locally (the last plane has no layer above)
         double* rd = rs + slot * RS;
-        const double* rq = op.rho + (long long)q * n * n;
+        const double* rq = SRC == 0 ? op.rho + (long long)q * n * n
+                                    : op.st + ((long long)q * 2 + 1) * 5 * P;  // K block of layer q
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
           const int e = tid + k * NTH;
-          if (e < ET) {
+          if (e < TILE) {
             const int sz = ((rval >> k) & 1u) ? 8 : 0;
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(su32(rd + e)), "l"(rq + roff[k]), "r"(sz));
           }
@@ -198,7 +214,7 @@ __global__ void __launch_bounds__(NTH, 3)
       phase ^= 1u << cur;
       asm volatile("cp.async.wait_group %0;\n" ::"n"(NB - 2));
       // k~ of layer q (above plane q), zero outside the domain / beyond the last layer
-      {
+      if (SRC == 0) {
         double* kd = kk + kb * ET;
         const double* rd = rs + cur * RS;
         const bool has = q < g.nt;
@@ -214,7 +230,24 @@ __global__ void __launch_bounds__(NTH, 3)
       __syncthreads();
       // weights of layer q for the thread's nodes (rows j0, j0+1): elements rows j0-1 .. j0+1
       double wKn[RY][9];
-      {
+      if (SRC == 1) {
+        // own forward coefficients and the neighbours' mirrored ones (zero beyond the last layer)
+        const double* ct = rs + cur * RS;
+        const bool has = q < g.nt;
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+          const int L = (ty * RY + r + 1) * CXW + tx + 1;  // node (i, j) in the tile
+          wKn[r][4] = has ? ct[0 * CT + L] : 0.0;
+          wKn[r][5] = has ? ct[1 * CT + L] : 0.0;
+          wKn[r][6] = has ? ct[2 * CT + L] : 0.0;
+          wKn[r][7] = has ? ct[3 * CT + L] : 0.0;
+          wKn[r][8] = has ? ct[4 * CT + L] : 0.0;
+          wKn[r][0] = has ? ct[4 * CT + L - CXW - 1] : 0.0;  // (i-1, j-1): its (+1, +1)
+          wKn[r][1] = has ? ct[3 * CT + L - CXW] : 0.0;      // (i,   j-1): its ( 0, +1)
+          wKn[r][2] = has ? ct[2 * CT + L - CXW + 1] : 0.0;  // (i+1, j-1): its (-1, +1)
+          wKn[r][3] = has ? ct[1 * CT + L - 1] : 0.0;        // (i-1, j  ): its (+1,  0)
+        }
+      } else {
         const double* kd = kk + kb * ET + (ty * RY) * EX + tx;
         double kw[RY + 1], ke[RY + 1];
 #pragma unroll
@@ -352,13 +385,14 @@ bool map3_tv(CUtensorMap* m, const void* base, unsigned long long d0, unsigned l
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MODE, bool TRANS>
+template <int SRC, int MODE, bool TRANS>
 void ltv(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, const double* x, double* y, double omega,
          cudaStream_t s) {
   using namespace tv;
   const Geom& g = op.g;
-  auto kern = tv2d_kernel<MODE, TRANS>;
+  auto kern = tv2d_kernel<SRC, MODE, TRANS>;
   constexpr bool NX = (MODE != MODE_JAC0), NBV = (MODE != MODE_APPLY);
+  constexpr int RS = SRC == 0 ? RS0 : RS1;
   constexpr size_t bytes = sizeof(double) * (16 + (NX ? NB * XS : 0) + (NBV ? NB * BS : 0) + NB * RS + 2 * ET);
   static int resident = 0, nsm = 0;
   if (!resident) {
@@ -372,9 +406,12 @@ void ltv(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, const d
   const long long ntx = (g.nn + TX - 1) / TX, nty = (g.nn + TY - 1) / TY;
   const long long wtot = ntx * nty * (g.nt + 1);
   long long grid = (long long)nsm * resident;
-  if (grid > wtot / 4) grid = wtot / 4;
+  // large levels: >= 4 planes per CTA (one reload plane per segment); small levels: every CTA a
+  // short chain so that the TMA round trips of a level overlap (launch-latency bound there)
+  const long long minw = (wtot >= 16LL * nsm * resident) ? 4 : 1;
+  if (grid > wtot / minw) grid = wtot / minw;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, op, x, y, omega, wtot, (int)ntx);
+  kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, op, x, y, omega, wtot, chunk_planes(g.P, g.nt + 1, g.sd), (int)ntx);
 }
 }  // namespace
 
@@ -382,7 +419,9 @@ void ltv(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, const d
 bool launch_op_tv2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                     double omega, cudaStream_t s) {
   const Geom& g = op.g;
-  if (g.sd != 2 || !mask || op.form != FORM_RHO || op.rho_tc || op.m.dC != 0.0) return false;
+  const bool rho_tv = op.form == FORM_RHO && !op.rho_tc && op.m.dC == 0.0;
+  const bool mk_tv = op.form == FORM_MK && op.tvl && op.msep;
+  if (g.sd != 2 || !mask || !(rho_tv || mk_tv)) return false;
   if (op.U[0][0] != 0.0 || op.U[0][1] != 0.0 || op.U[1][0] != -1.0 || op.U[1][1] != 1.0) return false;
   if (op.Tm[0][1] != op.Tm[1][0]) return false;
   CUtensorMap mx{}, mb{};
@@ -391,10 +430,12 @@ bool launch_op_tv2d(const OpDesc& op, int mode, bool trans, bool mask, const dou
   if (nx && !map3_tv(&mx, x - (g.pr + 2), (unsigned long long)g.pr + 2, nn + 1, g.nt + 1, s1, s2, tv::HX, tv::HY))
     return false;
   if (nbv && !map3_tv(&mb, b, nn, nn, g.nt + 1, s1, s2, tv::TX, tv::TY)) return false;
-#define C4(M)                                                      \
-  case M:                                                          \
-    if (trans) ltv<M, true>(mx, mb, op, x, y, omega, s);           \
-    else ltv<M, false>(mx, mb, op, x, y, omega, s);                \
+#define C4(M)                                                                            \
+  case M:                                                                                \
+    if (rho_tv) { if (trans) ltv<0, M, true>(mx, mb, op, x, y, omega, s);                \
+                  else ltv<0, M, false>(mx, mb, op, x, y, omega, s); }                   \
+    else { if (trans) ltv<1, M, true>(mx, mb, op, x, y, omega, s);                       \
+           else ltv<1, M, false>(mx, mb, op, x, y, omega, s); }                          \
     break;
   switch (mode) {
     C4(MODE_APPLY)

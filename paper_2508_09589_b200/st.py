@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libst.so")
+LIB_PATH = os.environ.get("ST_LIB_PATH") or os.path.join(HERE, "libst.so")  # override: A/B builds
 
 ST_OK = 0
 ST_E_NOT_CONVERGED = -3
@@ -88,7 +88,7 @@ class Hierarchy(C.Structure):
 
 
 EXPORTS = ["st_abi_version", "st_default_options", "st_setup", "st_destroy", "st_solve", "st_adjoint",
-           "st_sensitivity", "st_apply", "st_vcycle", "st_rhs", "st_level_apply", "st_bench_op", "st_get_stats", "st_get_hierarchy",
+           "st_sensitivity", "st_apply", "st_vcycle", "st_rhs", "st_filter", "st_oc_update", "st_dot", "st_pnorm", "st_level_apply", "st_bench_op", "st_get_stats", "st_get_hierarchy",
            "st_local_layout", "st_nccl_unique_id", "st_nccl_comm_init", "st_nccl_comm_destroy", "st_plan",
            "st_struct_sizes",
            "st_num_nodes", "st_num_design", "st_kernel_launches", "st_strerror", "st_last_error"]
@@ -121,6 +121,11 @@ def load_library(path: str = LIB_PATH):
     lib.st_apply.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]
     lib.st_rhs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.st_vcycle.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
+    lib.st_filter.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double]
+    lib.st_oc_update.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_void_p,
+                                 P(C.c_double)]
+    lib.st_dot.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, P(C.c_double)]
+    lib.st_pnorm.argtypes = [C.c_void_p, C.c_void_p, C.c_double, P(C.c_double), C.c_void_p]
     lib.st_level_apply.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
     lib.st_bench_op.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
     lib.st_get_stats.argtypes = [C.c_void_p, P(Stats)]
@@ -173,6 +178,12 @@ class TorchHostComm:
     def _t(self, ptr, n):
         return self.torch.from_numpy(self.np.ctypeslib.as_array(ptr, (int(n),)))
 
+    def _fail(self, what, e):
+        import sys
+        sys.stderr.write(f"TorchHostComm.{what} failed: {e!r}\n")
+        self.last_error = repr(e)
+        return 1
+
     def _sendrecv(self, user, peer, send, recv, count):
         try:
             s, r = self._t(send, count).clone(), self._t(recv, count)
@@ -180,15 +191,15 @@ class TorchHostComm:
             for q in reqs:
                 q.wait()
             return 0
-        except Exception:  # noqa: BLE001
-            return 1
+        except Exception as e:  # noqa: BLE001
+            return self._fail("sendrecv", e)
 
     def _allreduce(self, user, buf, count):
         try:
             self.dist.all_reduce(self._t(buf, count), group=self.group)
             return 0
-        except Exception:  # noqa: BLE001
-            return 1
+        except Exception as e:  # noqa: BLE001
+            return self._fail("allreduce", e)
 
     def _allgather(self, user, send, recv, count):
         try:
@@ -196,8 +207,8 @@ class TorchHostComm:
             self.dist.all_gather(parts, self._t(send, count).clone(), group=self.group)
             self._t(recv, count * self.size).copy_(self.torch.cat(parts))
             return 0
-        except Exception:  # noqa: BLE001
-            return 1
+        except Exception as e:  # noqa: BLE001
+            return self._fail("allgather", e)
 
 
 STRUCTS = [Grid, Materials, BCs, Source, Options, Dist, Stats, Hierarchy, Layout, Plan]
@@ -301,6 +312,28 @@ class Solver:
 
     def apply(self, rho, x, y, transpose=False, bc=True):
         return self._check(self.lib.st_apply(self.ctx, _ptr(rho), _ptr(x), _ptr(y), int(transpose), int(bc)))
+
+    def filter(self, x, out, transpose=False, radius=2.0):
+        """Density filter F (transpose: F^T, the chain rule) of config 5 (R-13)."""
+        return self._check(self.lib.st_filter(self.ctx, _ptr(x), _ptr(out), int(transpose), radius))
+
+    def oc_update(self, rho, dJ, rho_new, volfrac=0.4, move=0.2, rho_min=1e-3):
+        """Optimality-criteria step with bisection on the volume multiplier; returns Lambda."""
+        lam = C.c_double()
+        self._check(self.lib.st_oc_update(self.ctx, _ptr(rho), _ptr(dJ), volfrac, move, rho_min, _ptr(rho_new),
+                                          C.byref(lam)))
+        return lam.value
+
+    def pnorm(self, T, P=20.0, grad=None):
+        """phi = (sum_e Tavg_e^P)^(1/P); grad (optional) receives dphi/dT."""
+        phi = C.c_double()
+        self._check(self.lib.st_pnorm(self.ctx, _ptr(T), P, C.byref(phi), _ptr(grad)))
+        return phi.value
+
+    def dot(self, x, y):
+        out = C.c_double()
+        self._check(self.lib.st_dot(self.ctx, _ptr(x), _ptr(y), C.byref(out)))
+        return out.value
 
     def vcycle(self, rho, b, z, transpose=False):
         """z = one V-cycle applied to b (test hook)."""

@@ -1,23 +1,29 @@
-"""ncu target: config-2 fine-level operator kernel (bench_op) in a given mode."""
+"""ncu / timing target: a level operator kernel (bench_op) of a config-shaped problem.
+usage: prof_op.py MODE LEVEL [SDIM N NT tc|tv [c4]]"""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import st_inputs as I
 import paper_2508_09589_b200 as S
-mode = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-level = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-n = int(sys.argv[3]) if len(sys.argv) > 3 else 256
-tc = (sys.argv[4] != "tv") if len(sys.argv) > 4 else True
+a = sys.argv[1:]
+mode = int(a[0]) if len(a) > 0 else 2
+level = int(a[1]) if len(a) > 1 else 0
+sdim = int(a[2]) if len(a) > 2 else 2
+n = int(a[3]) if len(a) > 3 else 256
+nt = int(a[4]) if len(a) > 4 else n
+tc = (a[5] != "tv") if len(a) > 5 else True
+mats = (0.1, 1.0, 1.0, 1e-4, 1.0, 3.0) if (len(a) > 6 and a[6] == "c4") else (1.0, 1.0, 1.0, 1e-3, 1.0, 3.0)
 dev = torch.device("cuda:0")
 st = torch.cuda.Stream()
-s = S.Solver(2, n, n, time_constant=tc, stream=st.cuda_stream)
-rho = torch.as_tensor(I.rho_smooth((n, n), 0) if tc else I.rho_uniform((n, n, n), 0), device=dev)
+s = S.Solver(sdim, n, nt, mats=mats, time_constant=tc, stream=st.cuda_stream)
+rho = torch.as_tensor(I.design_for(sdim, n, nt, "smooth_tc" if tc else "smooth_layers", 0), device=dev).contiguous()
 H = s.hierarchy()
 N = H[level]["nodes"]
-x = torch.rand(N, dtype=torch.float64, device=dev); b = torch.rand_like(x); y = torch.empty_like(x)
 with torch.cuda.stream(st):
+    s.rhs(rho, None, None)            # rho-dependent setup (coarse levels, weights)
     s.bench_op(rho, level, mode, 3)
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record(st); s.bench_op(rho, level, mode, 10); e1.record(st)
 torch.cuda.synchronize()
-print("us per launch", e0.elapsed_time(e1) / 10 * 1e3, "nodes", N)
+us = e0.elapsed_time(e1) / 10 * 1e3
+print(f"us per launch {us:.2f} nodes {N} -> {24 * N / us / 1e3:.0f} GB/s (24 B/node)")

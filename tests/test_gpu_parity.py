@@ -274,3 +274,80 @@ def test_jacobi_weight_bound(sdim, n, nt, tc, mats):
     assert rho_spec <= H[0]["lam_max"] * (1 + 1e-12)
     assert abs(H[0]["omega"] - min(0.75, 1.8 / R_ref)) <= 1e-14
     solver.close()
+
+
+@pytest.mark.parametrize("tc", [False, True])
+def test_config5_design_loop_matches_oracle(tc):
+    """BASELINE config 5 (replica: 16^2 x 16, 3 OC iterations from rho = 0.4; R-13): the
+    GPU loop (st_filter / st_solve / st_adjoint / st_sensitivity / st_oc_update) gives the oracle's
+    designs and compliance history."""
+    import paper_2508_09589_b200 as S
+    n, nt = 16, 16
+    shape = (n, n) if tc else (nt, n, n)
+    solver, prob = make_pair(2, n, nt, time_constant=tc, rtol=1e-11, maxit=400)
+    rho0 = np.full(shape, 0.4)
+    designs, hist = O.design_loop(prob, rho0, 3)
+    rho = dev(rho0).reshape(-1).clone()
+    hist_g = S.design_loop(solver, rho, 3)
+    assert np.allclose(hist_g, hist, rtol=1e-9), (hist_g, hist)
+    assert rel(host(rho).reshape(shape), designs[-1]) <= 1e-7, rel(host(rho).reshape(shape), designs[-1])
+    solver.close()
+
+
+def test_filter_and_oc_kernels_match_oracle():
+    solver, prob = make_pair(2, 12, 10)
+    rng = np.random.default_rng(4)
+    a = rng.uniform(0, 1, (10, 12, 12))
+    out = torch.empty(a.size, dtype=torch.float64, device=DEV)
+    solver.filter(dev(a), out)
+    assert rel(host(out).reshape(a.shape), O.density_filter(a)) <= 1e-14
+    solver.filter(dev(a), out, transpose=True)
+    assert rel(host(out).reshape(a.shape), O.density_filter(a, transpose=True)) <= 1e-14
+    dJ = -rng.uniform(1e-6, 1e-3, a.shape)
+    new = torch.empty_like(out)
+    lam = solver.oc_update(dev(a), dev(dJ), new)
+    ref, lam_ref = O.oc_update(a, dJ)
+    assert abs(lam - lam_ref) <= 1e-10 * lam_ref
+    assert rel(host(new).reshape(a.shape), ref) <= 1e-12
+    solver.close()
+
+
+@pytest.mark.parametrize("sdim,n,nt,tc", [(2, 64, 64, True), (2, 32, 64, False), (3, 8, 16, True)])
+def test_fused_small_level_vcycle_equals_per_level_launches(sdim, n, nt, tc, monkeypatch):
+    """The cluster kernel that runs the small-level tail of the V-cycle (vsmall.cu) is the same
+    linear map as the per-level launches (up to summation order), forward and adjoint."""
+    rho = _rho(sdim, n, nt, "uniform", 6, tc)
+    x = I.rand_vector((n + 1) ** sdim * (nt + 1), 12)
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("ST_VSMALL", flag)
+        solver, prob = make_pair(sdim, n, nt, mats=CFG4_MATS, time_constant=tc, coarse_max_nodes=64)
+        z = torch.empty(x.size, dtype=torch.float64, device=DEV)
+        zt = torch.empty_like(z)
+        solver.vcycle(dev(rho), dev(x), z)
+        solver.vcycle(dev(rho), dev(x), zt, transpose=True)
+        outs.append((host(z), host(zt)))
+        solver.close()
+    assert rel(outs[1][0], outs[0][0]) <= 1e-12
+    assert rel(outs[1][1], outs[0][1]) <= 1e-12
+
+
+@pytest.mark.parametrize("sdim,n,nt,tc", [(2, 12, 10, False), (3, 4, 6, True)])
+def test_pnorm_objective_and_adjoint_rhs(sdim, n, nt, tc):
+    """The paper's objective phi = (sum Tavg^P)^(1/P), P = 20 and its gradient
+     equal the oracle's; the adjoint with that RHS matches the oracle's too."""
+    solver, prob = make_pair(sdim, n, nt, mats=CFG4_MATS, time_constant=tc, rtol=1e-11, maxit=400)
+    rho = _rho(sdim, n, nt, "uniform", 8, tc)
+    T_ref = prob.forward(rho)
+    phi_ref, g_ref = O.pnorm_objective(prob.mesh, T_ref, 20.0)
+    T = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+    solver.solve(dev(rho), T)
+    g = torch.empty_like(T)
+    phi = solver.pnorm(T, 20.0, g)
+    assert abs(phi - phi_ref) <= 1e-10 * abs(phi_ref)
+    assert rel(host(g), g_ref) <= 1e-9
+    lam = torch.zeros_like(T)
+    solver.adjoint(dev(rho), g, lam)
+    lam_ref = prob.adjoint(rho, g_ref)
+    assert rel(host(lam), lam_ref) <= 1e-8
+    solver.close()

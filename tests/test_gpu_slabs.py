@@ -155,3 +155,84 @@ def test_time_slabs_match_oracle(name, size):
     # partition invariance of the method: the same iteration counts as one rank (+-1: rounding order)
     assert abs(res[0]["its"][0] - ref1["its"][0]) <= 1 and abs(res[0]["its"][1] - ref1["its"][1]) <= 1, \
         (res[0]["its"], ref1["its"])
+
+
+def _design_worker(rank, size, port, q):
+    """Config-5 loop (3 OC iterations, 16^2 x 16 replica) on `size` time slabs."""
+    try:
+        import datetime
+        import torch
+        import torch.distributed as dist
+        import paper_2508_09589_b200 as S
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=size, timeout=datetime.timedelta(seconds=180))
+        torch.cuda.set_device(0)
+        hc = S.TorchHostComm() if size > 1 else None
+        solver = S.Solver(2, 16, 16, mats=CFG1_MATS, rank=rank, size=size, host_comm=hc, rtol=1e-11, maxit=400,
+                          agg_nodes=64)
+        lay = solver.layout()
+        # the design kernels on slabs, one at a time, on seeded global fields
+        a = np.random.default_rng(3).uniform(0.1, 1.0, (16, 16, 16))
+        g = -np.random.default_rng(4).uniform(1e-6, 1e-3, (16, 16, 16))
+        l0, nl = lay["layer0"], lay["n_layers"]
+        ad = torch.as_tensor(np.ascontiguousarray(a[l0:l0 + nl]).reshape(-1), device="cuda:0")
+        gd = torch.as_tensor(np.ascontiguousarray(g[l0:l0 + nl]).reshape(-1), device="cuda:0")
+        fa = torch.empty(lay["rho_layers"] * 256, dtype=torch.float64, device="cuda:0")
+        solver.filter(ad, fa)
+        fta = torch.empty_like(gd)
+        solver.filter(gd, fta, transpose=True)
+        oc = torch.empty_like(ad)
+        lam_oc = solver.oc_update(ad, gd, oc)
+        rho = torch.full((nl * 256,), 0.4, dtype=torch.float64, device="cuda:0")
+        hist = S.design_loop(solver, rho, 3)
+        out = dict(rank=rank, rho=rho.cpu().numpy(), hist=hist, fa=fa.cpu().numpy(), fta=fta.cpu().numpy(),
+                   oc=oc.cpu().numpy(), lam_oc=lam_oc, l0=l0, nl=nl, rl=lay["rho_layers"])
+        solver.close()
+        if size > 1:
+            dist.barrier()
+        dist.destroy_process_group()
+        q.put(out)
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put(dict(rank=rank, error=traceback.format_exc()))
+
+
+def test_config5_design_loop_on_slabs():
+    """The config-5 loop (density filter across slab boundaries, global OC volume, ...) on 2 slabs
+    gives the oracle's designs and compliance history (R-13, sec. 11)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    qq = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_design_worker, args=(r, 2, port, qq)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = []
+    try:
+        for _ in procs:
+            res.append(qq.get(timeout=400))
+        errs = [r["error"] for r in res if "error" in r]
+        assert not errs, "\n".join(errs)
+    finally:
+        for p in procs:
+            p.join(timeout=5)
+            if p.is_alive():
+                p.terminate()
+    res.sort(key=lambda r: r["rank"])
+    a = np.random.default_rng(3).uniform(0.1, 1.0, (16, 16, 16))
+    g = -np.random.default_rng(4).uniform(1e-6, 1e-3, (16, 16, 16))
+    Fa, Fta = O.density_filter(a), O.density_filter(g, transpose=True)
+    oc_ref, lam_ref = O.oc_update(a, g)
+    for r in res:
+        l0, nl, rl = r["l0"], r["nl"], r["rl"]
+        assert rel(r["fa"].reshape(rl, 16, 16), Fa[l0:l0 + rl]) <= 1e-14, ("F", r["rank"])
+        assert rel(r["fta"].reshape(nl, 16, 16), Fta[l0:l0 + nl]) <= 1e-14, ("F^T", r["rank"])
+        assert abs(r["lam_oc"] - lam_ref) <= 1e-10 * lam_ref, ("Lambda", r["rank"], r["lam_oc"], lam_ref)
+        assert rel(r["oc"].reshape(nl, 16, 16), oc_ref[l0:l0 + nl]) <= 1e-12, ("OC", r["rank"])
+    prob = O.Problem(O.Mesh(2, 16, 16), O.Materials(*CFG1_MATS), O.BCs(), O.Source())
+    designs, hist = O.design_loop(prob, np.full((16, 16, 16), 0.4), 3)
+    for r in res:
+        assert np.allclose(r["hist"], hist, rtol=1e-9), (r["hist"], hist)
+    rho = np.concatenate([r["rho"] for r in res]).reshape(16, 16, 16)
+    assert rel(rho, designs[-1]) <= 1e-7, rel(rho, designs[-1])
