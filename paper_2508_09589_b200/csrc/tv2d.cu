@@ -72,6 +72,14 @@ __device__ __forceinline__ double ap9(const double (&w)[9], const double (&nb)[R
   return a + b;
 }
 
+// 1/d for the per-plane Jacobi diagonal: float reciprocal + two Newton steps (full double accuracy
+// for the positive, float-range diagonals; ~8 instructions instead of a double division)
+__device__ __forceinline__ double rcp_d(double d) {
+  double r = (double)__frcp_rn((float)d);
+  r = r * fma(-d, r, 2.0);
+  return r * fma(-d, r, 2.0);
+}
+
 // 9 stiffness weights of the thread's row-r node from the 4 element conductivities (x 6)
 __device__ __forceinline__ void wk_from(double sw, double se, double nw, double ne, double (&w)[9]) {
   w[0] = -2.0 * sw; w[2] = -2.0 * se; w[6] = -2.0 * nw; w[8] = -2.0 * ne;
@@ -81,7 +89,9 @@ __device__ __forceinline__ void wk_from(double sw, double se, double nw, double 
 
 // SRC: 0 = fine level from rho (per-layer k~ from the element densities); 1 = stored per-layer
 // stiffness of a time-varying Galerkin space level (uniform capacity: the separable mass op.msc)
-template <int SRC, int MODE, bool TRANS>
+// PK3: SIMP conductivity exponent p_k = 3 (every BASELINE config) evaluated as rho^3 (a runtime
+// exponent costs a branch ladder and a pow call per element and layer)
+template <int SRC, int MODE, bool TRANS, bool PK3>
 __global__ void __launch_bounds__(NTH, SRC == 0 ? 3 : 2)
     tv2d_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, OpDesc op,
                 const double* __restrict__ x, double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx) {
@@ -223,7 +233,8 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 3 : 2)
           const int e = tid + k * NTH;
           if (e < ET) {
             const bool v = has && ((rval >> k) & 1u);
-            kd[e] = v ? op.m.kins + op.m.dk * powp(rd[e], op.m.pk) : 0.0;
+            const double rr = rd[e];
+            kd[e] = v ? op.m.kins + op.m.dk * (PK3 ? rr * rr * rr : powp(rr, op.m.pk)) : 0.0;
           }
         }
       }
@@ -295,7 +306,7 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 3 : 2)
           for (int r = 0; r < RY; ++r) {
             const double bot = fma(t00, Kaprev[r], t01 * Kb[r]);
             const double Ax = TRANS ? fma(-sm, Mq[r], carry[r] + bot) : carry[r] + bot;
-            const double od = ND ? omega / (dcarry[r] + t00 * dCc[r]) : 0.0;
+            const double od = ND ? omega * rcp_d(dcarry[r] + t00 * dCc[r]) : 0.0;
             double o;
             if (MODE == MODE_APPLY) o = Ax;
             else if (MODE == MODE_RESID) o = bp[r * TX] - Ax;
@@ -385,12 +396,12 @@ bool map3_tv(CUtensorMap* m, const void* base, unsigned long long d0, unsigned l
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int SRC, int MODE, bool TRANS>
+template <int SRC, int MODE, bool TRANS, bool PK3>
 void ltv(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, const double* x, double* y, double omega,
          cudaStream_t s) {
   using namespace tv;
   const Geom& g = op.g;
-  auto kern = tv2d_kernel<SRC, MODE, TRANS>;
+  auto kern = tv2d_kernel<SRC, MODE, TRANS, PK3>;
   constexpr bool NX = (MODE != MODE_JAC0), NBV = (MODE != MODE_APPLY);
   constexpr int RS = SRC == 0 ? RS0 : RS1;
   constexpr size_t bytes = sizeof(double) * (16 + (NX ? NB * XS : 0) + (NBV ? NB * BS : 0) + NB * RS + 2 * ET);
@@ -421,6 +432,7 @@ bool launch_op_tv2d(const OpDesc& op, int mode, bool trans, bool mask, const dou
   const Geom& g = op.g;
   const bool rho_tv = op.form == FORM_RHO && !op.rho_tc && op.m.dC == 0.0;
   const bool mk_tv = op.form == FORM_MK && op.tvl && op.msep;
+  const bool pk3 = op.m.pk == 3.0;
   if (g.sd != 2 || !mask || !(rho_tv || mk_tv)) return false;
   if (op.U[0][0] != 0.0 || op.U[0][1] != 0.0 || op.U[1][0] != -1.0 || op.U[1][1] != 1.0) return false;
   if (op.Tm[0][1] != op.Tm[1][0]) return false;
@@ -432,10 +444,12 @@ bool launch_op_tv2d(const OpDesc& op, int mode, bool trans, bool mask, const dou
   if (nbv && !map3_tv(&mb, b, nn, nn, g.nt + 1, s1, s2, tv::TX, tv::TY)) return false;
 #define C4(M)                                                                            \
   case M:                                                                                \
-    if (rho_tv) { if (trans) ltv<0, M, true>(mx, mb, op, x, y, omega, s);                \
-                  else ltv<0, M, false>(mx, mb, op, x, y, omega, s); }                   \
-    else { if (trans) ltv<1, M, true>(mx, mb, op, x, y, omega, s);                       \
-           else ltv<1, M, false>(mx, mb, op, x, y, omega, s); }                          \
+    if (rho_tv && pk3) { if (trans) ltv<0, M, true, true>(mx, mb, op, x, y, omega, s);   \
+                         else ltv<0, M, false, true>(mx, mb, op, x, y, omega, s); }      \
+    else if (rho_tv) { if (trans) ltv<0, M, true, false>(mx, mb, op, x, y, omega, s);    \
+                       else ltv<0, M, false, false>(mx, mb, op, x, y, omega, s); }       \
+    else { if (trans) ltv<1, M, true, true>(mx, mb, op, x, y, omega, s);                 \
+           else ltv<1, M, false, true>(mx, mb, op, x, y, omega, s); }                    \
     break;
   switch (mode) {
     C4(MODE_APPLY)
