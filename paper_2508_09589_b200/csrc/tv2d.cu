@@ -8,10 +8,17 @@
 //   M x_q (separable),  Kb_q = K^(q-1) x_q  (layer below),  Ka_q = K^(q) x_q  (layer above)
 // and completes row q-1 = carry + t00 Ka_{q-1} + t01 Kb_q (K^T: - M x_q), carry for row q =
 // M (x_q - x_{q-1}) + t01 Ka_{q-1} + t11 Kb_q (K^T: M x_q).
-// Design: persistent one-wave grid over (tile, plane) work as tc2d; x and b
-// tiles by TMA into a 6-slot mbarrier ring; the 33 x 9 element tile of rho for layer q by
-// cp.async (zero outside the domain), converted once to k~ in shared memory (two layer buffers);
-// 9 stiffness weights per node and layer rebuilt from 4 element values; 2 applies per plane.
+// Design: persistent one-wave grid over (tile, plane) work as tc2d; per plane
+// ONE mbarrier-tracked TMA group brings the x tile, the b tile and the layer tile (SRC 0: the
+// 34 x 9 element box of rho of layer q, SRC 1: the 5 x 34 x 9 forward stiffness coefficients of
+// layer q; box origin (max(x0-2, 0), max(y0-1, 0)): a tile-mode fp64 TMA box must start at a
+// non-negative, 16-byte aligned coordinate (else an illegal instruction, scripts/dev/tma_neg.cu,
+// scripts/dev/tv_probe.sh); entries beyond the last node/element are zero-filled, out-of-domain
+// neighbours masked) into a ring slot, so a plane
+// costs one barrier wait and one __syncthreads (slot release). SRC 0 keeps the 6 element
+// conductivities of the layer below in registers and applies K through the 4 element "brackets"
+// of x at the node (shared by the layer-below and layer-above products); SRC 1 re-reads the layer
+// below from the previous ring slot, which is only refilled after the plane is done.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -25,11 +32,13 @@ namespace tv {
 
 constexpr int TX = 32, TYT = 4, RY = 2, TY = TYT * RY;   // node tile 32 x 8
 constexpr int HX = TX + 4, HY = TY + 2;                  // x tile 36 x 10 (col 0 unused)
-constexpr int XS = 368, BS = 256;                        // slot sizes (doubles)
-constexpr int EX = TX + 1, EY = TY + 1, ET = EX * EY;    // element tile 33 x 9
-constexpr int CXW = TX + 2, CT = CXW * EY;               // stored-coefficient node tile 34 x 9
-constexpr int RS0 = 304, RS1 = 5 * CT + 2;               // per-layer slot: rho tile / 5 K coefficient tiles
-constexpr int NB = 6;
+constexpr int XS = 368, BS = 256;                        // slot sizes (doubles, multiples of 128 B)
+constexpr int EY = TY + 1;                               // layer box rows y0-1 .. y0+7
+constexpr int EX0 = TX + 2, EX1 = TX + 4;                // box columns from x0-2: elements x0-1 .. x0+31 /
+                                                         // nodes x0-1 .. x0+32 (even widths: 16-B rows)
+constexpr int ET0 = EX0 * EY, ET1 = EX1 * EY;
+constexpr int RS0 = 320, RS1 = 1664;                     // layer slot: rho box / 5 coefficient boxes
+constexpr int NB0 = 6, NB1 = 4;                          // ring depth (planes)
 constexpr int NTH = TX * TYT;
 constexpr unsigned XBYTES = HX * HY * 8, BBYTES = TX * TY * 8;
 
@@ -58,6 +67,13 @@ __device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, uint64_t
       "l"((uint64_t)map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ void tma4(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];\n" ::"r"(
+          su32(dst)),
+      "l"((uint64_t)map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
 
 __device__ __forceinline__ double ap9(const double (&w)[9], const double (&nb)[RY + 2][3], int r) {
   double a = w[4] * nb[r + 1][1];
@@ -80,11 +96,21 @@ __device__ __forceinline__ double rcp_d(double d) {
   return r * fma(-d, r, 2.0);
 }
 
-// 9 stiffness weights of the thread's row-r node from the 4 element conductivities (x 6)
-__device__ __forceinline__ void wk_from(double sw, double se, double nw, double ne, double (&w)[9]) {
-  w[0] = -2.0 * sw; w[2] = -2.0 * se; w[6] = -2.0 * nw; w[8] = -2.0 * ne;
-  w[1] = -(sw + se); w[7] = -(nw + ne); w[3] = -(sw + nw); w[5] = -(se + ne);
-  w[4] = 4.0 * ((sw + se) + (nw + ne));
+// the 9 stiffness weights (x 6) of a node from the forward coefficients of a layer box: its own
+// (centre, +1 0, -1 +1, 0 +1, +1 +1) and the mirrored ones of the (i-1, j-1), (i, j-1), (i+1, j-1),
+// (i-1, j) neighbours (the operator is symmetric in space)
+// (mi: i >= 1, mj: j >= 1; neighbours beyond the last node are zero-filled by the TMA)
+__device__ __forceinline__ void wk_box(const double* ct, int L, bool mi, bool mj, double (&w)[9]) {
+  constexpr int EX = EX1, ET = ET1;
+  w[4] = ct[0 * ET + L];
+  w[5] = ct[1 * ET + L];
+  w[6] = ct[2 * ET + L];
+  w[7] = ct[3 * ET + L];
+  w[8] = ct[4 * ET + L];
+  w[0] = (mi && mj) ? ct[4 * ET + L - EX - 1] : 0.0;
+  w[1] = mj ? ct[3 * ET + L - EX] : 0.0;
+  w[2] = mj ? ct[2 * ET + L - EX + 1] : 0.0;
+  w[3] = mi ? ct[1 * ET + L - 1] : 0.0;
 }
 
 // SRC: 0 = fine level from rho (per-layer k~ from the element densities); 1 = stored per-layer
@@ -92,19 +118,22 @@ __device__ __forceinline__ void wk_from(double sw, double se, double nw, double 
 // PK3: SIMP conductivity exponent p_k = 3 (every BASELINE config) evaluated as rho^3 (a runtime
 // exponent costs a branch ladder and a pow call per element and layer)
 template <int SRC, int MODE, bool TRANS, bool PK3>
-__global__ void __launch_bounds__(NTH, SRC == 0 ? 3 : 2)
-    tv2d_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, OpDesc op,
-                const double* __restrict__ x, double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx) {
+__global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
+    tv2d_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
+                const __grid_constant__ CUtensorMap tml, OpDesc op, const double* __restrict__ x,
+                double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx) {
   constexpr bool NX = (MODE != MODE_JAC0);
   constexpr bool NBV = (MODE != MODE_APPLY);
   constexpr bool ND = (MODE == MODE_JAC || MODE == MODE_JAC0);
+  constexpr int NB = SRC == 0 ? NB0 : NB1;
+  constexpr int RS = SRC == 0 ? RS0 : RS1;
+  constexpr int EX = SRC == 0 ? EX0 : EX1;
+  constexpr unsigned LBYTES = (SRC == 0 ? ET0 : 5 * ET1) * 8;
   extern __shared__ __align__(128) double smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   double* xs = smem + 16;                    // [NB][XS]
   double* bs = xs + (NX ? NB * XS : 0);      // [NB][BS]
-  constexpr int RS = SRC == 0 ? RS0 : RS1;
-  double* rs = bs + (NBV ? NB * BS : 0);     // [NB][RS] layer tiles (layer q arrives with plane q)
-  double* kk = rs + NB * RS;                 // [2][ET] k~ of the current / next layer (SRC 0)
+  double* ls = bs + (NBV ? NB * BS : 0);     // [NB][RS] layer boxes (layer q arrives with plane q)
 
   const Geom& g = op.g;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
@@ -113,8 +142,6 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 3 : 2)
   const long long NP = g.nt + 1;
   const int xo = (ty * RY) * HX + tx + 1;
   const int bo = (ty * RY) * TX + tx;
-  constexpr int TILE = SRC == 0 ? ET : 5 * CT;  // doubles copied per layer
-  constexpr int RPT = (TILE + NTH - 1) / NTH;
 
   if (tid == 0) {
 #pragma unroll
@@ -124,7 +151,7 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 3 : 2)
   const double sm = SRC == 0 ? g.dx * g.dx * (1.0 / 36.0) * op.m.Cins : op.msc;
   const double sk = SRC == 0 ? 1.0 / 6.0 : 1.0;
   const double t00 = op.Tm[0][0] * sk, t01 = op.Tm[0][1] * sk, t11 = op.Tm[1][1] * sk;
-  const unsigned tx_full = (NX ? XBYTES : 0u) + (NBV ? BBYTES : 0u);
+  const unsigned tx_plane = (NX ? XBYTES : 0u) + (NBV ? BBYTES : 0u);
 
   long long w = wtot * blockIdx.x / gridDim.x;
   const long long wend = wtot * (blockIdx.x + 1) / gridDim.x;
@@ -147,147 +174,116 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 3 : 2)
       cy[r] = (j == 0 || j == n) ? 2.0 : 4.0;
     }
     const double cx = (i == 0 || i == n) ? 2.0 : 4.0;
-    // this thread's per-layer copies: SRC 0 the 33 x 9 element tile of rho from (x0-1, y0-1);
-    // SRC 1 the 34 x 9 node tiles of the 5 forward stiffness coefficients from (x0-1, y0-1); zero outside
-    long long roff[RPT];
-    unsigned rval = 0u;
+    const int bx = max(x0 - 2, 0), by = max(y0 - 1, 0);  // layer box origin (x0 is a multiple of 32)
+    // box entry of element (i-1, j0-1) (SRC 0) / of node (i, j0) (SRC 1); entries left of / below
+    // the domain are never used unmasked
+    const int lo = SRC == 0 ? (j0 - 1 - by) * EX + (i - 1 - bx) : (j0 - by) * EX + (i - bx);
+    // SRC 0: the thread's 6 elements (i-1+d, j0-1+s) inside the domain
+    unsigned ev = 0u;
+    if (SRC == 0) {
 #pragma unroll
-    for (int k = 0; k < RPT; ++k) {
-      const int e = tid + k * NTH;
-      bool v;
-      if (SRC == 0) {
-        const int ly = e / EX, lx = e - ly * EX;
-        const int gi = x0 - 1 + lx, gj = y0 - 1 + ly;
-        v = (e < ET) && gi >= 0 && gi < n && gj >= 0 && gj < n;
-        roff[k] = v ? (long long)gj * n + gi : 0;
-      } else {
-        const int a = e / CT, loc = e - a * CT;
-        const int ly = loc / CXW, lx = loc - ly * CXW;
-        const int gi = x0 - 1 + lx, gj = y0 - 1 + ly;
-        v = (e < 5 * CT) && gi >= 0 && gi <= n && gj >= 0 && gj <= n;
-        roff[k] = v ? (long long)a * P + (long long)gj * pr + gi : 0;
-      }
-      if (v) rval |= 1u << k;
+      for (int s2 = 0; s2 <= RY; ++s2)
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          const int gi = i - 1 + d, gj = j0 - 1 + s2;
+          if (gi >= 0 && gi < n && gj >= 0 && gj < n) ev |= 1u << (2 * s2 + d);
+        }
     }
     __syncthreads();  // barrier init / previous segment fully consumed
 
-    // producer: x / b by TMA (elected thread), rho layer q by cp.async (all threads), one
-    // commit group per plane
-    auto issue_rho = [&](int q, unsigned slot) {
-      if (q < g.nt) {  // layer q exists locally (the last plane has no layer above)
-        double* rd = rs + slot * RS;
-        const double* rq = SRC == 0 ? op.rho + (long long)q * n * n
-                                    : op.st + ((long long)q * 2 + 1) * 5 * P;  // K block of layer q
-#pragma unroll
-        for (int k = 0; k < RPT; ++k) {
-          const int e = tid + k * NTH;
-          if (e < TILE) {
-            const int sz = ((rval >> k) & 1u) ? 8 : 0;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(su32(rd + e)), "l"(rq + roff[k]), "r"(sz));
-          }
-        }
+    auto issue = [&](int q, unsigned slot) {  // elected thread: plane q (+ layer q) into `slot`
+      const bool wb = NBV && q >= p0 && q < p1;
+      const bool hl = q < g.nt;               // layer q exists locally (the last plane has none above)
+      mbar_expect_tx(&bar[slot], tx_plane - ((NBV && !wb) ? BBYTES : 0u) + (hl ? LBYTES : 0u));
+      if (NX) tma3(xs + slot * XS, &tmx, &bar[slot], x0, y0, q);
+      if (wb) tma3(bs + slot * BS, &tmb, &bar[slot], x0, y0, q);
+      if (hl) {
+        if (SRC == 0) tma3(ls + slot * RS, &tml, &bar[slot], bx, by, q);
+        else tma4(ls + slot * RS, &tml, &bar[slot], bx, by, 0, 2 * q + 1);
       }
-      asm volatile("cp.async.commit_group;\n" ::);
     };
-    if (tid == 0) {
-      for (int k = 0; k < NB - 1 && qs + k <= qe; ++k) {
-        const int q = qs + k;
-        const unsigned slot = (ring + k) % NB;
-        const bool wb = NBV && q >= p0 && q < p1;
-        mbar_expect_tx(&bar[slot], tx_full - ((NBV && !wb) ? BBYTES : 0u));
-        if (NX) tma3(xs + slot * XS, &tmx, &bar[slot], x0, y0, q);
-        if (wb) tma3(bs + slot * BS, &tmb, &bar[slot], x0, y0, q);
-      }
-    }
-    for (int k = 0; k < NB - 1; ++k) {
-      if (qs + k <= qe) issue_rho(qs + k, (ring + k) % NB);
-      else asm volatile("cp.async.commit_group;\n" ::);
-    }
+    if (tid == 0)
+      for (int k = 0; k < NB - 1 && qs + k <= qe; ++k) issue(qs + k, (ring + k) % NB);
 
-    double wKc[RY][9];  // stiffness weights of layer q-1 (below plane q)
-    double dCc[RY];     // their centre weights
+    double kc[RY + 1][2];  // SRC 0: element conductivities of layer q-1 (below plane q)
+    double dCc[RY];        // centre stiffness weight of layer q-1
     double Mprev[RY], Kaprev[RY], carry[RY], dcarry[RY];
 #pragma unroll
-    for (int r = 0; r < RY; ++r) {
-      Mprev[r] = Kaprev[r] = carry[r] = dcarry[r] = dCc[r] = 0.0;
+    for (int r = 0; r < RY; ++r) Mprev[r] = Kaprev[r] = carry[r] = dcarry[r] = dCc[r] = 0.0;
 #pragma unroll
-      for (int k = 0; k < 9; ++k) wKc[r][k] = 0.0;
-    }
+    for (int s2 = 0; s2 <= RY; ++s2) kc[s2][0] = kc[s2][1] = 0.0;
     double* yrow = y + (long long)(qs - 1) * P + (long long)j0 * pr + i;
     unsigned cur = ring, prv = (ring + NB - 1) % NB;
-    const double* xq = xs + cur * XS + xo;
-    const double* xp = xs + prv * XS + xo;
-    const double* bp = bs + prv * BS + bo;
-    int kb = 0;  // k~ buffer of the layer above plane q
     for (int q = qs; q <= qe; ++q) {
       mbar_wait(&bar[cur], (phase >> cur) & 1u);
       phase ^= 1u << cur;
-      asm volatile("cp.async.wait_group %0;\n" ::"n"(NB - 2));
-      // k~ of layer q (above plane q), zero outside the domain / beyond the last layer
-      if (SRC == 0) {
-        double* kd = kk + kb * ET;
-        const double* rd = rs + cur * RS;
-        const bool has = q < g.nt;
+      const bool has = q < g.nt;
+      const double* xq = xs + cur * XS + xo;
+      double kn[RY + 1][2];
+      double dCn[RY];
+      if (SRC == 0) {  // k~ of layer q, zero outside the domain / beyond the last layer
+        const double* rd = ls + cur * RS + lo;
 #pragma unroll
-        for (int k = 0; k < RPT; ++k) {
-          const int e = tid + k * NTH;
-          if (e < ET) {
-            const bool v = has && ((rval >> k) & 1u);
-            const double rr = rd[e];
-            kd[e] = v ? op.m.kins + op.m.dk * (PK3 ? rr * rr * rr : powp(rr, op.m.pk)) : 0.0;
+        for (int s2 = 0; s2 <= RY; ++s2)
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            const double rr = rd[s2 * EX + d];
+            const bool v = has && ((ev >> (2 * s2 + d)) & 1u);
+            kn[s2][d] = v ? op.m.kins + op.m.dk * (PK3 ? rr * rr * rr : powp(rr, op.m.pk)) : 0.0;
           }
-        }
-      }
-      __syncthreads();
-      // weights of layer q for the thread's nodes (rows j0, j0+1): elements rows j0-1 .. j0+1
-      double wKn[RY][9];
-      if (SRC == 1) {
-        // own forward coefficients and the neighbours' mirrored ones (zero beyond the last layer)
-        const double* ct = rs + cur * RS;
-        const bool has = q < g.nt;
 #pragma unroll
-        for (int r = 0; r < RY; ++r) {
-          const int L = (ty * RY + r + 1) * CXW + tx + 1;  // node (i, j) in the tile
-          wKn[r][4] = has ? ct[0 * CT + L] : 0.0;
-          wKn[r][5] = has ? ct[1 * CT + L] : 0.0;
-          wKn[r][6] = has ? ct[2 * CT + L] : 0.0;
-          wKn[r][7] = has ? ct[3 * CT + L] : 0.0;
-          wKn[r][8] = has ? ct[4 * CT + L] : 0.0;
-          wKn[r][0] = has ? ct[4 * CT + L - CXW - 1] : 0.0;  // (i-1, j-1): its (+1, +1)
-          wKn[r][1] = has ? ct[3 * CT + L - CXW] : 0.0;      // (i,   j-1): its ( 0, +1)
-          wKn[r][2] = has ? ct[2 * CT + L - CXW + 1] : 0.0;  // (i+1, j-1): its (-1, +1)
-          wKn[r][3] = has ? ct[1 * CT + L - 1] : 0.0;        // (i-1, j  ): its (+1,  0)
-        }
-      } else {
-        const double* kd = kk + kb * ET + (ty * RY) * EX + tx;
-        double kw[RY + 1], ke[RY + 1];
-#pragma unroll
-        for (int s = 0; s <= RY; ++s) { kw[s] = kd[s * EX]; ke[s] = kd[s * EX + 1]; }
-#pragma unroll
-        for (int r = 0; r < RY; ++r) wk_from(kw[r], ke[r], kw[r + 1], ke[r + 1], wKn[r]);
+        for (int r = 0; r < RY; ++r) dCn[r] = 4.0 * ((kn[r][0] + kn[r][1]) + (kn[r + 1][0] + kn[r + 1][1]));
       }
       double Mq[RY], Kb[RY], Ka[RY];
       if (NX && q + g.pg0 > 0) {
         double nb[RY + 2][3];
 #pragma unroll
-        for (int s = 0; s < RY + 2; ++s)
+        for (int s2 = 0; s2 < RY + 2; ++s2)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) nb[s][c] = xq[s * HX + c];
+          for (int c = 0; c < 3; ++c) nb[s2][c] = xq[s2 * HX + c];
         double rsum[RY + 2];
 #pragma unroll
-        for (int s = 0; s < RY + 2; ++s) rsum[s] = fma(cx, nb[s][1], nb[s][0] + nb[s][2]);
+        for (int s2 = 0; s2 < RY + 2; ++s2) rsum[s2] = fma(cx, nb[s2][1], nb[s2][0] + nb[s2][2]);
         if (j0 == 0) rsum[0] = 0.0;  // row j = -1 aliases the previous plane's last row
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
           Mq[r] = fma(cy[r], rsum[r + 1], rsum[r] + rsum[r + 2]);
-          Kb[r] = ap9(wKc[r], nb, r);
-          Ka[r] = ap9(wKn[r], nb, r);
+          if (SRC == 0) {
+            // element brackets: sum_e k_e (K_e x)_node with K_e the unit Q1 stiffness (x 6)
+            const double c4 = 4.0 * nb[r + 1][1];
+            const double bsw = c4 - fma(2.0, nb[r][0], nb[r][1] + nb[r + 1][0]);
+            const double bse = c4 - fma(2.0, nb[r][2], nb[r][1] + nb[r + 1][2]);
+            const double bnw = c4 - fma(2.0, nb[r + 2][0], nb[r + 2][1] + nb[r + 1][0]);
+            const double bne = c4 - fma(2.0, nb[r + 2][2], nb[r + 2][1] + nb[r + 1][2]);
+            Ka[r] = fma(kn[r][0], bsw, fma(kn[r][1], bse, fma(kn[r + 1][0], bnw, kn[r + 1][1] * bne)));
+            Kb[r] = fma(kc[r][0], bsw, fma(kc[r][1], bse, fma(kc[r + 1][0], bnw, kc[r + 1][1] * bne)));
+          } else {
+            const int L = lo + r * EX;  // node (i, j0 + r) in the box
+            double wv[9];
+            if (q > qs) {
+              wk_box(ls + prv * RS, L, i >= 1, j0 + r >= 1, wv);
+              Kb[r] = ap9(wv, nb, r);
+            } else {
+              Kb[r] = 0.0;
+            }
+            if (has) {
+              wk_box(ls + cur * RS, L, i >= 1, j0 + r >= 1, wv);
+              Ka[r] = ap9(wv, nb, r);
+            } else {
+              Ka[r] = 0.0;
+            }
+          }
         }
       } else {
 #pragma unroll
         for (int r = 0; r < RY; ++r) Mq[r] = Kb[r] = Ka[r] = 0.0;
       }
+      if (SRC == 1) {
+#pragma unroll
+        for (int r = 0; r < RY; ++r) dCn[r] = has ? ls[cur * RS + lo + r * EX] : 0.0;
+      }
       if (q > qs && q - 1 >= p0) {  // row q-1 complete (bottom part of layer q-1)
+        const double* bp = bs + prv * BS + bo;
         if (q - 1 + g.pg0 == 0) {
 #pragma unroll
           for (int r = 0; r < RY; ++r) {
@@ -302,6 +298,7 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 3 : 2)
             yrow[r * pr] = o;
           }
         } else {
+          const double* xp = xs + prv * XS + xo;
 #pragma unroll
           for (int r = 0; r < RY; ++r) {
             const double bot = fma(t00, Kaprev[r], t01 * Kb[r]);
@@ -324,42 +321,36 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 3 : 2)
         dcarry[r] = lay ? fma(sm, cx * cy[r], t11 * dCc[r]) : 0.0;
         Mprev[r] = Mq[r];
         Kaprev[r] = Ka[r];
-        dCc[r] = wKn[r][4];
+        dCc[r] = dCn[r];
+      }
+      if (SRC == 0) {
 #pragma unroll
-        for (int k = 0; k < 9; ++k) wKc[r][k] = wKn[r][k];
+        for (int s2 = 0; s2 <= RY; ++s2) { kc[s2][0] = kn[s2][0]; kc[s2][1] = kn[s2][1]; }
       }
-      __syncthreads();  // planes q-1, q and the k~ buffer of layer q-1 consumed
-      if (tid == 0 && q + NB - 1 <= qe) {
-        const int qn = q + NB - 1;
-        const bool wb = NBV && qn >= p0 && qn < p1;
-        mbar_expect_tx(&bar[prv], tx_full - ((NBV && !wb) ? BBYTES : 0u));
-        if (NX) tma3(xs + prv * XS, &tmx, &bar[prv], x0, y0, qn);
-        if (wb) tma3(bs + prv * BS, &tmb, &bar[prv], x0, y0, qn);
-      }
-      if (q + NB - 1 <= qe) issue_rho(q + NB - 1, prv);
-      else asm volatile("cp.async.commit_group;\n" ::);
-      kb ^= 1;
+      if (q == qe) break;  // the last plane's slots stay for the tail row below
+      __syncthreads();     // slot of plane q-1 consumed by every thread
+      if (tid == 0 && q + NB - 1 <= qe) issue(q + NB - 1, prv);
       yrow += P;
       prv = cur;
-      xp = xq;
-      bp = bs + cur * BS + bo;
-      if (++cur == NB) { cur = 0u; xq -= (NB - 1) * XS; } else { xq += XS; }
+      if (++cur == NB) cur = 0u;
     }
     if (p1 == g.nt + 1) {  // last row: top part of layer nt-1 only
+      const double* bq = bs + cur * BS + bo;
+      const double* xq = xs + cur * XS + xo;
+      yrow += P;
 #pragma unroll
       for (int r = 0; r < RY; ++r) {
         const double od = ND ? omega / dcarry[r] : 0.0;
         const double Ax = carry[r];
         double o;
         if (MODE == MODE_APPLY) o = Ax;
-        else if (MODE == MODE_RESID) o = bp[r * TX] - Ax;
-        else if (MODE == MODE_JAC) o = fma(od, bp[r * TX] - Ax, xp[(r + 1) * HX + 1]);
-        else o = od * bp[r * TX];
+        else if (MODE == MODE_RESID) o = bq[r * TX] - Ax;
+        else if (MODE == MODE_JAC) o = fma(od, bq[r * TX] - Ax, xq[(r + 1) * HX + 1]);
+        else o = od * bq[r * TX];
         if (act[r]) yrow[r * pr] = patch[r] ? 0.0 : o;
       }
     }
-    asm volatile("cp.async.wait_group 0;\n" ::);
-    ring = cur;
+    ring = (cur + 1) % NB;
   }
 }
 
@@ -396,15 +387,29 @@ bool map3_tv(CUtensorMap* m, const void* base, unsigned long long d0, unsigned l
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 4D map of the stored per-layer stencils [layer][M|K][5][node]: dims (nn, nn, 5, 2 nl), box 34 x 9 x 5 x 1
+bool map4_tv(CUtensorMap* m, const void* base, unsigned long long nn, unsigned long long nl2, unsigned long long s1,
+             unsigned long long s2, unsigned long long s3) {
+  auto fn = encode_fn_tv();
+  if (!fn || ((uintptr_t)base & 15u) || (s1 & 15u) || (s2 & 15u) || (s3 & 15u)) return false;
+  cuuint64_t dims[4] = {nn, nn, 5, nl2};
+  cuuint64_t strides[3] = {s1, s2, s3};
+  cuuint32_t box[4] = {(cuuint32_t)tv::EX1, (cuuint32_t)tv::EY, 5, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int SRC, int MODE, bool TRANS, bool PK3>
-void ltv(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, const double* x, double* y, double omega,
-         cudaStream_t s) {
+void ltv(const CUtensorMap& mx, const CUtensorMap& mb, const CUtensorMap& ml, const OpDesc& op, const double* x,
+         double* y, double omega, cudaStream_t s) {
   using namespace tv;
   const Geom& g = op.g;
   auto kern = tv2d_kernel<SRC, MODE, TRANS, PK3>;
   constexpr bool NX = (MODE != MODE_JAC0), NBV = (MODE != MODE_APPLY);
-  constexpr int RS = SRC == 0 ? RS0 : RS1;
-  constexpr size_t bytes = sizeof(double) * (16 + (NX ? NB * XS : 0) + (NBV ? NB * BS : 0) + NB * RS + 2 * ET);
+  constexpr int RS = SRC == 0 ? RS0 : RS1, NB = SRC == 0 ? NB0 : NB1;
+  constexpr size_t bytes = sizeof(double) * (16 + NB * ((NX ? XS : 0) + (NBV ? BS : 0) + RS));
   static int resident = 0, nsm = 0;
   if (!resident) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -422,7 +427,7 @@ void ltv(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, const d
   const long long minw = (wtot >= 16LL * nsm * resident) ? 4 : 1;
   if (grid > wtot / minw) grid = wtot / minw;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, op, x, y, omega, wtot, chunk_planes(g.P, g.nt + 1, g.sd), (int)ntx);
+  kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, ml, op, x, y, omega, wtot, chunk_planes(g.P, g.nt + 1, g.sd), (int)ntx);
 }
 }  // namespace
 
@@ -442,14 +447,22 @@ bool launch_op_tv2d(const OpDesc& op, int mode, bool trans, bool mask, const dou
   if (nx && !map3_tv(&mx, x - (g.pr + 2), (unsigned long long)g.pr + 2, nn + 1, g.nt + 1, s1, s2, tv::HX, tv::HY))
     return false;
   if (nbv && !map3_tv(&mb, b, nn, nn, g.nt + 1, s1, s2, tv::TX, tv::TY)) return false;
+  CUtensorMap ml{};  // layer boxes from (x0-1, y0-1); entries outside the domain are zero-filled
+  if (g.nt < 1) return false;
+  if (rho_tv) {
+    const unsigned long long ne = (unsigned long long)g.n;
+    if (!map3_tv(&ml, op.rho, ne, ne, g.nt, ne * 8, ne * ne * 8, tv::EX0, tv::EY)) return false;
+  } else if (!map4_tv(&ml, op.st, nn, 2ull * g.nt, s1, s2, 5ull * s2)) {
+    return false;
+  }
 #define C4(M)                                                                            \
   case M:                                                                                \
-    if (rho_tv && pk3) { if (trans) ltv<0, M, true, true>(mx, mb, op, x, y, omega, s);   \
-                         else ltv<0, M, false, true>(mx, mb, op, x, y, omega, s); }      \
-    else if (rho_tv) { if (trans) ltv<0, M, true, false>(mx, mb, op, x, y, omega, s);    \
-                       else ltv<0, M, false, false>(mx, mb, op, x, y, omega, s); }       \
-    else { if (trans) ltv<1, M, true, true>(mx, mb, op, x, y, omega, s);                 \
-           else ltv<1, M, false, true>(mx, mb, op, x, y, omega, s); }                    \
+    if (rho_tv && pk3) { if (trans) ltv<0, M, true, true>(mx, mb, ml, op, x, y, omega, s);   \
+                         else ltv<0, M, false, true>(mx, mb, ml, op, x, y, omega, s); }      \
+    else if (rho_tv) { if (trans) ltv<0, M, true, false>(mx, mb, ml, op, x, y, omega, s);    \
+                       else ltv<0, M, false, false>(mx, mb, ml, op, x, y, omega, s); }       \
+    else { if (trans) ltv<1, M, true, true>(mx, mb, ml, op, x, y, omega, s);                 \
+           else ltv<1, M, false, true>(mx, mb, ml, op, x, y, omega, s); }                    \
     break;
   switch (mode) {
     C4(MODE_APPLY)

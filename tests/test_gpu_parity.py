@@ -149,15 +149,19 @@ def _P1(nf, kind):
     return P
 
 
-@pytest.mark.parametrize("sdim,n,nt,tc", [(2, 16, 16, False), (2, 32, 32, True), (3, 4, 8, False), (2, 8, 32, False),
-                                            (3, 8, 8, True)])
-def test_coarse_operators(sdim, n, nt, tc):
+@pytest.mark.parametrize("sdim,n,nt,tc,mats", [(2, 16, 16, False, CFG4_MATS), (2, 32, 32, True, CFG4_MATS),
+                                                 (3, 4, 8, False, CFG4_MATS), (2, 8, 32, False, CFG4_MATS),
+                                                 (3, 8, 8, True, CFG4_MATS),
+                                                 # uniform capacity, space-time design: the stored-stencil
+                                                 # TMA kernel (tv2d SRC 1) on levels of several ragged tiles
+                                                 (2, 80, 12, False, CFG1_MATS)])
+def test_coarse_operators(sdim, n, nt, tc, mats):
     """Each coarse level equals, with the Dirichlet masks of its own grid, the operator built
     here independently from assembled matrices: conduction part
     by Galerkin P^T A P with the space/time linear interpolation P; capacity
     part by Galerkin under space coarsening and re-stabilised (upwind U, layer-mean capacity)
     under time coarsening."""
-    solver, prob = make_pair(sdim, n, nt, mats=CFG4_MATS, time_constant=tc)
+    solver, prob = make_pair(sdim, n, nt, mats=mats, time_constant=tc)
     rho = I.rho_uniform((n,) * sdim if tc else (nt,) + (n,) * sdim, 3)
     H = solver.hierarchy()
     C, k, _, _, _ = prob.coefficients(rho)
