@@ -238,6 +238,8 @@ def run_cuda(args):
                 T.zero_(); lam.zero_()
             step(i)
         its.clear()
+        if design:  # the e2e leg below repeats the timed design iterations from the same state
+            snap = (rho_d.clone(), T.clone(), lam.clone())
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -293,12 +295,15 @@ def run_cuda(args):
     # ---- end-to-end through the C ABI with pinned host buffers ------------------------------
     e2e = None
     if args.e2e_steps > 0 and design:
-        # the design iteration through the public API: this step's design comes from pinned host
-        # memory, the new design and the compliance go back to the host
+        # the design iteration through the public API, repeating the timed iterations from their
+        # starting state: this step's design comes from pinned host memory, the new design and the
+        # compliance go back to the host
         rho_ht = torch.empty(rho_d.numel(), dtype=torch.float64).pin_memory()
         new_ht = torch.empty_like(rho_ht).pin_memory()
         saved = list(its)
         et = []
+        rho_d.copy_(snap[0]); T.copy_(snap[1]); lam.copy_(snap[2])
+        del snap
         with torch.cuda.stream(stream):
             for k in range(args.e2e_steps):
                 rho_ht.copy_(rho_d)

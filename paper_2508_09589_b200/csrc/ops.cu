@@ -265,6 +265,92 @@ __global__ void rap_space_kernel(OpDesc fop, Geom gc, int nl, double* __restrict
   for (int q = 0; q < NC; ++q) o[(long long)q * gc.P + pc] = acc[q];
 }
 
+// Spatial coarsening of the fine (rho) level, M and K per layer. The Galerkin weight P^T S P of
+// coarse node C and forward offset q is linear in the element coefficients of the 4^SD fine
+// elements around 2C: S_q = sum_e Tab[s][q][e] coef_e (coef = C~ for s = 0, k~ for s = 1, then the
+// spatial scale sM / sK). Tab (dyadic rationals, exact) is built on the host by the same loops as
+// rap_space_kernel (fine nodes f of supp C, stencil offsets k, elements adjacent to f and f + k,
+// interpolation weights); each thread evaluates its 4^SD element coefficients once instead of
+// once per (f, k) weight.
+__constant__ double c_rap2[2 * 5 * 16];
+__constant__ double c_rap3[2 * 14 * 64];
+
+template <int SD>
+void rap_rho_table(double* T) {
+  constexpr int NOFF = SG<SD>::NOFF, NC = SG<SD>::NC, CEN = SG<SD>::CEN, NBK = 1 << (2 * SD);
+  const double mhv[4] = {SD == 2 ? 4.0 : 8.0, SD == 2 ? 2.0 : 4.0, SD == 2 ? 1.0 : 2.0, 1.0};
+  const double khv[4] = {4.0, SD == 2 ? -1.0 : 0.0, SD == 2 ? -2.0 : -1.0, -1.0};
+  for (int i = 0; i < 2 * NC * NBK; ++i) T[i] = 0.0;
+  for (int e = 0; e < NBK; ++e)
+    for (int fa = 0; fa < NOFF; ++fa)
+      for (int k = 0; k < NOFF; ++k) {
+        bool in = true;
+        double wf = 1.0;
+        int h = 0;
+        for (int d = 0; d < SD; ++d) {
+          const int bc = (e >> (2 * d)) & 3, o = SG<SD>::od(fa, d), kd = SG<SD>::od(k, d), gr = o + kd;
+          in = in && (o == bc - 2 || o == bc - 1) && (gr == bc - 2 || gr == bc - 1);
+          wf *= (o == 0) ? 1.0 : 0.5;
+          h += kd != 0;
+        }
+        if (!in) continue;
+        for (int q = 0; q < NC; ++q) {
+          double wg = 1.0;
+          for (int d = 0; d < SD; ++d) {
+            const int diff = SG<SD>::od(fa, d) + SG<SD>::od(k, d) - 2 * SG<SD>::od(q + CEN, d);
+            wg *= (diff == 0) ? 1.0 : ((diff == 1 || diff == -1) ? 0.5 : 0.0);
+          }
+          T[(0 * NC + q) * NBK + e] += wf * wg * mhv[h];
+          T[(1 * NC + q) * NBK + e] += wf * wg * khv[h];
+        }
+      }
+}
+
+template <int SD>
+__global__ void rap_space_rho_kernel(OpDesc fop, Geom gc, int nl, double* __restrict__ out) {
+  constexpr int NC = SG<SD>::NC, NBK = 1 << (2 * SD);
+  const Geom& gf = fop.g;
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= gc.P * nl) return;
+  const long long pc = idx % gc.P;
+  const int tau = (int)(idx / gc.P);
+  int C[3] = {0, 0, 0};
+  if (!pdecode<SD>(gc, pc, C)) return;
+  const double* tab = SD == 2 ? c_rap2 : c_rap3;
+  long long per = 1;
+  for (int d = 0; d < SD; ++d) per *= gf.n;
+  const double* rl = fop.rho + (fop.rho_tc ? 0LL : (long long)tau * per);
+  double ce[NBK], ke[NBK];
+#pragma unroll
+  for (int e = 0; e < NBK; ++e) {
+    bool v = tau < gf.nt;
+    long long ei = 0, m = 1;
+#pragma unroll
+    for (int d = 0; d < SD; ++d) {
+      const int a = 2 * C[d] - 2 + ((e >> (2 * d)) & 3);
+      v = v && a >= 0 && a < gf.n;
+      ei += (long long)a * m;
+      m *= gf.n;
+    }
+    const double r = v ? __ldg(rl + ei) : 0.0;
+    ce[e] = v ? fop.m.Cins + fop.m.dC * powp(r, fop.m.pc) : 0.0;
+    ke[e] = v ? fop.m.kins + fop.m.dk * powp(r, fop.m.pk) : 0.0;
+  }
+  const double smf = sM<SD>(gf.dx), skf = sK<SD>(gf.dx);
+  double* o = out + (long long)tau * 2 * NC * gc.P + pc;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    double am = 0.0, ak = 0.0;
+#pragma unroll
+    for (int e = 0; e < NBK; ++e) {
+      am = fma(tab[q * NBK + e], ce[e], am);
+      ak = fma(tab[(NC + q) * NBK + e], ke[e], ak);
+    }
+    o[(long long)q * gc.P] = am * smf;
+    o[(long long)(NC + q) * gc.P] = ak * skf;
+  }
+}
+
 // Time coarsening: coarse layer T from fine layers 2T, 2T+1:
 // conduction blocks by Galerkin with the linear-in-time interpolation (fine plane 2T+1 =
 // (coarse T + coarse T+1)/2): K'^{AB} = sum_f sum_{a,b} W_f[a][A] W_f[b][B] K_f^{ab},
@@ -283,16 +369,27 @@ __global__ void rap_time_kernel(OpDesc fop, int nlc, double* __restrict__ out) {
   if (!pdecode<SD>(g, pn, c)) return;
   const double W[2][2][2] = {{{1.0, 0.0}, {0.5, 0.5}}, {{0.5, 0.5}, {0.0, 1.0}}};
   double* o = out + (long long)T * 5 * NC * g.P;
+  // FORM_RHO: element coefficients of the two fine layers once (not per weight)
+  double ce[2][SG<SD>::NE], ke[2][SG<SD>::NE];
+  if (FFORM == FORM_RHO)
+    for (int f = 0; f < 2; ++f) elem_ck<SD>(fop, c, fop.rho_tc ? 0 : 2 * T + f, ce[f], ke[f]);
   for (int q = 0; q < NC; ++q) {
     double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     double macc = 0.0;
     for (int f = 0; f < 2; ++f) {
       int tau = 2 * T + f;
       if ((FFORM == FORM_RHO && fop.rho_tc) || (FFORM != FORM_RHO && !fop.tvl)) tau = 0;
-      macc += 0.5 * mpart_weight<SD, FFORM>(fop, c, pn, tau, q + CEN);
       double s[2][2];
-      for (int a = 0; a < 2; ++a)
-        for (int b = 0; b < 2; ++b) s[a][b] = kblock_weight<SD, FFORM>(fop, c, pn, tau, a, b, q + CEN);
+      if (FFORM == FORM_RHO) {
+        macc += 0.5 * rho_weight<SD>(ce[f], ke[f], q + CEN, 0, g.dx);
+        const double kw = rho_weight<SD>(ce[f], ke[f], q + CEN, 1, g.dx);
+        for (int a = 0; a < 2; ++a)
+          for (int b = 0; b < 2; ++b) s[a][b] = fop.Tm[a][b] * kw;
+      } else {
+        macc += 0.5 * mpart_weight<SD, FFORM>(fop, c, pn, tau, q + CEN);
+        for (int a = 0; a < 2; ++a)
+          for (int b = 0; b < 2; ++b) s[a][b] = kblock_weight<SD, FFORM>(fop, c, pn, tau, a, b, q + CEN);
+      }
       for (int A = 0; A < 2; ++A)
         for (int B = 0; B < 2; ++B) {
           double v = 0.0;
@@ -329,6 +426,24 @@ void launch_rap_space(const OpDesc& fop, const Geom& gc, int nl, int ns, double*
   long long total = gc.P * nl * ns;
   int blk = 128;
   long long grd = (total + blk - 1) / blk;
+  if (fop.form == FORM_RHO && ns == 2) {  // table-driven (the tables are uploaded once per device)
+    static bool done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !done[dev]) {
+      static double t2[2 * 5 * 16], t3[2 * 14 * 64];
+      rap_rho_table<2>(t2);
+      rap_rho_table<3>(t3);
+      cudaMemcpyToSymbol(c_rap2, t2, sizeof(t2));
+      cudaMemcpyToSymbol(c_rap3, t3, sizeof(t3));
+      done[dev] = true;
+    }
+    const long long nth = gc.P * nl;
+    const unsigned g2 = (unsigned)((nth + blk - 1) / blk);
+    if (fop.g.sd == 2) rap_space_rho_kernel<2><<<g2, blk, 0, s>>>(fop, gc, nl, out);
+    else rap_space_rho_kernel<3><<<g2, blk, 0, s>>>(fop, gc, nl, out);
+    return;
+  }
 #define RS(SD, F, NS) rap_space_kernel<SD, F, NS><<<(unsigned)grd, blk, 0, s>>>(fop, gc, nl, out)
   if (fop.g.sd == 2) {
     if (ns == 2) { if (fop.form == FORM_RHO) RS(2, FORM_RHO, 2); else RS(2, FORM_MK, 2); }
@@ -378,6 +493,20 @@ __global__ void gersh_kernel(OpDesc op, int pa, int pb, unsigned long long* __re
     int c[3] = {0, 0, 0};
     if (pdecode<SD>(g, pn, c) && !is_cons<SD>(g, c, p)) {
       double diag = 0.0, sum = 0.0;
+      // FORM_RHO: the element coefficients of layers p-1 and p once (not per weight)
+      double ceL[SG<SD>::NE], keL[SG<SD>::NE], ceU[SG<SD>::NE], keU[SG<SD>::NE];
+      if (FORM == FORM_RHO) {
+        elem_ck<SD>(op, c, p - 1, ceL, keL);
+        elem_ck<SD>(op, c, p, ceU, keU);
+      }
+      auto bw = [&](bool upper, int a, int bb, int k) -> double {
+        if (FORM == FORM_RHO) {
+          const double m = upper ? rho_weight<SD>(ceU, keU, k, 0, g.dx) : rho_weight<SD>(ceL, keL, k, 0, g.dx);
+          const double kk = upper ? rho_weight<SD>(ceU, keU, k, 1, g.dx) : rho_weight<SD>(ceL, keL, k, 1, g.dx);
+          return op.U[a][bb] * m + op.Tm[a][bb] * kk;
+        }
+        return block_weight<SD, FORM>(op, c, pn, upper ? p : p - 1, a, bb, k);
+      };
       for (int k = 0; k < NOFF; ++k) {
         int nb[3] = {0, 0, 0};
         bool ok = true;
@@ -389,12 +518,12 @@ __global__ void gersh_kernel(OpDesc op, int pa, int pb, unsigned long long* __re
         // columns on planes p-1, p, p+1 (eliminated constrained columns are zero)
         double wlo = 0.0, wmid = 0.0, whi = 0.0;
         if (p >= 1) {  // layer p-1: top rows
-          wlo = block_weight<SD, FORM>(op, c, pn, p - 1, 1, 0, k);
-          wmid = block_weight<SD, FORM>(op, c, pn, p - 1, 1, 1, k);
+          wlo = bw(false, 1, 0, k);
+          wmid = bw(false, 1, 1, k);
         }
         if (p < g.nt) {  // layer p: bottom rows
-          wmid += block_weight<SD, FORM>(op, c, pn, p, 0, 0, k);
-          whi = block_weight<SD, FORM>(op, c, pn, p, 0, 1, k);
+          wmid += bw(true, 0, 0, k);
+          whi = bw(true, 0, 1, k);
         }
         if (k == CEN) diag = wmid;
         if (p >= 1 && !is_cons<SD>(g, nb, p - 1)) sum += fabs(wlo);
