@@ -214,7 +214,10 @@ int st_level_apply(st_ctx_t* ctx, const double* rho, int level, const double* x,
 /* Benchmark hook: enqueue `reps` back-to-back launches of the level-l operator kernel in
  * mode (0 apply, 1 residual y = b - A x, 2 damped-Jacobi sweep, 3 first sweep from zero)
  * on the context's internal work vectors and return WITHOUT synchronising (the caller
- * brackets them with events on the context stream). rho: device pointer. */
+ * brackets them with events on the context stream). rho: device pointer. Level 0 rebuilds its
+ * per-design tables (the k~ table of a (2+1)D space-time design) only when rho is a different
+ * pointer from the previous binding, so the launches are the only work enqueued when the same
+ * unchanged rho is passed again (the caller must not modify rho in place between such calls). */
 int st_bench_op(st_ctx_t* ctx, const double* rho, int level, int mode, int transpose, int reps);
 
 /* ---- Config-5 design loop (driver level: BASELINE config 5, R-13; NOT the paper's

@@ -82,6 +82,7 @@ struct st_ctx {
   double* dsmall = nullptr;
   double* hsmall = nullptr;
   double* rho_stage = nullptr;
+  double* kt = nullptr;          // padded k~ table of a (2+1)D space-time design (launch_ktilde; tv2d)
   double* io_stage[4] = {nullptr, nullptr, nullptr, nullptr};
   long long io_n[4] = {0, 0, 0, 0};
   double rho_ck[2] = {0.0, 0.0};
@@ -482,6 +483,17 @@ void gather_planes(st_ctx* c, const Level& Nx, const double* part, double* full)
   comm_call([&] { comm_allgather(c->comm, part + P, full + P, (long long)nlc * P, c->stream); });
 }
 
+// level-0 rho binding; a (2+1)D space-time fine level also gets its k~ table (one pass over the
+// design, read by tv2d instead of rho: the same bytes per sweep, no per-sweep rho^p)
+void set_fine_rho(st_ctx* c, const double* rho) {
+  c->lv[0].op.rho = rho;
+  if (c->kt) {
+    launch_ktilde(rho, c->grid.n, c->lv[0].g.nt, c->lv[0].op.m, c->kt, c->stream);
+    L(c);
+    c->lv[0].op.kt = c->kt;
+  }
+}
+
 // rho -> level-0 operator pointer; returns true if rho changed since the last full setup
 bool bind_rho(st_ctx* c, const double* rho_in) {
   const double* rho = rho_in;
@@ -489,7 +501,7 @@ bool bind_rho(st_ctx* c, const double* rho_in) {
     CK(cudaMemcpyAsync(c->rho_stage, rho_in, c->ndesign * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     rho = c->rho_stage;
   }
-  c->lv[0].op.rho = rho;
+  set_fine_rho(c, rho);
   launch_checksum(rho, c->ndesign, c->dsmall + 500, c->ws, c->stream);
   L(c);
   allreduce(c, c->dsmall + 500, 2);  // one decision on every rank
@@ -933,6 +945,7 @@ void free_ctx(st_ctx* c) {
   cudaFree(c->dsmall);
   if (c->hsmall) cudaFreeHost(c->hsmall);
   cudaFree(c->rho_stage);
+  cudaFree(c->kt);
   comm_release(c->comm);
   cudaFree(c->fbuf);
   cudaFree(c->fw);
@@ -1076,6 +1089,8 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       c->ndesign = c->tc ? nsp : nsp * L0.g.nt;   // space-time: owned layers + the ghost layer
       allocate(c);
       dalloc(&c->rho_stage, c->ndesign);
+      if (c->sd == 2 && !c->tc)  // padded k~ table (launch_ktilde)
+        dalloc(&c->kt, (long long)(grid->n + 2) * (grid->n + 2) * (L0.g.nt + 1));
       // source vector f: Q~ = Q tau
       launch_source(c->lv[0].g, src->kind, src->Q0 * grid->tau, src->a, src->w, grid->tau, c->f, c->stream);
       L(c);
@@ -1179,7 +1194,7 @@ int st_apply(st_ctx_t* c, const double* rho, const double* x, double* y, int tra
       CK(cudaMemcpyAsync(c->rho_stage, rho, c->ndesign * sizeof(double), cudaMemcpyHostToDevice, c->stream));
       r = c->rho_stage;
     }
-    c->lv[0].op.rho = r;
+    set_fine_rho(c, r);
     pack_in(c, x, c->tmpN, 1, true);
     masked_level_apply(c, 0, c->tmpN, c->tmpN2, c->lv[0].t, transpose != 0, bc != 0);
     unpack_out(c, c->lv[0].t, y, 2);
@@ -1390,7 +1405,7 @@ int st_bench_op(st_ctx_t* c, const double* rho, int level, int mode, int transpo
     CK(cudaSetDevice(c->device));
     if (level == 0) {
       if (!is_device_ptr(rho)) throw StErr{ST_E_INVALID_ARG, "rho must be a device pointer"};
-      c->lv[0].op.rho = rho;
+      if (c->lv[0].op.rho != rho || (c->kt && !c->lv[0].op.kt)) set_fine_rho(c, rho);  // st.h: same pointer = same rho
     } else {
       prepare(c, rho);
     }

@@ -48,6 +48,7 @@ struct OpDesc {
   int tvl;                // per-layer (time-varying) storage; a slab may hold a single layer
   double U[2][2], Tm[2][2];
   const double* rho;      // FORM_RHO
+  const double* kt;       // FORM_RHO, space-time (2+1)D design: k~ per element (set with rho), or null
   int rho_tc;             // rho time-constant
   MatsDev m;
   const double* st;       // MK: [nl][2][NC][P]; B4: [nl][5][NC][P] = M, Kbb, Kbt, Ktb, Ktt
@@ -124,23 +125,39 @@ template <int SD> __device__ __forceinline__ bool pdecode(const Geom& g, long lo
   return c[0] < g.nn;
 }
 
-// Work list of the persistent stencil kernels: (tile, time plane) items ordered by time chunks of K
-// planes (chunk-major, then tile, then plane), so that all CTAs sweep the same planes together and
-// the halo rows of neighbouring tiles are L2 hits. Decodes item w into a segment
-// (tile, planes [p0, p1)) that stays inside one chunk and one tile and ends at or before wend.
+// Work list of the persistent stencil kernels: (tile, time plane) items ordered by time chunks
+// (chunk-major, then tile, then plane); CTA c owns a contiguous range of the list, so with chunks
+// a CTA sweeps a run of tiles over the same few planes and the halo it shares with the previous
+// tile of its run is still in L2. The nch = ceil(NP / K) chunks are balanced
+// (sizes differ by at most one plane: a 1-plane tail chunk would give one CTA a run of 1-plane
+// segments that bounds the whole launch). Decodes item w into a segment (tile, planes [p0, p1))
+// that stays inside one chunk and one tile and ends at or before wend.
 __device__ __forceinline__ void work_segment(long long w, long long wend, long long tiles, int NP, int K,
                                              long long* tile, int* p0, int* p1) {
-  const long long csz = tiles * K;
   const int nch = (NP + K - 1) / K;
-  long long c = w / csz;
-  if (c > nch - 1) c = nch - 1;
-  const long long r = w - c * csz;
-  const int Kc = (c == nch - 1) ? NP - (int)c * K : K;
+  const int pp = (int)(w / tiles);  // chunk c covers items [tiles * cs(c), tiles * cs(c+1))
+  int c = (int)(((long long)pp * nch) / NP);
+  while (c + 1 < nch && (int)((long long)(c + 1) * NP / nch) <= pp) ++c;
+  while (c > 0 && (int)((long long)c * NP / nch) > pp) --c;
+  const int cs = (int)((long long)c * NP / nch), ce = (int)((long long)(c + 1) * NP / nch);
+  const int Kc = ce - cs;
+  const long long r = w - tiles * cs;
   *tile = r / Kc;
-  *p0 = (int)(c * K + r % Kc);
-  const int cend = (int)(c * K) + Kc;
+  *p0 = cs + (int)(r % Kc);
   const long long rem = wend - w;
-  *p1 = (rem < cend - *p0) ? *p0 + (int)rem : cend;
+  *p1 = (rem < ce - *p0) ? *p0 + (int)rem : ce;
+}
+
+// tile order inside a chunk for the (2+1)D kernels: 0 = row-major (x fastest), 1 = column-major
+// (consecutive tiles of a run are y-neighbours: the 2 halo rows of a 32 x 8 tile cost more than
+// its 4 halo columns). ST_TILE_ORDER selects it (experiments).
+inline int tile_order() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("ST_TILE_ORDER");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
 }
 
 // planes per chunk: the chunk's x and b planes (2 x K x P doubles) within `mb` MB of L2; mb <= 0:
@@ -154,6 +171,12 @@ inline int chunk_planes(long long P, int NP, int sd) {
     const char* e = getenv("ST_CHUNK_MB");
     env_mb = e ? atoi(e) : -1;
   }
+  static int env_k = -2;
+  if (env_k == -2) {
+    const char* e = getenv("ST_CHUNK_K");  // planes per chunk (experiments; overrides ST_CHUNK_MB)
+    env_k = e ? atoi(e) : -1;
+  }
+  if (env_k > 0) return env_k < NP ? env_k : NP;
   const long long mb = env_mb >= 0 ? env_mb : 0;
   (void)sd;
   if (mb <= 0) return NP;

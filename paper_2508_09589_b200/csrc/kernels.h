@@ -57,6 +57,10 @@ void launch_scale(const double* w, double* v, double alpha, long long n, cudaStr
 void launch_checksum(const double* a, long long n, double* out, RedWs ws, cudaStream_t s);
 
 // misc.cu
+// Per-design conductivity table of a (2+1)D space-time design, read by tv2d: layers 0 .. nl-1 of
+// k~(rho) = kins + dk rho^pk stored with a zero border, kt[t][gj+1][gi+1] (pitch n+2), plus a zero
+// layer nl; (nl+1) (n+2)^2 doubles. rho: [nl][n][n].
+void launch_ktilde(const double* rho, int n, int nl, const MatsDev& m, double* kt, cudaStream_t s);
 void launch_source(const Geom& g, int kind, double qscale, double a, double w, double tau, double* f, cudaStream_t s);
 void launch_mask_free(const Geom& g, const double* in, double* out, cudaStream_t s);       // out = m_f .* in
 void launch_copy_cons(const Geom& g, const double* src, double* dst, cudaStream_t s);     // dst_c = src_c

@@ -1,4 +1,6 @@
 // misc.cu — source assembly, Dirichlet helpers, element sensitivities, dense coarsest solve.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -32,6 +34,26 @@ __global__ void source_kernel(Geom g, int kind, double qscale, double a, double 
     }
   }
   f[idx] = sx * ft;
+}
+
+__global__ void ktilde_kernel(const double* __restrict__ rho, int n, int nl, MatsDev m, double* __restrict__ kt) {
+  const long long w = n + 2, per = w * w, tot = per * (nl + 1);
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(idx / per);
+    const long long r = idx - t * per;
+    const int pj = (int)(r / w), pi = (int)(r - pj * w);
+    double v = 0.0;
+    if (t < nl && pi >= 1 && pi <= n && pj >= 1 && pj <= n)
+      v = m.kins + m.dk * powp(__ldg(rho + ((long long)t * n + (pj - 1)) * n + (pi - 1)), m.pk);
+    kt[idx] = v;
+  }
+}
+
+void launch_ktilde(const double* rho, int n, int nl, const MatsDev& m, double* kt, cudaStream_t s) {
+  const long long tot = (long long)(n + 2) * (n + 2) * (nl + 1);
+  const long long blocks = std::min<long long>((tot + 255) / 256, 148LL * 16);
+  ktilde_kernel<<<(unsigned)blocks, 256, 0, s>>>(rho, n, nl, m, kt);
 }
 
 void launch_source(const Geom& g, int kind, double qscale, double a, double w, double tau, double* f, cudaStream_t s) {

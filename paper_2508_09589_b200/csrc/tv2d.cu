@@ -9,20 +9,24 @@
 // and completes row q-1 = carry + t00 Ka_{q-1} + t01 Kb_q (K^T: - M x_q), carry for row q =
 // M (x_q - x_{q-1}) + t01 Ka_{q-1} + t11 Kb_q (K^T: M x_q).
 // Design: persistent one-wave grid over (tile, plane) work as tc2d; per plane
-// ONE mbarrier-tracked TMA group brings the x tile, the b tile and the layer tile (SRC 0: the
-// 34 x 9 element box of rho of layer q, SRC 1: the 5 x 34 x 9 forward stiffness coefficients of
-// layer q; box origin (max(x0-2, 0), max(y0-1, 0)): a tile-mode fp64 TMA box must start at a
-// non-negative, 16-byte aligned coordinate (else an illegal instruction, scripts/dev/tma_neg.cu,
-// scripts/dev/tv_probe.sh); entries beyond the last node/element are zero-filled, out-of-domain
-// neighbours masked) into a ring slot, so a plane
-// costs one barrier wait and one __syncthreads (slot release). SRC 0 keeps the 6 element
-// conductivities of the layer below in registers and applies K through the 4 element "brackets"
-// of x at the node (shared by the layer-below and layer-above products); SRC 1 re-reads the layer
-// below from the previous ring slot, which is only refilled after the plane is done.
+// ONE mbarrier-tracked TMA group brings the x tile, the b tile and the layer tile into a ring
+// slot (SRC 0: the 34 x 9 box of the per-design k~ table of layer q, op.kt, filled once per
+// design by launch_ktilde; SRC 1: the 5 x 36 x 9 forward stiffness coefficients of layer q), so a
+// plane costs one barrier wait and one __syncthreads (slot release). Layer boxes start at
+// (max(x0-2, 0), max(y0-1, 0)): a tile-mode fp64 TMA box must start at a non-negative, 16-byte
+// aligned coordinate (else an illegal instruction: scripts/dev/tma_neg.cu, scripts/dev/tv_probe.sh);
+// entries beyond the last node / element are zero-filled, entries left of / below the domain are
+// read from the (zero-initialised) ring and masked. SRC 0 keeps the 6 element conductivities of
+// the layer below in registers and applies K through the 4 element "brackets" of x at the node
+// (shared by the layer-below and layer-above products); SRC 1 re-reads the layer below from the
+// previous ring slot, which is only refilled after the plane is done. The first plane of a
+// segment is peeled (no layer below it), so the steady-state body has no such selects.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -88,10 +92,11 @@ __device__ __forceinline__ double ap9(const double (&w)[9], const double (&nb)[R
   return a + b;
 }
 
-// 1/d for the per-plane Jacobi diagonal: float reciprocal + two Newton steps (full double accuracy
-// for the positive, float-range diagonals; ~8 instructions instead of a double division)
+// 1/d for the per-plane Jacobi diagonal: approximate reciprocal (MUFU.RCP64H) + two Newton steps
+// (full double accuracy for the positive, normal diagonals; no branch, no double division)
 __device__ __forceinline__ double rcp_d(double d) {
-  double r = (double)__frcp_rn((float)d);
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
   r = r * fma(-d, r, 2.0);
   return r * fma(-d, r, 2.0);
 }
@@ -113,15 +118,61 @@ __device__ __forceinline__ void wk_box(const double* ct, int L, bool mi, bool mj
   w[3] = mi ? ct[1 * ET + L - 1] : 0.0;
 }
 
-// SRC: 0 = fine level from rho (per-layer k~ from the element densities); 1 = stored per-layer
+// one (tile, plane-range) segment of a CTA's work list and the planes it loads
+struct Seg {
+  int p0, p1, qs, qe;  // rows p0 .. p1-1; planes qs .. qe (qs = p0 - 1 reloads the plane below)
+  int x0, y0, bx, by;  // node tile origin, layer box origin
+};
+// Sliced chunk schedule: the NP planes are cut into nch balanced chunks; CTA b of G takes the
+// b-th 1/G slice of every chunk's (tile, plane) items (tile-major inside the chunk), chunk after
+// chunk. All CTAs therefore sweep the same few planes together: a halo a tile shares with a
+// neighbour is loaded by another CTA at about the same time (or by this CTA's previous segment,
+// at most one chunk earlier) and hits L2, and a segment restart reloads an L2-resident plane.
+// nch = 1 is the plain contiguous split of the tile-major list.
+struct Sched {
+  long long tiles, w, we;
+  int NP, nch, c, cs, Kc;
+};
+__device__ __forceinline__ void sched_init(Sched& s, long long tiles, int NP, int K) {
+  s.tiles = tiles;
+  s.NP = NP;
+  s.nch = (NP + K - 1) / K;
+  s.c = -1;
+  s.w = s.we = 0;
+  s.cs = s.Kc = 0;
+}
+__device__ __forceinline__ bool next_seg(Sched& s, int ntx, int nt, int tord, Seg& sg) {
+  while (s.w >= s.we) {
+    if (++s.c >= s.nch) return false;
+    s.cs = (int)((long long)s.c * s.NP / s.nch);
+    s.Kc = (int)((long long)(s.c + 1) * s.NP / s.nch) - s.cs;
+    const long long items = s.tiles * s.Kc, base = s.tiles * s.cs;
+    s.w = base + items * blockIdx.x / gridDim.x;
+    s.we = base + items * (blockIdx.x + 1) / gridDim.x;
+  }
+  const long long r = s.w - s.tiles * s.cs;
+  const long long tile = r / s.Kc;
+  sg.p0 = s.cs + (int)(r % s.Kc);
+  const long long rem = s.we - s.w;
+  sg.p1 = (rem < s.cs + s.Kc - sg.p0) ? sg.p0 + (int)rem : s.cs + s.Kc;
+  s.w += sg.p1 - sg.p0;
+  sg.qs = max(sg.p0 - 1, 0);
+  sg.qe = min(sg.p1, nt);
+  const long long nty = s.tiles / ntx;
+  sg.x0 = (int)(tord ? tile / nty : tile % ntx) * TX;
+  sg.y0 = (int)(tord ? tile % nty : tile / ntx) * TY;
+  sg.bx = max(sg.x0 - 2, 0);  // stored-stencil box origin (x0 is a multiple of 32)
+  sg.by = max(sg.y0 - 1, 0);
+  return true;
+}
+
+// SRC: 0 = fine level from rho (the per-design k~ table op.kt, one entry per element and layer); 1 = stored per-layer
 // stiffness of a time-varying Galerkin space level (uniform capacity: the separable mass op.msc)
-// PK3: SIMP conductivity exponent p_k = 3 (every BASELINE config) evaluated as rho^3 (a runtime
-// exponent costs a branch ladder and a pow call per element and layer)
-template <int SRC, int MODE, bool TRANS, bool PK3>
+template <int SRC, int MODE, bool TRANS>
 __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
     tv2d_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
                 const __grid_constant__ CUtensorMap tml, OpDesc op, const double* __restrict__ x,
-                double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx) {
+                double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx, int tord) {
   constexpr bool NX = (MODE != MODE_JAC0);
   constexpr bool NBV = (MODE != MODE_APPLY);
   constexpr bool ND = (MODE == MODE_JAC || MODE == MODE_JAC0);
@@ -153,86 +204,90 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
   const double t00 = op.Tm[0][0] * sk, t01 = op.Tm[0][1] * sk, t11 = op.Tm[1][1] * sk;
   const unsigned tx_plane = (NX ? XBYTES : 0u) + (NBV ? BBYTES : 0u);
 
-  long long w = wtot * blockIdx.x / gridDim.x;
-  const long long wend = wtot * (blockIdx.x + 1) / gridDim.x;
-  unsigned ring = 0u, phase = 0u;
-  while (w < wend) {
-    long long tile;
-    int p0, p1;
-    work_segment(w, wend, wtot / NP, (int)NP, kchunk, &tile, &p0, &p1);
-    w += p1 - p0;
-    const int x0 = (int)(tile % ntx) * TX, y0 = (int)(tile / ntx) * TY;
-    const int qs = max(p0 - 1, 0), qe = min(p1, g.nt);
+  // zero the ring once: box entries a thread reads outside the domain (clamped origin, masked
+  // by 0) are then finite; the generic-proxy stores are ordered before the first TMA write
+  for (int k = tid; k < NB * ((NX ? XS : 0) + (NBV ? BS : 0) + RS); k += NTH) xs[k] = 0.0;
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();  // barriers initialised, ring zeroed
+
+  const long long tiles = wtot / NP;
+  // producer (thread 0): walks this CTA's (segment, plane) sequence NB-1 planes ahead of the
+  // consumer, across segment boundaries; a slot is refilled only after the __syncthreads that
+  // ends the plane consuming it
+  Sched psc;
+  sched_init(psc, tiles, (int)NP, kchunk);
+  Seg ps;
+  bool pv = next_seg(psc, ntx, g.nt, tord, ps);
+  int pq = ps.qs;
+  auto issue_next = [&](unsigned slot) {
+    if (!pv) return;
+    const int q = pq;
+    const bool wb = NBV && q >= ps.p0 && q < ps.p1;
+    const bool hl = SRC == 0 || q < g.nt;  // layer q (SRC 0: layer nt of the padded k~ table is zero)
+    mbar_expect_tx(&bar[slot], tx_plane - ((NBV && !wb) ? BBYTES : 0u) + (hl ? LBYTES : 0u));
+    if (NX) tma3(xs + slot * XS, &tmx, &bar[slot], ps.x0, ps.y0, q);
+    if (wb) tma3(bs + slot * BS, &tmb, &bar[slot], ps.x0, ps.y0, q);
+    if (hl) {
+      if (SRC == 0) tma3(ls + slot * RS, &tml, &bar[slot], ps.x0, ps.y0, q);  // padded: element x0-1 at x0
+      else tma4(ls + slot * RS, &tml, &bar[slot], ps.bx, ps.by, 0, 2 * q + 1);
+    }
+    if (++pq > ps.qe) {
+      pv = next_seg(psc, ntx, g.nt, tord, ps);
+      pq = ps.qs;
+    }
+  };
+  if (tid == 0)
+    for (int k = 0; k < NB - 1; ++k) issue_next((unsigned)k);
+
+  Sched csc;
+  sched_init(csc, tiles, (int)NP, kchunk);
+  Seg cs;
+  unsigned cur = 0u, prv = NB - 1, phase = 0u;
+  while (next_seg(csc, ntx, g.nt, tord, cs)) {
+    const int p0 = cs.p0, p1 = cs.p1, qs = cs.qs, qe = cs.qe;
+    const int x0 = cs.x0, y0 = cs.y0, bx = cs.bx, by = cs.by;
     const int i = x0 + tx, j0 = y0 + ty * RY;
     bool act[RY], patch[RY];
-    double cy[RY];
+    double cy[RY], smc[RY];
+    const double cx = (i == 0 || i == n) ? 2.0 : 4.0;
 #pragma unroll
     for (int r = 0; r < RY; ++r) {
       const int j = j0 + r;
       act[r] = (i <= n) && (j <= n);
       patch[r] = i == 0 && j >= g.plo && j <= g.phi;
       cy[r] = (j == 0 || j == n) ? 2.0 : 4.0;
+      smc[r] = sm * cx * cy[r];  // capacity part of the Jacobi diagonal (separable mass centre)
     }
-    const double cx = (i == 0 || i == n) ? 2.0 : 4.0;
-    const int bx = max(x0 - 2, 0), by = max(y0 - 1, 0);  // layer box origin (x0 is a multiple of 32)
-    // box entry of element (i-1, j0-1) (SRC 0) / of node (i, j0) (SRC 1); entries left of / below
-    // the domain are never used unmasked
-    const int lo = SRC == 0 ? (j0 - 1 - by) * EX + (i - 1 - bx) : (j0 - by) * EX + (i - bx);
-    // SRC 0: the thread's 6 elements (i-1+d, j0-1+s) inside the domain
-    unsigned ev = 0u;
-    if (SRC == 0) {
-#pragma unroll
-      for (int s2 = 0; s2 <= RY; ++s2)
-#pragma unroll
-        for (int d = 0; d < 2; ++d) {
-          const int gi = i - 1 + d, gj = j0 - 1 + s2;
-          if (gi >= 0 && gi < n && gj >= 0 && gj < n) ev |= 1u << (2 * s2 + d);
-        }
-    }
-    __syncthreads();  // barrier init / previous segment fully consumed
-
-    auto issue = [&](int q, unsigned slot) {  // elected thread: plane q (+ layer q) into `slot`
-      const bool wb = NBV && q >= p0 && q < p1;
-      const bool hl = q < g.nt;               // layer q exists locally (the last plane has none above)
-      mbar_expect_tx(&bar[slot], tx_plane - ((NBV && !wb) ? BBYTES : 0u) + (hl ? LBYTES : 0u));
-      if (NX) tma3(xs + slot * XS, &tmx, &bar[slot], x0, y0, q);
-      if (wb) tma3(bs + slot * BS, &tmb, &bar[slot], x0, y0, q);
-      if (hl) {
-        if (SRC == 0) tma3(ls + slot * RS, &tml, &bar[slot], bx, by, q);
-        else tma4(ls + slot * RS, &tml, &bar[slot], bx, by, 0, 2 * q + 1);
-      }
-    };
-    if (tid == 0)
-      for (int k = 0; k < NB - 1 && qs + k <= qe; ++k) issue(qs + k, (ring + k) % NB);
+    // box entry of element (i-1, j0-1) (SRC 0: padded table, box from (x0, y0) = element
+    // (x0-1, y0-1); outside the domain the border / the TMA fill is zero) / of node (i, j0) (SRC 1:
+    // entries left of / below the domain are read from the ring (finite) and masked)
+    const int lo = SRC == 0 ? (ty * RY) * EX + tx : (j0 - by) * EX + (i - bx);
 
     double kc[RY + 1][2];  // SRC 0: element conductivities of layer q-1 (below plane q)
     double dCc[RY];        // centre stiffness weight of layer q-1
     double Mprev[RY], Kaprev[RY], carry[RY], dcarry[RY];
-#pragma unroll
-    for (int r = 0; r < RY; ++r) Mprev[r] = Kaprev[r] = carry[r] = dcarry[r] = dCc[r] = 0.0;
-#pragma unroll
-    for (int s2 = 0; s2 <= RY; ++s2) kc[s2][0] = kc[s2][1] = 0.0;
     double* yrow = y + (long long)(qs - 1) * P + (long long)j0 * pr + i;
-    unsigned cur = ring, prv = (ring + NB - 1) % NB;
-    for (int q = qs; q <= qe; ++q) {
+
+    // one plane q; FIRST: the segment's first plane (no layer below it in this segment)
+    auto plane = [&](int q, auto first_tag) -> bool {
+      constexpr bool FIRST = decltype(first_tag)::value;
       mbar_wait(&bar[cur], (phase >> cur) & 1u);
       phase ^= 1u << cur;
       const bool has = q < g.nt;
       const double* xq = xs + cur * XS + xo;
       double kn[RY + 1][2];
       double dCn[RY];
-      if (SRC == 0) {  // k~ of layer q, zero outside the domain / beyond the last layer
+      if (SRC == 0) {  // k~ of layer q (zero outside the domain and beyond the last layer)
         const double* rd = ls + cur * RS + lo;
 #pragma unroll
         for (int s2 = 0; s2 <= RY; ++s2)
 #pragma unroll
-          for (int d = 0; d < 2; ++d) {
-            const double rr = rd[s2 * EX + d];
-            const bool v = has && ((ev >> (2 * s2 + d)) & 1u);
-            kn[s2][d] = v ? op.m.kins + op.m.dk * (PK3 ? rr * rr * rr : powp(rr, op.m.pk)) : 0.0;
-          }
+          for (int d = 0; d < 2; ++d) kn[s2][d] = rd[s2 * EX + d];
+        double rs2[RY + 1];
 #pragma unroll
-        for (int r = 0; r < RY; ++r) dCn[r] = 4.0 * ((kn[r][0] + kn[r][1]) + (kn[r + 1][0] + kn[r + 1][1]));
+        for (int s2 = 0; s2 <= RY; ++s2) rs2[s2] = kn[s2][0] + kn[s2][1];
+#pragma unroll
+        for (int r = 0; r < RY; ++r) dCn[r] = 4.0 * (rs2[r] + rs2[r + 1]);
       }
       double Mq[RY], Kb[RY], Ka[RY];
       if (NX && q + g.pg0 > 0) {
@@ -256,11 +311,11 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
             const double bnw = c4 - fma(2.0, nb[r + 2][0], nb[r + 2][1] + nb[r + 1][0]);
             const double bne = c4 - fma(2.0, nb[r + 2][2], nb[r + 2][1] + nb[r + 1][2]);
             Ka[r] = fma(kn[r][0], bsw, fma(kn[r][1], bse, fma(kn[r + 1][0], bnw, kn[r + 1][1] * bne)));
-            Kb[r] = fma(kc[r][0], bsw, fma(kc[r][1], bse, fma(kc[r + 1][0], bnw, kc[r + 1][1] * bne)));
+            Kb[r] = FIRST ? 0.0 : fma(kc[r][0], bsw, fma(kc[r][1], bse, fma(kc[r + 1][0], bnw, kc[r + 1][1] * bne)));
           } else {
             const int L = lo + r * EX;  // node (i, j0 + r) in the box
             double wv[9];
-            if (q > qs) {
+            if (!FIRST) {
               wk_box(ls + prv * RS, L, i >= 1, j0 + r >= 1, wv);
               Kb[r] = ap9(wv, nb, r);
             } else {
@@ -282,7 +337,7 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
 #pragma unroll
         for (int r = 0; r < RY; ++r) dCn[r] = has ? ls[cur * RS + lo + r * EX] : 0.0;
       }
-      if (q > qs && q - 1 >= p0) {  // row q-1 complete (bottom part of layer q-1)
+      if (!FIRST && q - 1 >= p0) {  // row q-1 complete (bottom part of layer q-1)
         const double* bp = bs + prv * BS + bo;
         if (q - 1 + g.pg0 == 0) {
 #pragma unroll
@@ -303,7 +358,7 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
           for (int r = 0; r < RY; ++r) {
             const double bot = fma(t00, Kaprev[r], t01 * Kb[r]);
             const double Ax = TRANS ? fma(-sm, Mq[r], carry[r] + bot) : carry[r] + bot;
-            const double od = ND ? omega * rcp_d(dcarry[r] + t00 * dCc[r]) : 0.0;
+            const double od = ND ? omega * rcp_d(fma(t00, dCc[r], dcarry[r])) : 0.0;
             double o;
             if (MODE == MODE_APPLY) o = Ax;
             else if (MODE == MODE_RESID) o = bp[r * TX] - Ax;
@@ -315,10 +370,13 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
       }
 #pragma unroll
       for (int r = 0; r < RY; ++r) {  // top part of layer q-1 -> row q; diagonal carried likewise
-        const double cap = TRANS ? Mq[r] : Mq[r] - Mprev[r];
-        const bool lay = q > qs;
-        carry[r] = lay ? fma(sm, cap, fma(t01, Kaprev[r], t11 * Kb[r])) : 0.0;
-        dcarry[r] = lay ? fma(sm, cx * cy[r], t11 * dCc[r]) : 0.0;
+        if (FIRST) {
+          carry[r] = dcarry[r] = 0.0;
+        } else {
+          const double cap = TRANS ? Mq[r] : Mq[r] - Mprev[r];
+          carry[r] = fma(sm, cap, fma(t01, Kaprev[r], t11 * Kb[r]));
+          dcarry[r] = fma(t11, dCc[r], smc[r]);
+        }
         Mprev[r] = Mq[r];
         Kaprev[r] = Ka[r];
         dCc[r] = dCn[r];
@@ -327,17 +385,19 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
 #pragma unroll
         for (int s2 = 0; s2 <= RY; ++s2) { kc[s2][0] = kn[s2][0]; kc[s2][1] = kn[s2][1]; }
       }
-      if (q == qe) break;  // the last plane's slots stay for the tail row below
-      __syncthreads();     // slot of plane q-1 consumed by every thread
-      if (tid == 0 && q + NB - 1 <= qe) issue(q + NB - 1, prv);
+      __syncthreads();  // slot of plane q-1 consumed by every thread
+      if (tid == 0) issue_next(prv);
       yrow += P;
       prv = cur;
       if (++cur == NB) cur = 0u;
-    }
+      return q < qe;  // plane qe's slot (now prv) stays until the next plane's barrier: tail row
+    };
+    if (plane(qs, std::true_type{}))
+      for (int q = qs + 1; plane(q, std::false_type{}); ++q) {
+      }
     if (p1 == g.nt + 1) {  // last row: top part of layer nt-1 only
-      const double* bq = bs + cur * BS + bo;
-      const double* xq = xs + cur * XS + xo;
-      yrow += P;
+      const double* bq = bs + prv * BS + bo;
+      const double* xq = xs + prv * XS + xo;
 #pragma unroll
       for (int r = 0; r < RY; ++r) {
         const double od = ND ? omega / dcarry[r] : 0.0;
@@ -350,7 +410,6 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
         if (act[r]) yrow[r * pr] = patch[r] ? 0.0 : o;
       }
     }
-    ring = (cur + 1) % NB;
   }
 }
 
@@ -374,6 +433,18 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn_tv() {
   return fn;
 }
 
+// L2 promotion of the tile maps (ST_L2PROMO = 0 / 64 / 128 / 256 bytes; experiments, default 128)
+CUtensorMapL2promotion l2promo_tv() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("ST_L2PROMO");
+    v = e ? atoi(e) : 128;
+  }
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                          : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+}
+
 bool map3_tv(CUtensorMap* m, const void* base, unsigned long long d0, unsigned long long d1, unsigned long long d2,
              unsigned long long s1, unsigned long long s2, unsigned b0, unsigned b1) {
   auto fn = encode_fn_tv();
@@ -383,7 +454,7 @@ bool map3_tv(CUtensorMap* m, const void* base, unsigned long long d0, unsigned l
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t es[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2promo_tv(),
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -397,16 +468,16 @@ bool map4_tv(CUtensorMap* m, const void* base, unsigned long long nn, unsigned l
   cuuint32_t box[4] = {(cuuint32_t)tv::EX1, (cuuint32_t)tv::EY, 5, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2promo_tv(),
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int SRC, int MODE, bool TRANS, bool PK3>
+template <int SRC, int MODE, bool TRANS>
 void ltv(const CUtensorMap& mx, const CUtensorMap& mb, const CUtensorMap& ml, const OpDesc& op, const double* x,
          double* y, double omega, cudaStream_t s) {
   using namespace tv;
   const Geom& g = op.g;
-  auto kern = tv2d_kernel<SRC, MODE, TRANS, PK3>;
+  auto kern = tv2d_kernel<SRC, MODE, TRANS>;
   constexpr bool NX = (MODE != MODE_JAC0), NBV = (MODE != MODE_APPLY);
   constexpr int RS = SRC == 0 ? RS0 : RS1, NB = SRC == 0 ? NB0 : NB1;
   constexpr size_t bytes = sizeof(double) * (16 + NB * ((NX ? XS : 0) + (NBV ? BS : 0) + RS));
@@ -427,7 +498,14 @@ void ltv(const CUtensorMap& mx, const CUtensorMap& mb, const CUtensorMap& ml, co
   const long long minw = (wtot >= 16LL * nsm * resident) ? 4 : 1;
   if (grid > wtot / minw) grid = wtot / minw;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, ml, op, x, y, omega, wtot, chunk_planes(g.P, g.nt + 1, g.sd), (int)ntx);
+  // plane chunks: with more tiles than CTAs the contiguous split leaves neighbouring tiles at
+  // unrelated planes (halo re-reads from DRAM: 1.77x the algorithmic bytes at 512^2 x 512);
+  // sliced 16-plane chunks keep them together (ST_CHUNK_K overrides)
+  const int NPl = g.nt + 1;
+  int kch = chunk_planes(g.P, NPl, g.sd);
+  if (kch >= NPl && !getenv("ST_CHUNK_K") && ntx * nty > grid) kch = 16;
+  kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, ml, op, x, y, omega, wtot, kch, (int)ntx,
+                                                       tile_order());
 }
 }  // namespace
 
@@ -437,7 +515,6 @@ bool launch_op_tv2d(const OpDesc& op, int mode, bool trans, bool mask, const dou
   const Geom& g = op.g;
   const bool rho_tv = op.form == FORM_RHO && !op.rho_tc && op.m.dC == 0.0;
   const bool mk_tv = op.form == FORM_MK && op.tvl && op.msep;
-  const bool pk3 = op.m.pk == 3.0;
   if (g.sd != 2 || !mask || !(rho_tv || mk_tv)) return false;
   if (op.U[0][0] != 0.0 || op.U[0][1] != 0.0 || op.U[1][0] != -1.0 || op.U[1][1] != 1.0) return false;
   if (op.Tm[0][1] != op.Tm[1][0]) return false;
@@ -451,18 +528,17 @@ bool launch_op_tv2d(const OpDesc& op, int mode, bool trans, bool mask, const dou
   if (g.nt < 1) return false;
   if (rho_tv) {
     const unsigned long long ne = (unsigned long long)g.n;
-    if (!map3_tv(&ml, op.rho, ne, ne, g.nt, ne * 8, ne * ne * 8, tv::EX0, tv::EY)) return false;
+    const unsigned long long w2 = ne + 2;  // padded table [nt+1][n+2][n+2] (launch_ktilde)
+    if (!op.kt || !map3_tv(&ml, op.kt, w2, w2, g.nt + 1, w2 * 8, w2 * w2 * 8, tv::EX0, tv::EY)) return false;
   } else if (!map4_tv(&ml, op.st, nn, 2ull * g.nt, s1, s2, 5ull * s2)) {
     return false;
   }
 #define C4(M)                                                                            \
   case M:                                                                                \
-    if (rho_tv && pk3) { if (trans) ltv<0, M, true, true>(mx, mb, ml, op, x, y, omega, s);   \
-                         else ltv<0, M, false, true>(mx, mb, ml, op, x, y, omega, s); }      \
-    else if (rho_tv) { if (trans) ltv<0, M, true, false>(mx, mb, ml, op, x, y, omega, s);    \
-                       else ltv<0, M, false, false>(mx, mb, ml, op, x, y, omega, s); }       \
-    else { if (trans) ltv<1, M, true, true>(mx, mb, ml, op, x, y, omega, s);                 \
-           else ltv<1, M, false, true>(mx, mb, ml, op, x, y, omega, s); }                    \
+    if (rho_tv) { if (trans) ltv<0, M, true>(mx, mb, ml, op, x, y, omega, s);           \
+                  else ltv<0, M, false>(mx, mb, ml, op, x, y, omega, s); }              \
+    else { if (trans) ltv<1, M, true>(mx, mb, ml, op, x, y, omega, s);                  \
+           else ltv<1, M, false>(mx, mb, ml, op, x, y, omega, s); }                     \
     break;
   switch (mode) {
     C4(MODE_APPLY)
