@@ -791,19 +791,28 @@ int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
       op_launch(c, 0, MODE_APPLY, trans, true, zj, nullptr, w);         // W = A Z_j
       launch_mdot(w + vo, c->V + vo, ld, j + 1, N, dh, c->ws, c->stream);  // g_i = V_i . W, ||W||^2
       allreduce(c, dh, j + 2);
-      launch_maxpy_norm(w + vo, c->V + vo, ld, j + 1, dh, ds2, N, dh + 196, c->ws, c->stream);  // W -= sum sg_i^2 g_i V_i
-      allreduce(c, dh + 196, 1);
+      // W -= sum sg_i^2 g_i V_i; with it (j + 1 <= 16) the DGKS coefficients V_i . W and ||W||^2
+      const bool fused = launch_maxpy_dots(w + vo, c->V + vo, ld, j + 1, dh, ds2, N, dh + 64, c->ws, c->stream);
+      if (fused) {
+        allreduce(c, dh + 64, j + 2);
+      } else {
+        launch_maxpy_norm(w + vo, c->V + vo, ld, j + 1, dh, ds2, N, dh + 196, c->ws, c->stream);
+        allreduce(c, dh + 196, 1);
+      }
       L(c, (j + 16) / 16 + 1);
       check_launch();
       CK(cudaMemcpyAsync(hh, dh, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaMemcpyAsync(hh + 196, dh + 196, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      if (fused) CK(cudaMemcpyAsync(hh + 64, dh + 64, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      else CK(cudaMemcpyAsync(hh + 196, dh + 196, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       double* hcol = &H[(size_t)j * (m + 1)];
       for (int i = 0; i <= j; ++i) hcol[i] = sg[i] * sg[j] * hh[i];  // h_ij = v_i . (A z_j)
-      double ww = hh[j + 1], w2 = hh[196];
+      double ww = hh[j + 1], w2 = fused ? hh[64 + j + 1] : hh[196];
       if (w2 < 0.5 * ww) {  // DGKS re-orthogonalisation
-        launch_mdot(w + vo, c->V + vo, ld, j + 1, N, dh + 64, c->ws, c->stream);
-        allreduce(c, dh + 64, j + 1);
+        if (!fused) {
+          launch_mdot(w + vo, c->V + vo, ld, j + 1, N, dh + 64, c->ws, c->stream);
+          allreduce(c, dh + 64, j + 1);
+        }
         launch_maxpy_norm(w + vo, c->V + vo, ld, j + 1, dh + 64, ds2, N, dh + 196, c->ws, c->stream);
         allreduce(c, dh + 196, 1);
         L(c, (j + 16) / 16 + 1);

@@ -49,6 +49,10 @@ void launch_mdot(const double* w, const double* V, long long ldv, int k, long lo
 // w -= sum_j h[j] s2[j] V_j (h, s2 on device; s2 = null: 1); out[0] = ||w||^2 after
 void launch_maxpy_norm(double* w, const double* V, long long ldv, int k, const double* h, const double* s2,
                        long long n, double* out, RedWs ws, cudaStream_t s);
+// w -= sum_j s2_j h_j V_j, then out[0..k-1] = V^T w (new w), out[k] = ||w||^2; k <= 16 (false otherwise:
+// nothing launched)
+bool launch_maxpy_dots(double* w, const double* V, long long ldv, int k, const double* h, const double* s2,
+                       long long n, double* out, RedWs ws, cudaStream_t s);
 // x += sum_j y[j] Z_j (y on device)
 void launch_lincomb(double* x, const double* Z, long long ldz, int k, const double* y, long long n, cudaStream_t s);
 // v = w / sqrt(nrm2[0]) (nrm2 on device) or v = alpha * w

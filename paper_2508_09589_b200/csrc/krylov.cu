@@ -121,6 +121,56 @@ __global__ void __launch_bounds__(kRedThreads) maxpy_norm_kernel(double* __restr
   block_partials<1>(acc, ws.partial, ws, out);
 }
 
+// Gram-Schmidt pass with the re-orthogonalisation coefficients of the next pass:
+// w' = w - sum_j s2_j h_j V_j, then out[j] = V_j . w' (j < J) and out[J] = ||w'||^2, from the same
+// V_j registers (saves the separate multi-dot pass over V and w' of the DGKS step).
+template <int J>
+__global__ void __launch_bounds__(kRedThreads) maxpy_dots_kernel(double* __restrict__ w, const double* __restrict__ V,
+                                                                 long long ldv, const double* __restrict__ h,
+                                                                 const double* __restrict__ s2, long long n,
+                                                                 double* out, RedWs ws) {
+  constexpr int U = J <= 8 ? 2 : 1;  // elements per iteration: (J + 1) U loads in flight
+  __shared__ double hs[J];
+  if (threadIdx.x < J) hs[threadIdx.x] = s2 ? h[threadIdx.x] * s2[threadIdx.x] : h[threadIdx.x];
+  __syncthreads();
+  double acc[J + 1];
+#pragma unroll
+  for (int v = 0; v <= J; ++v) acc[v] = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < n; i += U * stride) {
+    double v[U][J], a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a[u] = w[i + u * stride];
+#pragma unroll
+      for (int j = 0; j < J; ++j) v[u][j] = __ldg(V + j * ldv + i + u * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int j = 0; j < J; ++j) a[u] -= hs[j] * v[u][j];
+      w[i + u * stride] = a[u];
+#pragma unroll
+      for (int j = 0; j < J; ++j) acc[j] += v[u][j] * a[u];
+      acc[J] += a[u] * a[u];
+    }
+  }
+  if (U == 2 && i < n) {
+    double a = w[i];
+    double v[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) v[j] = __ldg(V + j * ldv + i);
+#pragma unroll
+    for (int j = 0; j < J; ++j) a -= hs[j] * v[j];
+    w[i] = a;
+#pragma unroll
+    for (int j = 0; j < J; ++j) acc[j] += v[j] * a;
+    acc[J] += a * a;
+  }
+  block_partials<J + 1>(acc, ws.partial, ws, out);
+}
+
 __global__ void lincomb_kernel(double* __restrict__ x, const double* __restrict__ Z, long long ldz, int k,
                                const double* __restrict__ y, long long n) {
   __shared__ double ys[128];
@@ -205,6 +255,21 @@ void launch_mdot(const double* w, const double* V, long long ldv, int k, long lo
 void launch_maxpy_norm(double* w, const double* V, long long ldv, int k, const double* h, const double* s2,
                        long long n, double* out, RedWs ws, cudaStream_t s) {
   maxpy_norm_kernel<<<red_blocks(n), kRedThreads, 0, s>>>(w, V, ldv, k, h, s2, n, out, ws);
+}
+
+bool launch_maxpy_dots(double* w, const double* V, long long ldv, int k, const double* h, const double* s2,
+                       long long n, double* out, RedWs ws, cudaStream_t s) {
+  const unsigned g = red_blocks(n);
+#define MX(JJ)                                                                              \
+  case JJ:                                                                                  \
+    maxpy_dots_kernel<JJ><<<g, kRedThreads, 0, s>>>(w, V, ldv, h, s2, n, out, ws);          \
+    return true;
+  switch (k) {
+    MX(1) MX(2) MX(3) MX(4) MX(5) MX(6) MX(7) MX(8)
+    MX(9) MX(10) MX(11) MX(12) MX(13) MX(14) MX(15) MX(16)
+    default: return false;
+  }
+#undef MX
 }
 
 static unsigned ew_blocks(long long n) {
