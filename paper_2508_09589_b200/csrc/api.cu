@@ -56,6 +56,11 @@ struct Level {
   double* bpart = nullptr;
   double* stpart = nullptr;
   long long stpart_elems = 0;
+  // full space-time coarsening of a time-varying level: the parent's stencils coarsened in space
+  // only (mid_ns stencils per parent layer on this level's spatial grid), then in time
+  double* mid = nullptr;
+  long long mid_elems = 0;
+  int mid_ns = 0;
 };
 }  // namespace
 
@@ -321,9 +326,26 @@ void setup_forms(st_ctx* c) {
     // stored layers: 1 (time-constant design) or every local layer of the level
     const bool tv = po.tvl != 0;  // explicit: a slab of a time-varying level may hold one layer
     op.tvl = tv ? 1 : 0;
-    if (Lv.kind == KIND_FULL) throw StErr{ST_E_UNSUPPORTED, "full space-time coarsening not implemented"};
     int ns = 2;
-    if (Lv.kind == KIND_SPACE) {
+    if (Lv.kind == KIND_FULL) {
+      // P = P_t (x) P_s: Galerkin P^T K P = time coarsening of the space coarsening (the capacity
+      // re-stabilised under the time step as on a KIND_TIME level, R-22)
+      if (Lv.dist || Pv.dist) throw StErr{ST_E_UNSUPPORTED, "full space-time coarsening on time slabs"};
+      op.U[0][0] = 0.0; op.U[0][1] = 0.0; op.U[1][0] = -1.0; op.U[1][1] = 1.0;
+      Lv.st_owned = true;
+      if (!tv) {
+        op.form = FORM_MK;
+        op.nl = 1;
+        time_coarsen_factor(po.Tm, op.Tm);
+        ns = 2;
+      } else {
+        op.form = FORM_B4;
+        op.nl = Lv.g.nt;
+        ns = 5;
+        Lv.mid_ns = (po.form == FORM_B4) ? 5 : 2;
+        Lv.mid_elems = (long long)Pv.g.nt * Lv.mid_ns * NC * Lv.g.P;
+      }
+    } else if (Lv.kind == KIND_SPACE) {
       op.nl = tv ? Lv.g.nt : 1;
       memcpy(op.U, po.U, sizeof(op.U));
       if (po.form == FORM_RHO || po.form == FORM_MK) {
@@ -407,6 +429,7 @@ void allocate(st_ctx* c) {
       if (Lv.st_owned) {
         dalloc(&Lv.st, Lv.st_elems);
         Lv.op.st = Lv.st;
+        if (Lv.mid_elems > 0) dalloc(&Lv.mid, Lv.mid_elems);
       } else {
         Lv.op.st = c->lv[l - 1].op.st;  // resolved again after build (shared)
       }
@@ -579,6 +602,24 @@ void build_ops(st_ctx* c) {
       } else {
         launch_rap_space(Pv.op, Lv.g, Lv.op.nl, ns, Lv.st, c->stream);
         L(c);
+      }
+    } else if (Lv.kind == KIND_FULL) {
+      if (!tv) {  // spatial stencils coarsened in space; the time factor is in op.Tm
+        launch_rap_space(Pv.op, Lv.g, 1, 2, Lv.st, c->stream);
+        L(c);
+      } else {  // space coarsening of every parent layer into mid, then time coarsening of mid
+        OpDesc mop = Pv.op;
+        mop.g = make_geom(c->sd, Lv.g.n, Pv.g.nt, Lv.g.plo, Lv.g.phi);
+        mop.form = Lv.mid_ns == 5 ? FORM_B4 : FORM_MK;
+        mop.nl = Pv.g.nt;
+        mop.tvl = 1;
+        mop.rho = nullptr;
+        mop.kt = nullptr;
+        mop.msep = 0;
+        mop.st = Lv.mid;
+        launch_rap_space(Pv.op, mop.g, Pv.g.nt, Lv.mid_ns, Lv.mid, c->stream);
+        launch_rap_time(mop, Lv.g.nt, Lv.st, c->stream);
+        L(c, 2);
       }
     } else if (Lv.kind == KIND_TIME) {
       if (!tv) {
@@ -947,6 +988,7 @@ void free_ctx(st_ctx* c) {
   cudaSetDevice(c->device);
   for (auto& Lv : c->lv) {
     if (Lv.st_owned && Lv.st) cudaFree(Lv.st);
+    cudaFree(Lv.mid);
     cudaFree(Lv.A); cudaFree(Lv.Ainv); cudaFree(Lv.info);
   }
   for (double* p : c->vallocs) cudaFree(p);

@@ -297,7 +297,92 @@ __global__ void __launch_bounds__(1024) dense_invert_kernel(double* __restrict__
   }
 }
 
+// In-place Gauss-Jordan inversion with partial pivoting, the whole matrix in shared memory (n <= 160):
+// step k swaps rows k and p_k, then with piv = a_kk, r_j = a_kj / piv (r_k = 1 / piv), c_i = a_ik:
+// a_kj = r_j, and for i != k: a_ik = 0, a_ij -= c_i r_j. The row swaps are undone at the end as
+// column swaps in reverse order. Same result as the augmented [A | I] elimination up to rounding,
+// with every access in shared memory (~1 us per pivot instead of ~11 us through L2).
+constexpr int kDenseSmemMax = 160;
+__global__ void __launch_bounds__(1024) dense_invert_smem_kernel(const double* __restrict__ A, double* __restrict__ Ainv,
+                                                                 int n, int* info) {
+  extern __shared__ double a[];  // [n][n], then r[n], c[n]
+  double* r = a + n * n;
+  double* c = r + n;
+  __shared__ int perm[kDenseSmemMax];
+  __shared__ double bv[32];
+  __shared__ int bi[32];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  for (int e = tid; e < n * n; e += nth) a[e] = A[e];
+  if (tid == 0) *info = 0;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    double best = -1.0;
+    int bidx = k;
+    for (int i = k + tid; i < n; i += nth) {
+      const double v = fabs(a[i * n + k]);
+      if (v > best) { best = v; bidx = i; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_down_sync(0xffffffffu, best, o);
+      const int oi = __shfl_down_sync(0xffffffffu, bidx, o);
+      if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+    }
+    if ((tid & 31) == 0) { bv[tid >> 5] = best; bi[tid >> 5] = bidx; }
+    __syncthreads();
+    if (tid == 0) {
+      double bb = bv[0];
+      int ii = bi[0];
+      for (int w = 1; w < nth / 32; ++w)
+        if (bv[w] > bb || (bv[w] == bb && bi[w] < ii)) { bb = bv[w]; ii = bi[w]; }
+      perm[k] = ii;
+      if (!(bb > 0.0) && *info == 0) *info = k + 1;
+    }
+    __syncthreads();
+    const int p = perm[k];
+    if (p != k)
+      for (int j = tid; j < n; j += nth) {
+        const double t = a[k * n + j];
+        a[k * n + j] = a[p * n + j];
+        a[p * n + j] = t;
+      }
+    __syncthreads();
+    const double piv = a[k * n + k];
+    const double ip = (piv != 0.0) ? 1.0 / piv : 0.0;
+    for (int j = tid; j < n; j += nth) r[j] = (j == k) ? ip : a[k * n + j] * ip;
+    for (int i = tid; i < n; i += nth) c[i] = (i == k) ? 0.0 : a[i * n + k];
+    __syncthreads();
+    for (int e = tid; e < n * n; e += nth) {
+      const int i = e / n, j = e - i * n;
+      if (i == k) a[e] = r[j];
+      else a[e] = (j == k ? 0.0 : a[e]) - c[i] * r[j];
+    }
+    __syncthreads();
+  }
+  for (int k = n - 1; k >= 0; --k) {  // undo the row swaps as column swaps
+    const int p = perm[k];
+    if (p != k)
+      for (int i = tid; i < n; i += nth) {
+        const double t = a[i * n + k];
+        a[i * n + k] = a[i * n + p];
+        a[i * n + p] = t;
+      }
+    __syncthreads();
+  }
+  for (int e = tid; e < n * n; e += nth) Ainv[e] = a[e];
+}
+
 void launch_dense_invert(double* A, double* Ainv, int n, int* info, cudaStream_t s) {
+  if (n <= kDenseSmemMax) {
+    const size_t bytes = (size_t)(n * n + 2 * n) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(dense_invert_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)((kDenseSmemMax * kDenseSmemMax + 2 * kDenseSmemMax) * sizeof(double)));
+      attr = true;
+    }
+    dense_invert_smem_kernel<<<1, 1024, bytes, s>>>(A, Ainv, n, info);
+    return;
+  }
   dense_invert_kernel<<<1, 1024, n * sizeof(double), s>>>(A, Ainv, n, info);
 }
 

@@ -117,6 +117,40 @@ def test_solve_adjoint_sensitivity_parity(case):
     solver.close()
 
 
+@pytest.mark.parametrize("case", [("cfg3-replica", 2, 32, 32, CFG1_MATS, ("sin", 1.0, 1.0, 2 * np.pi), "smooth_layers", False),
+                                  ("cfg2-replica", 2, 32, 32, CFG1_MATS, ("uniform", 1.0, 0.0, 0.0), "smooth_tc", True),
+                                  ("cfg4-replica", 3, 8, 16, CFG4_MATS, ("uniform", 1.0, 0.0, 0.0), "smooth_tc", True)],
+                         ids=lambda c: c[0])
+def test_full_coarsening_solves_and_semi_coarsening_needs_fewer_iterations(case):
+    """Full space-time coarsening (option full_coarsening) gives the oracle's T and
+    lambda, and Algorithm 1's semi-coarsening needs no more FGMRES iterations than it (PAPER.md:781,
+    Example 1B: 9.7 / 55.6 state / adjoint iterations with full coarsening vs 5.6 / 9.4 with
+    semi-coarsening; the paper's counts are for its GMRES-Jacobi smoother and grids, so only the
+    ordering is asserted)."""
+    name, sdim, n, nt, mats, src, design, tc = case
+    rho = I.design_for(sdim, n, nt, design, 0)
+    its = {}
+    for full in (0, 1):
+        solver, prob = make_pair(sdim, n, nt, mats=mats, source=src, time_constant=tc, rtol=1e-10, maxit=400,
+                                 full_coarsening=full)
+        if full:
+            assert all(h["kind"] == "full" for h in solver.hierarchy()[1:])
+        T_ref, lam_ref = prob.solve_both(rho)
+        rd = dev(rho)
+        T = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+        solver.solve(rd, T)
+        a = solver.stats()
+        assert a["converged"] == 1 and rel(host(T), T_ref) <= 1e-8, (full, rel(host(T), T_ref))
+        lam = torch.zeros_like(T)
+        solver.adjoint(rd, dev(prob.compliance_rhs()), lam)
+        b = solver.stats()
+        assert b["converged"] == 1 and rel(host(lam), lam_ref) <= 1e-8, (full, rel(host(lam), lam_ref))
+        its[full] = (a["iterations"], b["iterations"])
+        solver.close()
+    print(name, "semi", its[0], "full", its[1])
+    assert its[0][0] <= its[1][0] and its[0][1] <= its[1][1], its
+
+
 def test_host_pointer_path_and_warm_start():
     """C ABI with HOST buffers (library stages them) gives the same result; a warm start
     from the solution converges in zero iterations."""
@@ -154,30 +188,47 @@ def _P1(nf, kind):
                                                  (3, 8, 8, True, CFG4_MATS),
                                                  # uniform capacity, space-time design: the stored-stencil
                                                  # TMA kernel (tv2d SRC 1) on levels of several ragged tiles
-                                                 (2, 80, 12, False, CFG1_MATS)])
+                                                 (2, 80, 12, False, CFG1_MATS),
+                                                 # full space-time coarsening
+                                                 (2, 16, 16, False, "full4"), (2, 32, 32, True, "full4"),
+                                                 (2, 32, 16, False, "full1"), (3, 4, 8, False, "full4"),
+                                                 (3, 8, 8, True, "full4")])
 def test_coarse_operators(sdim, n, nt, tc, mats):
     """Each coarse level equals, with the Dirichlet masks of its own grid, the operator built
     here independently from assembled matrices: conduction part
     by Galerkin P^T A P with the space/time linear interpolation P; capacity
     part by Galerkin under space coarsening and re-stabilised (upwind U, layer-mean capacity)
     under time coarsening."""
-    solver, prob = make_pair(sdim, n, nt, mats=mats, time_constant=tc)
+    opts = {}
+    if isinstance(mats, str):  # "full<mats>": the full-coarsening hierarchy
+        opts = {"full_coarsening": 1}
+        mats = CFG4_MATS if mats == "full4" else CFG1_MATS
+    solver, prob = make_pair(sdim, n, nt, mats=mats, time_constant=tc, **opts)
     rho = I.rho_uniform((n,) * sdim if tc else (nt,) + (n,) * sdim, 3)
     H = solver.hierarchy()
+    if opts:
+        assert all(h["kind"] == "full" for h in H[1:]), H
     C, k, _, _, _ = prob.coefficients(rho)
     Kcap = O.assemble_K(prob.mesh, C, np.zeros_like(k)).tocsr()
     Kcon = O.assemble_K(prob.mesh, np.zeros_like(C), k).tocsr()
     nf, ntf = H[0]["n"], H[0]["nt"]
+    def space_step(Kcap, Kcon, nf, ntf):
+        Px = sp.csr_matrix(_P1(nf, "s"))
+        Ps = Px
+        for _ in range(sdim - 1):
+            Ps = sp.kron(Px, Ps)
+        P = sp.kron(sp.identity(ntf + 1), Ps).tocsr()
+        return (P.T @ Kcap @ P).tocsr(), (P.T @ Kcon @ P).tocsr()
+
     for l in range(1, len(H)):
         Psp = (nf + 1) ** sdim
-        if H[l]["kind"] == "space":
-            Px = sp.csr_matrix(_P1(nf, "s"))
-            Ps = Px
-            for _ in range(sdim - 1):
-                Ps = sp.kron(Px, Ps)
-            P = sp.kron(sp.identity(ntf + 1), Ps).tocsr()
-            Kcap = (P.T @ Kcap @ P).tocsr()
-        else:
+        if H[l]["kind"] in ("space", "full"):
+            Kcap, Kcon = space_step(Kcap, Kcon, nf, ntf)
+            P = None
+            if H[l]["kind"] == "full":  # P_t (x) P_s = the time step applied to the space-coarsened operator
+                nf = H[l]["n"]
+                Psp = (nf + 1) ** sdim
+        if H[l]["kind"] in ("time", "full"):
             P = sp.kron(sp.csr_matrix(_P1(ntf, "t")), sp.identity(Psp)).tocsr()
             # layer masses M_tau = -block(tau+1, tau) of the capacity part (U[1][0] = -1)
             ntc = ntf // 2
@@ -193,7 +244,8 @@ def test_coarse_operators(sdim, n, nt, tc, mats):
                         E[T + a, T + b] = U[a, b]
                 blocks.append(sp.kron(E.tocsr(), Mb))
             Kcap = sum(blocks).tocsr()
-        Kcon = (P.T @ Kcon @ P).tocsr()
+        if P is not None:
+            Kcon = (P.T @ Kcon @ P).tocsr()
         nf, ntf = H[l]["n"], H[l]["nt"]
         mesh_l = O.Mesh(sdim, nf, max(ntf, 2))
         cons, _ = O.dirichlet(mesh_l, O.BCs())
