@@ -53,6 +53,14 @@ WORKLOADS = {
 METRIC = "space-time DOFs solved/sec (FGMRES+MG to rtol 1e-8) & operator GB/s vs HBM peak"
 
 
+def solver_opts(args):
+    nu = args.nu or (10 if args.smoother == "gmres" else 3)
+    o = dict(smoother=2 if args.smoother == "gmres" else 0, nu_pre=nu, nu_post=nu)
+    if args.full_coarsening:
+        o["full_coarsening"] = 1
+    return o
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -63,6 +71,10 @@ def parse():
     ap.add_argument("--rtol", type=float, default=1e-8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--smoother", default="jacobi", choices=["jacobi", "gmres"],
+                    help="jacobi: damped Jacobi nu+nu (default); gmres: the paper's GMRES(nu)-Jacobi smoother")
+    ap.add_argument("--nu", type=int, default=0, help="sweeps / GMRES steps (default 3 for jacobi, 10 for gmres)")
+    ap.add_argument("--full-coarsening", action="store_true", help="the paper's full space-time coarsening")
     ap.add_argument("--cpu-worker", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--cpu-reps", type=int, default=1, help=argparse.SUPPRESS)
     return ap.parse_args()
@@ -184,7 +196,7 @@ def run_cuda(args):
         nccl_comm = S.nccl_comm_init(obj[0], rank, world)
     solver = S.Solver(wl["sdim"], wl["n"], wl["nt"], mats=wl["mats"], source=wl["source"], tau=wl["tau"],
                       time_constant=wl["tc"], stream=stream.cuda_stream, device=local, rtol=args.rtol, maxit=1000,
-                      rank=rank, size=world, nccl_comm=nccl_comm)
+                      rank=rank, size=world, nccl_comm=nccl_comm, **solver_opts(args))
     N = solver.n_nodes            # this rank's owned nodes
     nd = solver.n_design
     N_global = (wl["n"] + 1) ** wl["sdim"] * (wl["nt"] + 1)
@@ -377,7 +389,12 @@ def run_cuda(args):
                             "+ filter^T + OC update" if design else
                             "rho setup + forward solve + adjoint solve + sensitivities"),
                    "parallelism": f"{world} time slabs (NCCL)" if world > 1 else "1 GPU",
-                   "l2": "flushed (256 MB write) between steps"},
+                   "l2": "flushed (256 MB write) between steps",
+                   "preconditioner": ("V-cycle, " + ("GMRES(%d)-Jacobi" if args.smoother == "gmres" else "damped Jacobi %d+%d")
+                                      % ((solver_opts(args)["nu_pre"],) if args.smoother == "gmres"
+                                         else (solver_opts(args)["nu_pre"], solver_opts(args)["nu_post"]))
+                                      + (" smoother, full space-time coarsening" if args.full_coarsening
+                                         else " smoother, semi-coarsening (Algorithm 1)"))},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "fine-level damped-Jacobi sweep (" + ("tc2d_kernel, time-constant rho" if wl["tc"] and wl["sdim"] == 2
                                                               else "tv2d_kernel, space-time rho, uniform capacity" if wl["sdim"] == 2

@@ -59,7 +59,10 @@ enum {
 
 enum { ST_TIME_CONSTANT = 0, ST_SPACE_TIME = 1 };
 enum { ST_SRC_UNIFORM = 0, ST_SRC_SIN = 1 };
-enum { ST_SMOOTH_JACOBI = 0, ST_SMOOTH_CHEBYSHEV = 1 };
+/* Smoothers: damped Jacobi (default); the paper's GMRES(k)-Jacobi smoother
+ * (k = nu_pre / nu_post fixed steps, <= 24; one GPU). ST_SMOOTH_CHEBYSHEV is reserved
+ * (ST_E_UNSUPPORTED). */
+enum { ST_SMOOTH_JACOBI = 0, ST_SMOOTH_CHEBYSHEV = 1, ST_SMOOTH_GMRES = 2 };
 
 /* Regular space-time mesh of n^sdim x nt elements. L, tau only rescale. */
 typedef struct {
@@ -89,8 +92,8 @@ typedef struct {
   double rtol;              /* FGMRES stop: true ||b - K T|| / ||b|| <= rtol              */
   int32_t maxit;            /* max outer iterations (total over restarts)                */
   int32_t restart;          /* FGMRES restart length m                                   */
-  int32_t smoother;         /* ST_SMOOTH_JACOBI                                          */
-  int32_t nu_pre, nu_post;  /* smoothing sweeps                                          */
+  int32_t smoother;         /* ST_SMOOTH_JACOBI | ST_SMOOTH_GMRES                        */
+  int32_t nu_pre, nu_post;  /* Jacobi sweeps / GMRES smoother steps (pre, post)          */
   double omega;             /* Jacobi damping                                            */
   double lambda_crit;       /* Algorithm 1 threshold (0.5)                 */
   int64_t coarse_max_nodes; /* stop coarsening at <= this many nodes (R-19)     */

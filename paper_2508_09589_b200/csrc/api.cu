@@ -61,6 +61,9 @@ struct Level {
   double* mid = nullptr;
   long long mid_elems = 0;
   int mid_ns = 0;
+  // GMRES(k) smoother (ST_SMOOTH_GMRES): k+1 basis vectors with leading dimension gld
+  double* gv = nullptr;
+  long long gld = 0;
 };
 }  // namespace
 
@@ -109,6 +112,7 @@ struct st_ctx {
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
   // fused small-level V-cycle (vsmall.cu): levels >= vs0 in one cluster kernel (-1: off)
   int vs0 = -1;
+  double* gsm = nullptr;  // GMRES smoother: device Hessenberg / Givens / dots scratch (1024 doubles)
   // config-5 design update buffers (st_filter / st_oc_update), allocated on first use
   double *fbuf = nullptr, *fw = nullptr;
   long long gkernels[2] = {0, 0};
@@ -413,6 +417,17 @@ void allocate(st_ctx* c) {
   dalloc(&c->ws.counter, 1);
   CK(cudaMemsetAsync(c->ws.counter, 0, sizeof(unsigned), c->stream));
   dalloc(&c->dsmall, 512);
+  if (c->opt.smoother == ST_SMOOTH_GMRES) {  // the paper's smoother: basis per level
+    const int k = std::max(c->opt.nu_pre, c->opt.nu_post);
+    dzalloc(&c->gsm, 1024);
+    const double one = 1.0;
+    CK(cudaMemcpy(c->gsm + 1000, &one, sizeof(double), cudaMemcpyHostToDevice));
+    for (auto& Lv : c->lv) {
+      if (&Lv == &c->lv.back()) break;  // the coarsest level is solved densely
+      Lv.gld = (Lv.g.N + 31) / 32 * 32;
+      dzalloc(&Lv.gv, (long long)(k + 1) * Lv.gld);  // zero pads: the dots run over the padded length
+    }
+  }
   CK(cudaMallocHost((void**)&c->hsmall, 512 * sizeof(double)));
   if ((long long)c->comm.size * (long long)c->lv.size() > 140) throw StErr{ST_E_INVALID_ARG, "too many ranks x levels"};
   for (size_t l = 0; l < c->lv.size(); ++l) {
@@ -453,7 +468,7 @@ void allocate(st_ctx* c) {
     // (408 vs 441 MDOF/s with levels <= 4096 nodes fused; profiles/r01), kept for the experiment
     const char* e = getenv("ST_VSMALL");
     const int nl = (int)c->lv.size();
-    if (e && e[0] == '1')
+    if (e && e[0] == '1' && c->opt.smoother == ST_SMOOTH_JACOBI)
       for (int l = 1; l + 1 < nl; ++l) {
         bool ok = nl - l <= kMaxSmall;
         for (int k = l; k < nl && ok; ++k) ok = !c->lv[k].dist && nodes_of(c->lv[k].g) <= 4096;
@@ -710,6 +725,58 @@ bool vcycle_graph(st_ctx* c, int l, bool trans, const double* b, double* x) {
   return true;
 }
 
+// GMRES(k)-Jacobi smoother (the paper's smoother; option ST_SMOOTH_GMRES):
+// x <- x + D^-1 V y with V the Arnoldi basis of A D^-1 from r0 = b - A x and y minimising
+// ||beta e1 - H y|| (right Jacobi preconditioning, classical Gram-Schmidt). k = nu_pre (from
+// x = 0) or nu_post fixed steps, without the paper's inner rtol 1e-6 (10 steps rarely reach it):
+// every step stays on the device — no host synchronisation, so the small levels keep their CUDA
+// graph. Vectors: the basis Lv.gv, z = D^-1 V_j in Lv.t (read as the x tile of the apply), u = V y
+// in V_k (unused by y).
+void gmres_smooth(st_ctx* c, int l, bool trans, const double* b, double* x, bool from_zero) {
+  Level& Lv = c->lv[l];
+  const int k = from_zero ? c->opt.nu_pre : c->opt.nu_post;
+  if (k <= 0) return;
+  const long long N = Lv.g.N, ld = Lv.gld;
+  double* V = Lv.gv;
+  double* z = Lv.t;
+  double* st = c->gsm;
+  double* dd = c->gsm + 768;  // dots: [0..k+1], ||w'||^2 at +64
+  const double* r0 = b;
+  if (!from_zero) {
+    op_launch(c, l, MODE_RESID, trans, true, x, b, Lv.r);
+    r0 = Lv.r;
+  }
+  launch_mdot(r0, nullptr, 0, 0, N, dd, c->ws, c->stream);
+  launch_gm_init(st, k, dd, c->stream);
+  launch_scale_dev(r0, V, dd, N, c->stream);
+  L(c, 3);
+  for (int j = 0; j < k; ++j) {
+    double* vj = V + (long long)j * ld;
+    double* w = V + (long long)(j + 1) * ld;
+    launch_op(Lv.op, MODE_JAC0, trans, true, nullptr, vj, z, 1.0, c->stream);  // z = D^-1 V_j
+    op_launch(c, l, MODE_APPLY, trans, true, z, nullptr, w);                   // w = A z
+    launch_mdot(w, V, ld, j + 1, N, dd, c->ws, c->stream);                     // h = V^T w
+    launch_maxpy_norm(w, V, ld, j + 1, dd, nullptr, N, dd + 64, c->ws, c->stream);  // w -= V h
+    launch_gm_col(st, k, j, dd, dd + 64, c->stream);
+    launch_scale_dev(w, w, dd + 64, N, c->stream);                             // V_{j+1} = w / ||w||
+    L(c, 5 + (j + 16) / 16);
+  }
+  launch_gm_solve(st, k, c->stream);
+  double* u = V + (long long)k * ld;
+  CK(cudaMemsetAsync(u, 0, (size_t)N * sizeof(double), c->stream));
+  launch_lincomb(u, V, ld, k, st + gm_y_offset(k), N, c->stream);              // u = V y
+  L(c, 2);
+  if (from_zero) {
+    launch_op(Lv.op, MODE_JAC0, trans, true, nullptr, u, x, 1.0, c->stream);   // x = D^-1 u
+    L(c);
+  } else {
+    launch_op(Lv.op, MODE_JAC0, trans, true, nullptr, u, z, 1.0, c->stream);
+    launch_lincomb(x, z, 0, 1, c->gsm + 1000, N, c->stream);                   // x += z (gsm[1000] = 1)
+    L(c, 2);
+  }
+  check_launch();
+}
+
 void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_graph) {
   Level& Lv = c->lv[l];
   if (l == c->vs0 && b == Lv.b && x == Lv.x) {  // the small-level tail: one cluster kernel
@@ -739,6 +806,17 @@ void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_gr
     return;
   }
   Level& Nx = c->lv[l + 1];
+  if (c->opt.smoother == ST_SMOOTH_GMRES) {  // one replicated level (slabs are rejected at setup)
+    gmres_smooth(c, l, trans, b, x, true);
+    op_launch(c, l, MODE_RESID, trans, true, x, b, Lv.r);
+    launch_restrict(Lv.g, Nx.g, Nx.kind, Lv.r, Nx.b, c->stream);
+    L(c);
+    vcycle(c, l + 1, trans, Nx.b, Nx.x, in_graph);
+    launch_prolong_add(Lv.g, Nx.g, Nx.kind, Nx.x, x, c->stream);
+    L(c);
+    gmres_smooth(c, l, trans, b, x, false);
+    return;
+  }
   const int npre = c->opt.nu_pre, npost = c->opt.nu_post;
   const int total = npre + npost;
   double* cur = (total % 2 == 1) ? x : Lv.t;
@@ -989,6 +1067,7 @@ void free_ctx(st_ctx* c) {
   for (auto& Lv : c->lv) {
     if (Lv.st_owned && Lv.st) cudaFree(Lv.st);
     cudaFree(Lv.mid);
+    cudaFree(Lv.gv);
     cudaFree(Lv.A); cudaFree(Lv.Ainv); cudaFree(Lv.info);
   }
   for (double* p : c->vallocs) cudaFree(p);
@@ -996,6 +1075,7 @@ void free_ctx(st_ctx* c) {
   cudaFree(c->dsmall);
   if (c->hsmall) cudaFreeHost(c->hsmall);
   cudaFree(c->rho_stage);
+  cudaFree(c->gsm);
   cudaFree(c->kt);
   comm_release(c->comm);
   cudaFree(c->fbuf);
@@ -1076,6 +1156,8 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
         throw StErr{ST_E_INVALID_ARG, "host transport needs sendrecv, allreduce_sum and allgather"};
       if (dist->transport != ST_COMM_NCCL && dist->transport != ST_COMM_HOST)
         throw StErr{ST_E_INVALID_ARG, "size > 1 needs a transport (ST_COMM_NCCL or ST_COMM_HOST)"};
+      if (opts && (opts->smoother == ST_SMOOTH_GMRES || opts->full_coarsening))
+        throw StErr{ST_E_UNSUPPORTED, "time slabs: Jacobi smoother and semi-coarsening only"};
     }
     st_ctx* c = new st_ctx();
     try {
@@ -1087,6 +1169,10 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       else st_default_options(&c->opt);
       if (c->opt.restart < 1 || c->opt.restart > 60) throw StErr{ST_E_INVALID_ARG, "restart must be in [1, 60]"};
       if (c->opt.nu_pre < 1 || c->opt.nu_post < 0) throw StErr{ST_E_INVALID_ARG, "nu_pre >= 1, nu_post >= 0"};
+      if (c->opt.smoother != ST_SMOOTH_JACOBI && c->opt.smoother != ST_SMOOTH_GMRES)
+        throw StErr{ST_E_UNSUPPORTED, "smoother: ST_SMOOTH_JACOBI or ST_SMOOTH_GMRES"};
+      if (c->opt.smoother == ST_SMOOTH_GMRES && (c->opt.nu_pre > 24 || c->opt.nu_post > 24))
+        throw StErr{ST_E_INVALID_ARG, "GMRES smoother: nu_pre, nu_post <= 24"};
       if (c->opt.coarse_max_nodes < 8) c->opt.coarse_max_nodes = 8;
       {  // kernel family (test / bench hook): ST_NO_FAST=1 -> generic kernels; ST_FAST_KIND=1 -> cp.async
         const char* e = getenv("ST_NO_FAST");

@@ -59,6 +59,12 @@ void launch_lincomb(double* x, const double* Z, long long ldz, int k, const doub
 void launch_scale_dev(const double* w, double* v, const double* nrm2, long long n, cudaStream_t s);
 void launch_scale(const double* w, double* v, double alpha, long long n, cudaStream_t s);
 void launch_checksum(const double* a, long long n, double* out, RedWs ws, cudaStream_t s);
+// GMRES(k) smoother bookkeeping on the device (single-thread kernels): st holds g[k+1], the Givens
+// cs[k], sn[k], the Hessenberg H[k][k+1] and y[k] (at st + gm_y_offset(k)).
+void launch_gm_init(double* st, int k, const double* nrm2, cudaStream_t s);           // g = (||r0||, 0, ...)
+void launch_gm_col(double* st, int k, int j, const double* h, const double* nrm2w, cudaStream_t s);
+void launch_gm_solve(double* st, int k, cudaStream_t s);                              // y = R^-1 g
+int gm_y_offset(int k);
 
 // misc.cu
 // Per-design conductivity table of a (2+1)D space-time design, read by tv2d: layers 0 .. nl-1 of

@@ -191,7 +191,7 @@ __global__ void lincomb_kernel(double* __restrict__ x, const double* __restrict_
 }
 
 __global__ void scale_dev_kernel(const double* __restrict__ w, double* __restrict__ v, const double* nrm2, long long n) {
-  double a = 1.0 / sqrt(nrm2[0]);
+  const double a = nrm2[0] > 0.0 ? 1.0 / sqrt(nrm2[0]) : 0.0;  // a zero vector stays zero
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) v[i] = a * w[i];
 }
@@ -199,6 +199,54 @@ __global__ void scale_dev_kernel(const double* __restrict__ w, double* __restric
 __global__ void scale_kernel(const double* __restrict__ w, double* __restrict__ v, double a, long long n) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) v[i] = a * w[i];
+}
+
+// ---- GMRES(k) smoother bookkeeping on the device (one thread each; no host synchronisation) ----
+// st layout (gm_layout): g[k+1] | cs[k] | sn[k] | H[k][k+1] (column j at H + j (k+1)) | y[k]
+__device__ __forceinline__ void gm_layout(double* st, int k, double** g, double** cs, double** sn, double** H,
+                                          double** y) {
+  *g = st;
+  *cs = st + (k + 1);
+  *sn = *cs + k;
+  *H = *sn + k;
+  *y = *H + (long long)k * (k + 1);
+}
+__global__ void gm_init_kernel(double* st, int k, const double* nrm2) {
+  double *g, *cs, *sn, *H, *y;
+  gm_layout(st, k, &g, &cs, &sn, &H, &y);
+  for (int i = 0; i <= k; ++i) g[i] = 0.0;
+  g[0] = sqrt(fmax(nrm2[0], 0.0));
+}
+// column j: h_ij = V_i . w (i <= j, CGS), h_{j+1,j} = ||w'||; previous rotations, then a new one
+__global__ void gm_col_kernel(double* st, int k, int j, const double* h, const double* nrm2w) {
+  double *g, *cs, *sn, *H, *y;
+  gm_layout(st, k, &g, &cs, &sn, &H, &y);
+  double* col = H + (long long)j * (k + 1);
+  for (int i = 0; i <= j; ++i) col[i] = h[i];
+  col[j + 1] = sqrt(fmax(nrm2w[0], 0.0));
+  for (int i = 0; i < j; ++i) {
+    const double t = cs[i] * col[i] + sn[i] * col[i + 1];
+    col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
+    col[i] = t;
+  }
+  const double den = hypot(col[j], col[j + 1]);
+  cs[j] = den > 0.0 ? col[j] / den : 1.0;
+  sn[j] = den > 0.0 ? col[j + 1] / den : 0.0;
+  col[j] = den;
+  col[j + 1] = 0.0;
+  g[j + 1] = -sn[j] * g[j];
+  g[j] = cs[j] * g[j];
+}
+// y = R^-1 g (the rotated Hessenberg is upper triangular); a zero pivot (breakdown) gives y_i = 0
+__global__ void gm_solve_kernel(double* st, int k) {
+  double *g, *cs, *sn, *H, *y;
+  gm_layout(st, k, &g, &cs, &sn, &H, &y);
+  for (int i = k - 1; i >= 0; --i) {
+    double s = g[i];
+    for (int m = i + 1; m < k; ++m) s -= H[(long long)m * (k + 1) + i] * y[m];
+    const double d = H[(long long)i * (k + 1) + i];
+    y[i] = d != 0.0 ? s / d : 0.0;
+  }
 }
 
 __device__ __forceinline__ double hash_weight(long long i) {
@@ -288,6 +336,13 @@ void launch_scale_dev(const double* w, double* v, const double* nrm2, long long 
 void launch_scale(const double* w, double* v, double alpha, long long n, cudaStream_t s) {
   scale_kernel<<<ew_blocks(n), 256, 0, s>>>(w, v, alpha, n);
 }
+void launch_gm_init(double* st, int k, const double* nrm2, cudaStream_t s) { gm_init_kernel<<<1, 1, 0, s>>>(st, k, nrm2); }
+void launch_gm_col(double* st, int k, int j, const double* h, const double* nrm2w, cudaStream_t s) {
+  gm_col_kernel<<<1, 1, 0, s>>>(st, k, j, h, nrm2w);
+}
+void launch_gm_solve(double* st, int k, cudaStream_t s) { gm_solve_kernel<<<1, 1, 0, s>>>(st, k); }
+int gm_y_offset(int k) { return (k + 1) + 2 * k + k * (k + 1); }
+
 void launch_checksum(const double* a, long long n, double* out, RedWs ws, cudaStream_t s) {
   checksum_kernel<<<red_blocks(n), kRedThreads, 0, s>>>(a, n, out, ws);
 }

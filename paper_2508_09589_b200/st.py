@@ -14,6 +14,7 @@ ST_OK = 0
 ST_E_NOT_CONVERGED = -3
 ST_TIME_CONSTANT, ST_SPACE_TIME = 0, 1
 ST_SRC_UNIFORM, ST_SRC_SIN = 0, 1
+ST_SMOOTH_JACOBI, ST_SMOOTH_GMRES = 0, 2  # st.h: the GMRES(k)-Jacobi smoother of the paper (one GPU)
 
 
 class Grid(C.Structure):

@@ -94,3 +94,14 @@ def test_setup_validates_distribution_without_gpu():
     d = st.Dist(None, 0, 4, None, -1, st.ST_COMM_NONE, st.HostComm())
     assert lib.st_setup(ctypes.byref(g), ctypes.byref(m), ctypes.byref(b), ctypes.byref(s), None,
                         ctypes.byref(d), ctypes.byref(h)) == -1
+
+
+def test_smoother_constants_match_header():
+    """The binding's smoother constants are st.h's enum values (ST_SMOOTH_GMRES: the paper's
+    GMRES(k)-Jacobi smoother)."""
+    import re
+    from paper_2508_09589_b200 import st
+    hdr = open(os.path.join(ROOT, "include", "st.h")).read()
+    m = re.search(r"enum \{ ST_SMOOTH_JACOBI = (\d+), ST_SMOOTH_CHEBYSHEV = (\d+), ST_SMOOTH_GMRES = (\d+) \};", hdr)
+    assert m, "smoother enum"
+    assert (st.ST_SMOOTH_JACOBI, st.ST_SMOOTH_GMRES) == (int(m.group(1)), int(m.group(3)))

@@ -121,18 +121,21 @@ def test_solve_adjoint_sensitivity_parity(case):
                                   ("cfg2-replica", 2, 32, 32, CFG1_MATS, ("uniform", 1.0, 0.0, 0.0), "smooth_tc", True),
                                   ("cfg4-replica", 3, 8, 16, CFG4_MATS, ("uniform", 1.0, 0.0, 0.0), "smooth_tc", True)],
                          ids=lambda c: c[0])
-def test_full_coarsening_solves_and_semi_coarsening_needs_fewer_iterations(case):
+@pytest.mark.parametrize("smoother", [(0, 3), (2, 10)], ids=["jacobi3", "gmres10"])
+def test_full_coarsening_solves_and_semi_coarsening_needs_fewer_iterations(case, smoother):
     """Full space-time coarsening (option full_coarsening) gives the oracle's T and
     lambda, and Algorithm 1's semi-coarsening needs no more FGMRES iterations than it (PAPER.md:781,
     Example 1B: 9.7 / 55.6 state / adjoint iterations with full coarsening vs 5.6 / 9.4 with
     semi-coarsening; the paper's counts are for its GMRES-Jacobi smoother and grids, so only the
-    ordering is asserted)."""
+    ordering is asserted). Run with the damped-Jacobi smoother of this build and with the paper's
+    GMRES(10)-Jacobi smoother (ST_SMOOTH_GMRES)."""
     name, sdim, n, nt, mats, src, design, tc = case
     rho = I.design_for(sdim, n, nt, design, 0)
     its = {}
     for full in (0, 1):
         solver, prob = make_pair(sdim, n, nt, mats=mats, source=src, time_constant=tc, rtol=1e-10, maxit=400,
-                                 full_coarsening=full)
+                                 full_coarsening=full, smoother=smoother[0], nu_pre=smoother[1],
+                                 nu_post=smoother[1])
         if full:
             assert all(h["kind"] == "full" for h in solver.hierarchy()[1:])
         T_ref, lam_ref = prob.solve_both(rho)
@@ -147,7 +150,7 @@ def test_full_coarsening_solves_and_semi_coarsening_needs_fewer_iterations(case)
         assert b["converged"] == 1 and rel(host(lam), lam_ref) <= 1e-8, (full, rel(host(lam), lam_ref))
         its[full] = (a["iterations"], b["iterations"])
         solver.close()
-    print(name, "semi", its[0], "full", its[1])
+    print(name, smoother, "semi", its[0], "full", its[1])
     assert its[0][0] <= its[1][0] and its[0][1] <= its[1][1], its
 
 
