@@ -86,6 +86,11 @@ SOLVE_CASES = [
     ("cfg4-replica", 3, 6, 12, CFG4_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0), 1.0, "smooth_tc", True),
     ("cfg5-replica-G2", 2, 16, 32, CFG1_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0), 2.0, "const", False),
     ("nonzero-T0", 2, 12, 20, CFG4_MATS, 0.7, ("sin", 1.0, 1.0, 2 * np.pi), 1.0, "uniform", False),
+    # the paper's default materials: C 0.5 / 1, k 0.03 / 3, p_c = 2, p_k = 3
+    ("paper-materials", 2, 16, 16, (0.5, 1.0, 2.0, 0.03, 3.0, 3.0), 0.0, ("sin", 1.0, 1.0, 2 * np.pi), 1.0,
+     "uniform", False),
+    ("paper-materials-tc", 2, 24, 16, (0.5, 1.0, 2.0, 0.03, 3.0, 3.0), 0.0, ("uniform", 1.0, 0.0, 0.0), 1.0,
+     "smooth_tc", True),
 ]
 
 
