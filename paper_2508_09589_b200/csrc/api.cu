@@ -112,6 +112,8 @@ struct st_ctx {
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
   // fused small-level V-cycle (vsmall.cu): levels >= vs0 in one cluster kernel (-1: off)
   int vs0 = -1;
+  // single-CTA shared-memory tail (vsmall.cu, launch_vtail): levels >= vt0 in one launch (-1: off)
+  int vt0 = -1;
   double* gsm = nullptr;  // GMRES smoother: device Hessenberg / Givens / dots scratch (1024 doubles)
   // config-5 design update buffers (st_filter / st_oc_update), allocated on first use
   double *fbuf = nullptr, *fw = nullptr;
@@ -396,6 +398,33 @@ double* vec_alloc(st_ctx* c, long long count) {
 }
 
 void allocate(st_ctx* c) {
+  // single-CTA V-cycle tail in shared memory: the longest replicated tail whose level vectors fit.
+  // Opt-in (ST_VTAIL=1): measured slower than the graph-launched per-level kernels (config 2: 442.7
+  // vs 482.6 MDOF/s; config 3 shape: 393.5 vs 398.3; profiles/r01/vtail_ab.log) — one SM runs the
+  // tail's sweeps slower than 148 SMs run them inside the graph, whose launches cost far less than
+  // the ~6 us of an eager launch
+  c->vt0 = -1;
+  {
+    const char* e = getenv("ST_VTAIL");
+    const int nl = (int)c->lv.size();
+    if ((e && e[0] == '1') && c->vs0 < 0 && c->opt.smoother == ST_SMOOTH_JACOBI)
+      for (int l = 1; l + 1 < nl; ++l) {
+        bool ok = nl - l <= kMaxSmall;
+        long long words = 0, nmax = 0;
+        // one SM runs the tail: only levels whose sweeps cost less there than a launch on all SMs
+        // (~6 us each; measured by scripts/level_lat.py)
+        ok = ok && nodes_of(c->lv[l].g) <= 1500;
+        for (int k = l; k < nl && ok; ++k) {
+          ok = !c->lv[k].dist;
+          words += 2 * c->lv[k].g.N;
+          nmax = std::max(nmax, c->lv[k].g.N);
+        }
+        if (ok && (words + 2 * nmax) * (long long)sizeof(double) <= 200 * 1024) {
+          c->vt0 = l;
+          break;
+        }
+      }
+  }
   const long long N = c->N;
   const int m = c->opt.restart;
   // zeroed front guard: the TMA x maps are based one row (2D) / one slice + one row (3D) + 2
@@ -779,6 +808,26 @@ void gmres_smooth(st_ctx* c, int l, bool trans, const double* b, double* x, bool
 
 void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_graph) {
   Level& Lv = c->lv[l];
+  if (l == c->vt0 && b == Lv.b && x == Lv.x) {  // the small-level tail: one CTA, shared memory
+    SmallCycle cyc{};
+    cyc.nlev = (int)c->lv.size() - l;
+    cyc.npre = c->opt.nu_pre;
+    cyc.npost = c->opt.nu_post;
+    for (int k = 0; k < cyc.nlev; ++k) {
+      const Level& S = c->lv[l + k];
+      SmallLevel& d = cyc.L[k];
+      d.op = S.op;
+      d.x = S.x; d.b = S.b; d.r = S.r; d.t = S.t;
+      d.kind = S.kind;
+      d.dense = S.dense ? 1 : 0;
+      d.omega = S.omega > 0.0 ? S.omega : c->opt.omega;
+      d.Ainv = S.Ainv;
+    }
+    launch_vtail(cyc, c->sd, trans, c->stream);
+    L(c);
+    check_launch();
+    return;
+  }
   if (l == c->vs0 && b == Lv.b && x == Lv.x) {  // the small-level tail: one cluster kernel
     SmallCycle cyc{};
     cyc.nlev = (int)c->lv.size() - l;

@@ -98,6 +98,9 @@ struct SmallCycle {
   SmallLevel L[kMaxSmall];
 };
 void launch_vsmall(const SmallCycle& cyc, int sd, bool trans, cudaStream_t s);
+// single-CTA tail, every vector in shared memory (vtail_smem_bytes(cyc) <= 227 KB)
+size_t vtail_smem_bytes(const SmallCycle& cyc);
+void launch_vtail(const SmallCycle& cyc, int sd, bool trans, cudaStream_t s);
 
 // design.cu — config-5 design update (density filter, OC)
 void launch_filter(int sd, int n, int nl, int tdir, int lo_ok, int hi_ok, double r, const double* ghosted, double* out,

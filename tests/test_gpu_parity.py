@@ -376,24 +376,32 @@ def test_filter_and_oc_kernels_match_oracle():
     solver.close()
 
 
-@pytest.mark.parametrize("sdim,n,nt,tc", [(2, 64, 64, True), (2, 32, 64, False), (3, 8, 16, True)])
+@pytest.mark.parametrize("sdim,n,nt,tc", [(2, 64, 64, True), (2, 32, 64, False), (3, 8, 16, True), (2, 64, 32, False)])
 def test_fused_small_level_vcycle_equals_per_level_launches(sdim, n, nt, tc, monkeypatch):
-    """The cluster kernel that runs the small-level tail of the V-cycle (vsmall.cu) is the same
-    linear map as the per-level launches (up to summation order), forward and adjoint."""
+    """The fused small-level tails of the V-cycle (vsmall.cu) are the same linear map as the
+    per-level launches (up to summation order), forward and adjoint: the single-CTA shared-memory
+    tail (opt-in ST_VTAIL=1, `launch_vtail`) and the opt-in cluster kernel (ST_VSMALL=1); the
+    shared-memory tail also launches fewer kernels per V-cycle than the per-level path."""
     rho = _rho(sdim, n, nt, "uniform", 6, tc)
     x = I.rand_vector((n + 1) ** sdim * (nt + 1), 12)
-    outs = []
-    for flag in ("0", "1"):
-        monkeypatch.setenv("ST_VSMALL", flag)
-        solver, prob = make_pair(sdim, n, nt, mats=CFG4_MATS, time_constant=tc, coarse_max_nodes=64)
+    outs, launches = {}, {}
+    for name, vtail, vsmall in (("per-level", "0", "0"), ("smem-tail", "1", "0"), ("cluster", "0", "1")):
+        monkeypatch.setenv("ST_VTAIL", vtail)
+        monkeypatch.setenv("ST_VSMALL", vsmall)
+        solver, prob = make_pair(sdim, n, nt, mats=CFG4_MATS, time_constant=tc, coarse_max_nodes=64, use_graphs=0)
         z = torch.empty(x.size, dtype=torch.float64, device=DEV)
         zt = torch.empty_like(z)
         solver.vcycle(dev(rho), dev(x), z)
+        k0 = solver.kernel_launches()
+        solver.vcycle(dev(rho), dev(x), z)
+        launches[name] = solver.kernel_launches() - k0
         solver.vcycle(dev(rho), dev(x), zt, transpose=True)
-        outs.append((host(z), host(zt)))
+        outs[name] = (host(z), host(zt))
         solver.close()
-    assert rel(outs[1][0], outs[0][0]) <= 1e-12
-    assert rel(outs[1][1], outs[0][1]) <= 1e-12
+    for name in ("smem-tail", "cluster"):
+        assert rel(outs[name][0], outs["per-level"][0]) <= 1e-12, name
+        assert rel(outs[name][1], outs["per-level"][1]) <= 1e-12, name
+    assert launches["smem-tail"] < launches["per-level"], launches
 
 
 @pytest.mark.parametrize("sdim,n,nt,tc", [(2, 12, 10, False), (3, 4, 6, True)])
