@@ -54,8 +54,10 @@ METRIC = "space-time DOFs solved/sec (FGMRES+MG to rtol 1e-8) & operator GB/s vs
 
 
 def solver_opts(args):
-    nu = args.nu or (10 if args.smoother == "gmres" else 3)
+    nu = args.nu or (10 if args.smoother == "gmres" else 4)  # 4: the library default
     o = dict(smoother=2 if args.smoother == "gmres" else 0, nu_pre=nu, nu_post=nu)
+    if args.omega > 0:
+        o["omega"] = args.omega
     if args.full_coarsening:
         o["full_coarsening"] = 1
     return o
@@ -73,8 +75,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--smoother", default="jacobi", choices=["jacobi", "gmres"],
                     help="jacobi: damped Jacobi nu+nu (default); gmres: the paper's GMRES(nu)-Jacobi smoother")
-    ap.add_argument("--nu", type=int, default=0, help="sweeps / GMRES steps (default 3 for jacobi, 10 for gmres)")
+    ap.add_argument("--nu", type=int, default=0, help="sweeps / GMRES steps (default 4 for jacobi, 10 for gmres)")
     ap.add_argument("--full-coarsening", action="store_true", help="the paper's full space-time coarsening")
+    ap.add_argument("--omega", type=float, default=0.0, help="Jacobi weight cap (default: the library's 0.75)")
     ap.add_argument("--cpu-worker", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--cpu-reps", type=int, default=1, help=argparse.SUPPRESS)
     return ap.parse_args()

@@ -172,7 +172,7 @@ typedef struct {
   double lam_max[32];        /* Gershgorin bound on |lambda|_max(D^-1 A)     */
 } st_hierarchy_t;
 
-/* Fill `o` with the library defaults (rtol 1e-8, restart 16, Jacobi nu 3/3 omega 0.75,
+/* Fill `o` with the library defaults (rtol 1e-8, restart 16, Jacobi nu 4/4, weight cap 0.75,
  * lambda_crit 0.5, coarse_max_nodes 400, agg_nodes 16384). */
 void st_default_options(st_options_t* o);
 

@@ -1154,8 +1154,8 @@ void st_default_options(st_options_t* o) {
   o->maxit = 500;
   o->restart = 16;
   o->smoother = ST_SMOOTH_JACOBI;
-  o->nu_pre = 3;   // measured sweep on config 2 / a config-3-like grid
-  o->nu_post = 3;
+  o->nu_pre = 4;   // measured sweep over configs 2-5 (profiles/r01/nu_sweep.log)
+  o->nu_post = 4;
   o->omega = 0.75;
   o->lambda_crit = 0.5;
   o->coarse_max_nodes = 400;
