@@ -91,6 +91,7 @@ struct st_ctx {
   double* hsmall = nullptr;
   double* rho_stage = nullptr;
   double* kt = nullptr;          // padded k~ table of a (2+1)D space-time design (launch_ktilde; tv2d)
+  bool kt_design = false;        // kt belongs to the cached design (rho_ck); test hooks may rebuild it
   double* io_stage[4] = {nullptr, nullptr, nullptr, nullptr};
   long long io_n[4] = {0, 0, 0, 0};
   double rho_ck[2] = {0.0, 0.0};
@@ -568,7 +569,7 @@ bool bind_rho(st_ctx* c, const double* rho_in) {
     CK(cudaMemcpyAsync(c->rho_stage, rho_in, c->ndesign * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     rho = c->rho_stage;
   }
-  set_fine_rho(c, rho);
+  c->lv[0].op.rho = rho;  // the per-design tables follow in prepare() when rho changed
   launch_checksum(rho, c->ndesign, c->dsmall + 500, c->ws, c->stream);
   L(c);
   allreduce(c, c->dsmall + 500, 2);  // one decision on every rank
@@ -723,7 +724,12 @@ void build_ops(st_ctx* c) {
 }
 
 void prepare(st_ctx* c, const double* rho) {
-  if (bind_rho(c, rho)) build_ops(c);
+  const bool changed = bind_rho(c, rho);
+  if (changed || !c->kt_design) {  // k~ table (once per design, not per call)
+    set_fine_rho(c, c->lv[0].op.rho);
+    c->kt_design = true;
+  }
+  if (changed) build_ops(c);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1381,6 +1387,7 @@ int st_apply(st_ctx_t* c, const double* rho, const double* x, double* y, int tra
       r = c->rho_stage;
     }
     set_fine_rho(c, r);
+    c->kt_design = false;  // the table now follows r, not necessarily the cached design
     pack_in(c, x, c->tmpN, 1, true);
     masked_level_apply(c, 0, c->tmpN, c->tmpN2, c->lv[0].t, transpose != 0, bc != 0);
     unpack_out(c, c->lv[0].t, y, 2);
@@ -1591,7 +1598,10 @@ int st_bench_op(st_ctx_t* c, const double* rho, int level, int mode, int transpo
     CK(cudaSetDevice(c->device));
     if (level == 0) {
       if (!is_device_ptr(rho)) throw StErr{ST_E_INVALID_ARG, "rho must be a device pointer"};
-      if (c->lv[0].op.rho != rho || (c->kt && !c->lv[0].op.kt)) set_fine_rho(c, rho);  // st.h: same pointer = same rho
+      if (c->lv[0].op.rho != rho || (c->kt && !c->lv[0].op.kt)) {  // st.h: same pointer = same rho
+        set_fine_rho(c, rho);
+        c->kt_design = false;
+      }
     } else {
       prepare(c, rho);
     }

@@ -72,8 +72,13 @@ template <bool FACE0> __host__ __device__ constexpr int kslot(int k) {
 }
 
 // SRC: 0 = fine level from rho (time-constant design), 1 = stored MK stencils (nl = 1)
+#ifndef ST_TC3D_MINB
+#define ST_TC3D_MINB 2  // resident CTAs per SM of the fine-level variants (register cap 128); 1 CTA
+                        // (184 registers) with the 27 window loads batched ahead of the FMAs
+                        // measured slower: 634 vs ~580 us per config-4 sweep
+#endif
 template <int SRC, int MODE, bool TRANS>
-__global__ void __launch_bounds__(NTH, SRC == 0 ? 2 : 1)
+__global__ void __launch_bounds__(NTH, SRC == 0 ? ST_TC3D_MINB : 1)
     tc3d_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, OpDesc op,
                 const double* __restrict__ x, double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx,
                 int nty) {

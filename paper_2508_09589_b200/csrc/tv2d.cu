@@ -498,12 +498,15 @@ void ltv(const CUtensorMap& mx, const CUtensorMap& mb, const CUtensorMap& ml, co
   const long long minw = (wtot >= 16LL * nsm * resident) ? 4 : 1;
   if (grid > wtot / minw) grid = wtot / minw;
   if (grid < 1) grid = 1;
-  // plane chunks: with more tiles than CTAs the contiguous split leaves neighbouring tiles at
+  // plane chunks: with long per-CTA plane runs the contiguous split leaves neighbouring tiles at
   // unrelated planes (halo re-reads from DRAM: 1.77x the algorithmic bytes at 512^2 x 512);
-  // sliced 16-plane chunks keep them together (ST_CHUNK_K overrides)
+  // sliced chunks keep them together — 16 planes on the fine level, 32 on the stored-stencil
+  // levels (heavier restarts). Measured (profiles/r01/kbench_tv2d_sliced.log, tv2d_src1_chunk.log):
+  // 512^2 x 512 fine 1475 -> 1129 us, level 1 657 -> 553 us; with short runs (< 256 planes per CTA:
+  // 256^3 levels 0 / 1, 512^2 level 2) the restarts cost more than they save. ST_CHUNK_K overrides.
   const int NPl = g.nt + 1;
   int kch = chunk_planes(g.P, NPl, g.sd);
-  if (kch >= NPl && !getenv("ST_CHUNK_K") && ntx * nty > grid) kch = 16;
+  if (kch >= NPl && !getenv("ST_CHUNK_K") && wtot / grid >= 256) kch = SRC == 0 ? 16 : 32;
   kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, ml, op, x, y, omega, wtot, kch, (int)ntx,
                                                        tile_order());
 }

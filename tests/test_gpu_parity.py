@@ -423,3 +423,23 @@ def test_pnorm_objective_and_adjoint_rhs(sdim, n, nt, tc):
     lam_ref = prob.adjoint(rho, g_ref)
     assert rel(host(lam), lam_ref) <= 1e-8
     solver.close()
+
+
+def test_per_design_tables_follow_the_design_across_hooks():
+    """The per-design k~ table of a space-time design (tv2d) is rebuilt when rho changes and is not
+    left stale by a test hook that binds another rho: solve(A), apply(B), solve(A) gives the first
+    solution again, and solve(B) the oracle's solution for B."""
+    solver, prob = make_pair(2, 32, 16, rtol=1e-10, maxit=400)
+    ra = I.rho_uniform((16, 32, 32), 1)
+    rb = I.rho_uniform((16, 32, 32), 2)
+    T1 = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+    solver.solve(dev(ra), T1)
+    y = torch.empty_like(T1)
+    solver.apply(dev(rb), dev(I.rand_vector(prob.mesh.n_nodes, 3)), y)
+    T2 = torch.zeros_like(T1)
+    solver.solve(dev(ra), T2)
+    assert rel(host(T2), host(T1)) <= 1e-12
+    T3 = torch.zeros_like(T1)
+    solver.solve(dev(rb), T3)
+    assert rel(host(T3), prob.forward(rb)) <= 1e-8
+    solver.close()
