@@ -304,8 +304,11 @@ def run_cuda(args):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
-        if tj.get("config") == args.config:
-            traffic = tj.get("traffic_bytes_per_launch")
+        ent = tj.get("configs", {}).get(str(args.config))
+        if ent is None and tj.get("config") == args.config:
+            ent = tj
+        if ent is not None:
+            traffic = ent.get("traffic_bytes_per_launch")
 
     # ---- end-to-end through the C ABI with pinned host buffers ------------------------------
     e2e = None
