@@ -115,6 +115,7 @@ struct st_ctx {
   int vs0 = -1;
   // single-CTA shared-memory tail (vsmall.cu, launch_vtail): levels >= vt0 in one launch (-1: off)
   int vt0 = -1;
+  bool pro_fuse = true;  // prolongation fused into the first post-sweep (ST_NO_PRO=1: off)
   double* gsm = nullptr;  // GMRES smoother: device Hessenberg / Givens / dots scratch (1024 doubles)
   // config-5 design update buffers (st_filter / st_oc_update), allocated on first use
   double *fbuf = nullptr, *fw = nullptr;
@@ -404,6 +405,10 @@ void allocate(st_ctx* c) {
   // vs 482.6 MDOF/s; config 3 shape: 393.5 vs 398.3; profiles/r01/vtail_ab.log) — one SM runs the
   // tail's sweeps slower than 148 SMs run them inside the graph, whose launches cost far less than
   // the ~6 us of an eager launch
+  {
+    const char* e = getenv("ST_NO_PRO");
+    c->pro_fuse = !(e && e[0] == '1');
+  }
   c->vt0 = -1;
   {
     const char* e = getenv("ST_VTAIL");
@@ -894,10 +899,20 @@ void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_gr
     L(c);
   }
   vcycle(c, l + 1, trans, Nx.b, Nx.x, in_graph);
-  launch_prolong_add(Lv.g, Nx.g, Nx.kind, Nx.x, cur, c->stream);
-  L(c);
-  if (npost == 0) halo(c, l, cur);
-  for (int s = 0; s < npost; ++s) {
+  // prolongation + correction, fused into the first post-sweep where the level kernel can read
+  // x + P e itself (tc2d, space-coarsened next level, one GPU; ST_NO_PRO=1: separate kernels)
+  int s0 = 0;
+  if (npost > 0 && c->pro_fuse && Nx.kind == KIND_SPACE && c->comm.size <= 1 && c->fast && c->fast_kind == 0 &&
+      launch_op_tc2d_pro(Lv.op, Nx.g, trans, cur, Nx.x, b, oth, Lv.omega > 0.0 ? Lv.omega : c->opt.omega, c->stream)) {
+    L(c);
+    std::swap(cur, oth);
+    s0 = 1;
+  } else {
+    launch_prolong_add(Lv.g, Nx.g, Nx.kind, Nx.x, cur, c->stream);
+    L(c);
+    if (npost == 0) halo(c, l, cur);
+  }
+  for (int s = s0; s < npost; ++s) {
     op_launch(c, l, MODE_JAC, trans, true, cur, b, oth);
     halo(c, l, oth);
     std::swap(cur, oth);

@@ -17,6 +17,9 @@ bool launch_op_tma2d(const OpDesc& op, int mode, bool trans, bool mask, const do
 // tc2d.cu: lean TMA kernel for time-constant levels (fine from rho, stored MK), masked modes
 bool launch_op_tc2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                     double omega, cudaStream_t s);
+// damped-Jacobi sweep from x + P e, e the correction of a space-coarsened next level (2D, one GPU)
+bool launch_op_tc2d_pro(const OpDesc& op, const Geom& gc, bool trans, const double* x, const double* e,
+                        const double* b, double* y, double omega, cudaStream_t s);
 // tc3d.cu: (3+1)D TMA kernel for time-constant levels (fine from rho, stored MK), masked modes
 bool launch_op_tc3d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                     double omega, cudaStream_t s);

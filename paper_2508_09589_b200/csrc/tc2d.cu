@@ -45,6 +45,10 @@ constexpr int XS = 368, BS = 256;                        // slot sizes (doubles)
 constexpr int NB = 6;
 constexpr int NTH = TX * TYT;
 constexpr unsigned XBYTES = HX * HY * 8, BBYTES = TX * TY * 8;
+// prolongation fused into a Jacobi sweep (PRO): the coarse correction box of a space-coarsened
+// next level, coarse nodes (x0/2 - 2 .. x0/2 + 17) x (y0/2 - 1 .. y0/2 + 4) of the same time plane
+constexpr int EW = 20, EH = 6, ES = 128;
+constexpr unsigned EBYTES = EW * EH * 8;
 
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned cnt) {
@@ -87,10 +91,14 @@ __device__ __forceinline__ double ap9(const double (&w)[9], const double (&nb)[R
 }
 
 // SRC: 0 = fine level from rho (time-constant design), 1 = stored MK stencils (nl = 1)
-template <int SRC, bool CUNI, int MODE, bool TRANS>
+// PRO (MODE_JAC only): x + P e instead of x, e the correction of the space-coarsened next level
+// (tme: its TMA map) — the V-cycle's prolongation + correction fused into the first post-sweep
+template <int SRC, bool CUNI, int MODE, bool TRANS, bool PRO = false>
 __global__ void __launch_bounds__(NTH, CUNI ? ST_TC2D_MINB : 3)
-    tc2d_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, OpDesc op,
-                const double* __restrict__ x, double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx) {
+    tc2d_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
+                const __grid_constant__ CUtensorMap tme, OpDesc op, const double* __restrict__ x,
+                double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx) {
+  static_assert(!PRO || MODE == MODE_JAC, "prolongation is fused into Jacobi sweeps only");
   constexpr bool NX = (MODE != MODE_JAC0);
   constexpr bool NBV = (MODE != MODE_APPLY);
   constexpr bool ND = (MODE == MODE_JAC || MODE == MODE_JAC0);
@@ -98,6 +106,7 @@ __global__ void __launch_bounds__(NTH, CUNI ? ST_TC2D_MINB : 3)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   double* xs = smem + 16;                    // [NB][XS]
   double* bs = xs + (NX ? NB * XS : 0);      // [NB][BS]
+  double* es = bs + (NBV ? NB * BS : 0);     // [NB][ES] (PRO)
 
   const Geom& g = op.g;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
@@ -116,7 +125,7 @@ __global__ void __launch_bounds__(NTH, CUNI ? ST_TC2D_MINB : 3)
   const double sm = (SRC == 0) ? g.dx * g.dx * (1.0 / 36.0) * (CUNI ? op.m.Cins : 1.0) : (CUNI ? op.msc : 1.0);
   const double sk = (SRC == 0) ? (1.0 / 6.0) : 1.0;
   const double t00 = op.Tm[0][0] * sk, t01 = op.Tm[0][1] * sk, t11 = op.Tm[1][1] * sk;
-  const unsigned tx_full = (NX ? XBYTES : 0u) + (NBV ? BBYTES : 0u);
+  const unsigned tx_full = (NX ? XBYTES : 0u) + (NBV ? BBYTES : 0u) + (PRO ? EBYTES : 0u);
 
   long long w = wtot * blockIdx.x / gridDim.x;
   const long long wend = wtot * (blockIdx.x + 1) / gridDim.x;
@@ -139,6 +148,7 @@ __global__ void __launch_bounds__(NTH, CUNI ? ST_TC2D_MINB : 3)
         const bool wb = NBV && q >= p0 && q < p1;
         mbar_expect_tx(&bar[slot], tx_full - ((NBV && !wb) ? BBYTES : 0u));
         if (NX) tma3(xs + slot * XS, &tmx, &bar[slot], x0, y0, q);
+        if (PRO) tma3(es + slot * ES, &tme, &bar[slot], x0 >> 1, y0 >> 1, q);
         if (wb) tma3(bs + slot * BS, &tmb, &bar[slot], x0, y0, q);
       }
     }
@@ -219,6 +229,26 @@ __global__ void __launch_bounds__(NTH, CUNI ? ST_TC2D_MINB : 3)
     for (int q = qs; q <= qe; ++q) {
       mbar_wait(&bar[cur], (phase >> cur) & 1u);
       phase ^= 1u << cur;
+      if (PRO && q + g.pg0 > 0) {
+        // x += P e on the tile's in-domain, unconstrained nodes (the same weights and order as
+        // prolong2s_kernel); rows / columns outside the domain keep their zero or aliased values
+        double* xt = xs + cur * XS;
+        const double* et = es + cur * ES;
+        for (int e = tid; e < HY * (TX + 2); e += NTH) {
+          const int sr = e / (TX + 2), c = 1 + e % (TX + 2);
+          const int ii = x0 - 2 + c, jj = y0 - 1 + sr;
+          if (ii < 0 || ii > n || jj < 0 || jj > n) continue;
+          if (ii == 0 && jj >= g.plo && jj <= g.phi) continue;  // sink patch
+          const double* e0 = et + ((jj >> 1) - (y0 >> 1) + 1) * EW + ((ii >> 1) - (x0 >> 1) + 2);
+          double v;
+          if (!(ii & 1) && !(jj & 1)) v = e0[0];
+          else if (!(jj & 1)) v = 0.5 * (e0[0] + e0[1]);
+          else if (!(ii & 1)) v = 0.5 * (e0[0] + e0[EW]);
+          else v = 0.25 * ((e0[0] + e0[1]) + (e0[EW] + e0[EW + 1]));
+          xt[sr * HX + c] += v;
+        }
+        __syncthreads();
+      }
       double Mq[RY], Kq[RY];  // Mq without the scale sm
       if (NX && q + g.pg0 > 0) {
         double nb[RY + 2][3];
@@ -287,6 +317,7 @@ __global__ void __launch_bounds__(NTH, CUNI ? ST_TC2D_MINB : 3)
         const bool wb = NBV && qn >= p0 && qn < p1;
         mbar_expect_tx(&bar[prv], tx_full - ((NBV && !wb) ? BBYTES : 0u));
         if (NX) tma3(xs + prv * XS, &tmx, &bar[prv], x0, y0, qn);
+        if (PRO) tma3(es + prv * ES, &tme, &bar[prv], x0 >> 1, y0 >> 1, qn);
         if (wb) tma3(bs + prv * BS, &tmb, &bar[prv], x0, y0, qn);
       }
       yrow += P;
@@ -346,14 +377,14 @@ bool map3_tc(CUtensorMap* m, const void* base, unsigned long long d0, unsigned l
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int SRC, bool CUNI, int MODE, bool TRANS>
+template <int SRC, bool CUNI, int MODE, bool TRANS, bool PRO = false>
 void ltc(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, const double* x, double* y, double omega,
-         cudaStream_t s) {
+         cudaStream_t s, const CUtensorMap* me = nullptr) {
   using namespace tc;
   const Geom& g = op.g;
-  auto kern = tc2d_kernel<SRC, CUNI, MODE, TRANS>;
+  auto kern = tc2d_kernel<SRC, CUNI, MODE, TRANS, PRO>;
   constexpr bool NX = (MODE != MODE_JAC0), NBV = (MODE != MODE_APPLY);
-  constexpr size_t bytes = sizeof(double) * (16 + (NX ? NB * XS : 0) + (NBV ? NB * BS : 0));
+  constexpr size_t bytes = sizeof(double) * (16 + (NX ? NB * XS : 0) + (NBV ? NB * BS : 0) + (PRO ? NB * ES : 0));
   static int resident = 0, nsm = 0;
   if (!resident) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -371,7 +402,8 @@ void ltc(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, const d
   const long long minw = (wtot >= 16LL * nsm * resident) ? 4 : 1;
   if (grid > wtot / minw) grid = wtot / minw;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, op, x, y, omega, wtot, chunk_planes(g.P, g.nt + 1, g.sd), (int)ntx);
+  kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, me ? *me : mx, op, x, y, omega, wtot,
+                                                       chunk_planes(g.P, g.nt + 1, g.sd), (int)ntx);
 }
 
 template <int SRC, bool CUNI>
@@ -414,6 +446,36 @@ bool launch_op_tc2d(const OpDesc& op, int mode, bool trans, bool mask, const dou
   else if (rho_tc) ltc_modes<0, false>(mx, mb, op, mode, trans, x, y, omega, s);
   else if (op.msep) ltc_modes<1, true>(mx, mb, op, mode, trans, x, y, omega, s);
   else ltc_modes<1, false>(mx, mb, op, mode, trans, x, y, omega, s);
+  return true;
+}
+
+// Damped-Jacobi sweep from x + P e (the V-cycle's prolongation + correction fused into the first
+// post-smoothing sweep): e is the correction of the next level gc, a space coarsening of this one
+// (same time planes, one GPU). false if not covered (then: prolongation kernel + plain sweep).
+bool launch_op_tc2d_pro(const OpDesc& op, const Geom& gc, bool trans, const double* x, const double* e,
+                        const double* b, double* y, double omega, cudaStream_t s) {
+  const Geom& g = op.g;
+  if (g.sd != 2 || gc.nt != g.nt || gc.nn != g.n / 2 + 1 || g.pg0 != 0 || gc.pg0 != 0) return false;
+  const bool rho_tc = (op.form == FORM_RHO && op.rho_tc), mk_tc = (op.form == FORM_MK && !op.tvl);
+  if (!rho_tc && !mk_tc) return false;
+  if (op.U[0][0] != 0.0 || op.U[0][1] != 0.0 || op.U[1][0] != -1.0 || op.U[1][1] != 1.0) return false;
+  if (op.Tm[0][1] != op.Tm[1][0]) return false;
+  CUtensorMap mx{}, mb{}, me{};
+  const unsigned long long nn = g.nn, s1 = (unsigned long long)g.pr * 8, s2 = (unsigned long long)g.P * 8;
+  if (!map3_tc(&mx, x - (g.pr + 2), (unsigned long long)g.pr + 2, nn + 1, g.nt + 1, s1, s2, tc::HX, tc::HY)) return false;
+  if (!map3_tc(&mb, b, nn, nn, g.nt + 1, s1, s2, tc::TX, tc::TY)) return false;
+  // e: based like x (guarded internal vector): coordinate (X, Y, q) is coarse node (X - 2, Y - 1)
+  if (!map3_tc(&me, e - (gc.pr + 2), (unsigned long long)gc.pr + 2, (unsigned long long)gc.nn + 1, gc.nt + 1,
+               (unsigned long long)gc.pr * 8, (unsigned long long)gc.P * 8, tc::EW, tc::EH))
+    return false;
+#define PR(SRC, CU)                                                                          \
+  if (trans) ltc<SRC, CU, MODE_JAC, true, true>(mx, mb, op, x, y, omega, s, &me);            \
+  else ltc<SRC, CU, MODE_JAC, false, true>(mx, mb, op, x, y, omega, s, &me);
+  if (rho_tc && op.m.dC == 0.0) { PR(0, true) }
+  else if (rho_tc) { PR(0, false) }
+  else if (op.msep) { PR(1, true) }
+  else { PR(1, false) }
+#undef PR
   return true;
 }
 
