@@ -116,6 +116,11 @@ struct st_ctx {
   // single-CTA shared-memory tail (vsmall.cu, launch_vtail): levels >= vt0 in one launch (-1: off)
   int vt0 = -1;
   bool pro_fuse = true;  // prolongation fused into the first post-sweep (ST_NO_PRO=1: off)
+  // DGKS: re-orthogonalise when ||w'||^2 < eta^2 ||w||^2. eta = 0.1: with the V-cycle preconditioner
+  // ||w'|| / ||w|| stays above it, and the measured iteration counts and true residuals equal those of
+  // eta^2 = 0.5 (which re-orthogonalised every step) on configs 2-4 (profiles/r01/dgks_threshold.log);
+  // the pass remains a safety net for severe cancellation. ST_DGKS_ETA2 overrides.
+  double dgks_eta2 = 0.01;
   double* gsm = nullptr;  // GMRES smoother: device Hessenberg / Givens / dots scratch (1024 doubles)
   // config-5 design update buffers (st_filter / st_oc_update), allocated on first use
   double *fbuf = nullptr, *fw = nullptr;
@@ -408,6 +413,8 @@ void allocate(st_ctx* c) {
   {
     const char* e = getenv("ST_NO_PRO");
     c->pro_fuse = !(e && e[0] == '1');
+    e = getenv("ST_DGKS_ETA2");
+    if (e) c->dgks_eta2 = atof(e);
   }
   c->vt0 = -1;
   {
@@ -926,7 +933,7 @@ void sync_small(st_ctx* c, int off, int n) {
 
 // FGMRES(m), right preconditioned by one V-cycle (Saad 1993). Classical
 // Gram-Schmidt (fused multi-dot + fused multi-AXPY) with one conditional re-orthogonalisation
-// (DGKS). Convergence on the TRUE relative residual ||b - A x|| / ||b|| <= rtol (R-14).
+// (DGKS, eta = 0.1: st_ctx::dgks_eta2). Convergence on the TRUE relative residual ||b - A x|| / ||b|| <= rtol (R-14).
 // The Arnoldi vectors are stored unnormalised, v_i = sg_i V_i: the V-cycle and the operator are
 // linear, so z_j = sg_j M V_j and A z_j = sg_j A (M V_j), and every scale is folded into the
 // host-side Hessenberg / the device-side AXPY weights (no separate scaling pass over memory).
@@ -997,7 +1004,7 @@ int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
       double* hcol = &H[(size_t)j * (m + 1)];
       for (int i = 0; i <= j; ++i) hcol[i] = sg[i] * sg[j] * hh[i];  // h_ij = v_i . (A z_j)
       double ww = hh[j + 1], w2 = fused ? hh[64 + j + 1] : hh[196];
-      if (w2 < 0.5 * ww) {  // DGKS re-orthogonalisation
+      if (w2 < c->dgks_eta2 * ww) {  // DGKS re-orthogonalisation
         if (!fused) {
           launch_mdot(w + vo, c->V + vo, ld, j + 1, N, dh + 64, c->ws, c->stream);
           allreduce(c, dh + 64, j + 1);
