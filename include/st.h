@@ -104,6 +104,9 @@ typedef struct {
   int32_t verbose;
   int64_t agg_nodes;        /* time slabs: agglomerate a level once it has fewer than this
                                many nodes per rank (default 16384)                          */
+  int32_t nu_coarse;        /* Jacobi sweeps (pre = post) on the coarse levels; 0 = nu_pre /
+                               nu_post there too (default 5; nu_pre = nu_post = 2 on the fine
+                               level: DESIGN.md sec. 9)                                     */
 } st_options_t;
 
 /* Distribution over time slabs. NULL or size == 1 => one GPU.
@@ -172,7 +175,7 @@ typedef struct {
   double lam_max[32];        /* Gershgorin bound on |lambda|_max(D^-1 A)     */
 } st_hierarchy_t;
 
-/* Fill `o` with the library defaults (rtol 1e-8, restart 16, Jacobi nu 4/4, weight cap 0.75,
+/* Fill `o` with the library defaults (rtol 1e-8, restart 16, Jacobi nu 2/2 on the fine level and 5/5 on the coarse levels, weight cap 0.75,
  * lambda_crit 0.5, coarse_max_nodes 400, agg_nodes 16384). */
 void st_default_options(st_options_t* o);
 

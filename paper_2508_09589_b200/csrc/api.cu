@@ -415,6 +415,7 @@ void allocate(st_ctx* c) {
     c->pro_fuse = !(e && e[0] == '1');
     e = getenv("ST_DGKS_ETA2");
     if (e) c->dgks_eta2 = atof(e);
+
   }
   c->vt0 = -1;
   {
@@ -833,8 +834,8 @@ void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_gr
   if (l == c->vt0 && b == Lv.b && x == Lv.x) {  // the small-level tail: one CTA, shared memory
     SmallCycle cyc{};
     cyc.nlev = (int)c->lv.size() - l;
-    cyc.npre = c->opt.nu_pre;
-    cyc.npost = c->opt.nu_post;
+    cyc.npre = c->opt.nu_coarse > 0 ? c->opt.nu_coarse : c->opt.nu_pre;    // the tail holds coarse levels
+    cyc.npost = c->opt.nu_coarse > 0 ? c->opt.nu_coarse : c->opt.nu_post;
     for (int k = 0; k < cyc.nlev; ++k) {
       const Level& S = c->lv[l + k];
       SmallLevel& d = cyc.L[k];
@@ -853,8 +854,8 @@ void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_gr
   if (l == c->vs0 && b == Lv.b && x == Lv.x) {  // the small-level tail: one cluster kernel
     SmallCycle cyc{};
     cyc.nlev = (int)c->lv.size() - l;
-    cyc.npre = c->opt.nu_pre;
-    cyc.npost = c->opt.nu_post;
+    cyc.npre = c->opt.nu_coarse > 0 ? c->opt.nu_coarse : c->opt.nu_pre;    // the tail holds coarse levels
+    cyc.npost = c->opt.nu_coarse > 0 ? c->opt.nu_coarse : c->opt.nu_post;
     for (int k = 0; k < cyc.nlev; ++k) {
       const Level& S = c->lv[l + k];
       SmallLevel& d = cyc.L[k];
@@ -888,7 +889,8 @@ void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_gr
     gmres_smooth(c, l, trans, b, x, false);
     return;
   }
-  const int npre = c->opt.nu_pre, npost = c->opt.nu_post;
+  const int npre = (l > 0 && c->opt.nu_coarse > 0) ? c->opt.nu_coarse : c->opt.nu_pre;
+  const int npost = (l > 0 && c->opt.nu_coarse > 0) ? c->opt.nu_coarse : c->opt.nu_post;
   const int total = npre + npost;
   double* cur = (total % 2 == 1) ? x : Lv.t;
   double* oth = (cur == x) ? Lv.t : x;
@@ -1186,8 +1188,11 @@ void st_default_options(st_options_t* o) {
   o->maxit = 500;
   o->restart = 16;
   o->smoother = ST_SMOOTH_JACOBI;
-  o->nu_pre = 4;   // measured sweep over configs 2-5 (profiles/r01/nu_sweep.log)
-  o->nu_post = 4;
+  // measured over configs 2-5 (profiles/r01/nu_sweep.log, nu_split*.log): the
+  // fine-level sweeps are the expensive ones, the coarse ones buy the convergence
+  o->nu_pre = 2;
+  o->nu_post = 2;
+  o->nu_coarse = 5;
   o->omega = 0.75;
   o->lambda_crit = 0.5;
   o->coarse_max_nodes = 400;
@@ -1249,7 +1254,8 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       if (opts) c->opt = *opts;
       else st_default_options(&c->opt);
       if (c->opt.restart < 1 || c->opt.restart > 60) throw StErr{ST_E_INVALID_ARG, "restart must be in [1, 60]"};
-      if (c->opt.nu_pre < 1 || c->opt.nu_post < 0) throw StErr{ST_E_INVALID_ARG, "nu_pre >= 1, nu_post >= 0"};
+      if (c->opt.nu_pre < 1 || c->opt.nu_post < 0 || c->opt.nu_coarse < 0)
+        throw StErr{ST_E_INVALID_ARG, "nu_pre >= 1, nu_post >= 0, nu_coarse >= 0"};
       if (c->opt.smoother != ST_SMOOTH_JACOBI && c->opt.smoother != ST_SMOOTH_GMRES)
         throw StErr{ST_E_UNSUPPORTED, "smoother: ST_SMOOTH_JACOBI or ST_SMOOTH_GMRES"};
       if (c->opt.smoother == ST_SMOOTH_GMRES && (c->opt.nu_pre > 24 || c->opt.nu_post > 24))

@@ -40,7 +40,7 @@ class Options(C.Structure):
                 ("smoother", C.c_int32), ("nu_pre", C.c_int32), ("nu_post", C.c_int32), ("omega", C.c_double),
                 ("lambda_crit", C.c_double), ("coarse_max_nodes", C.c_int64), ("max_levels", C.c_int32),
                 ("full_coarsening", C.c_int32), ("use_graphs", C.c_int32), ("verbose", C.c_int32),
-                ("agg_nodes", C.c_int64)]
+                ("agg_nodes", C.c_int64), ("nu_coarse", C.c_int32)]
 
 
 ST_COMM_NONE, ST_COMM_NCCL, ST_COMM_HOST = 0, 1, 2
@@ -287,6 +287,10 @@ class Solver:
         self._check(self.lib.st_setup(C.byref(self.grid), C.byref(self.mats), C.byref(self.bcs),
                                       C.byref(self.src), C.byref(o), C.byref(d), C.byref(h)))
         self.ctx = h
+
+    def options(self):
+        """The st_options_t this context was set up with (library defaults + the caller's overrides)."""
+        return {name: getattr(self.opts, name) for name, _ in Options._fields_}
 
     def _check(self, rc, allow_nc=False):
         if rc == ST_OK or (allow_nc and rc == ST_E_NOT_CONVERGED):

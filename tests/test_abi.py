@@ -35,7 +35,7 @@ def test_default_options_and_errors():
     lib = st.load_library()
     o = st.Options()
     lib.st_default_options(ctypes.byref(o))
-    assert o.rtol == 1e-8 and o.lambda_crit == 0.5 and o.restart == 16 and o.nu_pre == 4 and o.nu_post == 4
+    assert o.rtol == 1e-8 and o.lambda_crit == 0.5 and o.restart == 16 and o.nu_pre == 2 and o.nu_post == 2 and o.nu_coarse == 5
     assert lib.st_abi_version() == 2
     assert lib.st_strerror(-2).decode().startswith("grid not divisible")
 
