@@ -121,6 +121,10 @@ struct st_ctx {
   // eta^2 = 0.5 (which re-orthogonalised every step) on configs 2-4 (profiles/r01/dgks_threshold.log);
   // the pass remains a safety net for severe cancellation. ST_DGKS_ETA2 overrides.
   double dgks_eta2 = 0.01;
+  // small 2D time-constant levels as one thread per node (tiny2d.cu) up to this many nodes; opt-in
+  // (ST_TINY_NODES): inside the V-cycle's graph the TMA kernels cost no more (config 2: 633.9 MDOF/s
+  // off, 635.2 at <= 20000 nodes, 619.9 at <= 300000; profiles/r01/tiny2d_ab.log)
+  long long tiny_nodes = 0;
   double* gsm = nullptr;  // GMRES smoother: device Hessenberg / Givens / dots scratch (1024 doubles)
   // config-5 design update buffers (st_filter / st_oc_update), allocated on first use
   double *fbuf = nullptr, *fw = nullptr;
@@ -415,6 +419,8 @@ void allocate(st_ctx* c) {
     c->pro_fuse = !(e && e[0] == '1');
     e = getenv("ST_DGKS_ETA2");
     if (e) c->dgks_eta2 = atof(e);
+    e = getenv("ST_TINY_NODES");
+    if (e) c->tiny_nodes = atoll(e);
 
   }
   c->vt0 = -1;
@@ -538,6 +544,12 @@ void allocate(st_ctx* c) {
 void op_launch(st_ctx* c, int l, int mode, bool trans, bool mask, const double* x, const double* b, double* y) {
   g_use_fast = c->fast;
   g_fast_kind = c->fast_kind;
+  const Level& Lv = c->lv[l];
+  if (c->fast && l > 0 && !Lv.dist && nodes_of(Lv.g) <= c->tiny_nodes &&
+      launch_op_tiny2d(Lv.op, mode, trans, mask, x, b, y, Lv.omega > 0.0 ? Lv.omega : c->opt.omega, c->stream)) {
+    L(c);
+    return;
+  }
   launch_op(c->lv[l].op, mode, trans, mask, x, b, y, c->lv[l].omega > 0.0 ? c->lv[l].omega : c->opt.omega, c->stream);
   L(c);
 }
@@ -915,7 +927,9 @@ void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_gr
   // prolongation + correction, fused into the first post-sweep where the level kernel can read
   // x + P e itself (tc2d, space-coarsened next level, one GPU; ST_NO_PRO=1: separate kernels)
   int s0 = 0;
-  if (npost > 0 && c->pro_fuse && Nx.kind == KIND_SPACE && c->comm.size <= 1 && c->fast && c->fast_kind == 0 &&
+  // not on level 0: there the fused sweep (201 us) costs more than sweep + prolongation (90 + 45 us;
+  // profiles/r01/launches_c2_v42_summary.txt) — the correction pass weighs on an issue-bound kernel
+  if (l > 0 && npost > 0 && c->pro_fuse && Nx.kind == KIND_SPACE && c->comm.size <= 1 && c->fast && c->fast_kind == 0 &&
       launch_op_tc2d_pro(Lv.op, Nx.g, trans, cur, Nx.x, b, oth, Lv.omega > 0.0 ? Lv.omega : c->opt.omega, c->stream)) {
     L(c);
     std::swap(cur, oth);

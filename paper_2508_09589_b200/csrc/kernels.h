@@ -15,6 +15,9 @@ bool launch_op_fast2d(const OpDesc& op, int mode, bool trans, bool mask, const d
 bool launch_op_tma2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                      double omega, cudaStream_t s);
 // tc2d.cu: lean TMA kernel for time-constant levels (fine from rho, stored MK), masked modes
+// one thread per node: small replicated time-constant (2+1)D levels with stored M, K (tiny2d.cu)
+bool launch_op_tiny2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
+                      double omega, cudaStream_t s);
 bool launch_op_tc2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                     double omega, cudaStream_t s);
 // damped-Jacobi sweep from x + P e, e the correction of a space-coarsened next level (2D, one GPU)

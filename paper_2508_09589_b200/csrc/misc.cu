@@ -351,10 +351,15 @@ __global__ void __launch_bounds__(1024) dense_invert_smem_kernel(const double* _
     for (int j = tid; j < n; j += nth) r[j] = (j == k) ? ip : a[k * n + j] * ip;
     for (int i = tid; i < n; i += nth) c[i] = (i == k) ? 0.0 : a[i * n + k];
     __syncthreads();
-    for (int e = tid; e < n * n; e += nth) {
-      const int i = e / n, j = e - i * n;
-      if (i == k) a[e] = r[j];
-      else a[e] = (j == k ? 0.0 : a[e]) - c[i] * r[j];
+    // rows strided over the warps, columns over the lanes (no per-element integer division)
+    for (int i = tid >> 5; i < n; i += nth >> 5) {
+      double* ai = a + i * n;
+      const double ci = c[i];
+      if (i == k) {
+        for (int j = tid & 31; j < n; j += 32) ai[j] = r[j];
+      } else {
+        for (int j = tid & 31; j < n; j += 32) ai[j] = (j == k ? 0.0 : ai[j]) - ci * r[j];
+      }
     }
     __syncthreads();
   }
