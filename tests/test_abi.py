@@ -105,3 +105,29 @@ def test_smoother_constants_match_header():
     m = re.search(r"enum \{ ST_SMOOTH_JACOBI = (\d+), ST_SMOOTH_CHEBYSHEV = (\d+), ST_SMOOTH_GMRES = (\d+) \};", hdr)
     assert m, "smoother enum"
     assert (st.ST_SMOOTH_JACOBI, st.ST_SMOOTH_GMRES) == (int(m.group(1)), int(m.group(3)))
+
+
+@pytest.mark.parametrize("sdim,n,nt", [(2, 32, 32), (2, 64, 16), (3, 8, 16)])
+def test_full_coarsening_plan_halves_space_and_time(sdim, n, nt):
+    """Host-only plan of the full space-time coarsening hierarchy (option
+    full_coarsening): every level below the fine one is of kind 'full' and halves n and nt, and
+    the semi-coarsened plan of the same grid (Algorithm 1) coarsens one direction per level."""
+    from paper_2508_09589_b200 import st
+    full = st.plan(sdim, n, nt, full_coarsening=1)["levels"]
+    assert len(full) >= 2 and full[0]["kind"] == "fine"
+    for a, b in zip(full, full[1:]):
+        assert b["kind"] == "full" and b["n"] == a["n"] // 2 and b["nt"] == a["nt"] // 2
+    semi = st.plan(sdim, n, nt)["levels"]
+    for a, b in zip(semi, semi[1:]):
+        assert (b["kind"], b["n"], b["nt"]) in (("space", a["n"] // 2, a["nt"]), ("time", a["n"], a["nt"] // 2))
+
+
+def test_options_layout_appends_nu_coarse():
+    """nu_coarse (per-level smoothing) is the last st_options_t field, so the
+    earlier fields keep their offsets; the binding's struct matches the library's size."""
+    from paper_2508_09589_b200 import st
+    assert st.Options._fields_[-1][0] == "nu_coarse"
+    o = st.Options()
+    lib = st.load_library()
+    lib.st_default_options(ctypes.byref(o))
+    assert o.nu_coarse == 5 and o.nu_pre == 2 and o.smoother == st.ST_SMOOTH_JACOBI
