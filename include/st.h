@@ -99,8 +99,8 @@ typedef struct {
   int64_t coarse_max_nodes; /* stop coarsening at <= this many nodes (R-19)     */
   int32_t max_levels;       /* 0 = unlimited                                             */
   int32_t full_coarsening;  /* 1 = coarsen space and time together    */
-  int32_t use_graphs;       /* 1 (default): the small replicated levels of the V-cycle (< 2^19
-                               nodes) run as one CUDA graph launch per cycle                */
+  int32_t use_graphs;       /* 1 (default): every replicated coarse level of the V-cycle runs as
+                               one CUDA graph launch per cycle                              */
   int32_t verbose;
   int64_t agg_nodes;        /* time slabs: agglomerate a level once it has fewer than this
                                many nodes per rank (default 16384)                          */
