@@ -614,7 +614,8 @@ bool bind_rho(st_ctx* c, const double* rho_in) {
 // so on capacity-dominated levels the spectrum of D^-1 A fills a disk through 0 of diameter
 // R = |lambda|_max (R = 2 x mass row-sum / diagonal: 4.5 in 2D, 6.75 in 3D) and damped Jacobi is
 // stable iff omega R / 2 < 1. R is bounded by the row-wise Gershgorin ratio max_i sum_j |A_ij| /
-// |A_ii| (one pass over the level's stencils, every design); omega_l = min(omega_cap, 1.8 / R).
+// |A_ii| (one pass over the level's stencils, every design); omega_l = min(omega_cap, 1.9 / R).
+constexpr double kOmegaFactor = 1.9;
 void estimate_omegas(st_ctx* c) {
   unsigned long long* d = reinterpret_cast<unsigned long long*>(c->dsmall + 320);
   const int nl = (int)c->lv.size();
@@ -647,7 +648,10 @@ void estimate_omegas(st_ctx* c) {
     double R = 0.0;
     for (int r = 0; r < G; ++r) R = std::max(R, c->hsmall[352 + r * nl + l]);
     Lv.lam_max = R;
-    Lv.omega = (R > 0.0 && std::isfinite(R)) ? std::min(c->opt.omega, 1.8 / R) : c->opt.omega;
+    // 1.9: stable (omega R / 2 < 1) with a 5 % margin; measured 1.5 / 1.8 / 1.9 / 1.95 on configs 2-5
+    // (profiles/r01/omega_factor.log, ST_OMEGA_FAC overrides for experiments)
+    static const double fac = getenv("ST_OMEGA_FAC") ? atof(getenv("ST_OMEGA_FAC")) : kOmegaFactor;
+    Lv.omega = (R > 0.0 && std::isfinite(R)) ? std::min(c->opt.omega, fac / R) : c->opt.omega;
   }
 }
 

@@ -336,7 +336,7 @@ def test_jacobi_weight_bound(sdim, n, nt, tc, mats):
     DinvK = (Kbc.toarray() / Kbc.diagonal()[:, None])
     rho_spec = np.abs(np.linalg.eigvals(DinvK)).max()
     assert rho_spec <= H[0]["lam_max"] * (1 + 1e-12)
-    assert abs(H[0]["omega"] - min(0.75, 1.8 / R_ref)) <= 1e-14
+    assert abs(H[0]["omega"] - min(0.75, 1.9 / R_ref)) <= 1e-14
     solver.close()
 
 
