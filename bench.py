@@ -62,6 +62,8 @@ def solver_opts(args):
         o["nu_coarse"] = args.nu_coarse
     if args.omega > 0:
         o["omega"] = args.omega
+    if args.restart > 0:
+        o["restart"] = args.restart
     if args.full_coarsening:
         o["full_coarsening"] = 1
     return o
@@ -94,6 +96,7 @@ def parse():
                     help="Jacobi sweeps on the coarse levels (default: the library's 5; 0 = --nu)")
     ap.add_argument("--full-coarsening", action="store_true", help="the paper's full space-time coarsening")
     ap.add_argument("--omega", type=float, default=0.0, help="Jacobi weight cap (default: the library's 0.75)")
+    ap.add_argument("--restart", type=int, default=0, help="FGMRES restart length (default: the library's 16)")
     ap.add_argument("--cpu-worker", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--cpu-reps", type=int, default=1, help=argparse.SUPPRESS)
     return ap.parse_args()
