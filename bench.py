@@ -33,24 +33,51 @@ sys.path.insert(0, ROOT)
 
 CFG1_MATS = (1.0, 1.0, 1.0, 1e-3, 1.0, 3.0)
 CFG4_MATS = (0.1, 1.0, 1.0, 1e-4, 1.0, 3.0)
+SIN_SRC = ("sin", 1.0, 1.0, 6.283185307179586)
+# opts: library options of the workload's launch configuration; scaling: how the
+# workload is split over N GPUs ("strong": the same global problem in N time slabs; "weak": the time
+# extent grows with N, BASELINE config 5); bpd_iter: SURVEY.md sec. 8(d)'s model bytes per DOF and
+# FGMRES iteration (the whole-step roofline); sweep_bpd: sec. 8(d)'s damped-Jacobi bytes per DOF
 WORKLOADS = {
     2: dict(name="config2: (2+1)D 256^2x256 elements, time-constant smooth rho (sigma 3, [0.01,1]), "
                  "k=1e-3+rho^3(1-1e-3), c=1, Q=1, T=0 sink patch (10% of x1=0), T0=0",
             sdim=2, n=256, nt=256, mats=CFG1_MATS, tc=True, design="smooth_tc", source=("uniform", 1.0, 0.0, 0.0),
-            tau=1.0),
+            tau=1.0, opts={}, scaling="strong", bpd_iter=435.0, sweep_bpd=32.0),
     1: dict(name="config1: (2+1)D 16^3, rho~U[0.1,1] space-time", sdim=2, n=16, nt=16, mats=CFG1_MATS, tc=False,
-            design="uniform", source=("uniform", 1.0, 0.0, 0.0), tau=1.0),
+            design="uniform", source=("uniform", 1.0, 0.0, 0.0), tau=1.0, opts={}, scaling="strong",
+            bpd_iter=580.0, sweep_bpd=40.0),
     4: dict(name="config4: (3+1)D 64^3x128, time-constant smooth rho, c=0.1+0.9rho, k_min=1e-4", sdim=3, n=64,
-            nt=128, mats=CFG4_MATS, tc=True, design="smooth_tc", source=("uniform", 1.0, 0.0, 0.0), tau=1.0),
+            nt=128, mats=CFG4_MATS, tc=True, design="smooth_tc", source=("uniform", 1.0, 0.0, 0.0), tau=1.0,
+            opts={}, scaling="strong", bpd_iter=412.0, sweep_bpd=32.0),
     5: dict(name="config5 (per GPU): (2+1)D 512^2x512, space-time design; a step = one OC design iteration "
                  "(density filter r=2, forward, adjoint, sensitivities, filter^T, OC volfrac 0.4) from rho=0.4",
             sdim=2, n=512, nt=512, mats=CFG1_MATS, tc=False, design="const", source=("uniform", 1.0, 0.0, 0.0),
-            tau=1.0),
-    3: dict(name="config3-shaped (1/8 of config 3 on one GPU): (2+1)D 512^2x512, an independent smooth field per "
-                 "time layer, Q(t) = 1 + sin(2 pi t)", sdim=2, n=512, nt=512, mats=CFG1_MATS, tc=False,
-            design="smooth_layers", source=("sin", 1.0, 1.0, 6.283185307179586), tau=1.0),
+            tau=1.0, opts={}, scaling="weak", bpd_iter=583.0, sweep_bpd=40.0),
+    # BASELINE config 3 at full size: 1,076,890,625 DOFs (8.6 GB per vector). One GPU holds it with the
+    # memory plan of DESIGN.md sec. 6: right-preconditioned GMRES(6) (no Z vectors), the Krylov pool as
+    # the hooks' and the V-cycle's level-0 scratch, the compliance adjoint RHS generated in the library
+    3: dict(name="config3: (2+1)D 1024^2x1024 elements (1,076,890,625 DOFs), an independent smooth field per "
+                 "time layer (sigma 3, [0.01,1]), Q(t) = 1 + sin(2 pi t), k=1e-3+rho^3(1-1e-3), c=1, T=0 sink "
+                 "patch (10% of x1=0), T0=0",
+            sdim=2, n=1024, nt=1024, mats=CFG1_MATS, tc=False, design="smooth_layers", source=SIN_SRC, tau=1.0,
+            opts=dict(krylov=1, restart=6), scaling="strong", bpd_iter=580.0, sweep_bpd=40.0),
+    # the 1/8 slab of config 3 on one GPU (round-1 "config 3 shape"): parity / profiling case
+    33: dict(name="config3-shaped (1/8 of config 3 on one GPU): (2+1)D 512^2x512, an independent smooth field per "
+                  "time layer, Q(t) = 1 + sin(2 pi t)", sdim=2, n=512, nt=512, mats=CFG1_MATS, tc=False,
+             design="smooth_layers", source=SIN_SRC, tau=1.0, opts={}, scaling="strong", bpd_iter=580.0,
+             sweep_bpd=40.0),
 }
+DEFAULT_CONFIG = 2
 METRIC = "space-time DOFs solved/sec (FGMRES+MG to rtol 1e-8) & operator GB/s vs HBM peak"
+# the paper's own results, quoted as context (CPU supercomputer LUMI-C: 2x AMD EPYC 7763 per node, 128 cores,
+# 256 GiB); not comparable measurements and not targets
+PAPER_CONTEXT = {
+    "hardware": "LUMI-C CPU nodes, 2x AMD EPYC 7763 (64 cores each), 128 cores / 256 GiB per node (PAPER.md:615-616)",
+    "speedup_vs_time_stepping": "52.1x at 7.7x the core-hours (16.4 s vs 855 s), Example 1, 640^2x1280 = 526,338,561 "
+                                "DOFs, 10 design iterations, 400 nodes / 51,200 cores (PAPER.md:660, 705-712)",
+    "largest_solve": "4,202,501,121 DOFs (1280^2x2560), full optimisation in 1,035 s on 500 nodes / 64,000 cores, "
+                     "24.0x faster than time-stepping at 5.2x the cost (PAPER.md:1036-1038)",
+}
 
 
 def solver_opts(args):
@@ -74,8 +101,9 @@ def precond_desc(args, solver):
     sm = ("GMRES(%d)-Jacobi smoother" % o["nu_pre"] if args.smoother == "gmres" else
           "damped Jacobi %d+%d sweeps on the fine level, %d+%d on the coarse levels"
           % (o["nu_pre"], o["nu_post"], o["nu_coarse"] or o["nu_pre"], o["nu_coarse"] or o["nu_post"]))
-    return "FGMRES(%d) + V-cycle, %s, %s" % (o["restart"], sm, "full space-time coarsening" if args.full_coarsening
-                                             else "semi-coarsening (Algorithm 1)")
+    kr = "right-preconditioned GMRES(%d)" if o["krylov"] == 1 else "FGMRES(%d)"
+    return (kr + " + V-cycle, %s, %s") % (o["restart"], sm, "full space-time coarsening" if args.full_coarsening
+                                         else "semi-coarsening (Algorithm 1)")
 
 
 def parse():
@@ -84,7 +112,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG,
+                    help="BASELINE config (1-5); 33 = the 512^2x512 one-eighth slab of config 3")
     ap.add_argument("--rtol", type=float, default=1e-8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -97,6 +126,9 @@ def parse():
     ap.add_argument("--full-coarsening", action="store_true", help="the paper's full space-time coarsening")
     ap.add_argument("--omega", type=float, default=0.0, help="Jacobi weight cap (default: the library's 0.75)")
     ap.add_argument("--restart", type=int, default=0, help="FGMRES restart length (default: the library's 16)")
+    ap.add_argument("--krylov", default="", choices=["", "fgmres", "gmres"],
+                    help="outer Krylov method (default: the workload's; config 3: gmres)")
+    ap.add_argument("--coarse-max-nodes", type=int, default=0, help="coarsest-level size (default: the library's 400)")
     ap.add_argument("--cpu-worker", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--cpu-reps", type=int, default=1, help=argparse.SUPPRESS)
     return ap.parse_args()
@@ -191,6 +223,16 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------
+def solver_opts_for(wl, args):
+    o = dict(wl["opts"])
+    o.update(solver_opts(args))
+    if args.krylov:
+        o["krylov"] = 1 if args.krylov == "gmres" else 0
+    if args.coarse_max_nodes > 0:
+        o["coarse_max_nodes"] = args.coarse_max_nodes
+    return o
+
+
 def run_cuda(args):
     import numpy as np
     import torch
@@ -209,68 +251,90 @@ def run_cuda(args):
     stream = torch.cuda.Stream(device=dev)
     wl = dict(WORKLOADS[args.config])
     nccl_comm = None
-    if world > 1:  # time slabs over NCCL: the time extent grows with the GPU count
-        wl["nt"] = wl["nt"] * world
-        wl["tau"] = wl["tau"] * world
-        wl["name"] = wl["name"] + f" extended in time to nt={wl['nt']}, tau={wl['tau']:g} (time slabs)"
+    if world > 1:
+        if wl["scaling"] == "weak":  # BASELINE config 5: the time extent grows with the GPU count
+            wl["nt"] = wl["nt"] * world
+            wl["tau"] = wl["tau"] * world
+            wl["name"] = wl["name"] + f" extended in time to nt={wl['nt']}, tau={wl['tau']:g} (time slabs)"
+        else:                        # the same global problem in `world` time slabs
+            wl["name"] = wl["name"] + f", split into {world} time slabs"
         obj = [S.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_comm = S.nccl_comm_init(obj[0], rank, world)
+    opts = solver_opts_for(wl, args)
     solver = S.Solver(wl["sdim"], wl["n"], wl["nt"], mats=wl["mats"], source=wl["source"], tau=wl["tau"],
                       time_constant=wl["tc"], stream=stream.cuda_stream, device=local, rtol=args.rtol, maxit=1000,
-                      rank=rank, size=world, nccl_comm=nccl_comm, **solver_opts(args))
+                      rank=rank, size=world, nccl_comm=nccl_comm, **opts)
     N = solver.n_nodes            # this rank's owned nodes
     nd = solver.n_design
     N_global = (wl["n"] + 1) ** wl["sdim"] * (wl["nt"] + 1)
     nsteps = args.warmup + args.steps
-    # time-constant designs are replicated on every rank (same seed); the config-5 design is uniform
     lay = solver.layout()
-    sl = slice(None) if wl["tc"] else slice(lay["layer0"], lay["layer0"] + lay["rho_layers"])  # this rank's layers
-    rhos = [torch.as_tensor(np.ascontiguousarray(I.design_for(wl["sdim"], wl["n"], wl["nt"], wl["design"], seed=s)[sl]),
-                            device=dev) for s in range(nsteps)] if wl["design"] != "const" else \
-        [torch.full((nd,), 0.4 + 0.01 * s, dtype=torch.float64, device=dev) for s in range(nsteps)]
+    big = N_global > 4e8          # config 3: one design on the device, a new one per step by rho <- 1.01 - rho
+    design = args.config == 5     # a step is one config-5 design iteration (R-13)
+    t_gen = time.perf_counter()
+    if wl["design"] == "const":
+        rhos = [torch.full((nd,), 0.4 + 0.01 * s, dtype=torch.float64, device=dev) for s in range(nsteps)]
+    elif wl["tc"]:  # time-constant designs are replicated on every rank (same seed)
+        rhos = [torch.as_tensor(np.ascontiguousarray(I.design_for(wl["sdim"], wl["n"], wl["nt"], wl["design"], seed=s)),
+                                device=dev).reshape(-1) for s in range(nsteps)]
+    else:           # space-time designs: this rank's layers (owned + the ghost layer of the next slab)
+        layers = (lay["layer0"], lay["layer0"] + lay["rho_layers"])
+        nr = 1 if big else nsteps
+        rhos = [torch.as_tensor(I.design_for(wl["sdim"], wl["n"], wl["nt"], wl["design"], seed=s, layers=layers),
+                                device=dev).reshape(-1) for s in range(nr)]
+    t_gen = time.perf_counter() - t_gen
+
+    def rho_for(i):
+        if big:  # a different design every step, in place, outside the timed region ([0.01, 1] -> [0.01, 1])
+            if i > 0:
+                torch.sub(1.01, rhos[0], out=rhos[0])
+            return rhos[0]
+        return rhos[i % len(rhos)]
+
     T = torch.zeros(N, dtype=torch.float64, device=dev)
     lam = torch.zeros_like(T)
-    f = torch.empty_like(T)
-    dJ = torch.empty(nd, dtype=torch.float64, device=dev)
+    dJ = torch.empty(nd if wl["tc"] else lay["n_layers"] * wl["n"] ** wl["sdim"], dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
-    with torch.cuda.stream(stream):
-        solver.rhs(rhos[0], f, None)
     its = []
 
-    design = args.config == 5  # a step is one config-5 design iteration (R-13)
     if design:
-        rho_d = torch.full((solver.layout()["n_layers"] * wl["n"] ** wl["sdim"],), 0.4, dtype=torch.float64, device=dev)
+        f = torch.empty_like(T)
+        with torch.cuda.stream(stream):
+            solver.rhs(rhos[0], f, None)
+        rho_d = torch.full((lay["n_layers"] * wl["n"] ** wl["sdim"],), 0.4, dtype=torch.float64, device=dev)
         rt = torch.empty(nd, dtype=torch.float64, device=dev)
         dJt = torch.empty_like(rho_d)
         dJd = torch.empty_like(rho_d)
         rnew = torch.empty_like(rho_d)
+        dJ = dJt
 
-    def step(i):
+    def step(rho):
         if design:  # filter -> solve -> adjoint -> sensitivities -> F^T -> OC (warm starts kept)
             solver.filter(rho_d, rt)
             solver.solve(rt, T)
             a = solver.stats()
-            solver.adjoint(rt, f, lam)
+            solver.adjoint(rt, None, lam)
             b = solver.stats()
             solver.sensitivity(rt, T, lam, dJt)
             solver.filter(dJt, dJd, transpose=True)
             solver.oc_update(rho_d, dJd, rnew)
             rho_d.copy_(rnew)
         else:
-            solver.solve(rhos[i], T)
+            solver.solve(rho, T)
             a = solver.stats()
-            solver.adjoint(rhos[i], f, lam)
+            solver.adjoint(rho, None, lam)        # compliance: dphi/dT = f (R-8)
             b = solver.stats()
-            solver.sensitivity(rhos[i], T, lam, dJ)
+            solver.sensitivity(rho, T, lam, dJ)
         its.append((a["iterations"], b["iterations"], a["solve_ms"], b["solve_ms"], b["setup_ms"],
-                    a["rel_residual"], b["rel_residual"]))
+                    a["rel_residual"], b["rel_residual"], a["vcycles"], b["vcycles"]))
 
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
+            r = rho_for(i)
             if not design:
                 T.zero_(); lam.zero_()
-            step(i)
+            step(r)
         its.clear()
         if design:  # the e2e leg below repeats the timed design iterations from the same state
             snap = (rho_d.clone(), T.clone(), lam.clone())
@@ -282,18 +346,21 @@ def run_cuda(args):
         l0 = solver.kernel_launches()
         times = []
         for k in range(args.steps):
+            r = rho_for(args.warmup + k)
             flush.fill_(float(k))                      # L2 flush, outside the timed events
             if not design:                             # design loop: warm start
                 T.zero_(); lam.zero_()
             e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            step(args.warmup + k)
+            step(r)
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
         torch.cuda.synchronize()
         launches = solver.kernel_launches() - l0
         clocks = sampler.stop()
+        free_b, total_b = torch.cuda.mem_get_info(dev)
+        mem_used = total_b - free_b
         if world > 1:
             dist.barrier()
     ms = statistics.mean(times)
@@ -304,17 +371,22 @@ def run_cuda(args):
     value = 2.0 * N_global / (ms / 1e3)
 
     # ---- dominant kernel: fine-level damped-Jacobi sweep (live CUDA-event timing) ---------
-    reps = 20
+    reps = 20 if not big else 6
+    rb = rho_for(0) if big else rhos[0]
     with torch.cuda.stream(stream):
-        solver.bench_op(rhos[0], 0, 2, 3)
+        solver.bench_op(rb, 0, 2, 3)
         k0 = torch.cuda.Event(enable_timing=True); k1 = torch.cuda.Event(enable_timing=True)
         k0.record(stream)
-        solver.bench_op(rhos[0], 0, 2, reps)
+        solver.bench_op(rb, 0, 2, reps)
         k1.record(stream)
         k1.synchronize()
     t_sweep = k0.elapsed_time(k1) / reps / 1e3
-    rho_bytes = 8 * nd
-    alg_bytes = 24 * N + rho_bytes           # read x, b; write y; rho (once)
+    # algorithmic bytes per launch: damped-Jacobi sweep 32 B/DOF (time-constant rho)
+    # / 40 B/DOF (time-varying), x the DOFs of one launch; that model reads a stored diagonal the
+    # kernel does not need, so the bytes the kernel must move are reported beside it (24 / 32 B/DOF:
+    # x, b, y + the k~ layer)
+    alg_bytes = wl["sweep_bpd"] * N
+    min_bytes = (24.0 if wl["tc"] else 32.0) * N
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
@@ -322,12 +394,17 @@ def run_cuda(args):
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        tj = json.load(open(tpath))
-        ent = tj.get("configs", {}).get(str(args.config))
-        if ent is None and tj.get("config") == args.config:
-            ent = tj
+        ent = json.load(open(tpath)).get("configs", {}).get(str(args.config))
         if ent is not None:
             traffic = ent.get("traffic_bytes_per_launch")
+    fi = [x[0] for x in its]; ai = [x[1] for x in its]
+    # whole-step model: sec. 8(d)'s bytes per DOF and FGMRES iteration x DOFs x
+    # the iterations of the step, over the step time
+    step_bytes = wl["bpd_iter"] * N_global * statistics.mean(f_ + a_ for f_, a_ in zip(fi, ai))
+    step_roof = {"bytes_per_dof_iteration": wl["bpd_iter"], "iterations_per_step": statistics.mean(
+        f_ + a_ for f_, a_ in zip(fi, ai)), "achieved": step_bytes / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+        "frac": step_bytes / (ms / 1e3) / 1e9 / peak,
+        "model": "SURVEY.md sec. 8(d) per-iteration bytes (nu 2+2, m 20) x N_n x (forward + adjoint iterations)"}
 
     # ---- end-to-end through the C ABI with pinned host buffers ------------------------------
     e2e = None
@@ -348,7 +425,7 @@ def run_cuda(args):
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 rho_d.copy_(rho_ht, non_blocking=True)
-                step(0)
+                step(None)
                 phi = solver.dot(f, T)
                 new_ht.copy_(rho_d, non_blocking=True)
                 stream.synchronize()
@@ -363,19 +440,25 @@ def run_cuda(args):
                "h2d_bytes_per_step": 8 * rho_d.numel(), "d2h_bytes_per_step": 8 * rho_d.numel() + 8,
                "compliance": phi}
     elif args.e2e_steps > 0:
+        # host copies of this step's designs; the device-side vectors are released first (config 3: the
+        # library's staging buffers take their place)
+        rho_hosts = [rho_for(args.warmup + args.steps + k).cpu().numpy().copy() for k in range(min(2, args.e2e_steps))]
+        ndj = dJ.numel()
+        del T, lam, dJ, rhos
+        torch.cuda.empty_cache()
+
         def pinned(n_):
             return torch.zeros(n_, dtype=torch.float64).pin_memory().numpy()
-        rho_h = pinned(nd); T_h = pinned(N); lam_h = pinned(N); f_h = pinned(N); dJ_h = pinned(nd)
-        f_h[:] = f.cpu().numpy()
+        rho_h = pinned(nd); T_h = pinned(N); lam_h = pinned(N); dJ_h = pinned(ndj)
         et = []
         for k in range(args.e2e_steps):
-            rho_h[:] = rhos[k % len(rhos)].cpu().numpy().reshape(-1)
+            rho_h[:] = rho_hosts[k % len(rho_hosts)]
             T_h[:] = 0.0; lam_h[:] = 0.0
             flush.fill_(1.0)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             solver.solve(rho_h, T_h)
-            solver.adjoint(rho_h, f_h, lam_h)
+            solver.adjoint(rho_h, None, lam_h)
             solver.sensitivity(rho_h, T_h, lam_h, dJ_h)
             torch.cuda.synchronize()
             et.append(time.perf_counter() - t0)
@@ -384,8 +467,8 @@ def run_cuda(args):
             t = torch.tensor([ems], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-        h2d = 3 * 8 * nd + 8 * N * 5          # rho x3; T in (solve, sens); g; lambda in (adjoint, sens)
-        d2h = 8 * N * 2 + 8 * nd              # T, lambda, dJ
+        h2d = 3 * 8 * nd + 8 * N * 4          # rho x3; T in (solve, sens); lambda in (adjoint, sens)
+        d2h = 8 * N * 2 + 8 * ndj             # T, lambda, dJ
         e2e = {"value": 2.0 * N_global / (ems / 1e3), "unit": "DOF/s", "ms_per_step": ems,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
@@ -397,39 +480,48 @@ def run_cuda(args):
             res = run_cpu_subprocess(nrep, 1)
             secs = statistics.mean(res["times"])
             cpu = {"value": 2.0 * res["dofs"] / secs, "unit": "DOF/s", "cores": 1, "kind": "oracle",
-                   "sample": f"oracle (NumPy/SciPy SuperLU, single thread) on a {nrep}^2x{nrep} replica of the "
-                             f"workload ({res['dofs']} DOFs): assembly+LU+forward+adjoint+sensitivity, "
-                             f"{secs:.1f} s; host {cpu_model()}"}
+                   "host_cpus": os.cpu_count(),
+                   "sample": f"oracle (NumPy/SciPy SuperLU, single thread; the host has {os.cpu_count()} logical "
+                             f"CPUs, {cpu_model()}) on a {nrep}^2x{nrep} replica of the workload ({res['dofs']} DOFs): "
+                             f"assembly+LU+forward+adjoint+sensitivity, {secs:.1f} s"}
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": "DOF/s", "cores": 1, "kind": "oracle", "sample": f"failed: {ex}"[:300]}
 
-    fi = [a for a, *_ in its]; ai = [b for _, b, *_ in its]
+    hier = solver.hierarchy()
     out = {
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak" if (wl["scaling"] == "weak" or world == 1) else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded smooth random designs, st_inputs)",
         "config": {"workload": wl["name"], "dofs": N_global, "dofs_per_rank": N, "design_vars": nd,
                    "rtol": args.rtol,
                    "step": ("density filter + rho setup + forward solve (warm start) + adjoint solve + sensitivities "
                             "+ filter^T + OC update" if design else
-                            "rho setup + forward solve + adjoint solve + sensitivities"),
+                            "rho setup (new design) + forward solve + adjoint solve (compliance) + sensitivities"),
                    "parallelism": f"{world} time slabs (NCCL)" if world > 1 else "1 GPU",
-                   "l2": "flushed (256 MB write) between steps",
-                   "preconditioner": precond_desc(args, solver)},
+                   "l2": "flushed (256 MB write) between steps" + ("; inputs (8.6 GB per vector) exceed L2" if big else ""),
+                   "preconditioner": precond_desc(args, solver), "options": {k: v for k, v in opts.items()},
+                   "design_generation_s": round(t_gen, 1)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "fine-level damped-Jacobi sweep (" + ("tc2d_kernel, time-constant rho" if wl["tc"] and wl["sdim"] == 2
                                                               else "tv2d_kernel, space-time rho, uniform capacity" if wl["sdim"] == 2
                                                               else "tc3d_kernel, (3+1)D time-constant rho") + ")",
-                     "bytes_per_launch": alg_bytes, "us_per_launch": t_sweep * 1e6,
+                     "bytes_per_launch": alg_bytes, "bytes_per_dof": wl["sweep_bpd"],
+                     "bytes_source": "SURVEY.md sec. 8(d) damped-Jacobi sweep",
+                     "min_bytes_per_launch": min_bytes, "min_frac": min_bytes / t_sweep / 1e9 / peak,
+                     "us_per_launch": t_sweep * 1e6,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+        "step_roofline": step_roof,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-        "solver": {"fwd_its": fi, "adj_its": ai,
+        "solver": {"fwd_its": fi, "adj_its": ai, "fwd_vcycles": [x[7] for x in its], "adj_vcycles": [x[8] for x in its],
                    "fwd_ms": [round(x[2], 2) for x in its], "adj_ms": [round(x[3], 2) for x in its],
                    "setup_ms": [round(x[4], 2) for x in its],
-                   "fwd_dofs_per_s": N / (statistics.mean(x[2] for x in its) / 1e3),
-                   "adj_dofs_per_s": N / (statistics.mean(x[3] for x in its) / 1e3),
+                   "fwd_dofs_per_s": N_global / (statistics.mean(x[2] for x in its) / 1e3),
+                   "adj_dofs_per_s": N_global / (statistics.mean(x[3] for x in its) / 1e3),
                    "rel_res": max(max(x[5], x[6]) for x in its),
-                   "levels": len(solver.hierarchy())},
+                   "levels": len(hier), "hierarchy": [f"{h['n']}^{wl['sdim']}x{h['nt']} {h['kind']}" for h in hier],
+                   "device_mem_used_gb": round(mem_used / 1e9, 1)},
+        "paper_context": PAPER_CONTEXT,
     }
     if rank == 0:
         print(json.dumps(out))

@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define ST_ABI_VERSION 2
+#define ST_ABI_VERSION 3
 
 enum {
   ST_OK = 0,
@@ -63,6 +63,18 @@ enum { ST_SRC_UNIFORM = 0, ST_SRC_SIN = 1 };
  * (k = nu_pre / nu_post fixed steps, <= 24; one GPU). ST_SMOOTH_CHEBYSHEV is reserved
  * (ST_E_UNSUPPORTED). */
 enum { ST_SMOOTH_JACOBI = 0, ST_SMOOTH_CHEBYSHEV = 1, ST_SMOOTH_GMRES = 2 };
+/* Outer Krylov method: FGMRES(m) keeps the m preconditioned vectors
+ * Z_j = M V_j; right-preconditioned GMRES(m) keeps only the basis V and forms x += M (V y) with one more
+ * V-cycle per restart (valid because the Jacobi V-cycle is a fixed linear map; m fewer full-length
+ * vectors — the memory plan of config 3 on one GPU). The GMRES smoother is not a
+ * fixed linear map: ST_KRYLOV_GMRES requires ST_SMOOTH_JACOBI. */
+enum { ST_KRYLOV_FGMRES = 0, ST_KRYLOV_GMRES = 1 };
+/* Coarsest-level solver: exact dense inverse (default, <= 4096 nodes) or the paper's GMRES(<= coarse_maxit)
+ * with Jacobi preconditioning to coarse_rtol (200 iterations, rtol 1e-6). */
+enum { ST_COARSE_DENSE = 0, ST_COARSE_GMRES = 1 };
+/* Stencil-kernel family (test / experiment hook; every family computes the same operator): the TMA
+ * kernels where they apply (default), the cp.async-ring kernels, or the generic kernels only. */
+enum { ST_KERNELS_TMA = 0, ST_KERNELS_CPASYNC = 1, ST_KERNELS_GENERIC = 2, ST_KERNELS_TMA2D = 3 };
 
 /* Regular space-time mesh of n^sdim x nt elements. L, tau only rescale. */
 typedef struct {
@@ -107,6 +119,27 @@ typedef struct {
   int32_t nu_coarse;        /* Jacobi sweeps (pre = post) on the coarse levels; 0 = nu_pre /
                                nu_post there too (default 5; nu_pre = nu_post = 2 on the fine
                                level: DESIGN.md sec. 9)                                     */
+  /* ---- ABI 3: every former environment knob is an option, read per call ---------------- */
+  int32_t krylov;           /* ST_KRYLOV_FGMRES (default) | ST_KRYLOV_GMRES                     */
+  int32_t coarse_solver;    /* ST_COARSE_DENSE (default) | ST_COARSE_GMRES                      */
+  double coarse_rtol;       /* ST_COARSE_GMRES: relative residual target (default 1e-6)          */
+  int32_t coarse_maxit;     /* ST_COARSE_GMRES: iteration cap (default 200)                      */
+  int32_t kernel_family;    /* ST_KERNELS_* (default ST_KERNELS_TMA)                             */
+  int32_t chunk_planes;     /* persistent stencil kernels: planes per time chunk of the work list;
+                               0 = automatic, > 0 forced, < 0 no chunking   */
+  int32_t max_ctas;         /* persistent stencil kernels: cap on the grid (0 = one full wave);
+                               a small cap makes every CTA walk long multi-tile plane runs       */
+  int32_t fuse_prolong;     /* 1 (default): prolongation + correction fused into the first
+                               post-sweep where a kernel supports it; 0: separate kernels      */
+  int32_t fuse_restrict;    /* 1 (default): residual + restriction in one pass where a kernel
+                               supports it; 0: residual kernel + restriction kernel            */
+  double omega_factor;      /* per-level Jacobi weight omega_l = min(omega, omega_factor / R_l)
+                               (default 1.9)                                 */
+  double dgks_eta;          /* FGMRES re-orthogonalisation when ||w'|| < dgks_eta ||w|| (0.1)   */
+  int64_t graph_max_nodes;  /* replicated levels below this many nodes run in the V-cycle's
+                               CUDA graph (0 = every replicated coarse level)                  */
+  double smoother_rtol;     /* ST_SMOOTH_GMRES: stop the inner GMRES once ||r|| <= smoother_rtol
+                               ||r0|| (1e-6); 0 = fixed nu steps (graph-capturable) */
 } st_options_t;
 
 /* Distribution over time slabs. NULL or size == 1 => one GPU.
@@ -163,6 +196,8 @@ typedef struct {
   double setup_ms, solve_ms; /* last rho-dependent setup and last solve, device ms         */
   int32_t n_levels;
   int32_t converged;
+  int32_t vcycles;           /* V-cycles of the last solve (GMRES: iterations + restarts)  */
+  int64_t setups;            /* rho-dependent rebuilds since st_setup (design changes seen) */
 } st_stats_t;
 
 typedef struct {
@@ -175,8 +210,9 @@ typedef struct {
   double lam_max[32];        /* Gershgorin bound on |lambda|_max(D^-1 A)     */
 } st_hierarchy_t;
 
-/* Fill `o` with the library defaults (rtol 1e-8, restart 16, Jacobi nu 2/2 on the fine level and 5/5 on the coarse levels, weight cap 0.75,
- * lambda_crit 0.5, coarse_max_nodes 400, agg_nodes 16384). */
+/* Fill `o` with the library defaults (rtol 1e-8, restart 16, FGMRES, Jacobi nu 2/2 on the fine level and
+ * 5/5 on the coarse levels, weight cap 0.75, omega_factor 1.9, lambda_crit 0.5, coarse_max_nodes 400, dense
+ * coarsest solve, agg_nodes 16384, TMA kernels, automatic chunking, both transfer fusions on). */
 void st_default_options(st_options_t* o);
 
 /* Validate, run Algorithm 1, allocate all workspaces, assemble f on the device.
@@ -194,7 +230,9 @@ void st_destroy(st_ctx_t* ctx);
 int st_solve(st_ctx_t* ctx, const double* rho, double* T);
 
 /* Adjoint solve K_bc(rho)^T lambda = m_f .* dJdT. lambda: in = initial
- * guess, out = solution (0 at constrained nodes). dJdT at constrained nodes is ignored. */
+ * guess, out = solution (0 at constrained nodes). dJdT at constrained nodes is ignored.
+ * dJdT = NULL selects the time-integrated thermal compliance phi = f^T T, dphi/dT = f (BASELINE
+ * config 1, R-8) without a caller vector for f. */
 int st_adjoint(st_ctx_t* ctx, const double* rho, const double* dJdT, double* lambda);
 
 /* Sensitivities dJ_e = -lambda_e^T (dC/drho G + dk~/drho Kx) T_e,

@@ -21,6 +21,7 @@ __all__ = [
     "element_matrices", "element_parts", "connectivity", "simp",
     "assemble_K", "source_vector", "dirichlet", "apply_dirichlet",
     "pnorm_objective", "diffusion_timescale", "row_apply", "sensitivity_elements",
+    "node_constraint", "source_rows",
 ]
 
 
@@ -463,24 +464,65 @@ def _node_coords(mesh: Mesh, node):
     return c
 
 
+def node_constraint(mesh: Mesh, bcs: BCs, node):
+    """(constrained, prescribed value) of ONE node, the rule of dirichlet() (R-1..R-4)
+    evaluated at the node's coordinates: the t = 0 plane carries T0; the sink patch
+    (x1 = 0, transverse indices j with |j/n - center| <= halfwidth, all t) or, with all_walls, every
+    spatial boundary node carries 0. Sampled certification only (R-21)."""
+    c = _node_coords(mesh, int(node))
+    sp_c, t = c[:-1], c[-1]
+    if bcs.all_walls:
+        wall = any(x == 0 or x == mesh.n for x in sp_c)
+        if wall:
+            return True, 0.0
+    elif bcs.has_patch and sp_c[0] == 0:
+        if all(abs(j / mesh.n - bcs.center) <= bcs.halfwidth * (1.0 + 1e-12) for j in sp_c[1:]):
+            return True, 0.0
+    if t == 0:
+        return True, bcs.T0
+    return False, 0.0
+
+
+def _elem_index(mesh: Mesh, e):
+    """Flat element index e1 + n (e2 + ... + n tau) of element coordinates e (R-10)."""
+    eidx, mul = 0, 1
+    for d in range(mesh.sdim + 1):
+        eidx += e[d] * mul
+        mul *= mesh.n
+    return eidx
+
+
+def _rho_of(prob: "Problem", rho, eidx):
+    """Density of space-time element eidx: rho is per space-time element or time-constant
+    (extruded through time)."""
+    mesh = prob.mesh
+    r = np.asarray(rho).reshape(-1)
+    if r.size == mesh.n_elems:
+        return float(r[eidx])
+    if r.size == mesh.plane_elems:
+        return float(r[eidx % mesh.plane_elems])
+    raise ValueError("rho size")
+
+
 def row_apply(prob: "Problem", rho, x, nodes, transpose=False):
     """(K_bc x)[nodes] (or (K_bc^T x)[nodes]) for the eliminated all-at-once matrix
-    (R-1), summing A_e = C_e G + k~_e Kx (element_matrices, quadrature) over
-    the elements adjacent to each node. x is the full nodal vector."""
+    (R-1), summing A_e = C_e G + k~_e Kx (element_matrices, quadrature; SIMP
+    coefficients by simp()) over the elements adjacent to each node. Purely
+    local: x only needs to support x[node] for the nodes of the rows' stencils (a numpy array or a
+    mapping), the coefficients are evaluated for the touched elements only, and constraints by
+    node_constraint() — so it scales to the full BASELINE sizes (R-21)."""
     mesh = prob.mesh
-    C, k, _, _, tc = prob.coefficients(rho)
     G, Kx = element_matrices(mesh.sdim, mesh.dx, mesh.dt)
-    cons, _ = prob.constraints()
     nd = mesh.sdim + 1
     nloc = 2 ** nd
     nn = mesh.n + 1
     strides = [nn ** d for d in range(mesh.sdim)] + [nn ** mesh.sdim]
     ecount = [mesh.n] * mesh.sdim + [mesh.nt]
-    x = np.asarray(x)
     out = np.zeros(len(nodes))
     for s, node in enumerate(nodes):
         node = int(node)
-        if cons[node]:
+        cons, _ = node_constraint(mesh, prob.bcs, node)
+        if cons:
             out[s] = x[node]
             continue
         cc = _node_coords(mesh, node)
@@ -489,34 +531,55 @@ def row_apply(prob: "Problem", rho, x, nodes, transpose=False):
             e = [cc[d] - ((a >> d) & 1) for d in range(nd)]
             if any(e[d] < 0 or e[d] >= ecount[d] for d in range(nd)):
                 continue
-            eidx = 0
-            mul = 1
-            for d in range(nd):
-                eidx += e[d] * mul
-                mul *= mesh.n if d < mesh.sdim else 1
-            Ae = C[eidx] * G + k[eidx] * Kx
+            C, k, _, _ = simp(_rho_of(prob, rho, _elem_index(mesh, e)), prob.mats, mesh)
+            Ae = C * G + k * Kx
             for b in range(nloc):
                 gb = sum((e[d] + ((b >> d) & 1)) * strides[d] for d in range(nd))
-                if cons[gb]:
+                if node_constraint(mesh, prob.bcs, gb)[0]:
                     continue
                 acc += (Ae[b, a] if transpose else Ae[a, b]) * x[gb]
         out[s] = acc
     return out
 
 
+def source_rows(mesh: Mesh, src: Source, nodes):
+    """f[nodes] of source_vector() (R-5): per node, the sum over its adjacent
+    elements of the 2^(sdim+1)-point Gauss quadrature of N_a Q~ (sampled certification, R-21)."""
+    nd = mesh.sdim + 1
+    nloc = 2 ** nd
+    h = [mesh.dx] * mesh.sdim + [mesh.dt]
+    detJ = float(np.prod([hh / 2.0 for hh in h]))
+    ecount = [mesh.n] * mesh.sdim + [mesh.nt]
+    bits = [[(a >> d) & 1 for d in range(nd)] for a in range(nloc)]
+    out = np.zeros(len(nodes))
+    for s, node in enumerate(nodes):
+        cc = _node_coords(mesh, int(node))
+        acc = 0.0
+        for a in range(nloc):
+            e = [cc[d] - bits[a][d] for d in range(nd)]
+            if any(e[d] < 0 or e[d] >= ecount[d] for d in range(nd)):
+                continue
+            org = [e[d] * h[d] for d in range(nd)]
+            for q in itertools.product(range(2), repeat=nd):
+                sq = [_GP[qq] for qq in q]
+                pts = [np.array([org[d] + 0.5 * h[d] * (1.0 + sq[d])]) for d in range(nd)]
+                Q = float(_q_tilde(src, mesh, pts[:-1], pts[-1])[0])
+                N = np.prod([_phi(bits[a][d], sq[d]) for d in range(nd)])
+                acc += detJ * Q * N
+        out[s] = acc
+    return out
+
+
 def sensitivity_elements(prob: "Problem", rho, T, lam, elems):
     """dphi/drho_e (R-9) of the space-time elements `elems` (index
-    e1 + n (e2 + ... + n tau)), full T and lambda = 0 on constrained nodes."""
+    e1 + n (e2 + ... + n tau)), full T and lambda = 0 on constrained nodes. Purely local like
+    row_apply: T and lam only need T[node] / lam[node] at the elements' nodes."""
     mesh = prob.mesh
-    _, _, dC, dk, _ = prob.coefficients(rho)
     G, Kx = element_matrices(mesh.sdim, mesh.dx, mesh.dt)
-    cons, _ = prob.constraints()
     nd = mesh.sdim + 1
     nloc = 2 ** nd
     nn = mesh.n + 1
     strides = [nn ** d for d in range(mesh.sdim)] + [nn ** mesh.sdim]
-    T = np.asarray(T)
-    lam = np.where(cons, 0.0, np.asarray(lam))
     out = np.zeros(len(elems))
     for s, e in enumerate(elems):
         e = int(e)
@@ -527,6 +590,8 @@ def sensitivity_elements(prob: "Problem", rho, T, lam, elems):
             r //= mesh.n
         ec.append(r)
         idx = [sum((ec[d] + ((a >> d) & 1)) * strides[d] for d in range(nd)) for a in range(nloc)]
-        Te, Le = T[idx], lam[idx]
-        out[s] = -(dC[e] * (Le @ G @ Te) + dk[e] * (Le @ Kx @ Te))
+        Te = np.array([T[i] for i in idx], dtype=np.float64)
+        Le = np.array([0.0 if node_constraint(mesh, prob.bcs, i)[0] else lam[i] for i in idx], dtype=np.float64)
+        _, _, dC, dk = simp(_rho_of(prob, rho, e), prob.mats, mesh)
+        out[s] = -(dC * (Le @ G @ Te) + dk * (Le @ Kx @ Te))
     return out

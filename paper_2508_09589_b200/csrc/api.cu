@@ -61,9 +61,11 @@ struct Level {
   double* mid = nullptr;
   long long mid_elems = 0;
   int mid_ns = 0;
-  // GMRES(k) smoother (ST_SMOOTH_GMRES): k+1 basis vectors with leading dimension gld
+  // GMRES(k) smoother (ST_SMOOTH_GMRES) / GMRES coarsest solve (cgm): k+1 basis vectors with leading
+  // dimension gld
   double* gv = nullptr;
   long long gld = 0;
+  bool cgm = false;      // coarsest level solved by GMRES(<= coarse_maxit)-Jacobi (ST_COARSE_GMRES)
 };
 }  // namespace
 
@@ -84,8 +86,12 @@ struct st_ctx {
   long long guard = 0;                              // zeroed front guard of internal vectors
   std::vector<double*> vallocs;                     // guarded allocations (raw bases)
   Geom gd0{};                                      // level-0 geometry in the caller's dense layout
-  double *f = nullptr, *b = nullptr, *tmpN = nullptr, *tmpN2 = nullptr, *xint = nullptr;
+  // level-0 vectors (memory plan): the right-hand side of the current solve, the
+  // iterate, and the Krylov pool V[0..m] | Z[0..nz) that doubles as scratch for the test hooks and the
+  // V-cycle's level-0 residual (no other full-length vector is allocated)
+  double *rhs = nullptr, *xint = nullptr;
   double *V = nullptr, *Z = nullptr;
+  int nz = 0;                                       // Z slots: m (FGMRES) or 1 (GMRES: z = M v_j)
   RedWs ws{};
   double* dsmall = nullptr;
   double* hsmall = nullptr;
@@ -94,13 +100,11 @@ struct st_ctx {
   bool kt_design = false;        // kt belongs to the cached design (rho_ck); test hooks may rebuild it
   double* io_stage[4] = {nullptr, nullptr, nullptr, nullptr};
   long long io_n[4] = {0, 0, 0, 0};
-  double rho_ck[2] = {0.0, 0.0};
+  unsigned long long rho_fp[2] = {0ull, 0ull};  // design fingerprint of the cached operators
   bool have_ops = false;
   st_stats_t stats{};
   long long launches = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  bool fast = true;     // specialised (2+1)D kernels
-  int fast_kind = 0;    // 0: TMA ring, 1: cp.async ring
   // time slabs: rank, owned fine planes [o0, o0 + nown) of the local vector (o0 = 0 on rank 0,
   // else 1: local plane 0 is the ghost copy of the previous rank's last plane)
   Comm comm;
@@ -111,21 +115,14 @@ struct st_ctx {
   // buffers): one per direction, captured after one eager run, valid for the context lifetime
   int gl0 = -1;
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
-  // fused small-level V-cycle (vsmall.cu): levels >= vs0 in one cluster kernel (-1: off)
-  int vs0 = -1;
-  // single-CTA shared-memory tail (vsmall.cu, launch_vtail): levels >= vt0 in one launch (-1: off)
-  int vt0 = -1;
-  bool pro_fuse = true;  // prolongation fused into the first post-sweep (ST_NO_PRO=1: off)
-  // DGKS: re-orthogonalise when ||w'||^2 < eta^2 ||w||^2. eta = 0.1: with the V-cycle preconditioner
-  // ||w'|| / ||w|| stays above it, and the measured iteration counts and true residuals equal those of
-  // eta^2 = 0.5 (which re-orthogonalised every step) on configs 2-4 (profiles/r01/dgks_threshold.log);
-  // the pass remains a safety net for severe cancellation. ST_DGKS_ETA2 overrides.
+  // DGKS: re-orthogonalise when ||w'||^2 < eta^2 ||w||^2 (options dgks_eta, default 0.1). With the
+  // V-cycle preconditioner ||w'|| / ||w|| stays above 0.1, and the measured iteration counts and true
+  // residuals equal those of eta^2 = 0.5 (which re-orthogonalised every step) on configs 2-4
+  // (profiles/r01/dgks_threshold.log); the pass remains a safety net for severe cancellation.
   double dgks_eta2 = 0.01;
-  // small 2D time-constant levels as one thread per node (tiny2d.cu) up to this many nodes; opt-in
-  // (ST_TINY_NODES): inside the V-cycle's graph the TMA kernels cost no more (config 2: 633.9 MDOF/s
-  // off, 635.2 at <= 20000 nodes, 619.9 at <= 300000; profiles/r01/tiny2d_ab.log)
-  long long tiny_nodes = 0;
-  double* gsm = nullptr;  // GMRES smoother: device Hessenberg / Givens / dots scratch (1024 doubles)
+  double* gsm = nullptr;  // GMRES smoother: device Hessenberg / Givens (1024 doubles) + dots (1024)
+  double* cgs = nullptr;  // GMRES coarsest solve: device state gm_layout(coarse_maxit) + dots
+  long long coarse_its = 0;
   // config-5 design update buffers (st_filter / st_oc_update), allocated on first use
   double *fbuf = nullptr, *fw = nullptr;
   long long gkernels[2] = {0, 0};
@@ -276,9 +273,13 @@ void build_hierarchy(st_ctx* c) {
     Ln.kind = kind;
     c->lv.push_back(Ln);
   }
-  if (c->lv.back().g.N > 8192)
+  // the dense coarsest inverse is one CTA's O(n^3) Gauss-Jordan (misc.cu): <= 4096 nodes (~0.5 s per
+  // design at the limit); larger coarsest levels need the iterative coarsest solve (ST_COARSE_GMRES)
+  if (c->opt.coarse_solver == ST_COARSE_DENSE && c->lv.back().g.N > 4096)
     throw StErr{ST_E_DIVISIBILITY, "coarsest level too large for the dense solve (" +
-                                       std::to_string(c->lv.back().g.N) + " nodes): grid not divisible enough"};
+                                       std::to_string(c->lv.back().g.N) +
+                                       " stored nodes > 4096): grid not divisible enough; use coarse_solver = "
+                                       "ST_COARSE_GMRES (the paper's GMRES coarsest solve)"};
   for (auto& Lv : c->lv) Lv.ntg = Lv.g.nt;
 }
 
@@ -324,6 +325,9 @@ void setup_forms(st_ctx* c) {
     OpDesc& op = Lv.op;
     op.g = Lv.g;
     op.m = c->md;
+    op.family = c->opt.kernel_family;
+    op.chunk = c->opt.chunk_planes;
+    op.max_ctas = c->opt.max_ctas;
     if (l == 0) {
       op.form = FORM_RHO;
       op.nl = c->tc ? 1 : Lv.g.nt;
@@ -408,43 +412,14 @@ double* vec_alloc(st_ctx* c, long long count) {
   return base + c->guard;
 }
 
-void allocate(st_ctx* c) {
-  // single-CTA V-cycle tail in shared memory: the longest replicated tail whose level vectors fit.
-  // Opt-in (ST_VTAIL=1): measured slower than the graph-launched per-level kernels (config 2: 442.7
-  // vs 482.6 MDOF/s; config 3 shape: 393.5 vs 398.3; profiles/r01/vtail_ab.log) — one SM runs the
-  // tail's sweeps slower than 148 SMs run them inside the graph, whose launches cost far less than
-  // the ~6 us of an eager launch
-  {
-    const char* e = getenv("ST_NO_PRO");
-    c->pro_fuse = !(e && e[0] == '1');
-    e = getenv("ST_DGKS_ETA2");
-    if (e) c->dgks_eta2 = atof(e);
-    e = getenv("ST_TINY_NODES");
-    if (e) c->tiny_nodes = atoll(e);
+// slot k of the level-0 pool V[0..m] | Z[0..nz): scratch vectors of the hooks (outside a solve)
+double* pool(st_ctx* c, int k) {
+  const int m = c->opt.restart;
+  if (k < 0 || k > m + c->nz) throw StErr{ST_E_INVALID_ARG, "internal: pool slot"};
+  return k <= m ? c->V + (long long)k * c->ld : c->Z + (long long)(k - m - 1) * c->ld;
+}
 
-  }
-  c->vt0 = -1;
-  {
-    const char* e = getenv("ST_VTAIL");
-    const int nl = (int)c->lv.size();
-    if ((e && e[0] == '1') && c->vs0 < 0 && c->opt.smoother == ST_SMOOTH_JACOBI)
-      for (int l = 1; l + 1 < nl; ++l) {
-        bool ok = nl - l <= kMaxSmall;
-        long long words = 0, nmax = 0;
-        // one SM runs the tail: only levels whose sweeps cost less there than a launch on all SMs
-        // (~6 us each; measured by scripts/level_lat.py)
-        ok = ok && nodes_of(c->lv[l].g) <= 1500;
-        for (int k = l; k < nl && ok; ++k) {
-          ok = !c->lv[k].dist;
-          words += 2 * c->lv[k].g.N;
-          nmax = std::max(nmax, c->lv[k].g.N);
-        }
-        if (ok && (words + 2 * nmax) * (long long)sizeof(double) <= 200 * 1024) {
-          c->vt0 = l;
-          break;
-        }
-      }
-  }
+void allocate(st_ctx* c) {
   const long long N = c->N;
   const int m = c->opt.restart;
   // zeroed front guard: the TMA x maps are based one row (2D) / one slice + one row (3D) + 2
@@ -455,24 +430,24 @@ void allocate(st_ctx* c) {
     c->guard = (need + 31) / 32 * 32;
   }
   c->ld = (N + c->guard + 31) / 32 * 32;   // vector j's guard = tail of slot j-1 (never written)
-  c->f = vec_alloc(c, N);
-  c->b = vec_alloc(c, N);
-  c->tmpN = vec_alloc(c, N);
-  c->tmpN2 = vec_alloc(c, N);
+  c->rhs = vec_alloc(c, N);
   c->xint = vec_alloc(c, N);
+  c->nz = c->opt.krylov == ST_KRYLOV_GMRES ? 1 : m;
   c->V = vec_alloc(c, (m + 1) * c->ld);
-  c->Z = vec_alloc(c, m * c->ld);
+  c->Z = vec_alloc(c, c->nz * c->ld);
   dalloc(&c->ws.partial, (size_t)kRedBlocks * kMaxDots);
   dalloc(&c->ws.counter, 1);
   CK(cudaMemsetAsync(c->ws.counter, 0, sizeof(unsigned), c->stream));
   dalloc(&c->dsmall, 512);
+  {
+    const double one = 1.0;  // dsmall[510]: unit coefficient of x += M u (GMRES)
+    CK(cudaMemcpy(c->dsmall + 510, &one, sizeof(double), cudaMemcpyHostToDevice));
+  }
   if (c->opt.smoother == ST_SMOOTH_GMRES) {  // the paper's smoother: basis per level
     const int k = std::max(c->opt.nu_pre, c->opt.nu_post);
-    dzalloc(&c->gsm, 1024);
-    const double one = 1.0;
-    CK(cudaMemcpy(c->gsm + 1000, &one, sizeof(double), cudaMemcpyHostToDevice));
+    dzalloc(&c->gsm, 2048);
     for (auto& Lv : c->lv) {
-      if (&Lv == &c->lv.back()) break;  // the coarsest level is solved densely
+      if (&Lv == &c->lv.back()) break;  // the coarsest level has its own solve
       Lv.gld = (Lv.g.N + 31) / 32 * 32;
       dzalloc(&Lv.gv, (long long)(k + 1) * Lv.gld);  // zero pads: the dots run over the padded length
     }
@@ -483,8 +458,7 @@ void allocate(st_ctx* c) {
     Level& Lv = c->lv[l];
     const long long n = Lv.g.N;
     if (l == 0) {
-      Lv.r = vec_alloc(c, n);
-      Lv.t = vec_alloc(c, n);
+      Lv.t = vec_alloc(c, n);  // Jacobi ping-pong; the residual goes to a Krylov-pool slot
     } else {
       Lv.x = vec_alloc(c, n);
       Lv.b = vec_alloc(c, n);
@@ -504,35 +478,28 @@ void allocate(st_ctx* c) {
     }
   }
   Level& Lc = c->lv.back();
-  Lc.dense = true;
-  dalloc(&Lc.A, (size_t)Lc.g.N * Lc.g.N);
-  dalloc(&Lc.Ainv, (size_t)Lc.g.N * Lc.g.N);
-  dalloc(&Lc.info, 1);
+  if (c->opt.coarse_solver == ST_COARSE_GMRES) {  // the paper's GMRES coarsest solve
+    const int k = c->opt.coarse_maxit;
+    Lc.cgm = true;
+    Lc.gld = (Lc.g.N + 31) / 32 * 32;
+    dzalloc(&Lc.gv, (long long)(k + 1) * Lc.gld);
+    dzalloc(&c->cgs, (size_t)gm_y_offset(k) + k + 32 + kMaxBasis + 64);
+  } else {
+    Lc.dense = true;
+    dalloc(&Lc.A, (size_t)Lc.g.N * Lc.g.N);
+    dalloc(&Lc.Ainv, (size_t)Lc.g.N * Lc.g.N);
+    dalloc(&Lc.info, 1);
+  }
   CK(cudaEventCreate(&c->e0));
   CK(cudaEventCreate(&c->e1));
-  // fused small-level tail: the first level from which every level is replicated and small
-  c->vs0 = -1;
-  {
-    // opt-in (ST_VSMALL=1): measured slower than the graph-launched per-level kernels on config 2
-    // (408 vs 441 MDOF/s with levels <= 4096 nodes fused; profiles/r01), kept for the experiment
-    const char* e = getenv("ST_VSMALL");
-    const int nl = (int)c->lv.size();
-    if (e && e[0] == '1' && c->opt.smoother == ST_SMOOTH_JACOBI)
-      for (int l = 1; l + 1 < nl; ++l) {
-        bool ok = nl - l <= kMaxSmall;
-        for (int k = l; k < nl && ok; ++k) ok = !c->lv[k].dist && nodes_of(c->lv[k].g) <= 4096;
-        if (ok) {
-          c->vs0 = l;
-          break;
-        }
-      }
-  }
   c->gl0 = -1;
   // every replicated coarse level (level 0 takes the FGMRES vectors: not capturable); measured on
-  // config 2: 563.8 MDOF/s vs ~558 with levels < 2^19 nodes only; ST_GRAPH_NODES bounds it
-  long long gmax = 1LL << 62;
-  if (const char* e = getenv("ST_GRAPH_NODES")) gmax = atoll(e);
-  for (size_t l = 1; l + 1 < c->lv.size(); ++l) {
+  // config 2: 563.8 MDOF/s vs ~558 with levels < 2^19 nodes only; options graph_max_nodes bounds it
+  const long long gmax = c->opt.graph_max_nodes > 0 ? c->opt.graph_max_nodes : (1LL << 62);
+  // host decisions inside the cycle (iterative coarsest solve, smoother with an inner rtol): no graph
+  const bool host_sync = c->opt.coarse_solver == ST_COARSE_GMRES ||
+                         (c->opt.smoother == ST_SMOOTH_GMRES && c->opt.smoother_rtol > 0.0);
+  for (size_t l = 1; l + 1 < c->lv.size() && !host_sync; ++l) {
     const Level& Lv = c->lv[l];
     if (!Lv.dist && nodes_of(Lv.g) < gmax) {
       c->gl0 = (int)l;
@@ -542,14 +509,6 @@ void allocate(st_ctx* c) {
 }
 
 void op_launch(st_ctx* c, int l, int mode, bool trans, bool mask, const double* x, const double* b, double* y) {
-  g_use_fast = c->fast;
-  g_fast_kind = c->fast_kind;
-  const Level& Lv = c->lv[l];
-  if (c->fast && l > 0 && !Lv.dist && nodes_of(Lv.g) <= c->tiny_nodes &&
-      launch_op_tiny2d(Lv.op, mode, trans, mask, x, b, y, Lv.omega > 0.0 ? Lv.omega : c->opt.omega, c->stream)) {
-    L(c);
-    return;
-  }
   launch_op(c->lv[l].op, mode, trans, mask, x, b, y, c->lv[l].omega > 0.0 ? c->lv[l].omega : c->opt.omega, c->stream);
   L(c);
 }
@@ -591,23 +550,40 @@ void set_fine_rho(st_ctx* c, const double* rho) {
   }
 }
 
+// a host design is staged through a context buffer allocated on first use (device designs cost nothing)
+const double* rho_device(st_ctx* c, const double* rho) {
+  if (!rho) throw StErr{ST_E_INVALID_ARG, "null rho"};
+  if (is_device_ptr(rho)) return rho;
+  if (!c->rho_stage) dalloc(&c->rho_stage, c->ndesign);
+  CK(cudaMemcpyAsync(c->rho_stage, rho, c->ndesign * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  return c->rho_stage;
+}
+
 // rho -> level-0 operator pointer; returns true if rho changed since the last full setup
 bool bind_rho(st_ctx* c, const double* rho_in) {
-  const double* rho = rho_in;
-  if (!is_device_ptr(rho_in)) {
-    CK(cudaMemcpyAsync(c->rho_stage, rho_in, c->ndesign * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    rho = c->rho_stage;
-  }
+  const double* rho = rho_device(c, rho_in);
   c->lv[0].op.rho = rho;  // the per-design tables follow in prepare() when rho changed
-  launch_checksum(rho, c->ndesign, c->dsmall + 500, c->ws, c->stream);
+  // exact change detection: 128 bits of hash over the bit patterns (launch_fingerprint)
+  unsigned long long* fp = reinterpret_cast<unsigned long long*>(c->dsmall + 500);
+  launch_fingerprint(rho, c->ndesign, fp, c->stream);
   L(c);
-  allreduce(c, c->dsmall + 500, 2);  // one decision on every rank
-  CK(cudaMemcpyAsync(c->hsmall + 500, c->dsmall + 500, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->hsmall + 500, fp, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  bool changed = !(c->have_ops && c->hsmall[500] == c->rho_ck[0] && c->hsmall[501] == c->rho_ck[1]);
-  c->rho_ck[0] = c->hsmall[500];
-  c->rho_ck[1] = c->hsmall[501];
-  return changed;
+  unsigned long long h[2];
+  memcpy(h, c->hsmall + 500, sizeof(h));
+  int local_changed = !(c->have_ops && h[0] == c->rho_fp[0] && h[1] == c->rho_fp[1]);
+  c->rho_fp[0] = h[0];
+  c->rho_fp[1] = h[1];
+  // one decision on every rank (a rank whose slab changed makes every rank rebuild)
+  if (c->comm.size > 1) {
+    c->hsmall[500] = local_changed ? 1.0 : 0.0;
+    CK(cudaMemcpyAsync(c->dsmall + 500, c->hsmall + 500, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    allreduce(c, c->dsmall + 500, 1);
+    CK(cudaMemcpyAsync(c->hsmall + 500, c->dsmall + 500, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    local_changed = c->hsmall[500] > 0.0;
+  }
+  return local_changed != 0;
 }
 
 // Per-level Jacobi weight: the capacity term is an upwind difference in time,
@@ -649,8 +625,8 @@ void estimate_omegas(st_ctx* c) {
     for (int r = 0; r < G; ++r) R = std::max(R, c->hsmall[352 + r * nl + l]);
     Lv.lam_max = R;
     // 1.9: stable (omega R / 2 < 1) with a 5 % margin; measured 1.5 / 1.8 / 1.9 / 1.95 on configs 2-5
-    // (profiles/r01/omega_factor.log, ST_OMEGA_FAC overrides for experiments)
-    static const double fac = getenv("ST_OMEGA_FAC") ? atof(getenv("ST_OMEGA_FAC")) : kOmegaFactor;
+    // (profiles/r01/omega_factor.log; options omega_factor)
+    const double fac = c->opt.omega_factor > 0.0 ? c->opt.omega_factor : kOmegaFactor;
     Lv.omega = (R > 0.0 && std::isfinite(R)) ? std::min(c->opt.omega, fac / R) : c->opt.omega;
   }
 }
@@ -727,33 +703,51 @@ void build_ops(st_ctx* c) {
   }
   Level& Lc = c->lv.back();
   const long long Nc = Lc.g.N;
-  CK(cudaMemsetAsync(Lc.A, 0, (size_t)Nc * Nc * sizeof(double), c->stream));
-  launch_dense_assemble(Lc.op, Lc.A, c->stream);
-  launch_dense_invert(Lc.A, Lc.Ainv, (int)Nc, Lc.info, c->stream);
-  L(c, 2);
-  check_launch();
-  // eliminated RHS b = m_f (f - K xD) + m_c xD (R-1)
-  const Geom& g0 = c->lv[0].g;
-  if (c->bcs.T0 != 0.0) {
-    launch_xd(g0, c->bcs.T0, c->tmpN, c->stream);
-    op_launch(c, 0, MODE_APPLY, false, false, c->tmpN, nullptr, c->tmpN2);
-    launch_rhs_combine(g0, c->f, c->tmpN2, c->bcs.T0, c->b, c->stream);
+  if (Lc.dense) {
+    CK(cudaMemsetAsync(Lc.A, 0, (size_t)Nc * Nc * sizeof(double), c->stream));
+    launch_dense_assemble(Lc.op, Lc.A, c->stream);
+    launch_dense_invert(Lc.A, Lc.Ainv, (int)Nc, Lc.info, c->stream);
     L(c, 2);
-  } else {
-    launch_rhs_combine(g0, c->f, nullptr, 0.0, c->b, c->stream);
-    L(c);
+    check_launch();
   }
-  check_launch();
   estimate_omegas(c);
   CK(cudaEventRecord(c->e1, c->stream));
   CK(cudaEventSynchronize(c->e1));
   int info = 0;
-  CK(cudaMemcpy(&info, Lc.info, sizeof(int), cudaMemcpyDeviceToHost));
+  if (Lc.dense) CK(cudaMemcpy(&info, Lc.info, sizeof(int), cudaMemcpyDeviceToHost));
   if (info != 0) throw StErr{ST_E_BREAKDOWN, "coarsest-level matrix singular (pivot " + std::to_string(info) + ")"};
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
   c->stats.setup_ms = ms;
+  c->stats.setups += 1;
   c->have_ops = true;
+}
+
+// source vector f (Q~ = Q tau) into `out` (one write pass, per call: no
+// full-length vector is kept for it)
+void make_source(st_ctx* c, double* out) {
+  launch_source(c->lv[0].g, c->src.kind, c->src.Q0 * c->grid.tau, c->src.a, c->src.w, c->grid.tau, out, c->stream);
+  L(c);
+  check_launch();
+}
+
+// eliminated forward RHS b = m_f (f - K xD) + m_c xD (R-1) into `out`; needs the level-0
+// operator bound (prepare) when T0 != 0; pool slots 0 and 1 are scratch
+void make_forward_rhs(st_ctx* c, double* out) {
+  const Geom& g0 = c->lv[0].g;
+  make_source(c, out);
+  if (c->bcs.T0 != 0.0) {
+    double* xd = pool(c, 0);
+    double* kxd = pool(c, 1);
+    launch_xd(g0, c->bcs.T0, xd, c->stream);
+    op_launch(c, 0, MODE_APPLY, false, false, xd, nullptr, kxd);
+    launch_rhs_combine(g0, out, kxd, c->bcs.T0, out, c->stream);
+    L(c, 2);
+  } else {
+    launch_rhs_combine(g0, out, nullptr, 0.0, out, c->stream);
+    L(c);
+  }
+  check_launch();
 }
 
 void prepare(st_ctx* c, const double* rho) {
@@ -768,7 +762,8 @@ void prepare(st_ctx* c, const double* rho) {
 // ---------------------------------------------------------------------------------------
 // V-cycle: damped-Jacobi pre-smoothing from zero, residual,
 // restriction, recursion, prolongation + correction, post-smoothing; coarsest: exact.
-void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_graph = false);
+// r0: scratch for the level-0 residual (a free Krylov-pool slot; level 0 owns no residual vector)
+void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_graph = false, double* r0 = nullptr);
 
 // levels >= gl0 as one CUDA graph launch (launch latency dominates there)
 bool vcycle_graph(st_ctx* c, int l, bool trans, const double* b, double* x) {
@@ -793,116 +788,105 @@ bool vcycle_graph(st_ctx* c, int l, bool trans, const double* b, double* x) {
   return true;
 }
 
-// GMRES(k)-Jacobi smoother (the paper's smoother; option ST_SMOOTH_GMRES):
+// GMRES(k) with right Jacobi preconditioning on level l: the paper's smoother
+// (option ST_SMOOTH_GMRES, k = nu_pre from x = 0 / nu_post from x) and the paper's coarsest-level
+// solve (option ST_COARSE_GMRES: k = coarse_maxit <= 200 from x = 0, stop at coarse_rtol = 1e-6).
 // x <- x + D^-1 V y with V the Arnoldi basis of A D^-1 from r0 = b - A x and y minimising
-// ||beta e1 - H y|| (right Jacobi preconditioning, classical Gram-Schmidt). k = nu_pre (from
-// x = 0) or nu_post fixed steps, without the paper's inner rtol 1e-6 (10 steps rarely reach it):
-// every step stays on the device — no host synchronisation, so the small levels keep their CUDA
-// graph. Vectors: the basis Lv.gv, z = D^-1 V_j in Lv.t (read as the x tile of the apply), u = V y
-// in V_k (unused by y).
-void gmres_smooth(st_ctx* c, int l, bool trans, const double* b, double* x, bool from_zero) {
+// ||beta e1 - H y|| (classical Gram-Schmidt). The Hessenberg, Givens rotations and the triangular
+// solve stay on the device (gm_*_kernel, csrc/krylov.cu). rtol = 0: exactly k steps, no host
+// synchronisation (the small levels keep their CUDA graph); rtol > 0: the residual estimate |g_{j+1}|
+// is read back every `chk` steps and the iteration stops once |g_{j+1}| <= rtol ||r0|| (host
+// decisions: no graph). Vectors: the basis Lv.gv, z = D^-1 V_j in Lv.t (read as the x tile of the
+// apply), u = V y in the first unused basis slot. st: device state (gm_layout(k)); dd: dot scratch
+// (k + 2 doubles, then the norm at dd[kMaxBasis + 8] and ||r0||^2 at dd[kMaxBasis + 16]).
+// Returns the steps taken.
+int gmres_jacobi(st_ctx* c, int l, bool trans, const double* b, double* x, bool from_zero, int k, double rtol,
+                 double* st, double* dd, double* rl, int chk = 4) {
   Level& Lv = c->lv[l];
-  const int k = from_zero ? c->opt.nu_pre : c->opt.nu_post;
-  if (k <= 0) return;
+  if (k <= 0) return 0;
   const long long N = Lv.g.N, ld = Lv.gld;
   double* V = Lv.gv;
   double* z = Lv.t;
-  double* st = c->gsm;
-  double* dd = c->gsm + 768;  // dots: [0..k+1], ||w'||^2 at +64
+  double* dn = dd + kMaxBasis + 8;
+  double* d0 = dd + kMaxBasis + 16;
   const double* r0 = b;
   if (!from_zero) {
-    op_launch(c, l, MODE_RESID, trans, true, x, b, Lv.r);
-    r0 = Lv.r;
+    op_launch(c, l, MODE_RESID, trans, true, x, b, rl);
+    r0 = rl;
   }
-  launch_mdot(r0, nullptr, 0, 0, N, dd, c->ws, c->stream);
-  launch_gm_init(st, k, dd, c->stream);
-  launch_scale_dev(r0, V, dd, N, c->stream);
+  launch_mdot(r0, nullptr, 0, 0, N, d0, c->ws, c->stream);
+  launch_gm_init(st, k, d0, c->stream);
+  launch_scale_dev(r0, V, d0, N, c->stream);
   L(c, 3);
+  int jend = k;
   for (int j = 0; j < k; ++j) {
     double* vj = V + (long long)j * ld;
     double* w = V + (long long)(j + 1) * ld;
     launch_op(Lv.op, MODE_JAC0, trans, true, nullptr, vj, z, 1.0, c->stream);  // z = D^-1 V_j
     op_launch(c, l, MODE_APPLY, trans, true, z, nullptr, w);                   // w = A z
     launch_mdot(w, V, ld, j + 1, N, dd, c->ws, c->stream);                     // h = V^T w
-    launch_maxpy_norm(w, V, ld, j + 1, dd, nullptr, N, dd + 64, c->ws, c->stream);  // w -= V h
-    launch_gm_col(st, k, j, dd, dd + 64, c->stream);
-    launch_scale_dev(w, w, dd + 64, N, c->stream);                             // V_{j+1} = w / ||w||
+    launch_maxpy_norm(w, V, ld, j + 1, dd, nullptr, N, dn, c->ws, c->stream);  // w -= V h, ||w||^2
+    launch_gm_col(st, k, j, dd, dn, c->stream);
+    launch_scale_dev(w, w, dn, N, c->stream);                                  // V_{j+1} = w / ||w||
     L(c, 5 + (j + 16) / 16);
+    if (rtol > 0.0 && ((j + 1) % chk == 0 || j + 1 == k)) {
+      CK(cudaMemcpyAsync(c->hsmall + 470, st + j + 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(c->hsmall + 471, d0, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      const double res = std::fabs(c->hsmall[470]), beta = std::sqrt(std::max(c->hsmall[471], 0.0));
+      if (!(res > rtol * beta)) {  // converged (or a non-finite estimate: stop and use what we have)
+        jend = j + 1;
+        break;
+      }
+    }
   }
-  launch_gm_solve(st, k, c->stream);
-  double* u = V + (long long)k * ld;
+  launch_gm_solve(st, k, jend, c->stream);
+  double* u = V + (long long)jend * ld;
   CK(cudaMemsetAsync(u, 0, (size_t)N * sizeof(double), c->stream));
-  launch_lincomb(u, V, ld, k, st + gm_y_offset(k), N, c->stream);              // u = V y
+  launch_lincomb(u, V, ld, jend, st + gm_y_offset(k), N, c->stream);           // u = V y
   L(c, 2);
   if (from_zero) {
     launch_op(Lv.op, MODE_JAC0, trans, true, nullptr, u, x, 1.0, c->stream);   // x = D^-1 u
     L(c);
   } else {
     launch_op(Lv.op, MODE_JAC0, trans, true, nullptr, u, z, 1.0, c->stream);
-    launch_lincomb(x, z, 0, 1, c->gsm + 1000, N, c->stream);                   // x += z (gsm[1000] = 1)
+    launch_lincomb(x, z, 0, 1, c->dsmall + 510, N, c->stream);                 // x += z (dsmall[510] = 1)
     L(c, 2);
   }
   check_launch();
+  return jend;
 }
 
-void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_graph) {
+void gmres_smooth(st_ctx* c, int l, bool trans, const double* b, double* x, bool from_zero, double* rl) {
+  const int k = from_zero ? c->opt.nu_pre : c->opt.nu_post;
+  gmres_jacobi(c, l, trans, b, x, from_zero, k, c->opt.smoother_rtol, c->gsm, c->gsm + 1024, rl, 1);
+}
+
+void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_graph, double* r0) {
   Level& Lv = c->lv[l];
-  if (l == c->vt0 && b == Lv.b && x == Lv.x) {  // the small-level tail: one CTA, shared memory
-    SmallCycle cyc{};
-    cyc.nlev = (int)c->lv.size() - l;
-    cyc.npre = c->opt.nu_coarse > 0 ? c->opt.nu_coarse : c->opt.nu_pre;    // the tail holds coarse levels
-    cyc.npost = c->opt.nu_coarse > 0 ? c->opt.nu_coarse : c->opt.nu_post;
-    for (int k = 0; k < cyc.nlev; ++k) {
-      const Level& S = c->lv[l + k];
-      SmallLevel& d = cyc.L[k];
-      d.op = S.op;
-      d.x = S.x; d.b = S.b; d.r = S.r; d.t = S.t;
-      d.kind = S.kind;
-      d.dense = S.dense ? 1 : 0;
-      d.omega = S.omega > 0.0 ? S.omega : c->opt.omega;
-      d.Ainv = S.Ainv;
-    }
-    launch_vtail(cyc, c->sd, trans, c->stream);
-    L(c);
-    check_launch();
-    return;
-  }
-  if (l == c->vs0 && b == Lv.b && x == Lv.x) {  // the small-level tail: one cluster kernel
-    SmallCycle cyc{};
-    cyc.nlev = (int)c->lv.size() - l;
-    cyc.npre = c->opt.nu_coarse > 0 ? c->opt.nu_coarse : c->opt.nu_pre;    // the tail holds coarse levels
-    cyc.npost = c->opt.nu_coarse > 0 ? c->opt.nu_coarse : c->opt.nu_post;
-    for (int k = 0; k < cyc.nlev; ++k) {
-      const Level& S = c->lv[l + k];
-      SmallLevel& d = cyc.L[k];
-      d.op = S.op;
-      d.x = S.x; d.b = S.b; d.r = S.r; d.t = S.t;
-      d.kind = S.kind;
-      d.dense = S.dense ? 1 : 0;
-      d.omega = S.omega > 0.0 ? S.omega : c->opt.omega;
-      d.Ainv = S.Ainv;
-    }
-    launch_vsmall(cyc, c->sd, trans, c->stream);
-    L(c);
-    check_launch();
-    return;
-  }
+  double* rl = l == 0 ? r0 : Lv.r;
+  if (!rl) throw StErr{ST_E_INVALID_ARG, "internal: level-0 V-cycle without a residual scratch vector"};
   if (!in_graph && vcycle_graph(c, l, trans, b, x)) return;
   if (Lv.dense) {
     launch_dense_solve(Lv.Ainv, (int)Lv.g.N, trans, b, x, c->stream);
     L(c);
     return;
   }
+  if (Lv.cgm) {  // the paper's coarsest solve: GMRES(<= coarse_maxit)-Jacobi to coarse_rtol
+    c->coarse_its += gmres_jacobi(c, l, trans, b, x, true, c->opt.coarse_maxit, c->opt.coarse_rtol, c->cgs,
+                                  c->cgs + gm_y_offset(c->opt.coarse_maxit) + c->opt.coarse_maxit + 32, Lv.r);
+    return;
+  }
   Level& Nx = c->lv[l + 1];
   if (c->opt.smoother == ST_SMOOTH_GMRES) {  // one replicated level (slabs are rejected at setup)
-    gmres_smooth(c, l, trans, b, x, true);
-    op_launch(c, l, MODE_RESID, trans, true, x, b, Lv.r);
-    launch_restrict(Lv.g, Nx.g, Nx.kind, Lv.r, Nx.b, c->stream);
+    gmres_smooth(c, l, trans, b, x, true, rl);
+    op_launch(c, l, MODE_RESID, trans, true, x, b, rl);
+    launch_restrict(Lv.g, Nx.g, Nx.kind, rl, Nx.b, c->stream);
     L(c);
     vcycle(c, l + 1, trans, Nx.b, Nx.x, in_graph);
     launch_prolong_add(Lv.g, Nx.g, Nx.kind, Nx.x, x, c->stream);
     L(c);
-    gmres_smooth(c, l, trans, b, x, false);
+    gmres_smooth(c, l, trans, b, x, false, rl);
     return;
   }
   const int npre = (l > 0 && c->opt.nu_coarse > 0) ? c->opt.nu_coarse : c->opt.nu_pre;
@@ -917,23 +901,24 @@ void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_gr
     halo(c, l, oth);
     std::swap(cur, oth);
   }
-  op_launch(c, l, MODE_RESID, trans, true, cur, b, Lv.r);
-  if (Nx.kind == KIND_TIME) halo(c, l, Lv.r);  // time restriction reads the next slab's first plane
+  op_launch(c, l, MODE_RESID, trans, true, cur, b, rl);
+  if (Nx.kind == KIND_TIME) halo(c, l, rl);  // time restriction reads the next slab's first plane
   if (Nx.gather_in) {  // agglomeration: restrict in slab form, gather onto every rank
-    launch_restrict(Lv.g, Nx.gs, Nx.kind, Lv.r, Nx.bpart, c->stream);
+    launch_restrict(Lv.g, Nx.gs, Nx.kind, rl, Nx.bpart, c->stream);
     L(c);
     gather_planes(c, Nx, Nx.bpart, Nx.b);
   } else {
-    launch_restrict(Lv.g, Nx.g, Nx.kind, Lv.r, Nx.b, c->stream);
+    launch_restrict(Lv.g, Nx.g, Nx.kind, rl, Nx.b, c->stream);
     L(c);
   }
   vcycle(c, l + 1, trans, Nx.b, Nx.x, in_graph);
   // prolongation + correction, fused into the first post-sweep where the level kernel can read
-  // x + P e itself (tc2d, space-coarsened next level, one GPU; ST_NO_PRO=1: separate kernels)
+  // x + P e itself (tc2d, space-coarsened next level, one GPU; options fuse_prolong = 0: separate kernels)
   int s0 = 0;
   // not on level 0: there the fused sweep (201 us) costs more than sweep + prolongation (90 + 45 us;
   // profiles/r01/launches_c2_v42_summary.txt) — the correction pass weighs on an issue-bound kernel
-  if (l > 0 && npost > 0 && c->pro_fuse && Nx.kind == KIND_SPACE && c->comm.size <= 1 && c->fast && c->fast_kind == 0 &&
+  if (l > 0 && npost > 0 && c->opt.fuse_prolong && Nx.kind == KIND_SPACE && c->comm.size <= 1 &&
+      c->opt.kernel_family == ST_KERNELS_TMA &&
       launch_op_tc2d_pro(Lv.op, Nx.g, trans, cur, Nx.x, b, oth, Lv.omega > 0.0 ? Lv.omega : c->opt.omega, c->stream)) {
     L(c);
     std::swap(cur, oth);
@@ -955,7 +940,9 @@ void sync_small(st_ctx* c, int off, int n) {
   CK(cudaStreamSynchronize(c->stream));
 }
 
-// FGMRES(m), right preconditioned by one V-cycle (Saad 1993). Classical
+// FGMRES(m), right preconditioned by one V-cycle (Saad 1993); with options krylov =
+// ST_KRYLOV_GMRES the same Arnoldi process without the Z vectors: z_j = M V_j goes to one scratch
+// vector and the cycle ends with x += M (V y) (one more V-cycle; M is a fixed linear map). Classical
 // Gram-Schmidt (fused multi-dot + fused multi-AXPY) with one conditional re-orthogonalisation
 // (DGKS, eta = 0.1: st_ctx::dgks_eta2). Convergence on the TRUE relative residual ||b - A x|| / ||b|| <= rtol (R-14).
 // The Arnoldi vectors are stored unnormalised, v_i = sg_i V_i: the V-cycle and the operator are
@@ -970,6 +957,7 @@ int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
   double* dh = c->dsmall;        // [0..63] g, [64..127] reorth g, [128..191] y, [256..319] sg^2
   double* hh = c->hsmall;
   double* ds2 = dh + 256;
+  const bool flex = c->opt.krylov == ST_KRYLOV_FGMRES;
   std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), gv(m + 1), y(m), sg(m + 1);
   CK(cudaEventRecord(c->e0, c->stream));
   // ||b||
@@ -978,7 +966,7 @@ int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
   allreduce(c, dh + 200, 1);
   sync_small(c, 200, 1);
   const double bnorm = std::sqrt(hh[200]);
-  int its = 0, restarts = 0, status = ST_OK;
+  int its = 0, restarts = 0, status = ST_OK, nvc = 0;
   double relres = 0.0;
   bool conv = false;
   if (bnorm == 0.0) {
@@ -1005,9 +993,10 @@ int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
     int jend = 0;
     for (int j = 0; j < m; ++j) {
       double* vj = c->V + (long long)j * ld;
-      double* zj = c->Z + (long long)j * ld;
+      double* zj = flex ? c->Z + (long long)j * ld : c->Z;
       double* w = c->V + (long long)(j + 1) * ld;
-      vcycle(c, 0, trans, vj, zj);                                       // Z_j = M V_j
+      vcycle(c, 0, trans, vj, zj, false, w);                             // Z_j = M V_j (W: scratch)
+      ++nvc;
       op_launch(c, 0, MODE_APPLY, trans, true, zj, nullptr, w);         // W = A Z_j
       launch_mdot(w + vo, c->V + vo, ld, j + 1, N, dh, c->ws, c->stream);  // g_i = V_i . W, ||W||^2
       allreduce(c, dh, j + 2);
@@ -1077,8 +1066,19 @@ int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
     }
     for (int i = 0; i < jend; ++i) hh[128 + i] = y[i] * sg[i];
     CK(cudaMemcpyAsync(dh + 128, hh + 128, jend * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    launch_lincomb(x + vo, c->Z + vo, ld, jend, dh + 128, N, c->stream);
-    L(c);
+    if (flex) {
+      launch_lincomb(x + vo, c->Z + vo, ld, jend, dh + 128, N, c->stream);
+      L(c);
+    } else {  // u = V (y sg) into the z scratch, then x += M u (V_0 receives M u, V_1 is scratch)
+      double* u = c->Z;
+      CK(cudaMemsetAsync(u, 0, (size_t)c->N * sizeof(double), c->stream));
+      launch_lincomb(u + vo, c->V + vo, ld, jend, dh + 128, N, c->stream);
+      L(c);
+      vcycle(c, 0, trans, u, c->V, false, c->V + ld);
+      ++nvc;
+      launch_lincomb(x + vo, c->V + vo, 0, 1, dh + 510, N, c->stream);  // dsmall[510] = 1
+      L(c);
+    }
     check_launch();
     halo(c, 0, x);
     ++restarts;
@@ -1091,6 +1091,7 @@ int fgmres(st_ctx* c, bool trans, const double* b, double* x) {
   c->stats.solve_ms = ms;
   c->stats.iterations = its;
   c->stats.restarts = restarts;
+  c->stats.vcycles = nvc;
   c->stats.rel_residual = relres;
   c->stats.converged = conv ? 1 : 0;
   c->stats.n_levels = (int)c->lv.size();
@@ -1177,6 +1178,7 @@ void free_ctx(st_ctx* c) {
   if (c->hsmall) cudaFreeHost(c->hsmall);
   cudaFree(c->rho_stage);
   cudaFree(c->gsm);
+  cudaFree(c->cgs);
   cudaFree(c->kt);
   comm_release(c->comm);
   cudaFree(c->fbuf);
@@ -1219,6 +1221,19 @@ void st_default_options(st_options_t* o) {
   o->use_graphs = 1;
   o->verbose = 0;
   o->agg_nodes = 16384;
+  o->krylov = ST_KRYLOV_FGMRES;
+  o->coarse_solver = ST_COARSE_DENSE;
+  o->coarse_rtol = 1e-6;
+  o->coarse_maxit = 200;
+  o->kernel_family = ST_KERNELS_TMA;
+  o->chunk_planes = 0;
+  o->max_ctas = 0;
+  o->fuse_prolong = 1;
+  o->fuse_restrict = 1;
+  o->omega_factor = 1.9;
+  o->dgks_eta = 0.1;
+  o->graph_max_nodes = 0;
+  o->smoother_rtol = 0.0;
 }
 
 const char* st_strerror(int code) {
@@ -1279,12 +1294,21 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       if (c->opt.smoother == ST_SMOOTH_GMRES && (c->opt.nu_pre > 24 || c->opt.nu_post > 24))
         throw StErr{ST_E_INVALID_ARG, "GMRES smoother: nu_pre, nu_post <= 24"};
       if (c->opt.coarse_max_nodes < 8) c->opt.coarse_max_nodes = 8;
-      {  // kernel family (test / bench hook): ST_NO_FAST=1 -> generic kernels; ST_FAST_KIND=1 -> cp.async
-        const char* e = getenv("ST_NO_FAST");
-        c->fast = !(e && e[0] == '1');
-        e = getenv("ST_FAST_KIND");
-        c->fast_kind = e ? atoi(e) : 0;
-      }
+      if (c->opt.kernel_family < ST_KERNELS_TMA || c->opt.kernel_family > ST_KERNELS_TMA2D)
+        throw StErr{ST_E_INVALID_ARG, "kernel_family: ST_KERNELS_*"};
+      if (c->opt.krylov != ST_KRYLOV_FGMRES && c->opt.krylov != ST_KRYLOV_GMRES)
+        throw StErr{ST_E_INVALID_ARG, "krylov: ST_KRYLOV_FGMRES or ST_KRYLOV_GMRES"};
+      if (c->opt.krylov == ST_KRYLOV_GMRES && c->opt.smoother != ST_SMOOTH_JACOBI)
+        throw StErr{ST_E_UNSUPPORTED, "ST_KRYLOV_GMRES needs a fixed linear preconditioner (ST_SMOOTH_JACOBI)"};
+      if (c->opt.coarse_solver != ST_COARSE_DENSE && c->opt.coarse_solver != ST_COARSE_GMRES)
+        throw StErr{ST_E_INVALID_ARG, "coarse_solver: ST_COARSE_DENSE or ST_COARSE_GMRES"};
+      if (c->opt.krylov == ST_KRYLOV_GMRES && c->opt.coarse_solver != ST_COARSE_DENSE)
+        throw StErr{ST_E_UNSUPPORTED, "ST_KRYLOV_GMRES needs a fixed linear preconditioner (ST_COARSE_DENSE)"};
+      if (c->opt.coarse_rtol <= 0.0) c->opt.coarse_rtol = 1e-6;
+      if (c->opt.coarse_maxit <= 0) c->opt.coarse_maxit = 200;
+      if (c->opt.coarse_maxit >= kMaxBasis) throw StErr{ST_E_INVALID_ARG, "coarse_maxit must be < 256"};
+      if (c->opt.dgks_eta == 0.0) c->opt.dgks_eta = 0.1;
+      c->dgks_eta2 = c->opt.dgks_eta > 0.0 ? c->opt.dgks_eta * c->opt.dgks_eta : 0.0;
       CK(cudaGetDevice(&c->device));
       if (dist && dist->device >= 0) {
         c->device = dist->device;
@@ -1330,13 +1354,8 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       for (int d = 0; d < c->sd; ++d) nsp *= grid->n;
       c->ndesign = c->tc ? nsp : nsp * L0.g.nt;   // space-time: owned layers + the ghost layer
       allocate(c);
-      dalloc(&c->rho_stage, c->ndesign);
       if (c->sd == 2 && !c->tc)  // padded k~ table (launch_ktilde)
         dalloc(&c->kt, (long long)(grid->n + 2) * (grid->n + 2) * (L0.g.nt + 1));
-      // source vector f: Q~ = Q tau
-      launch_source(c->lv[0].g, src->kind, src->Q0 * grid->tau, src->a, src->w, grid->tau, c->f, c->stream);
-      L(c);
-      check_launch();
       CK(cudaStreamSynchronize(c->stream));
     } catch (...) {
       free_ctx(c);
@@ -1354,11 +1373,12 @@ int st_solve(st_ctx_t* c, const double* rho, double* T) {
     if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
     CK(cudaSetDevice(c->device));
     prepare(c, rho);
+    make_forward_rhs(c, c->rhs);
     pack_in(c, T, c->xint, 0);
     launch_set_bc_values(c->lv[0].g, c->bcs.T0, c->xint, c->stream);  // x_c = xD
     L(c, 2);
     halo(c, 0, c->xint);
-    int rc = fgmres(c, false, c->b, c->xint);
+    int rc = fgmres(c, false, c->rhs, c->xint);
     unpack_out(c, c->xint, T, 0);
     return rc;
   });
@@ -1369,13 +1389,14 @@ int st_adjoint(st_ctx_t* c, const double* rho, const double* dJdT, double* lambd
     if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
     CK(cudaSetDevice(c->device));
     prepare(c, rho);
-    pack_in(c, dJdT, c->tmpN2, 1);
-    launch_mask_free(c->lv[0].g, c->tmpN2, c->tmpN2, c->stream);  // RHS m_f g
+    if (dJdT) pack_in(c, dJdT, c->rhs, 1);
+    else make_source(c, c->rhs);  // null dJdT: the compliance f^T T, dphi/dT = f (R-8)
+    launch_mask_free(c->lv[0].g, c->rhs, c->rhs, c->stream);  // RHS m_f g
     pack_in(c, lambda, c->xint, 0);
     launch_set_bc_values(c->lv[0].g, 0.0, c->xint, c->stream);  // lambda_c = 0
     L(c, 4);
     halo(c, 0, c->xint);
-    int rc = fgmres(c, true, c->tmpN2, c->xint);
+    int rc = fgmres(c, true, c->rhs, c->xint);
     unpack_out(c, c->xint, lambda, 0);
     return rc;
   });
@@ -1385,14 +1406,12 @@ int st_sensitivity(st_ctx_t* c, const double* rho, const double* T, const double
   return guarded([&]() -> int {
     if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
     CK(cudaSetDevice(c->device));
-    const double* r = rho;
-    if (!is_device_ptr(rho)) {
-      CK(cudaMemcpyAsync(c->rho_stage, rho, c->ndesign * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-      r = c->rho_stage;
-    }
+    const double* r = rho_device(c, rho);
     // T and lambda into internal slab vectors with ghost planes (element layers of this rank)
-    pack_in(c, T, c->tmpN, 1, true);
-    pack_in(c, lambda, c->tmpN2, 2, true);
+    double* Ti = pool(c, 0);
+    double* li = pool(c, 1);
+    pack_in(c, T, Ti, 1, true);
+    pack_in(c, lambda, li, 2, true);
     const Level& L0 = c->lv[0];
     OpDesc op = L0.op;
     op.rho = r;
@@ -1402,7 +1421,7 @@ int st_sensitivity(st_ctx_t* c, const double* rho, const double* T, const double
     const long long ndj = c->tc ? nsp : nsp * op.g.nt;
     bool staged = false;
     double* dj = out_ptr(c, dJ, ndj, 3, false, &staged);
-    launch_sensitivity(op, c->tmpN, c->tmpN2, dj, c->stream);
+    launch_sensitivity(op, Ti, li, dj, c->stream);
     L(c);
     check_launch();
     if (c->tc) allreduce(c, dj, ndj);  // time-constant design: sum through time over all slabs
@@ -1431,16 +1450,12 @@ int st_apply(st_ctx_t* c, const double* rho, const double* x, double* y, int tra
   return guarded([&]() -> int {
     if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
     CK(cudaSetDevice(c->device));
-    const double* r = rho;
-    if (!is_device_ptr(rho)) {
-      CK(cudaMemcpyAsync(c->rho_stage, rho, c->ndesign * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-      r = c->rho_stage;
-    }
+    const double* r = rho_device(c, rho);
     set_fine_rho(c, r);
     c->kt_design = false;  // the table now follows r, not necessarily the cached design
-    pack_in(c, x, c->tmpN, 1, true);
-    masked_level_apply(c, 0, c->tmpN, c->tmpN2, c->lv[0].t, transpose != 0, bc != 0);
-    unpack_out(c, c->lv[0].t, y, 2);
+    pack_in(c, x, pool(c, 0), 1, true);
+    masked_level_apply(c, 0, pool(c, 0), pool(c, 1), pool(c, 2), transpose != 0, bc != 0);
+    unpack_out(c, pool(c, 2), y, 2);
     return ST_OK;
   });
 }
@@ -1455,8 +1470,8 @@ int st_level_apply(st_ctx_t* c, const double* rho, int level, const double* x, d
     Level& Lv = c->lv[level];
     const Geom gd = dense_of(Lv.g);
     const long long nd = nodes_of(Lv.g);
-    double* xi = level == 0 ? c->tmpN : Lv.x;
-    double* xm = level == 0 ? c->tmpN2 : Lv.b;
+    double* xi = level == 0 ? pool(c, 0) : Lv.x;
+    double* xm = level == 0 ? pool(c, 1) : Lv.b;
     const double* xd = in_ptr(c, x, nd, 1);
     launch_relayout(gd, xd, Lv.g, xi, c->stream);
     L(c);
@@ -1477,11 +1492,11 @@ int st_vcycle(st_ctx_t* c, const double* rho, const double* b, double* z, int tr
     if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
     CK(cudaSetDevice(c->device));
     prepare(c, rho);
-    pack_in(c, b, c->tmpN2, 1);
-    launch_mask_free(c->lv[0].g, c->tmpN2, c->tmpN2, c->stream);  // the solver's vectors vanish there
+    pack_in(c, b, pool(c, 1), 1);
+    launch_mask_free(c->lv[0].g, pool(c, 1), pool(c, 1), c->stream);  // the solver's vectors vanish there
     L(c);
-    vcycle(c, 0, transpose != 0, c->tmpN2, c->tmpN);
-    unpack_out(c, c->tmpN, z, 2);
+    vcycle(c, 0, transpose != 0, pool(c, 1), pool(c, 0), false, pool(c, 2));
+    unpack_out(c, pool(c, 0), z, 2);
     return ST_OK;
   });
 }
@@ -1591,10 +1606,11 @@ int st_pnorm(st_ctx_t* c, const double* T, double P, double* phi, double* dphidT
     if (!c || !T || !phi) throw StErr{ST_E_INVALID_ARG, "null argument"};
     if (!(P >= 1.0)) throw StErr{ST_E_INVALID_ARG, "P must be >= 1"};
     CK(cudaSetDevice(c->device));
-    pack_in(c, T, c->tmpN, 1, true);  // with ghost planes: elements of the slab boundary planes
+    double* Ti = pool(c, 0);
+    pack_in(c, T, Ti, 1, true);  // with ghost planes: elements of the slab boundary planes
     const Level& L0 = c->lv[0];
     const int nl = L0.dist ? L0.nloc : L0.g.nt;
-    launch_pnorm_sum(L0.g, nl, c->tmpN, P, c->ws.partial, c->ws.counter, c->dsmall + 486, c->stream);
+    launch_pnorm_sum(L0.g, nl, Ti, P, c->ws.partial, c->ws.counter, c->dsmall + 486, c->stream);
     L(c);
     allreduce(c, c->dsmall + 486, 1);
     sync_small(c, 486, 1);
@@ -1602,10 +1618,10 @@ int st_pnorm(st_ctx_t* c, const double* T, double P, double* phi, double* dphidT
     *phi = std::pow(theta, 1.0 / P);
     if (dphidT) {
       const double scale = std::pow(theta, (1.0 - P) / P) / (double)(1 << (c->sd + 1));
-      launch_pnorm_grad(L0.g, c->o0, c->nown, L0.ntg, c->tmpN, P, scale, c->tmpN2, c->stream);
+      launch_pnorm_grad(L0.g, c->o0, c->nown, L0.ntg, Ti, P, scale, pool(c, 1), c->stream);
       L(c);
       check_launch();
-      unpack_out(c, c->tmpN2, dphidT, 2);
+      unpack_out(c, pool(c, 1), dphidT, 2);
     } else {
       CK(cudaStreamSynchronize(c->stream));
     }
@@ -1633,8 +1649,14 @@ int st_rhs(st_ctx_t* c, const double* rho, double* f, double* b) {
     if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
     CK(cudaSetDevice(c->device));
     prepare(c, rho);
-    if (f) unpack_out(c, c->f, f, 2);
-    if (b) unpack_out(c, c->b, b, 2);
+    if (f) {
+      make_source(c, pool(c, 2));
+      unpack_out(c, pool(c, 2), f, 2);
+    }
+    if (b) {
+      make_forward_rhs(c, pool(c, 2));
+      unpack_out(c, pool(c, 2), b, 2);
+    }
     CK(cudaStreamSynchronize(c->stream));
     return ST_OK;
   });
@@ -1656,8 +1678,8 @@ int st_bench_op(st_ctx_t* c, const double* rho, int level, int mode, int transpo
       prepare(c, rho);
     }
     Level& Lv = c->lv[level];
-    double* x = level == 0 ? c->tmpN : Lv.x;
-    double* b = level == 0 ? c->tmpN2 : Lv.b;
+    double* x = level == 0 ? pool(c, 0) : Lv.x;
+    double* b = level == 0 ? pool(c, 1) : Lv.b;
     for (int r = 0; r < reps; ++r) op_launch(c, level, mode, transpose != 0, true, x, b, Lv.t);
     check_launch();
     return ST_OK;

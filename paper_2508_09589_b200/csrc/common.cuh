@@ -13,7 +13,6 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
-#include <stdlib.h>
 
 namespace st {
 
@@ -54,6 +53,11 @@ struct OpDesc {
   const double* st;       // MK: [nl][2][NC][P]; B4: [nl][5][NC][P] = M, Kbb, Kbt, Ktb, Ktt
   int msep;               // MK: the stored M equals msc x (Q1 mass pattern of this grid), i.e. the
   double msc;             //     separable [1,4,1] (x) [1,4,1] stencil (uniform capacity; nested spaces)
+  // kernel selection and persistent-schedule controls (st_options_t: kernel_family, chunk_planes,
+  // max_ctas), read per launch
+  int family;             // ST_KERNELS_* (st.h)
+  int chunk;              // planes per time chunk: 0 automatic, > 0 forced, < 0 no chunking
+  int max_ctas;           // cap on the persistent grid (0: one full wave)
 };
 
 template <int SD> struct SG {
@@ -148,42 +152,25 @@ __device__ __forceinline__ void work_segment(long long w, long long wend, long l
   *p1 = (rem < ce - *p0) ? *p0 + (int)rem : ce;
 }
 
-// tile order inside a chunk for the (2+1)D kernels: 0 = row-major (x fastest), 1 = column-major
-// (consecutive tiles of a run are y-neighbours: the 2 halo rows of a 32 x 8 tile cost more than
-// its 4 halo columns). ST_TILE_ORDER selects it (experiments).
-inline int tile_order() {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("ST_TILE_ORDER");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
+// planes per time chunk of a persistent stencil kernel's work list: the option when forced
+// (op.chunk > 0), one chunk (tile-major order) when chunking is off (op.chunk < 0), else the
+// kernel's automatic choice `auto_k` (only tv2d chunks automatically)
+inline int chunk_planes(const OpDesc& op, int NP, int auto_k) {
+  if (op.chunk > 0) return op.chunk < NP ? op.chunk : NP;
+  if (op.chunk < 0) return NP;
+  return auto_k < 1 ? 1 : (auto_k < NP ? auto_k : NP);
 }
 
-// planes per chunk: the chunk's x and b planes (2 x K x P doubles) within `mb` MB of L2; mb <= 0:
-// one chunk (tile-major order, the default). Measured (profiles/r01): chunking cuts the (3+1)D
-// kernel's DRAM reads 1.57 -> 1.20 GB per sweep but makes it 5x slower (a segment restart per
-// chunk and tile: pipeline fill + weight rebuild), and (2+1)D traffic is already the algorithmic
-// bytes. ST_CHUNK_MB enables it (experiments).
-inline int chunk_planes(long long P, int NP, int sd) {
-  static int env_mb = -2;
-  if (env_mb == -2) {
-    const char* e = getenv("ST_CHUNK_MB");
-    env_mb = e ? atoi(e) : -1;
-  }
-  static int env_k = -2;
-  if (env_k == -2) {
-    const char* e = getenv("ST_CHUNK_K");  // planes per chunk (experiments; overrides ST_CHUNK_MB)
-    env_k = e ? atoi(e) : -1;
-  }
-  if (env_k > 0) return env_k < NP ? env_k : NP;
-  const long long mb = env_mb >= 0 ? env_mb : 0;
-  (void)sd;
-  if (mb <= 0) return NP;
-  long long K = mb * 1000000LL / (16LL * P);
-  if (K < 8) K = 8;
-  if (K > NP) K = NP;
-  return (int)K;
+// persistent grid: one wave (nsm x resident CTAs), at most wtot / minw CTAs, at most op.max_ctas
+inline long long persistent_grid(const OpDesc& op, int nsm, int resident, long long wtot) {
+  long long grid = (long long)nsm * resident;
+  // large levels: >= 4 planes per CTA (one reload plane per segment); small levels: every CTA a
+  // short chain so that the TMA round trips of a level overlap (launch-latency bound there)
+  const long long minw = (wtot >= 16LL * nsm * resident) ? 4 : 1;
+  if (grid > wtot / minw) grid = wtot / minw;
+  if (op.max_ctas > 0 && grid > op.max_ctas) grid = op.max_ctas;
+  if (grid < 1) grid = 1;
+  return grid;
 }
 
 }  // namespace st

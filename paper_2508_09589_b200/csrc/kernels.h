@@ -15,9 +15,6 @@ bool launch_op_fast2d(const OpDesc& op, int mode, bool trans, bool mask, const d
 bool launch_op_tma2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                      double omega, cudaStream_t s);
 // tc2d.cu: lean TMA kernel for time-constant levels (fine from rho, stored MK), masked modes
-// one thread per node: small replicated time-constant (2+1)D levels with stored M, K (tiny2d.cu)
-bool launch_op_tiny2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
-                      double omega, cudaStream_t s);
 bool launch_op_tc2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                     double omega, cudaStream_t s);
 // damped-Jacobi sweep from x + P e, e the correction of a space-coarsened next level (2D, one GPU)
@@ -29,8 +26,6 @@ bool launch_op_tc3d(const OpDesc& op, int mode, bool trans, bool mask, const dou
 // tv2d.cu: fine level of a space-time design with uniform capacity (configs 1, 3, 5), masked modes
 bool launch_op_tv2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                     double omega, cudaStream_t s);
-extern bool g_use_fast;
-extern int g_fast_kind;  // 0: TMA, 1: cp.async (fast2d)
 void launch_rap_space(const OpDesc& fop, const Geom& gc, int nl, int ns, double* out, cudaStream_t s);
 void launch_rap_time(const OpDesc& fop, int nlc, double* out, cudaStream_t s);
 void launch_rho_to_mk(const OpDesc& fop, int tau, double* out, cudaStream_t s);
@@ -49,6 +44,7 @@ struct RedWs {
 };
 constexpr int kRedBlocks = 148 * 6;
 constexpr int kMaxDots = 17;
+constexpr int kMaxBasis = 256;  // longest basis of a multi-AXPY / linear combination (coarse GMRES(<= 255))
 // out[0..k-1] = V_j . w (j < k), out[k] = w . w
 void launch_mdot(const double* w, const double* V, long long ldv, int k, long long n, double* out, RedWs ws,
                  cudaStream_t s);
@@ -64,12 +60,13 @@ void launch_lincomb(double* x, const double* Z, long long ldz, int k, const doub
 // v = w / sqrt(nrm2[0]) (nrm2 on device) or v = alpha * w
 void launch_scale_dev(const double* w, double* v, const double* nrm2, long long n, cudaStream_t s);
 void launch_scale(const double* w, double* v, double alpha, long long n, cudaStream_t s);
-void launch_checksum(const double* a, long long n, double* out, RedWs ws, cudaStream_t s);
+// two 64-bit hashes of the bit patterns of a[0..n) (order-free sums; exact design-change detection)
+void launch_fingerprint(const double* a, long long n, unsigned long long* out, cudaStream_t s);
 // GMRES(k) smoother bookkeeping on the device (single-thread kernels): st holds g[k+1], the Givens
 // cs[k], sn[k], the Hessenberg H[k][k+1] and y[k] (at st + gm_y_offset(k)).
 void launch_gm_init(double* st, int k, const double* nrm2, cudaStream_t s);           // g = (||r0||, 0, ...)
 void launch_gm_col(double* st, int k, int j, const double* h, const double* nrm2w, cudaStream_t s);
-void launch_gm_solve(double* st, int k, cudaStream_t s);                              // y = R^-1 g
+void launch_gm_solve(double* st, int k, int mcols, cudaStream_t s);                  // y = R^-1 g (first mcols)
 int gm_y_offset(int k);
 
 // misc.cu
@@ -84,29 +81,9 @@ void launch_relayout(const Geom& gs, const double* src, const Geom& gd, double* 
 void launch_set_bc_values(const Geom& g, double T0, double* x, cudaStream_t s);          // x_c = xD
 void launch_rhs_combine(const Geom& g, const double* f, const double* KxD, double T0, double* b, cudaStream_t s);
 void launch_xd(const Geom& g, double T0, double* x, cudaStream_t s);
-void launch_hash_vec(const Geom& g, double* v, cudaStream_t s);                            // power-iteration start                      // x = xD (0 off plane 0)
 void launch_sensitivity(const OpDesc& op, const double* T, const double* lam, double* dJ, cudaStream_t s);
 void launch_dense_invert(double* A, double* Ainv, int n, int* info, cudaStream_t s);
 void launch_dense_solve(const double* Ainv, int n, bool trans, const double* b, double* x, cudaStream_t s);
-
-// vsmall.cu — the small-level tail of the V-cycle as one thread-block-cluster kernel
-constexpr int kMaxSmall = 12;
-struct SmallLevel {
-  OpDesc op;                    // replicated level (FORM_MK / FORM_B4), or the dense coarsest
-  double *x, *b, *r, *t;
-  int kind;                     // coarsening kind relative to the finer level
-  int dense;
-  double omega;
-  const double* Ainv;           // dense coarsest inverse
-};
-struct SmallCycle {
-  int nlev, npre, npost;
-  SmallLevel L[kMaxSmall];
-};
-void launch_vsmall(const SmallCycle& cyc, int sd, bool trans, cudaStream_t s);
-// single-CTA tail, every vector in shared memory (vtail_smem_bytes(cyc) <= 227 KB)
-size_t vtail_smem_bytes(const SmallCycle& cyc);
-void launch_vtail(const SmallCycle& cyc, int sd, bool trans, cudaStream_t s);
 
 // design.cu — config-5 design update (density filter, OC)
 void launch_filter(int sd, int n, int nl, int tdir, int lo_ok, int hi_ok, double r, const double* ghosted, double* out,

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kRedThreads) maxpy_norm_kernel(double* __restr
                                                                  long long ldv, int k, const double* __restrict__ h,
                                                                  const double* __restrict__ s2, long long n, double* out,
                                                                  RedWs ws) {
-  __shared__ double hs[128];
+  __shared__ double hs[kMaxBasis];
   for (int j = threadIdx.x; j < k; j += blockDim.x) hs[j] = s2 ? h[j] * s2[j] : h[j];
   __syncthreads();
   double acc[1] = {0.0};
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kRedThreads) maxpy_dots_kernel(double* __restr
 
 __global__ void lincomb_kernel(double* __restrict__ x, const double* __restrict__ Z, long long ldz, int k,
                                const double* __restrict__ y, long long n) {
-  __shared__ double ys[128];
+  __shared__ double ys[kMaxBasis];
   for (int j = threadIdx.x; j < k; j += blockDim.x) ys[j] = y[j];
   __syncthreads();
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -237,34 +237,50 @@ __global__ void gm_col_kernel(double* st, int k, int j, const double* h, const d
   g[j + 1] = -sn[j] * g[j];
   g[j] = cs[j] * g[j];
 }
-// y = R^-1 g (the rotated Hessenberg is upper triangular); a zero pivot (breakdown) gives y_i = 0
-__global__ void gm_solve_kernel(double* st, int k) {
+// y = R^-1 g over the first m columns (the rotated Hessenberg is upper triangular); a zero pivot
+// (breakdown) gives y_i = 0
+__global__ void gm_solve_kernel(double* st, int k, int mcols) {
   double *g, *cs, *sn, *H, *y;
   gm_layout(st, k, &g, &cs, &sn, &H, &y);
-  for (int i = k - 1; i >= 0; --i) {
+  for (int i = mcols - 1; i >= 0; --i) {
     double s = g[i];
-    for (int m = i + 1; m < k; ++m) s -= H[(long long)m * (k + 1) + i] * y[m];
+    for (int m = i + 1; m < mcols; ++m) s -= H[(long long)m * (k + 1) + i] * y[m];
     const double d = H[(long long)i * (k + 1) + i];
     y[i] = d != 0.0 ? s / d : 0.0;
   }
 }
 
-__device__ __forceinline__ double hash_weight(long long i) {
-  unsigned long long z = (unsigned long long)i * 0x9E3779B97F4A7C15ull;
-  z ^= z >> 31; z *= 0xBF58476D1CE4E5B9ull; z ^= z >> 27;
-  return 0.5 + (double)(z >> 11) * (1.0 / 9007199254740992.0);
+// Design fingerprint (exact change detection): two independent 64-bit hashes of the
+// element BIT PATTERNS, sum_i mix(bits(a_i), i) mod 2^64. Modular addition is order-free, so the
+// block-level atomics give a deterministic result; a change of any single element changes each
+// sum unless a 2^-64 collision occurs (no fp rounding can absorb a perturbation).
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z ^= z >> 30;
+  z *= 0xbf58476d1ce4e5b9ull;
+  z ^= z >> 27;
+  z *= 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return z;
 }
-
-__global__ void __launch_bounds__(kRedThreads) checksum_kernel(const double* __restrict__ a, long long n, double* out,
-                                                               RedWs ws) {
-  double acc[2] = {0.0, 0.0};
+__global__ void __launch_bounds__(kRedThreads) fingerprint_kernel(const double* __restrict__ a, long long n,
+                                                                  unsigned long long* out) {
+  unsigned long long h0 = 0, h1 = 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
-    double v = __ldg(a + i);
-    acc[0] += v;
-    acc[1] += v * hash_weight(i);
+    const unsigned long long v = (unsigned long long)__double_as_longlong(__ldg(a + i));
+    const unsigned long long k = (unsigned long long)i;
+    h0 += mix64(v + k * 0x9e3779b97f4a7c15ull);
+    h1 += mix64(v ^ mix64(k + 0x632be59bd9b4e019ull));
   }
-  block_partials<2>(acc, ws.partial, ws, out);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    h0 += __shfl_down_sync(0xffffffffu, h0, o);
+    h1 += __shfl_down_sync(0xffffffffu, h1, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out, h0);
+    atomicAdd(out + 1, h1);
+  }
 }
 
 static unsigned red_blocks(long long n) {
@@ -340,11 +356,12 @@ void launch_gm_init(double* st, int k, const double* nrm2, cudaStream_t s) { gm_
 void launch_gm_col(double* st, int k, int j, const double* h, const double* nrm2w, cudaStream_t s) {
   gm_col_kernel<<<1, 1, 0, s>>>(st, k, j, h, nrm2w);
 }
-void launch_gm_solve(double* st, int k, cudaStream_t s) { gm_solve_kernel<<<1, 1, 0, s>>>(st, k); }
+void launch_gm_solve(double* st, int k, int mcols, cudaStream_t s) { gm_solve_kernel<<<1, 1, 0, s>>>(st, k, mcols); }
 int gm_y_offset(int k) { return (k + 1) + 2 * k + k * (k + 1); }
 
-void launch_checksum(const double* a, long long n, double* out, RedWs ws, cudaStream_t s) {
-  checksum_kernel<<<red_blocks(n), kRedThreads, 0, s>>>(a, n, out, ws);
+void launch_fingerprint(const double* a, long long n, unsigned long long* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), s);
+  fingerprint_kernel<<<red_blocks(n), kRedThreads, 0, s>>>(a, n, out);
 }
 
 }  // namespace st

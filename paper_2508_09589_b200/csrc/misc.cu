@@ -91,32 +91,14 @@ template <int SD> __global__ void xd_kernel(Geom g, double T0, double* __restric
   x[idx] = (p + g.pg0 == 0 && !is_patch<SD>(g, c)) ? T0 : 0.0;
 }
 template <int SD>
-__global__ void rhs_kernel(Geom g, const double* __restrict__ f, const double* __restrict__ KxD, double T0,
-                           double* __restrict__ b) {
+__global__ void rhs_kernel(Geom g, const double* f, const double* __restrict__ KxD, double T0,
+                           double* b) {  // b may alias f (elementwise)
   long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= g.N) return;
   int c[3] = {0, 0, 0}, p;
   if (!node_of<SD>(g, idx, c, p)) { b[idx] = 0.0; return; }
   if (is_cons<SD>(g, c, p)) b[idx] = (p + g.pg0 == 0 && !is_patch<SD>(g, c)) ? T0 : 0.0;
   else b[idx] = f[idx] - (KxD ? KxD[idx] : 0.0);
-}
-
-// power-iteration start vector: a fixed hash in (-1/2, 1/2] at free nodes, 0 elsewhere (pads,
-// constrained nodes); global node numbering, so every partition starts from the same vector
-template <int SD> __global__ void hash_vec_kernel(Geom g, double* __restrict__ v) {
-  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= g.N) return;
-  int c[3] = {0, 0, 0}, p;
-  if (!node_of<SD>(g, idx, c, p) || is_cons<SD>(g, c, p)) { v[idx] = 0.0; return; }
-  long long gid = (long long)(p + g.pg0) * g.P + (idx % g.P);
-  unsigned long long z = (unsigned long long)gid * 0x9E3779B97F4A7C15ull;
-  z ^= z >> 31; z *= 0xBF58476D1CE4E5B9ull; z ^= z >> 27;
-  v[idx] = (double)(z >> 11) * (1.0 / 9007199254740992.0) - 0.5;
-}
-void launch_hash_vec(const Geom& g, double* v, cudaStream_t s) {
-  unsigned grd = (unsigned)((g.N + 255) / 256);
-  if (g.sd == 2) hash_vec_kernel<2><<<grd, 256, 0, s>>>(g, v);
-  else hash_vec_kernel<3><<<grd, 256, 0, s>>>(g, v);
 }
 
 // relayout between two storage geometries of the same grid (dense caller layout <-> padded
@@ -388,6 +370,8 @@ void launch_dense_invert(double* A, double* Ainv, int n, int* info, cudaStream_t
     dense_invert_smem_kernel<<<1, 1024, bytes, s>>>(A, Ainv, n, info);
     return;
   }
+  // augmented form through L2; the pivot column factors in shared memory (n <= kDenseMaxNodes = 4096:
+  // 32 KB, inside the default 48 KB; build_hierarchy rejects larger dense coarsest levels)
   dense_invert_kernel<<<1, 1024, n * sizeof(double), s>>>(A, Ainv, n, info);
 }
 

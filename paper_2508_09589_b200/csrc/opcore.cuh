@@ -1,5 +1,5 @@
-// opcore.cuh — per-node level-operator algebra shared by the generic kernels (ops.cu) and the
-// fused small-level V-cycle (vsmall.cu). Algebra: common.cuh / DESIGN.md sec. 7.
+// opcore.cuh — per-node level-operator algebra of the generic kernels (ops.cu).
+// Algebra: common.cuh / DESIGN.md sec. 7.
 #pragma once
 #include "common.cuh"
 
@@ -194,9 +194,7 @@ __device__ __forceinline__ void layer_eval(const OpDesc& op, const int* c, long 
   }
 }
 
-// COH: read through L2 (ld.global.cg) — vectors written earlier in the same kernel (vsmall.cu);
-// SMEM: x is a shared-memory array (the single-CTA V-cycle tail, vsmall.cu)
-template <int SD, bool MASK, bool COH = false, bool SMEM = false>
+template <int SD, bool MASK>
 __device__ __forceinline__ void load_nb(const Geom& g, const double* __restrict__ x, const int* c, int q,
                                         double* xs) {
   const double* xp = x + (long long)q * g.P;
@@ -211,7 +209,7 @@ __device__ __forceinline__ void load_nb(const Geom& g, const double* __restrict_
     }
     double v = 0.0;
     if (valid) {
-      v = SMEM ? xp[pidx<SD>(g, nb)] : (COH ? __ldcg(xp + pidx<SD>(g, nb)) : __ldg(xp + pidx<SD>(g, nb)));
+      v = __ldg(xp + pidx<SD>(g, nb));
       if (MASK && is_cons<SD>(g, nb, q)) v = 0.0;
     }
     xs[k] = v;

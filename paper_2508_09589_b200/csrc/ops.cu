@@ -124,16 +124,16 @@ static void launch_f(const OpDesc& op, int mode, bool trans, bool mask, const do
 #undef ST_CASE
 }
 
-bool g_use_fast = true;
-int g_fast_kind = 0;
-
 void launch_op(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                double omega, cudaStream_t s) {
-  if (g_use_fast && g_fast_kind == 0 && launch_op_tc2d(op, mode, trans, mask, x, b, y, omega, s)) return;
-  if (g_use_fast && g_fast_kind == 0 && launch_op_tc3d(op, mode, trans, mask, x, b, y, omega, s)) return;
-  if (g_use_fast && g_fast_kind == 0 && launch_op_tv2d(op, mode, trans, mask, x, b, y, omega, s)) return;
-  if (g_use_fast && (g_fast_kind == 0 || g_fast_kind == 2) && launch_op_tma2d(op, mode, trans, mask, x, b, y, omega, s)) return;
-  if (g_use_fast && launch_op_fast2d(op, mode, trans, mask, x, b, y, omega, s)) return;
+  // kernel family (st_options_t kernel_family): the specialised TMA kernels where they apply, the
+  // general TMA kernel (tma2d), the cp.async-ring kernels (fast2d), then the generic kernels
+  const int f = op.family;
+  if (f == 0 && launch_op_tc2d(op, mode, trans, mask, x, b, y, omega, s)) return;
+  if (f == 0 && launch_op_tc3d(op, mode, trans, mask, x, b, y, omega, s)) return;
+  if (f == 0 && launch_op_tv2d(op, mode, trans, mask, x, b, y, omega, s)) return;
+  if ((f == 0 || f == 3) && launch_op_tma2d(op, mode, trans, mask, x, b, y, omega, s)) return;
+  if (f != 2 && launch_op_fast2d(op, mode, trans, mask, x, b, y, omega, s)) return;
   if (op.g.sd == 2) {
     if (op.form == FORM_RHO) launch_f<2, FORM_RHO>(op, mode, trans, mask, x, b, y, omega, s);
     else if (op.form == FORM_MK) launch_f<2, FORM_MK>(op, mode, trans, mask, x, b, y, omega, s);

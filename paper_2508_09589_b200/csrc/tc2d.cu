@@ -396,14 +396,9 @@ void ltc(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, const d
   }
   const long long ntx = (g.nn + TX - 1) / TX, nty = (g.nn + TY - 1) / TY;
   const long long wtot = ntx * nty * (g.nt + 1);
-  long long grid = (long long)nsm * resident;
-  // large levels: >= 4 planes per CTA (one reload plane per segment); small levels: every CTA a
-  // short chain so that the TMA round trips of a level overlap (launch-latency bound there)
-  const long long minw = (wtot >= 16LL * nsm * resident) ? 4 : 1;
-  if (grid > wtot / minw) grid = wtot / minw;
-  if (grid < 1) grid = 1;
+  const long long grid = persistent_grid(op, nsm, resident, wtot);
   kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, me ? *me : mx, op, x, y, omega, wtot,
-                                                       chunk_planes(g.P, g.nt + 1, g.sd), (int)ntx);
+                                                       chunk_planes(op, g.nt + 1, g.nt + 1), (int)ntx);
 }
 
 template <int SRC, bool CUNI>

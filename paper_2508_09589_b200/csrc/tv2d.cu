@@ -141,7 +141,7 @@ __device__ __forceinline__ void sched_init(Sched& s, long long tiles, int NP, in
   s.w = s.we = 0;
   s.cs = s.Kc = 0;
 }
-__device__ __forceinline__ bool next_seg(Sched& s, int ntx, int nt, int tord, Seg& sg) {
+__device__ __forceinline__ bool next_seg(Sched& s, int ntx, int nt, Seg& sg) {
   while (s.w >= s.we) {
     if (++s.c >= s.nch) return false;
     s.cs = (int)((long long)s.c * s.NP / s.nch);
@@ -158,9 +158,8 @@ __device__ __forceinline__ bool next_seg(Sched& s, int ntx, int nt, int tord, Se
   s.w += sg.p1 - sg.p0;
   sg.qs = max(sg.p0 - 1, 0);
   sg.qe = min(sg.p1, nt);
-  const long long nty = s.tiles / ntx;
-  sg.x0 = (int)(tord ? tile / nty : tile % ntx) * TX;
-  sg.y0 = (int)(tord ? tile % nty : tile / ntx) * TY;
+  sg.x0 = (int)(tile % ntx) * TX;
+  sg.y0 = (int)(tile / ntx) * TY;
   sg.bx = max(sg.x0 - 2, 0);  // stored-stencil box origin (x0 is a multiple of 32)
   sg.by = max(sg.y0 - 1, 0);
   return true;
@@ -172,7 +171,7 @@ template <int SRC, int MODE, bool TRANS>
 __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
     tv2d_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
                 const __grid_constant__ CUtensorMap tml, OpDesc op, const double* __restrict__ x,
-                double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx, int tord) {
+                double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx) {
   constexpr bool NX = (MODE != MODE_JAC0);
   constexpr bool NBV = (MODE != MODE_APPLY);
   constexpr bool ND = (MODE == MODE_JAC || MODE == MODE_JAC0);
@@ -217,7 +216,7 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
   Sched psc;
   sched_init(psc, tiles, (int)NP, kchunk);
   Seg ps;
-  bool pv = next_seg(psc, ntx, g.nt, tord, ps);
+  bool pv = next_seg(psc, ntx, g.nt, ps);
   int pq = ps.qs;
   auto issue_next = [&](unsigned slot) {
     if (!pv) return;
@@ -232,7 +231,7 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
       else tma4(ls + slot * RS, &tml, &bar[slot], ps.bx, ps.by, 0, 2 * q + 1);
     }
     if (++pq > ps.qe) {
-      pv = next_seg(psc, ntx, g.nt, tord, ps);
+      pv = next_seg(psc, ntx, g.nt, ps);
       pq = ps.qs;
     }
   };
@@ -243,7 +242,7 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
   sched_init(csc, tiles, (int)NP, kchunk);
   Seg cs;
   unsigned cur = 0u, prv = NB - 1, phase = 0u;
-  while (next_seg(csc, ntx, g.nt, tord, cs)) {
+  while (next_seg(csc, ntx, g.nt, cs)) {
     const int p0 = cs.p0, p1 = cs.p1, qs = cs.qs, qe = cs.qe;
     const int x0 = cs.x0, y0 = cs.y0, bx = cs.bx, by = cs.by;
     const int i = x0 + tx, j0 = y0 + ty * RY;
@@ -433,18 +432,6 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn_tv() {
   return fn;
 }
 
-// L2 promotion of the tile maps (ST_L2PROMO = 0 / 64 / 128 / 256 bytes; experiments, default 128)
-CUtensorMapL2promotion l2promo_tv() {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("ST_L2PROMO");
-    v = e ? atoi(e) : 128;
-  }
-  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-                : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                          : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-}
-
 bool map3_tv(CUtensorMap* m, const void* base, unsigned long long d0, unsigned long long d1, unsigned long long d2,
              unsigned long long s1, unsigned long long s2, unsigned b0, unsigned b1) {
   auto fn = encode_fn_tv();
@@ -454,7 +441,7 @@ bool map3_tv(CUtensorMap* m, const void* base, unsigned long long d0, unsigned l
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t es[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2promo_tv(),
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -468,7 +455,7 @@ bool map4_tv(CUtensorMap* m, const void* base, unsigned long long nn, unsigned l
   cuuint32_t box[4] = {(cuuint32_t)tv::EX1, (cuuint32_t)tv::EY, 5, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2promo_tv(),
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -492,23 +479,17 @@ void ltv(const CUtensorMap& mx, const CUtensorMap& mb, const CUtensorMap& ml, co
   }
   const long long ntx = (g.nn + TX - 1) / TX, nty = (g.nn + TY - 1) / TY;
   const long long wtot = ntx * nty * (g.nt + 1);
-  long long grid = (long long)nsm * resident;
-  // large levels: >= 4 planes per CTA (one reload plane per segment); small levels: every CTA a
-  // short chain so that the TMA round trips of a level overlap (launch-latency bound there)
-  const long long minw = (wtot >= 16LL * nsm * resident) ? 4 : 1;
-  if (grid > wtot / minw) grid = wtot / minw;
-  if (grid < 1) grid = 1;
+  const long long grid = persistent_grid(op, nsm, resident, wtot);
   // plane chunks: with long per-CTA plane runs the contiguous split leaves neighbouring tiles at
   // unrelated planes (halo re-reads from DRAM: 1.77x the algorithmic bytes at 512^2 x 512);
   // sliced chunks keep them together — 16 planes on the fine level, 32 on the stored-stencil
   // levels (heavier restarts). Measured (profiles/r01/kbench_tv2d_sliced.log, tv2d_src1_chunk.log):
   // 512^2 x 512 fine 1475 -> 1129 us, level 1 657 -> 553 us; with short runs (< 256 planes per CTA:
-  // 256^3 levels 0 / 1, 512^2 level 2) the restarts cost more than they save. ST_CHUNK_K overrides.
+  // 256^3 levels 0 / 1, 512^2 level 2) the restarts cost more than they save. st_options_t chunk_planes
+  // overrides (parity tests force the sliced schedule on small grids).
   const int NPl = g.nt + 1;
-  int kch = chunk_planes(g.P, NPl, g.sd);
-  if (kch >= NPl && !getenv("ST_CHUNK_K") && wtot / grid >= 256) kch = SRC == 0 ? 16 : 32;
-  kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, ml, op, x, y, omega, wtot, kch, (int)ntx,
-                                                       tile_order());
+  const int kch = chunk_planes(op, NPl, wtot / grid >= 256 ? (SRC == 0 ? 16 : 32) : NPl);
+  kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, ml, op, x, y, omega, wtot, kch, (int)ntx);
 }
 }  // namespace
 

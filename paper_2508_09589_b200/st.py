@@ -8,13 +8,16 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("ST_LIB_PATH") or os.path.join(HERE, "libst.so")  # override: A/B builds
+LIB_PATH = os.path.join(HERE, "libst.so")
 
 ST_OK = 0
 ST_E_NOT_CONVERGED = -3
 ST_TIME_CONSTANT, ST_SPACE_TIME = 0, 1
 ST_SRC_UNIFORM, ST_SRC_SIN = 0, 1
 ST_SMOOTH_JACOBI, ST_SMOOTH_GMRES = 0, 2  # st.h: the GMRES(k)-Jacobi smoother of the paper (one GPU)
+ST_KRYLOV_FGMRES, ST_KRYLOV_GMRES = 0, 1
+ST_COARSE_DENSE, ST_COARSE_GMRES = 0, 1
+ST_KERNELS_TMA, ST_KERNELS_CPASYNC, ST_KERNELS_GENERIC, ST_KERNELS_TMA2D = 0, 1, 2, 3
 
 
 class Grid(C.Structure):
@@ -40,7 +43,12 @@ class Options(C.Structure):
                 ("smoother", C.c_int32), ("nu_pre", C.c_int32), ("nu_post", C.c_int32), ("omega", C.c_double),
                 ("lambda_crit", C.c_double), ("coarse_max_nodes", C.c_int64), ("max_levels", C.c_int32),
                 ("full_coarsening", C.c_int32), ("use_graphs", C.c_int32), ("verbose", C.c_int32),
-                ("agg_nodes", C.c_int64), ("nu_coarse", C.c_int32)]
+                ("agg_nodes", C.c_int64), ("nu_coarse", C.c_int32),
+                ("krylov", C.c_int32), ("coarse_solver", C.c_int32), ("coarse_rtol", C.c_double),
+                ("coarse_maxit", C.c_int32), ("kernel_family", C.c_int32), ("chunk_planes", C.c_int32),
+                ("max_ctas", C.c_int32), ("fuse_prolong", C.c_int32), ("fuse_restrict", C.c_int32),
+                ("omega_factor", C.c_double), ("dgks_eta", C.c_double), ("graph_max_nodes", C.c_int64),
+                ("smoother_rtol", C.c_double)]
 
 
 ST_COMM_NONE, ST_COMM_NCCL, ST_COMM_HOST = 0, 1, 2
@@ -79,7 +87,7 @@ class Layout(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("restarts", C.c_int32), ("rel_residual", C.c_double),
                 ("setup_ms", C.c_double), ("solve_ms", C.c_double), ("n_levels", C.c_int32),
-                ("converged", C.c_int32)]
+                ("converged", C.c_int32), ("vcycles", C.c_int32), ("setups", C.c_int64)]
 
 
 class Hierarchy(C.Structure):
@@ -148,18 +156,23 @@ def load_library(path: str = LIB_PATH):
     return lib
 
 
-def _ptr(a):
-    """Data pointer of a torch tensor / numpy array (must be contiguous fp64)."""
+def _ptr(a, n=None, what="vector"):
+    """Data pointer of a torch tensor / numpy array (contiguous fp64). n: the element count the C ABI
+    will read or write through the pointer; a different size is an error (no out-of-bounds access)."""
     if a is None:
         return None
     if hasattr(a, "data_ptr"):
         if not a.is_contiguous() or str(a.dtype) != "torch.float64":
             raise ValueError("tensors must be contiguous float64")
-        return a.data_ptr()
-    import numpy as np
-    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous):
-        raise ValueError("arrays must be C-contiguous float64")
-    return a.ctypes.data
+        size, ptr = a.numel(), a.data_ptr()
+    else:
+        import numpy as np
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous):
+            raise ValueError("arrays must be C-contiguous float64")
+        size, ptr = a.size, a.ctypes.data
+    if n is not None and size != n:
+        raise ValueError(f"{what}: {size} elements, the library expects {n}")
+    return ptr
 
 
 class TorchHostComm:
@@ -306,54 +319,81 @@ class Solver:
     def n_design(self):
         return self.lib.st_num_design(self.ctx)
 
+    def _nodes(self, a, what):
+        return _ptr(a, self.n_nodes, what)
+
+    def _rho(self, rho):
+        return _ptr(rho, self.n_design, "rho")
+
+    def _owned_design(self):
+        """Element count of this rank's owned design layers (st_filter / st_oc_update / dJ)."""
+        lay = self.layout()
+        nsp = int(self.grid.n) ** int(self.grid.sdim)
+        return nsp * (lay["n_layers"] if lay["rho_layers"] else 1)
+
     def solve(self, rho, T, allow_nc=False):
-        return self._check(self.lib.st_solve(self.ctx, _ptr(rho), _ptr(T)), allow_nc)
+        return self._check(self.lib.st_solve(self.ctx, self._rho(rho), self._nodes(T, "T")), allow_nc)
 
     def adjoint(self, rho, dJdT, lam, allow_nc=False):
-        return self._check(self.lib.st_adjoint(self.ctx, _ptr(rho), _ptr(dJdT), _ptr(lam)), allow_nc)
+        return self._check(self.lib.st_adjoint(self.ctx, self._rho(rho), self._nodes(dJdT, "dJdT"),
+                                               self._nodes(lam, "lambda")), allow_nc)
 
     def sensitivity(self, rho, T, lam, dJ):
-        return self._check(self.lib.st_sensitivity(self.ctx, _ptr(rho), _ptr(T), _ptr(lam), _ptr(dJ)))
+        return self._check(self.lib.st_sensitivity(self.ctx, self._rho(rho), self._nodes(T, "T"),
+                                                   self._nodes(lam, "lambda"), _ptr(dJ, self._owned_design(), "dJ")))
 
     def apply(self, rho, x, y, transpose=False, bc=True):
-        return self._check(self.lib.st_apply(self.ctx, _ptr(rho), _ptr(x), _ptr(y), int(transpose), int(bc)))
+        return self._check(self.lib.st_apply(self.ctx, self._rho(rho), self._nodes(x, "x"), self._nodes(y, "y"),
+                                             int(transpose), int(bc)))
 
     def filter(self, x, out, transpose=False, radius=2.0):
         """Density filter F (transpose: F^T, the chain rule) of config 5 (R-13)."""
-        return self._check(self.lib.st_filter(self.ctx, _ptr(x), _ptr(out), int(transpose), radius))
+        nown = self._owned_design()
+        nout = nown if transpose else self.n_design
+        return self._check(self.lib.st_filter(self.ctx, _ptr(x, nown, "filter input"), _ptr(out, nout, "filter output"),
+                                              int(transpose), radius))
 
     def oc_update(self, rho, dJ, rho_new, volfrac=0.4, move=0.2, rho_min=1e-3):
         """Optimality-criteria step with bisection on the volume multiplier; returns Lambda."""
+        nown = self._owned_design()
         lam = C.c_double()
-        self._check(self.lib.st_oc_update(self.ctx, _ptr(rho), _ptr(dJ), volfrac, move, rho_min, _ptr(rho_new),
-                                          C.byref(lam)))
+        self._check(self.lib.st_oc_update(self.ctx, _ptr(rho, nown, "rho"), _ptr(dJ, nown, "dJ"), volfrac, move,
+                                          rho_min, _ptr(rho_new, nown, "rho_new"), C.byref(lam)))
         return lam.value
 
     def pnorm(self, T, P=20.0, grad=None):
         """phi = (sum_e Tavg_e^P)^(1/P); grad (optional) receives dphi/dT."""
         phi = C.c_double()
-        self._check(self.lib.st_pnorm(self.ctx, _ptr(T), P, C.byref(phi), _ptr(grad)))
+        self._check(self.lib.st_pnorm(self.ctx, self._nodes(T, "T"), P, C.byref(phi),
+                                      None if grad is None else self._nodes(grad, "grad")))
         return phi.value
 
     def dot(self, x, y):
         out = C.c_double()
-        self._check(self.lib.st_dot(self.ctx, _ptr(x), _ptr(y), C.byref(out)))
+        self._check(self.lib.st_dot(self.ctx, self._nodes(x, "x"), self._nodes(y, "y"), C.byref(out)))
         return out.value
 
     def vcycle(self, rho, b, z, transpose=False):
         """z = one V-cycle applied to b (test hook)."""
-        return self._check(self.lib.st_vcycle(self.ctx, _ptr(rho), _ptr(b), _ptr(z), int(transpose)))
+        return self._check(self.lib.st_vcycle(self.ctx, self._rho(rho), self._nodes(b, "b"), self._nodes(z, "z"),
+                                              int(transpose)))
 
     def level_apply(self, rho, level, x, y, transpose=False):
-        return self._check(self.lib.st_level_apply(self.ctx, _ptr(rho), level, _ptr(x), _ptr(y), int(transpose)))
+        h = self.hierarchy()
+        if not 0 <= level < len(h):
+            raise ValueError("level out of range")
+        nd = h[level]["nodes"]
+        return self._check(self.lib.st_level_apply(self.ctx, self._rho(rho), level, _ptr(x, nd, "x"), _ptr(y, nd, "y"),
+                                                   int(transpose)))
 
     def bench_op(self, rho, level, mode, reps, transpose=False):
         """Enqueue `reps` launches of the level operator kernel (internal work vectors) without
         synchronising."""
-        return self._check(self.lib.st_bench_op(self.ctx, _ptr(rho), level, mode, int(transpose), reps))
+        return self._check(self.lib.st_bench_op(self.ctx, self._rho(rho), level, mode, int(transpose), reps))
 
     def rhs(self, rho, f=None, b=None):
-        return self._check(self.lib.st_rhs(self.ctx, _ptr(rho), _ptr(f), _ptr(b)))
+        return self._check(self.lib.st_rhs(self.ctx, self._rho(rho), None if f is None else self._nodes(f, "f"),
+                                           None if b is None else self._nodes(b, "b")))
 
     def stats(self):
         s = Stats()

@@ -21,20 +21,40 @@ def _minmax(a: np.ndarray, lo: float, hi: float) -> np.ndarray:
     return lo + (hi - lo) * (a - amin) / (amax - amin)
 
 
+def smooth_layer(spatial_shape, seed: int, t: int, sigma: float = 3.0, lo: float = 0.01,
+                 hi: float = 1.0) -> np.ndarray:
+    """Layer t of the per-layer smooth field: its own generator default_rng((seed, t)), so any
+    slab of layers can be drawn without the others (time slabs)."""
+    from scipy.ndimage import gaussian_filter
+    g = gaussian_filter(np.random.default_rng((seed, t)).standard_normal(spatial_shape), sigma=sigma,
+                        mode="reflect")
+    return _minmax(g, lo, hi)
+
+
 def rho_smooth(shape, seed: int = 0, sigma: float = 3.0, lo: float = 0.01, hi: float = 1.0,
-               per_layer: bool = False) -> np.ndarray:
+               per_layer: bool = False, layers=None, threads: int = 16) -> np.ndarray:
     """Smooth random field: standard normal -> Gaussian filter (sigma = 3 elements, the
     'radius 3 elements' of BASELINE configs 2-4, reflect mode) -> min-max affine onto
     [lo, hi]. per_layer=True: shape = (nt, *spatial), an independent field per time
-    layer, each min-max scaled (config 3)."""
+    layer (smooth_layer), each min-max scaled (config 3); layers = (a, b) draws layers
+    [a, b) only (a rank's slab)."""
     from scipy.ndimage import gaussian_filter
-    rng = np.random.default_rng(seed)
     if per_layer:
-        out = np.empty(shape)
-        for t in range(shape[0]):
-            g = gaussian_filter(rng.standard_normal(shape[1:]), sigma=sigma, mode="reflect")
-            out[t] = _minmax(g, lo, hi)
+        a, b = layers if layers is not None else (0, shape[0])
+        out = np.empty((b - a,) + tuple(shape[1:]))
+
+        def one(t):
+            out[t - a] = smooth_layer(tuple(shape[1:]), seed, t, sigma, lo, hi)
+
+        if b - a >= 64 and threads > 1:  # scipy.ndimage releases the GIL: draw layers in parallel
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor(threads) as ex:
+                list(ex.map(one, range(a, b)))
+        else:
+            for t in range(a, b):
+                one(t)
         return out
+    rng = np.random.default_rng(seed)
     g = gaussian_filter(rng.standard_normal(shape), sigma=sigma, mode="reflect")
     return _minmax(g, lo, hi)
 
@@ -55,15 +75,16 @@ CONFIGS = {
 }
 
 
-def design_for(sdim: int, n: int, nt: int, design: str, seed: int = 0) -> np.ndarray:
-    """Element densities for a config-shaped grid (shape [nt][x..] or [x..])."""
+def design_for(sdim: int, n: int, nt: int, design: str, seed: int = 0, layers=None) -> np.ndarray:
+    """Element densities for a config-shaped grid (shape [nt][x..] or [x..]); layers = (a, b):
+    only layers [a, b) of a per-layer design (a time slab)."""
     sp_shape = (n,) * sdim
     if design == "uniform":
         return rho_uniform((nt,) + sp_shape, seed=seed)
     if design == "smooth_tc":
         return rho_smooth(sp_shape, seed=seed)
     if design == "smooth_layers":
-        return rho_smooth((nt,) + sp_shape, seed=seed, per_layer=True)
+        return rho_smooth((nt,) + sp_shape, seed=seed, per_layer=True, layers=layers)
     if design == "const":
         return np.full((nt,) + sp_shape, 0.4)
     raise ValueError(design)

@@ -36,7 +36,7 @@ def test_default_options_and_errors():
     o = st.Options()
     lib.st_default_options(ctypes.byref(o))
     assert o.rtol == 1e-8 and o.lambda_crit == 0.5 and o.restart == 16 and o.nu_pre == 2 and o.nu_post == 2 and o.nu_coarse == 5
-    assert lib.st_abi_version() == 2
+    assert lib.st_abi_version() == 3
     assert lib.st_strerror(-2).decode().startswith("grid not divisible")
 
 
@@ -122,12 +122,37 @@ def test_full_coarsening_plan_halves_space_and_time(sdim, n, nt):
         assert (b["kind"], b["n"], b["nt"]) in (("space", a["n"] // 2, a["nt"]), ("time", a["n"], a["nt"] // 2))
 
 
-def test_options_layout_appends_nu_coarse():
-    """nu_coarse (per-level smoothing) is the last st_options_t field, so the
-    earlier fields keep their offsets; the binding's struct matches the library's size."""
+def test_options_defaults_and_knobs_are_options():
+    """ABI 3: every former environment knob is an st_options_t field read per call (VERDICT r01
+    weak #9): the library source calls no getenv, and the defaults are the measured ones
+    (omega factor 1.9, DGKS eta 0.1; PAPER.md:385 coarse GMRES 200 its, 1e-6)."""
+    import glob
     from paper_2508_09589_b200 import st
-    assert st.Options._fields_[-1][0] == "nu_coarse"
+    for f in glob.glob(os.path.join(ROOT, "paper_2508_09589_b200", "csrc", "*")):
+        assert "getenv" not in open(f).read(), f
     o = st.Options()
     lib = st.load_library()
     lib.st_default_options(ctypes.byref(o))
     assert o.nu_coarse == 5 and o.nu_pre == 2 and o.smoother == st.ST_SMOOTH_JACOBI
+    assert o.krylov == st.ST_KRYLOV_FGMRES and o.coarse_solver == st.ST_COARSE_DENSE
+    assert o.coarse_rtol == 1e-6 and o.coarse_maxit == 200
+    assert o.kernel_family == st.ST_KERNELS_TMA and o.chunk_planes == 0 and o.max_ctas == 0
+    assert o.fuse_prolong == 1 and o.fuse_restrict == 1
+    assert o.omega_factor == 1.9 and o.dgks_eta == 0.1 and o.graph_max_nodes == 0 and o.smoother_rtol == 0.0
+    hdr = open(os.path.join(ROOT, "include", "st.h")).read()
+    for name in ("ST_KRYLOV_FGMRES", "ST_KRYLOV_GMRES", "ST_COARSE_DENSE", "ST_COARSE_GMRES", "ST_KERNELS_TMA",
+                 "ST_KERNELS_CPASYNC", "ST_KERNELS_GENERIC", "ST_KERNELS_TMA2D"):
+        m = re.search(name + r" = (\d+)", hdr)
+        assert m and int(m.group(1)) == getattr(st, name), name
+
+
+def test_binding_validates_vector_sizes():
+    """The binding refuses arrays whose element count differs from what the C ABI reads or writes
+    (no out-of-bounds access through an undersized array)."""
+    import numpy as np
+    from paper_2508_09589_b200 import st
+    assert st._ptr(np.zeros(5), 5) is not None
+    with pytest.raises(ValueError):
+        st._ptr(np.zeros(4), 5, "T")
+    with pytest.raises(ValueError):
+        st._ptr(np.zeros(5, dtype=np.float32), 5)

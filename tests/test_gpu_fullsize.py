@@ -3,16 +3,26 @@ the GPU result is certified by the oracle's own element matrices on sampled rows
 
 For a solve to true relative residual rtol, every row satisfies |b_i - (K_bc T)_i| <= ||b - K_bc T||
 <= rtol ||b||; the test recomputes (K_bc T)_i with oracle.row_apply (quadrature element matrices,
-no code shared with the CUDA path) at random rows plus every row of the first, second and last time
-planes, and bounds the residual there. Sensitivities of sampled elements are recomputed from the GPU
-T and lambda with oracle.sensitivity_elements. Launch configuration = bench.py's (config 2: default
-options, rtol 1e-8)."""
+no code shared with the CUDA path) at random rows plus rows of the first, second, middle and last
+time planes, and bounds the residual there; b_i comes from oracle.source_rows / node_constraint, and
+||b|| (||f||) from the library's own f only as the scale of the bound. Sensitivities of sampled
+elements are recomputed from the GPU T and lambda with oracle.sensitivity_elements. The oracle
+helpers are purely local (R-21), so the certification scales to config 3 (1.08e9 DOFs):
+only the stencil entries of the sampled rows are copied to the host.
+
+Launch configuration = bench.py's: the library defaults (rtol 1e-8), the automatic schedules of the
+persistent kernels (tv2d sliced chunks at 512^2 x 512 and above, tc3d multi-plane runs at config 4),
+and for config 3 the bench's one-GPU memory plan (bench.WORKLOADS)."""
+import itertools
+import os
+import sys
+
 import numpy as np
 import pytest
 
 import oracle as O
 import st_inputs as I
-from gpu_util import CFG1_MATS, rel
+from gpu_util import CFG1_MATS, CFG4_MATS, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -21,65 +31,139 @@ if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 
 DEV = torch.device("cuda:0")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _rows(mesh, rng, k):
     P = (mesh.n + 1) ** mesh.sdim
     planes = [0, 1, 2, mesh.nt // 2, mesh.nt - 1, mesh.nt]
-    fixed = np.concatenate([np.arange(p * P, (p + 1) * P)[:: max(1, P // 400)] for p in planes])
+    fixed = np.concatenate([p * P + rng.integers(0, P, 150) for p in planes])
     return np.unique(np.concatenate([fixed, rng.integers(0, mesh.n_nodes, k)]))
 
 
-@pytest.mark.parametrize("name", ["config2", "config3-shaped-256"])
-def test_fullsize_solution_certified_by_oracle_rows(name):
+def _stencil_nodes(mesh, rows):
+    nn = mesh.n + 1
+    nd = mesh.sdim + 1
+    strides = [nn ** d for d in range(mesh.sdim)] + [nn ** mesh.sdim]
+    lim = [mesh.n] * mesh.sdim + [mesh.nt]
+    out = set()
+    for r in rows:
+        c, q = [], int(r)
+        for d in range(mesh.sdim):
+            c.append(q % nn)
+            q //= nn
+        c.append(q)
+        for off in itertools.product((-1, 0, 1), repeat=nd):
+            cc = [c[d] + off[d] for d in range(nd)]
+            if all(0 <= cc[d] <= lim[d] for d in range(nd)):
+                out.add(sum(cc[d] * strides[d] for d in range(nd)))
+    return np.array(sorted(out), dtype=np.int64)
+
+
+def _gather(vec, idx):
+    """{node: value} of a device vector at the given nodes (one gather, one copy)."""
+    vals = vec[torch.as_tensor(idx, device=vec.device)].cpu().numpy()
+    return dict(zip(idx.tolist(), vals.tolist()))
+
+
+def _elem_nodes(mesh, elems):
+    nn = mesh.n + 1
+    nd = mesh.sdim + 1
+    strides = [nn ** d for d in range(mesh.sdim)] + [nn ** mesh.sdim]
+    out = set()
+    for e in elems:
+        ec, r = [], int(e)
+        for d in range(mesh.sdim):
+            ec.append(r % mesh.n)
+            r //= mesh.n
+        ec.append(r)
+        for a in range(2 ** nd):
+            out.add(sum((ec[d] + ((a >> d) & 1)) * strides[d] for d in range(nd)))
+    return np.array(sorted(out), dtype=np.int64)
+
+
+CASES = {
+    # name: sdim, n, nt, time_constant, design, source, mats, solver options (bench's launch configuration)
+    "config2": (2, 256, 256, True, "smooth_tc", ("uniform", 1.0, 0.0, 0.0), CFG1_MATS, {}),
+    "config3-shaped-256": (2, 256, 256, False, "smooth_layers", ("sin", 1.0, 1.0, 2 * np.pi), CFG1_MATS, {}),
+    "config3-shaped-512": (2, 512, 512, False, "smooth_layers", ("sin", 1.0, 1.0, 2 * np.pi), CFG1_MATS, {}),
+    "config4": (3, 64, 128, True, "smooth_tc", ("uniform", 1.0, 0.0, 0.0), CFG4_MATS, {}),
+}
+
+
+def certify(name, sdim, n, nt, tc, design, src, mats, opts, rho=None, nrows=2500, nel=2500, rtol=1e-8):
     import paper_2508_09589_b200 as S
-    if name == "config2":
-        sdim, n, nt, tc, design, src = 2, 256, 256, True, "smooth_tc", ("uniform", 1.0, 0.0, 0.0)
-    else:
-        sdim, n, nt, tc, design, src = 2, 256, 256, False, "smooth_layers", ("sin", 1.0, 1.0, 2 * np.pi)
-    rtol = 1e-8
-    solver = S.Solver(sdim, n, nt, mats=CFG1_MATS, source=src, time_constant=tc, rtol=rtol, maxit=500)
-    rho = I.design_for(sdim, n, nt, design, 0)
+    solver = S.Solver(sdim, n, nt, mats=mats, source=src, time_constant=tc, rtol=rtol, maxit=1000, **opts)
+    if rho is None:
+        rho = I.design_for(sdim, n, nt, design, 0)
     rd = torch.as_tensor(np.ascontiguousarray(rho), device=DEV)
-    prob = O.Problem(O.Mesh(sdim, n, nt), O.Materials(*CFG1_MATS), O.BCs(), O.Source(*src))
-    N = prob.mesh.n_nodes
+    prob = O.Problem(O.Mesh(sdim, n, nt), O.Materials(*mats), O.BCs(), O.Source(*src))
+    mesh = prob.mesh
+    N = mesh.n_nodes
+    rng = np.random.default_rng(5)
+    rows = _rows(mesh, rng, nrows)
+    need = _stencil_nodes(mesh, rows)
+    f = torch.empty(N, dtype=torch.float64, device=DEV)
+    solver.rhs(rd, f, None)                       # only ||f|| (the bound's scale) comes from the library
+    fnorm = float(torch.linalg.vector_norm(f))
+    del f
+    # oracle b on the sampled rows (T0 = 0: b = f on free rows, 0 on constrained rows, R-1)
+    cons = np.array([O.node_constraint(mesh, prob.bcs, r)[0] for r in rows])
+    f_rows = O.source_rows(mesh, prob.src, rows)
+    b_rows = np.where(cons, 0.0, f_rows)
     T = torch.zeros(N, dtype=torch.float64, device=DEV)
     solver.solve(rd, T)
     st = solver.stats()
     assert st["converged"] == 1 and st["rel_residual"] <= rtol
-    f = prob.f()
-    cons, xD = prob.constraints()
-    b = np.where(cons, xD, f)  # T0 = 0: b = f on free rows (R-1)
-    bnorm = np.linalg.norm(b)
-    rng = np.random.default_rng(5)
-    rows = _rows(prob.mesh, rng, 3000)
-    Th = T.cpu().numpy()
-    r = b[rows] - O.row_apply(prob, rho, Th, rows)
-    assert np.max(np.abs(r)) <= rtol * bnorm * (1 + 1e-6), (np.max(np.abs(r)), rtol * bnorm)
-    # constrained rows hold the prescribed values exactly
-    assert np.array_equal(Th[cons], xD[cons])
-    # adjoint of the compliance: K_bc^T lambda = m_f f
-    g = prob.compliance_rhs()
+    Tm = _gather(T, need)
+    r = b_rows - O.row_apply(prob, rho, Tm, rows)
+    # ||b|| >= ||m_f f||: bound with the free-row norm of f computed from the library's f is loose-safe
+    assert np.max(np.abs(r)) <= rtol * fnorm * (1 + 1e-6), (name, np.max(np.abs(r)), rtol * fnorm)
+    assert all(Tm[int(q)] == 0.0 for q, c in zip(rows, cons) if c)   # prescribed values (T0 = 0)
     lam = torch.zeros_like(T)
-    solver.adjoint(rd, torch.as_tensor(g, device=DEV), lam)
+    solver.adjoint(rd, None, lam)                 # compliance: K_bc^T lambda = m_f f
     assert solver.stats()["converged"] == 1
-    Lh = lam.cpu().numpy()
-    ra = g[rows] - O.row_apply(prob, rho, Lh, rows, transpose=True)
-    assert np.max(np.abs(ra)) <= rtol * np.linalg.norm(g) * (1 + 1e-6)
-    assert np.all(Lh[cons] == 0.0)
+    Lm = _gather(lam, need)
+    ra = b_rows - O.row_apply(prob, rho, Lm, rows, transpose=True)
+    assert np.max(np.abs(ra)) <= rtol * fnorm * (1 + 1e-6), (name, np.max(np.abs(ra)))
+    assert all(Lm[int(q)] == 0.0 for q, c in zip(rows, cons) if c)
     # sensitivities of sampled elements from the GPU T and lambda
     nsp = n ** sdim
     dJ = torch.empty(nsp if tc else nsp * nt, dtype=torch.float64, device=DEV)
     solver.sensitivity(rd, T, lam, dJ)
-    dJh = dJ.cpu().numpy()
-    rho_st = np.broadcast_to(rho, (nt,) + rho.shape).copy() if tc else rho
     if tc:
-        sp = rng.integers(0, nsp, 24)
-        ref = np.array([O.sensitivity_elements(prob, rho_st, Th, Lh, e + nsp * np.arange(nt)).sum() for e in sp])
-        got = dJh[sp]
+        sp = rng.integers(0, nsp, 6)
+        els = np.concatenate([e + nsp * np.arange(nt) for e in sp])
+        en = _elem_nodes(mesh, els)
+        Tm, Lm = _gather(T, en), _gather(lam, en)
+        ref = np.array([O.sensitivity_elements(prob, rho, Tm, Lm, e + nsp * np.arange(nt)).sum() for e in sp])
+        got = dJ[torch.as_tensor(sp, device=DEV)].cpu().numpy()
     else:
-        el = rng.integers(0, nsp * nt, 3000)
-        ref = O.sensitivity_elements(prob, rho_st, Th, Lh, el)
-        got = dJh[el]
-    assert rel(got, ref) <= 1e-10, rel(got, ref)
+        el = rng.integers(0, nsp * nt, nel)
+        en = _elem_nodes(mesh, el)
+        Tm, Lm = _gather(T, en), _gather(lam, en)
+        ref = O.sensitivity_elements(prob, rho, Tm, Lm, el)
+        got = dJ[torch.as_tensor(el, device=DEV)].cpu().numpy()
+    assert rel(got, ref) <= 1e-10, (name, rel(got, ref))
+    out = dict(st)
     solver.close()
+    return out
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_fullsize_solution_certified_by_oracle_rows(name):
+    certify(name, *CASES[name])
+
+
+def test_config3_fullsize_one_gpu_certified():
+    """BASELINE config 3 at full size (1024^2 x 1024 elements, 1,076,890,625 DOFs, an independent
+    smooth field per time layer, Q(t) = 1 + sin 2 pi t) on ONE GPU with the bench's memory plan."""
+    sys.path.insert(0, ROOT)
+    import bench
+    free, _ = torch.cuda.mem_get_info()
+    if free < 150e9:
+        pytest.skip("config 3 needs a 180 GB B200")
+    wl = bench.WORKLOADS[3]
+    rho = I.design_for(2, 1024, 1024, "smooth_layers", 0)
+    certify("config3", 2, 1024, 1024, False, "smooth_layers", wl["source"], CFG1_MATS, dict(wl["opts"]),
+            rho=rho, nrows=1200, nel=1500)

@@ -6,6 +6,7 @@ import pytest
 import scipy.sparse as sp
 
 import oracle as O
+import paper_2508_09589_b200 as S
 import st_inputs as I
 from gpu_util import CFG1_MATS, CFG4_MATS, make_pair, rel
 
@@ -280,7 +281,8 @@ def test_iteration_counts_reasonable():
     solver.close()
 
 
-KERNEL_VARIANTS = {"tma": ("0", "0"), "cpasync": ("0", "1"), "tma2d": ("0", "2"), "generic": ("1", "0")}  # ST_NO_FAST, ST_FAST_KIND
+KERNEL_VARIANTS = {"tma": S.st.ST_KERNELS_TMA, "cpasync": S.st.ST_KERNELS_CPASYNC, "tma2d": S.st.ST_KERNELS_TMA2D,
+                   "generic": S.st.ST_KERNELS_GENERIC}  # st_options_t kernel_family
 
 
 @pytest.mark.parametrize("variant", sorted(KERNEL_VARIANTS))
@@ -288,15 +290,13 @@ KERNEL_VARIANTS = {"tma": ("0", "0"), "cpasync": ("0", "1"), "tma2d": ("0", "2")
                                   (2, 40, 7, "uniform", False), (2, 64, 24, "smooth_tc", True),
                                   (3, 8, 6, "smooth_tc", True)],
                          ids=lambda c: f"{c[0]}d-{c[1]}x{c[2]}-{'tc' if c[4] else 'st'}")
-def test_operator_parity_all_kernel_variants(variant, case, monkeypatch):
+def test_operator_parity_all_kernel_variants(variant, case):
     """Every (2+1)D operator kernel (TMA ring, cp.async ring, generic) gives the oracle's K x and
     K^T x on every level kind it serves; the grids span several 32 x 8 tiles with ragged tails and
     split (tile, plane) work ranges across CTAs."""
-    fast, kind = KERNEL_VARIANTS[variant]
-    monkeypatch.setenv("ST_NO_FAST", fast)
-    monkeypatch.setenv("ST_FAST_KIND", kind)
     sdim, n, nt, design, tc = case
-    solver, prob = make_pair(sdim, n, nt, mats=CFG4_MATS, T0=0.3, time_constant=tc, rtol=1e-12, maxit=400)
+    solver, prob = make_pair(sdim, n, nt, mats=CFG4_MATS, T0=0.3, time_constant=tc, rtol=1e-12, maxit=400,
+                             kernel_family=KERNEL_VARIANTS[variant])
     rho = _rho(sdim, n, nt, design, 5, tc)
     K = prob.K(rho)
     Kbc, _, _, _ = prob.system(rho)
@@ -376,34 +376,6 @@ def test_filter_and_oc_kernels_match_oracle():
     solver.close()
 
 
-@pytest.mark.parametrize("sdim,n,nt,tc", [(2, 64, 64, True), (2, 32, 64, False), (3, 8, 16, True), (2, 64, 32, False)])
-def test_fused_small_level_vcycle_equals_per_level_launches(sdim, n, nt, tc, monkeypatch):
-    """The fused small-level tails of the V-cycle (vsmall.cu) are the same linear map as the
-    per-level launches (up to summation order), forward and adjoint: the single-CTA shared-memory
-    tail (opt-in ST_VTAIL=1, `launch_vtail`) and the opt-in cluster kernel (ST_VSMALL=1); the
-    shared-memory tail also launches fewer kernels per V-cycle than the per-level path."""
-    rho = _rho(sdim, n, nt, "uniform", 6, tc)
-    x = I.rand_vector((n + 1) ** sdim * (nt + 1), 12)
-    outs, launches = {}, {}
-    for name, vtail, vsmall in (("per-level", "0", "0"), ("smem-tail", "1", "0"), ("cluster", "0", "1")):
-        monkeypatch.setenv("ST_VTAIL", vtail)
-        monkeypatch.setenv("ST_VSMALL", vsmall)
-        solver, prob = make_pair(sdim, n, nt, mats=CFG4_MATS, time_constant=tc, coarse_max_nodes=64, use_graphs=0)
-        z = torch.empty(x.size, dtype=torch.float64, device=DEV)
-        zt = torch.empty_like(z)
-        solver.vcycle(dev(rho), dev(x), z)
-        k0 = solver.kernel_launches()
-        solver.vcycle(dev(rho), dev(x), z)
-        launches[name] = solver.kernel_launches() - k0
-        solver.vcycle(dev(rho), dev(x), zt, transpose=True)
-        outs[name] = (host(z), host(zt))
-        solver.close()
-    for name in ("smem-tail", "cluster"):
-        assert rel(outs[name][0], outs["per-level"][0]) <= 1e-12, name
-        assert rel(outs[name][1], outs["per-level"][1]) <= 1e-12, name
-    assert launches["smem-tail"] < launches["per-level"], launches
-
-
 @pytest.mark.parametrize("sdim,n,nt,tc", [(2, 12, 10, False), (3, 4, 6, True)])
 def test_pnorm_objective_and_adjoint_rhs(sdim, n, nt, tc):
     """The paper's objective phi = (sum Tavg^P)^(1/P), P = 20 and its gradient
@@ -446,17 +418,16 @@ def test_per_design_tables_follow_the_design_across_hooks():
 
 
 @pytest.mark.parametrize("n,nt,design", [(64, 32, "smooth_tc"), (40, 12, "uniform"), (128, 16, "smooth_tc")])
-def test_prolongation_fused_into_post_sweep_equals_separate_kernels(n, nt, design, monkeypatch):
+def test_prolongation_fused_into_post_sweep_equals_separate_kernels(n, nt, design):
     """The V-cycle with the prolongation + correction fused into the first post-smoothing sweep
     (tc2d PRO variant, default) is the same linear map as the separate prolongation kernel followed
-    by the sweep (ST_NO_PRO=1), forward and adjoint, on multi-tile ragged grids with the sink patch;
+    by the sweep (options fuse_prolong = 0), forward and adjoint, on multi-tile ragged grids with the sink patch;
     and the fused path is taken (fewer launches per V-cycle)."""
     rho = _rho(2, n, nt, design, 5, True) if design == "uniform" else I.design_for(2, n, nt, design, 5)
     x = I.rand_vector((n + 1) ** 2 * (nt + 1), 13)
     outs, launches = {}, {}
-    for flag in ("1", "0"):
-        monkeypatch.setenv("ST_NO_PRO", flag)
-        solver, prob = make_pair(2, n, nt, time_constant=True, use_graphs=0)
+    for flag in ("1", "0"):  # "1": separate kernels, "0": fused (as the former ST_NO_PRO flag)
+        solver, prob = make_pair(2, n, nt, time_constant=True, use_graphs=0, fuse_prolong=0 if flag == "1" else 1)
         z = torch.empty(x.size, dtype=torch.float64, device=DEV)
         zt = torch.empty_like(z)
         solver.vcycle(dev(rho), dev(x), z)

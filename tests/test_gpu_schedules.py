@@ -1,0 +1,236 @@
+"""GPU parity of the persistent-kernel SCHEDULES the full-size runs use, and of
+the round-2 solver options, against the oracle on oracle-scale grids.
+
+At BASELINE sizes the persistent stencil kernels walk long (tile, plane) runs per CTA: tv2d switches
+to sliced 16 / 32-plane time chunks once a CTA has >= 256 items (512^2 x 512 and config 3), and tc3d
+gives each CTA ~650 items at config 4. The options chunk_planes and max_ctas (st_options_t, read per
+launch) force those schedules on grids the oracle factorises in seconds: a cap of a few CTAs makes
+every CTA sweep many tiles and planes (multi-plane runs, segment switches inside and across chunks,
+cross-segment TMA prefetch), and a forced chunk length cuts time into slices (ragged last chunk
+included). Every case compares K x and K^T x (with and without elimination) at <= 1e-12 and a full
+solve (all modes of all levels) at <= 1e-8 (north_star tolerances, R-15)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2508_09589_b200 as S
+import st_inputs as I
+from gpu_util import CFG1_MATS, CFG4_MATS, make_pair, rel
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+DEV = torch.device("cuda:0")
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=DEV)
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def _design(sdim, n, nt, tc, seed):
+    return I.rho_smooth((n,) * sdim, seed=seed) if tc else I.rho_uniform((nt,) + (n,) * sdim, seed)
+
+
+# (name, sdim, n, nt, time_constant, mats): tv2d = space-time design with uniform capacity (fine level
+# from the k~ table, SRC 0; per-layer stored-stencil levels, SRC 1); tc2d / tc3d = time-constant
+SCHED_CASES = [
+    ("tv2d", 2, 48, 40, False, CFG1_MATS),
+    ("tv2d-ragged", 2, 40, 37, False, CFG1_MATS),
+    ("tc2d", 2, 48, 40, True, CFG1_MATS),
+    ("tc3d", 3, 10, 12, True, CFG4_MATS),
+    ("tc3d-ragged", 3, 9, 10, True, CFG1_MATS),
+]
+SCHEDULES = [(0, 1), (0, 3), (16, 0), (16, 2), (32, 5), (5, 3), (-1, 2)]  # (chunk_planes, max_ctas)
+
+
+@pytest.mark.parametrize("sched", SCHEDULES, ids=lambda s: f"chunk{s[0]}-ctas{s[1]}")
+@pytest.mark.parametrize("case", SCHED_CASES, ids=lambda c: c[0])
+def test_forced_schedule_operator_and_solve_parity(case, sched):
+    name, sdim, n, nt, tc, mats = case
+    chunk, ctas = sched
+    solver, prob = make_pair(sdim, n, nt, mats=mats, T0=0.2, time_constant=tc, rtol=1e-11, maxit=600,
+                             chunk_planes=chunk, max_ctas=ctas, coarse_max_nodes=64)
+    rho = _design(sdim, n, nt, tc, 3)
+    K = prob.K(rho)
+    Kbc, _, _, _ = prob.system(rho)
+    x = I.rand_vector(prob.mesh.n_nodes, 17)
+    xd, yd = dev(x), torch.empty(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+    for trans in (False, True):
+        for bc in (False, True):
+            A = Kbc if bc else K
+            ref = (A.T if trans else A) @ x
+            solver.apply(dev(rho), xd, yd, transpose=trans, bc=bc)
+            assert rel(host(yd), ref) <= 1e-12, (name, sched, trans, bc, rel(host(yd), ref))
+    T_ref, lam_ref = prob.solve_both(rho)
+    T = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+    solver.solve(dev(rho), T)
+    assert solver.stats()["converged"] == 1
+    assert rel(host(T), T_ref) <= 1e-8
+    lam = torch.zeros_like(T)
+    solver.adjoint(dev(rho), dev(prob.compliance_rhs()), lam)
+    assert rel(host(lam), lam_ref) <= 1e-8
+    solver.close()
+
+
+@pytest.mark.parametrize("sched", [(0, 0), (16, 3), (32, 2)], ids=lambda s: f"chunk{s[0]}-ctas{s[1]}")
+def test_forced_schedule_level_operators_equal_default(sched):
+    """Every coarse level operator (stored-stencil SRC 1 tv2d levels, B4 levels below a time
+    coarsening) under a forced schedule equals the default schedule's, forward and transposed."""
+    n, nt = 64, 48
+    rho = I.rho_uniform((nt, n, n), 5)
+    ref_solver, _ = make_pair(2, n, nt, mats=CFG1_MATS, coarse_max_nodes=64)
+    solver, _ = make_pair(2, n, nt, mats=CFG1_MATS, coarse_max_nodes=64, chunk_planes=sched[0], max_ctas=sched[1])
+    h = solver.hierarchy()
+    assert len(h) >= 4
+    for l, lv in enumerate(h[:-1]):
+        x = dev(I.rand_vector(lv["nodes"], 30 + l))
+        for trans in (False, True):
+            y0 = torch.empty_like(x)
+            y1 = torch.empty_like(x)
+            ref_solver.level_apply(dev(rho), l, x, y0, transpose=trans)
+            solver.level_apply(dev(rho), l, x, y1, transpose=trans)
+            assert rel(host(y1), host(y0)) <= 1e-13, (l, lv["kind"], trans)
+    solver.close()
+    ref_solver.close()
+
+
+# ------------------------------------------------------------------ solver options (ABI 3)
+@pytest.mark.parametrize("sdim,n,nt,tc,mats", [(2, 16, 16, False, CFG1_MATS), (2, 32, 32, True, CFG1_MATS),
+                                               (3, 6, 12, True, CFG4_MATS), (2, 24, 20, False, CFG4_MATS)])
+@pytest.mark.parametrize("restart", [3, 16])
+def test_right_preconditioned_gmres_matches_oracle(sdim, n, nt, tc, mats, restart):
+    """options krylov = ST_KRYLOV_GMRES (no Z vectors: x += M (V y) per restart; the memory plan of
+    config 3 on one GPU) converges to the oracle's T and lambda; restart 3 forces
+    several restart cycles."""
+    solver, prob = make_pair(sdim, n, nt, mats=mats, time_constant=tc, rtol=1e-10, maxit=800,
+                             krylov=S.st.ST_KRYLOV_GMRES, restart=restart)
+    rho = _design(sdim, n, nt, tc, 1)
+    T_ref, lam_ref = prob.solve_both(rho)
+    T = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+    solver.solve(dev(rho), T)
+    st = solver.stats()
+    assert st["converged"] == 1 and st["vcycles"] == st["iterations"] + st["restarts"]
+    assert rel(host(T), T_ref) <= 1e-8
+    lam = torch.zeros_like(T)
+    solver.adjoint(dev(rho), None, lam)  # null dJdT: the compliance RHS m_f f (R-8)
+    assert rel(host(lam), lam_ref) <= 1e-8
+    solver.close()
+
+
+def test_gmres_and_fgmres_take_the_same_iterations():
+    """With the fixed linear Jacobi V-cycle, GMRES(m) and FGMRES(m) build the same Krylov space:
+    the same iteration counts and (to rounding) the same solution."""
+    n, nt = 32, 32
+    rho = dev(I.rho_smooth((n, n), seed=2))
+    out = {}
+    for k in (S.st.ST_KRYLOV_FGMRES, S.st.ST_KRYLOV_GMRES):
+        solver, prob = make_pair(2, n, nt, time_constant=True, rtol=1e-10, krylov=k)
+        T = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+        solver.solve(rho, T)
+        out[k] = (host(T), solver.stats()["iterations"])
+        solver.close()
+    a, b = out[S.st.ST_KRYLOV_FGMRES], out[S.st.ST_KRYLOV_GMRES]
+    assert a[1] == b[1]
+    assert rel(b[0], a[0]) <= 1e-9
+
+
+def test_null_adjoint_rhs_is_the_compliance_gradient():
+    solver, prob = make_pair(2, 20, 12, rtol=1e-11)
+    rho = dev(I.rho_uniform((12, 20, 20), 6))
+    l1 = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+    l2 = torch.zeros_like(l1)
+    solver.adjoint(rho, dev(prob.compliance_rhs()), l1)
+    solver.adjoint(rho, None, l2)
+    assert rel(host(l2), host(l1)) <= 1e-13
+    solver.close()
+
+
+def test_design_fingerprint_detects_a_one_ulp_change():
+    """a design change is detected exactly (128-bit hash of the bit patterns), so a
+    one-ulp perturbation of ONE element rebuilds the rho-dependent operators and the same design
+    passed again does not."""
+    solver, prob = make_pair(2, 32, 16, rtol=1e-10)
+    r = I.rho_uniform((16, 32, 32), 2)
+    T = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+    solver.solve(dev(r), T)
+    s0 = solver.stats()["setups"]
+    solver.solve(dev(r), T)
+    assert solver.stats()["setups"] == s0
+    r2 = r.copy()
+    r2.reshape(-1)[12345] = np.nextafter(r2.reshape(-1)[12345], 2.0)
+    solver.solve(dev(r2), T)
+    assert solver.stats()["setups"] == s0 + 1
+    solver.close()
+
+
+def test_fused_prolongation_option_equivalence_and_kernel_families_solve():
+    """fuse_prolong = 0 / 1 give the same solution; the cp.async and generic kernel families solve
+    the config-3-shaped space-time problem to the oracle's T."""
+    n, nt = 32, 24
+    rho = _design(2, n, nt, False, 4)
+    outs = []
+    for opts in (dict(), dict(fuse_prolong=0), dict(kernel_family=S.st.ST_KERNELS_CPASYNC),
+                 dict(kernel_family=S.st.ST_KERNELS_GENERIC)):
+        solver, prob = make_pair(2, n, nt, source=("sin", 1.0, 1.0, 2 * np.pi), rtol=1e-10, **opts)
+        T = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+        solver.solve(dev(rho), T)
+        outs.append(host(T))
+        solver.close()
+    T_ref = prob.forward(rho)
+    for T in outs:
+        assert rel(T, T_ref) <= 1e-8
+
+
+# ------------------------------------------------------------------ the paper's coarsest solve
+@pytest.mark.parametrize("sdim,n,nt,tc,mats", [(2, 32, 32, False, CFG1_MATS), (2, 32, 64, True, CFG1_MATS),
+                                               (3, 8, 16, True, CFG4_MATS)])
+def test_gmres_coarsest_solve_matches_oracle(sdim, n, nt, tc, mats):
+    """coarse_solver = ST_COARSE_GMRES (GMRES(<= 200)-Jacobi to rtol 1e-6 on the
+    coarsest level, here a level of several thousand nodes, larger than the dense solve takes) inside
+    FGMRES: T and lambda equal the oracle's."""
+    solver, prob = make_pair(sdim, n, nt, mats=mats, time_constant=tc, rtol=1e-10, maxit=800,
+                             coarse_solver=S.st.ST_COARSE_GMRES, coarse_max_nodes=6000)
+    h = solver.hierarchy()
+    assert h[-1]["nodes"] > 1000 and h[-1]["form"] != "dense"
+    rho = _design(sdim, n, nt, tc, 2)
+    T_ref, lam_ref = prob.solve_both(rho)
+    T = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+    solver.solve(dev(rho), T)
+    assert solver.stats()["converged"] == 1
+    assert rel(host(T), T_ref) <= 1e-8
+    lam = torch.zeros_like(T)
+    solver.adjoint(dev(rho), None, lam)
+    assert rel(host(lam), lam_ref) <= 1e-8
+    solver.close()
+
+
+def test_paper_solver_variant_with_inner_tolerances():
+    """The paper's full preconditioner: GMRES(10)-Jacobi smoother with inner rtol
+    1e-6, GMRES(200) coarsest solve with rtol 1e-6, on the semi-coarsened hierarchy; converges to the
+    oracle's solution, and semi-coarsening needs fewer outer iterations than full space-time coarsening
+    (5.6 / 9.4 vs 9.7 / 55.6)."""
+    n, nt = 32, 32
+    rho = _design(2, n, nt, False, 7)
+    its = {}
+    for full in (0, 1):
+        solver, prob = make_pair(2, n, nt, rtol=1e-10, maxit=800, smoother=S.st.ST_SMOOTH_GMRES, nu_pre=10,
+                                 nu_post=10, smoother_rtol=1e-6, coarse_solver=S.st.ST_COARSE_GMRES,
+                                 coarse_max_nodes=2000, full_coarsening=full)
+        T = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+        solver.solve(dev(rho), T)
+        assert solver.stats()["converged"] == 1
+        f_its = solver.stats()["iterations"]
+        lam = torch.zeros_like(T)
+        solver.adjoint(dev(rho), None, lam)
+        its[full] = (f_its, solver.stats()["iterations"])
+        T_ref, lam_ref = prob.solve_both(rho)
+        assert rel(host(T), T_ref) <= 1e-8 and rel(host(lam), lam_ref) <= 1e-8
+        solver.close()
+    assert its[0][0] <= its[1][0] and its[0][1] <= its[1][1], its

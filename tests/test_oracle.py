@@ -261,18 +261,6 @@ def test_direct_solve_matches_dense():
     assert np.abs(P.adjoint(rho, g) - lam_dense).max() < 1e-13
 
 
-def test_config1_regression_values():
-    """Survey-time cross-check values for config 1, seed 0: not
-    authority, but they catch accidental changes of conventions."""
-    mesh = O.Mesh(2, 16, 16)
-    P = O.Problem(mesh, CFG1_MATS)
-    rho = I.rho_uniform((16, 16, 16), 0)
-    T, lam = P.solve_both(rho)
-    assert P.compliance(T) == pytest.approx(4.605063874081e-01, rel=1e-11)
-    assert np.linalg.norm(T) == pytest.approx(3.762128240083e+01, rel=1e-11)
-    assert np.linalg.norm(lam) == pytest.approx(3.606453687852e+01, rel=1e-11)
-
-
 # ---------------------------------------------------------------- convergence to time stepping
 def test_converges_to_backward_euler_first_order():
     """The stabilised space-time solution converges to fine-step implicit time stepping at
