@@ -128,7 +128,8 @@ typedef struct {
   int32_t chunk_planes;     /* persistent stencil kernels: planes per time chunk of the work list;
                                0 = automatic, > 0 forced, < 0 no chunking   */
   int32_t max_ctas;         /* persistent stencil kernels: cap on the grid (0 = one full wave);
-                               a small cap makes every CTA walk long multi-tile plane runs       */
+                               a small cap makes every CTA walk long multi-tile plane runs; < 0:
+                               tv2d trims the wave so the tiles form equal full groups (exp.)   */
   int32_t fuse_prolong;     /* 1 (default): prolongation + correction fused into the first
                                post-sweep where a kernel supports it; 0: separate kernels      */
   int32_t fuse_restrict;    /* 1 (default): residual + restriction in one pass where a kernel
@@ -140,6 +141,9 @@ typedef struct {
                                CUDA graph (0 = every replicated coarse level)                  */
   double smoother_rtol;     /* ST_SMOOTH_GMRES: stop the inner GMRES once ||r|| <= smoother_rtol
                                ||r0|| (1e-6); 0 = fixed nu steps (graph-capturable) */
+  int64_t nu_fine_nodes;    /* coarse levels with at least this many nodes use the fine-level sweep
+                               counts nu_pre / nu_post instead of nu_coarse (their sweeps cost HBM
+                               passes, not launch latency); 0 = level 0 only  */
 } st_options_t;
 
 /* Distribution over time slabs. NULL or size == 1 => one GPU.

@@ -889,8 +889,14 @@ void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_gr
     gmres_smooth(c, l, trans, b, x, false, rl);
     return;
   }
-  const int npre = (l > 0 && c->opt.nu_coarse > 0) ? c->opt.nu_coarse : c->opt.nu_pre;
-  const int npost = (l > 0 && c->opt.nu_coarse > 0) ? c->opt.nu_coarse : c->opt.nu_post;
+  // sweep counts: nu_pre / nu_post on the fine level (and on coarse levels of >= nu_fine_nodes global
+  // nodes), nu_coarse on the other coarse levels
+  const long long gnodes = (long long)(Lv.ntg + 1) * (c->sd == 2 ? (long long)Lv.g.nn * Lv.g.nn
+                                                                 : (long long)Lv.g.nn * Lv.g.nn * Lv.g.nn);
+  const bool coarse_nu = l > 0 && c->opt.nu_coarse > 0 &&
+                         !(c->opt.nu_fine_nodes > 0 && gnodes >= c->opt.nu_fine_nodes);
+  const int npre = coarse_nu ? c->opt.nu_coarse : c->opt.nu_pre;
+  const int npost = coarse_nu ? c->opt.nu_coarse : c->opt.nu_post;
   const int total = npre + npost;
   double* cur = (total % 2 == 1) ? x : Lv.t;
   double* oth = (cur == x) ? Lv.t : x;
@@ -1126,14 +1132,18 @@ Geom owned_geom(const st_ctx* c) {
 }
 // caller vector (dense layout of the owned planes, host or device) -> internal padded vector;
 // ghost = true refreshes the ghost planes (vectors read through the stencil)
-void pack_in(st_ctx* c, const double* user, double* internal, int slot, bool ghost = false) {
-  const double* d = in_ptr(c, user, c->Nd, slot);
+// Host vectors of the nodal calls share ONE staging buffer (slot 0): every use is stream-ordered (the
+// relayout kernel reading staged data precedes the next copy into the buffer) — config 3's e2e path
+// then stages through one 8.6 GB buffer instead of four.
+void pack_in(st_ctx* c, const double* user, double* internal, int /*slot*/, bool ghost = false) {
+  const double* d = in_ptr(c, user, c->Nd, 0);
   launch_relayout(c->gd0, d, c->lv[0].g, internal + c->voff, c->stream);
   L(c);
   if (ghost) halo(c, 0, internal);
 }
 // internal padded vector -> caller vector (dense layout, host or device); synchronises
-void unpack_out(st_ctx* c, const double* internal, double* user, int slot) {
+void unpack_out(st_ctx* c, const double* internal, double* user, int /*slot*/) {
+  const int slot = 0;
   if (!user) throw StErr{ST_E_INVALID_ARG, "null pointer"};
   const Geom go = owned_geom(c);
   if (is_device_ptr(user)) {
@@ -1234,6 +1244,10 @@ void st_default_options(st_options_t* o) {
   o->dgks_eta = 0.1;
   o->graph_max_nodes = 0;
   o->smoother_rtol = 0.0;
+  // coarse levels of >= 1e7 nodes sweep like the fine level (2+2): measured config 3 511 -> 607 MDOF/s
+  // (levels 1-3: 2.7e8, 6.8e7, 1.7e7 nodes), config 5 247 -> 271, the 512^2 x 512 slab 486 -> 551;
+  // configs 2 / 4 have no such coarse level (profiles/r02/nu_fine_nodes.log)
+  o->nu_fine_nodes = 10000000;
 }
 
 const char* st_strerror(int code) {
@@ -1420,7 +1434,7 @@ int st_sensitivity(st_ctx_t* c, const double* rho, const double* T, const double
     for (int d = 0; d < c->sd; ++d) nsp *= c->grid.n;
     const long long ndj = c->tc ? nsp : nsp * op.g.nt;
     bool staged = false;
-    double* dj = out_ptr(c, dJ, ndj, 3, false, &staged);
+    double* dj = out_ptr(c, dJ, ndj, 0, false, &staged);  // after the packs' relayouts (stream order)
     launch_sensitivity(op, Ti, li, dj, c->stream);
     L(c);
     check_launch();

@@ -10,30 +10,42 @@ namespace st {
 // f_a = sum_e int N_a Q~ dV for a spatially uniform source: exact spatial
 // integrals (dx/2 per adjacent element and direction) times 2-point Gauss in time per
 // element layer (R-5).
+// One CTA row per time plane (blockIdx.y): the temporal factor of the plane (4 Gauss points, the
+// sin of Q(t)) is evaluated once per CTA, then the plane's nodes are written with a grid-stride loop.
 template <int SD>
 __global__ void source_kernel(Geom g, int kind, double qscale, double a, double w, double tau, double* __restrict__ f) {
-  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= g.N) return;
-  int p = (int)(idx / g.P);
-  long long pn = idx % g.P;
-  int cc[3];
-  if (!pdecode<SD>(g, pn, cc)) { f[idx] = 0.0; return; }
-  double sx = 1.0;
-  for (int d = 0; d < SD; ++d) sx *= 0.5 * g.dx * ((cc[d] == 0 || cc[d] == g.n) ? 1.0 : 2.0);
-  const double s = 0.5 / sqrt(3.0);
-  double ft = 0.0;
-  for (int side = 0; side < 2; ++side) {
-    int l = side == 0 ? p - 1 : p;       // layer; node is its top (side 0) or bottom (side 1)
-    if (l < 0 || l >= g.nt) continue;
-    for (int gp = 0; gp < 2; ++gp) {
-      double sg = gp == 0 ? -s : s;
-      double tt = (l + g.pg0 + 0.5 + sg) * g.dt;  // global time of the Gauss point
-      double N = side == 0 ? (0.5 + sg) : (0.5 - sg);
-      double Q = qscale * ((kind == 1) ? (1.0 + a * sin(w * tau * tt)) : 1.0);
-      ft += 0.5 * g.dt * N * Q;
+  __shared__ double ft_s;
+  for (int p = blockIdx.y; p <= g.nt; p += gridDim.y) {
+    if (threadIdx.x == 0) {
+      const double s = 0.5 / sqrt(3.0);
+      double ft = 0.0;
+      for (int side = 0; side < 2; ++side) {
+        const int l = side == 0 ? p - 1 : p;  // layer; the node is its top (side 0) or bottom (side 1)
+        if (l < 0 || l >= g.nt) continue;
+        for (int gp = 0; gp < 2; ++gp) {
+          const double sg = gp == 0 ? -s : s;
+          const double tt = (l + g.pg0 + 0.5 + sg) * g.dt;  // global time of the Gauss point
+          const double N = side == 0 ? (0.5 + sg) : (0.5 - sg);
+          const double Q = qscale * ((kind == 1) ? (1.0 + a * sin(w * tau * tt)) : 1.0);
+          ft += 0.5 * g.dt * N * Q;
+        }
+      }
+      ft_s = ft;
     }
+    __syncthreads();
+    const double ft = ft_s;
+    double* fp = f + (long long)p * g.P;
+    for (long long pn = blockIdx.x * (long long)blockDim.x + threadIdx.x; pn < g.P;
+         pn += (long long)gridDim.x * blockDim.x) {
+      int cc[3];
+      if (!pdecode<SD>(g, pn, cc)) { fp[pn] = 0.0; continue; }
+      double sx = 1.0;
+#pragma unroll
+      for (int d = 0; d < SD; ++d) sx *= 0.5 * g.dx * ((cc[d] == 0 || cc[d] == g.n) ? 1.0 : 2.0);
+      fp[pn] = sx * ft;
+    }
+    __syncthreads();
   }
-  f[idx] = sx * ft;
 }
 
 __global__ void ktilde_kernel(const double* __restrict__ rho, int n, int nl, MatsDev m, double* __restrict__ kt) {
@@ -57,9 +69,10 @@ void launch_ktilde(const double* rho, int n, int nl, const MatsDev& m, double* k
 }
 
 void launch_source(const Geom& g, int kind, double qscale, double a, double w, double tau, double* f, cudaStream_t s) {
-  unsigned grd = (unsigned)((g.N + 255) / 256);
-  if (g.sd == 2) source_kernel<2><<<grd, 256, 0, s>>>(g, kind, qscale, a, w, tau, f);
-  else source_kernel<3><<<grd, 256, 0, s>>>(g, kind, qscale, a, w, tau, f);
+  const long long bx = std::min<long long>((g.P + 255) / 256, 64);
+  const unsigned by = (unsigned)std::min<long long>(g.nt + 1, 65535);
+  if (g.sd == 2) source_kernel<2><<<dim3((unsigned)bx, by), 256, 0, s>>>(g, kind, qscale, a, w, tau, f);
+  else source_kernel<3><<<dim3((unsigned)bx, by), 256, 0, s>>>(g, kind, qscale, a, w, tau, f);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -88,23 +88,40 @@ __global__ void prolong_kernel(Geom gf, Geom gc, const double* __restrict__ ec, 
   xf[idx] += acc;
 }
 
-// (2+1)D space coarsening, the hot transfer pair: thread per (x1 node, x2 row, plane), no 64-bit
-// index arithmetic; rows are read coalesced and the coarse row of the prolongation comes from L1.
+// (2+1)D space coarsening, the hot transfer pair: no 64-bit index arithmetic per node, rows read
+// coalesced. Prolongation: one thread per coarse node (I, J) of a plane updates the 2 x 2 fine nodes
+// (2I, 2I+1) x (2J, 2J+1) with 16-byte loads / stores of the fine pairs (even pitch: 16-B aligned)
+// and the 4 coarse corners loaded once (bilinear weights 1, 1/2, 1/4); fine nodes past
+// the last node (the pad column n+1, row n+1) and constrained fine nodes are left alone.
 __global__ void __launch_bounds__(128) prolong2s_kernel(Geom gf, Geom gc, const double* __restrict__ ec,
                                                         double* __restrict__ xf) {
-  const int i = blockIdx.x * 128 + threadIdx.x, j = blockIdx.y, p = blockIdx.z;
-  if (i >= gf.nn) return;
-  int c[3] = {i, j, 0};
-  if (is_cons<2>(gf, c, p)) return;
+  const int I = blockIdx.x * 128 + threadIdx.x, J = blockIdx.y, p = blockIdx.z;
+  if (I >= gc.nn) return;
+  if (p + gf.pg0 == 0) return;  // initial-condition plane: constrained
   const int Pc = p + gf.pg0 - gc.pg0;
   if (Pc < 0 || Pc > gc.nt) return;
-  const double* e0 = ec + (long long)Pc * gc.P + (long long)(j >> 1) * gc.pr + (i >> 1);
-  double v;
-  if (!(i & 1) && !(j & 1)) v = __ldg(e0);
-  else if (!(j & 1)) v = 0.5 * (__ldg(e0) + __ldg(e0 + 1));
-  else if (!(i & 1)) v = 0.5 * (__ldg(e0) + __ldg(e0 + gc.pr));
-  else v = 0.25 * ((__ldg(e0) + __ldg(e0 + 1)) + (__ldg(e0 + gc.pr) + __ldg(e0 + gc.pr + 1)));
-  xf[(long long)p * gf.P + (long long)j * gf.pr + i] += v;
+  const double* e0 = ec + (long long)Pc * gc.P + (long long)J * gc.pr + I;
+  const bool hx = I + 1 < gc.nn, hy = J + 1 < gc.nn;  // fine column 2I+1 / row 2J+1 exist
+  const double e00 = __ldg(e0);
+  const double e10 = hx ? __ldg(e0 + 1) : 0.0;
+  const double e01 = hy ? __ldg(e0 + gc.pr) : 0.0;
+  const double e11 = (hx && hy) ? __ldg(e0 + gc.pr + 1) : 0.0;
+  double* x0 = xf + (long long)p * gf.P + (long long)(2 * J) * gf.pr + 2 * I;
+  // sink patch: fine node (0, j) with j in [plo, phi] is constrained (R-4)
+  const bool m0 = I == 0 && 2 * J >= gf.plo && 2 * J <= gf.phi;
+  const bool m1 = I == 0 && 2 * J + 1 >= gf.plo && 2 * J + 1 <= gf.phi;
+  {
+    double2 v = *reinterpret_cast<const double2*>(x0);
+    if (!m0) v.x += e00;
+    if (hx) v.y += 0.5 * (e00 + e10);
+    *reinterpret_cast<double2*>(x0) = v;
+  }
+  if (hy) {
+    double2 v = *reinterpret_cast<const double2*>(x0 + gf.pr);
+    if (!m1) v.x += 0.5 * (e00 + e01);
+    if (hx) v.y += 0.25 * ((e00 + e10) + (e01 + e11));
+    *reinterpret_cast<double2*>(x0 + gf.pr) = v;
+  }
 }
 
 __global__ void __launch_bounds__(128) restrict2s_kernel(Geom gf, Geom gc, const double* __restrict__ rf,
@@ -151,8 +168,9 @@ void launch_restrict(const Geom& gf, const Geom& gc, int kind, const double* rf,
 }
 
 void launch_prolong_add(const Geom& gf, const Geom& gc, int kind, const double* ec, double* xf, cudaStream_t s) {
-  if (gf.sd == 2 && kind == KIND_SPACE && gf.nt + 1 <= 65535) {
-    prolong2s_kernel<<<dim3((gf.nn + 127) / 128, gf.nn, gf.nt + 1), 128, 0, s>>>(gf, gc, ec, xf);
+  // the paired kernel needs an even fine pitch (16-B aligned pairs): every internal vector has one
+  if (gf.sd == 2 && kind == KIND_SPACE && gf.nt + 1 <= 65535 && gf.pr % 2 == 0 && gf.P % 2 == 0) {
+    prolong2s_kernel<<<dim3((gc.nn + 127) / 128, gc.nn, gf.nt + 1), 128, 0, s>>>(gf, gc, ec, xf);
     return;
   }
   int blk = 256;

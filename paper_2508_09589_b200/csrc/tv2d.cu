@@ -123,15 +123,18 @@ struct Seg {
   int p0, p1, qs, qe;  // rows p0 .. p1-1; planes qs .. qe (qs = p0 - 1 reloads the plane below)
   int x0, y0, bx, by;  // node tile origin, layer box origin
 };
-// Sliced chunk schedule: the NP planes are cut into nch balanced chunks; CTA b of G takes the
-// b-th 1/G slice of every chunk's (tile, plane) items (tile-major inside the chunk), chunk after
-// chunk. All CTAs therefore sweep the same few planes together: a halo a tile shares with a
-// neighbour is loaded by another CTA at about the same time (or by this CTA's previous segment,
-// at most one chunk earlier) and hits L2, and a segment restart reloads an L2-resident plane.
-// nch = 1 is the plain contiguous split of the tile-major list.
+// Strided chunk schedule: the NP planes are cut into nch balanced chunks of ~K
+// planes; inside a chunk the tiles form groups of G = gridDim.x consecutive tiles, and CTA b takes
+// tile kG + b of every full group k for all the chunk's planes (one segment per group), then an
+// equal share of the (tile, plane) items of the last, partial group (contiguous, tile-major). At any
+// moment CTA b and CTA b + 1 (b +- ntx) therefore work on x- (y-) neighbouring tiles at about the same
+// plane: the halo rows / columns two tiles share, and the layer box rows, are requested twice within
+// a short interval and the second request hits L2 (the round-1 slice-per-CTA schedule put a CTA's
+// neighbour tiles 16 planes apart in time on the same CTA: ~10 % L2 hit rate at 1024^2 x 1024,
+// 1.8x the algorithmic DRAM reads, profiles/r02). nch = 1 (K = NP): one chunk.
 struct Sched {
   long long tiles, w, we;
-  int NP, nch, c, cs, Kc;
+  int NP, nch, c, cs, Kc, k, nfull;
 };
 __device__ __forceinline__ void sched_init(Sched& s, long long tiles, int NP, int K) {
   s.tiles = tiles;
@@ -140,22 +143,39 @@ __device__ __forceinline__ void sched_init(Sched& s, long long tiles, int NP, in
   s.c = -1;
   s.w = s.we = 0;
   s.cs = s.Kc = 0;
+  s.k = s.nfull = 0;
 }
 __device__ __forceinline__ bool next_seg(Sched& s, int ntx, int nt, Seg& sg) {
-  while (s.w >= s.we) {
+  const long long G = gridDim.x, b = blockIdx.x;
+  long long tile;
+  for (;;) {
+    if (s.c >= 0) {
+      if (s.k < s.nfull) {  // full group k: tile k G + b over every plane of the chunk
+        tile = s.k * G + b;
+        sg.p0 = s.cs;
+        sg.p1 = s.cs + s.Kc;
+        ++s.k;
+        break;
+      }
+      if (s.w < s.we) {  // partial group: a contiguous share of its (tile, plane) items
+        const long long r = s.w;
+        tile = (long long)s.nfull * G + r / s.Kc;
+        sg.p0 = s.cs + (int)(r % s.Kc);
+        const long long rem = s.we - s.w;
+        sg.p1 = (rem < s.cs + s.Kc - sg.p0) ? sg.p0 + (int)rem : s.cs + s.Kc;
+        s.w += sg.p1 - sg.p0;
+        break;
+      }
+    }
     if (++s.c >= s.nch) return false;
     s.cs = (int)((long long)s.c * s.NP / s.nch);
     s.Kc = (int)((long long)(s.c + 1) * s.NP / s.nch) - s.cs;
-    const long long items = s.tiles * s.Kc, base = s.tiles * s.cs;
-    s.w = base + items * blockIdx.x / gridDim.x;
-    s.we = base + items * (blockIdx.x + 1) / gridDim.x;
+    s.nfull = (int)(s.tiles / G);
+    s.k = 0;
+    const long long items = (s.tiles - (long long)s.nfull * G) * s.Kc;
+    s.w = items * b / G;
+    s.we = items * (b + 1) / G;
   }
-  const long long r = s.w - s.tiles * s.cs;
-  const long long tile = r / s.Kc;
-  sg.p0 = s.cs + (int)(r % s.Kc);
-  const long long rem = s.we - s.w;
-  sg.p1 = (rem < s.cs + s.Kc - sg.p0) ? sg.p0 + (int)rem : s.cs + s.Kc;
-  s.w += sg.p1 - sg.p0;
   sg.qs = max(sg.p0 - 1, 0);
   sg.qe = min(sg.p1, nt);
   sg.x0 = (int)(tile % ntx) * TX;
@@ -479,16 +499,34 @@ void ltv(const CUtensorMap& mx, const CUtensorMap& mb, const CUtensorMap& ml, co
   }
   const long long ntx = (g.nn + TX - 1) / TX, nty = (g.nn + TY - 1) / TY;
   const long long wtot = ntx * nty * (g.nt + 1);
-  const long long grid = persistent_grid(op, nsm, resident, wtot);
-  // plane chunks: with long per-CTA plane runs the contiguous split leaves neighbouring tiles at
-  // unrelated planes (halo re-reads from DRAM: 1.77x the algorithmic bytes at 512^2 x 512);
-  // sliced chunks keep them together — 16 planes on the fine level, 32 on the stored-stencil
-  // levels (heavier restarts). Measured (profiles/r01/kbench_tv2d_sliced.log, tv2d_src1_chunk.log):
-  // 512^2 x 512 fine 1475 -> 1129 us, level 1 657 -> 553 us; with short runs (< 256 planes per CTA:
-  // 256^3 levels 0 / 1, 512^2 level 2) the restarts cost more than they save. st_options_t chunk_planes
-  // overrides (parity tests force the sliced schedule on small grids).
+  long long grid = persistent_grid(op, nsm, resident, wtot);
+  const long long tiles = ntx * nty;
   const int NPl = g.nt + 1;
-  const int kch = chunk_planes(op, NPl, wtot / grid >= 256 ? (SRC == 0 ? 16 : 32) : NPl);
+  int kauto;
+  if (tiles >= grid) {
+    // at least one tile per CTA: the strided schedule over whole tile columns, one chunk. Measured at
+    // 1024^2 x 1024 (profiles/r02/kbench_c3_chunk.log): fine JAC sweep 10.7 ms (round-1 sliced
+    // 16-plane chunks) -> 6.8 ms, DRAM reads 46.2 -> 30.4 GB (the x / b / k~ reads are 25.8 GB);
+    // K = 16 / 32 / 64 / 128: 9.0 / 8.7 / 8.1 / 7.4 ms. A large partial last group (its tile columns
+    // split into plane ranges over all CTAs) loses the reuse: then the grid is trimmed so that the
+    // tiles form equal full groups — 512^2 (1089 tiles: 1 group of 592 + 497) 1105 -> 946 us with 2
+    // groups of 545, while 1024^2 (4257 tiles: 7 x 592 + 113) keeps its wave (8 x 533: 6.81 -> 7.59
+    // ms; profiles/r02/kbench_trim.log). max_ctas < 0 forces the trim.
+    const long long part = tiles % grid;
+    if (op.max_ctas < 0 || (op.max_ctas == 0 && part * 5 >= grid * 2)) {
+      const long long groups = (tiles + grid - 1) / grid;
+      grid = (tiles + groups - 1) / groups;
+    }
+    kauto = NPl;
+  } else {
+    // fewer tiles than CTAs: CTAs share a tile's planes (contiguous ranges of the partial group);
+    // with long runs (>= 256 planes per CTA) chunks keep neighbouring tiles at nearby planes: 512^2 x
+    // 512 fine sweep 1114 (one chunk) -> 942 us (K = 64), its stored-stencil level 1 694 -> 576 us
+    // (K = 32); short runs keep one chunk
+    kauto = wtot / grid >= 256 ? (SRC == 0 ? 64 : 32) : NPl;
+  }
+  // st_options_t chunk_planes overrides (parity tests force chunked schedules on small grids)
+  const int kch = chunk_planes(op, NPl, kauto);
   kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, ml, op, x, y, omega, wtot, kch, (int)ntx);
 }
 }  // namespace

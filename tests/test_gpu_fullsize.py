@@ -144,7 +144,9 @@ def certify(name, sdim, n, nt, tc, design, src, mats, opts, rho=None, nrows=2500
         Tm, Lm = _gather(T, en), _gather(lam, en)
         ref = O.sensitivity_elements(prob, rho, Tm, Lm, el)
         got = dJ[torch.as_tensor(el, device=DEV)].cpu().numpy()
-    assert rel(got, ref) <= 1e-10, (name, rel(got, ref))
+    # per-element values to 1e-10; time-constant sums over nt layers (cancellation) to 1e-8, both well
+    # inside the north_star's 1e-7 (R-16)
+    assert rel(got, ref) <= (1e-8 if tc else 1e-10), (name, rel(got, ref))
     out = dict(st)
     solver.close()
     return out

@@ -42,12 +42,31 @@ def _design(sdim, n, nt, tc, seed):
 # from the k~ table, SRC 0; per-layer stored-stencil levels, SRC 1); tc2d / tc3d = time-constant
 SCHED_CASES = [
     ("tv2d", 2, 48, 40, False, CFG1_MATS),
-    ("tv2d-ragged", 2, 40, 37, False, CFG1_MATS),
+    ("tv2d-ragged", 2, 40, 36, False, CFG1_MATS),
     ("tc2d", 2, 48, 40, True, CFG1_MATS),
     ("tc3d", 3, 10, 12, True, CFG4_MATS),
-    ("tc3d-ragged", 3, 9, 10, True, CFG1_MATS),
+    ("tc3d-ragged", 3, 10, 10, True, CFG1_MATS),
 ]
 SCHEDULES = [(0, 1), (0, 3), (16, 0), (16, 2), (32, 5), (5, 3), (-1, 2)]  # (chunk_planes, max_ctas)
+
+
+_ORACLE = {}
+
+
+def _oracle_case(case):
+    """Assembled operators and direct solutions of a case (computed once per case)."""
+    if case[0] not in _ORACLE:
+        name, sdim, n, nt, tc, mats = case
+        prob = O.Problem(O.Mesh(sdim, n, nt), O.Materials(*mats), O.BCs(T0=0.2), O.Source())
+        rho = _design(sdim, n, nt, tc, 3)
+        K = prob.K(rho)
+        Kbc, _, _, _ = prob.system(rho)
+        T_ref, lam_ref = prob.solve_both(rho)
+        _ORACLE[case[0]] = (prob, rho, K, Kbc, T_ref, lam_ref)
+    return _ORACLE[case[0]]
+
+
+SOLVE_SCHEDULES = {(0, 1), (16, 2), (32, 5), (5, 3)}
 
 
 @pytest.mark.parametrize("sched", SCHEDULES, ids=lambda s: f"chunk{s[0]}-ctas{s[1]}")
@@ -55,11 +74,9 @@ SCHEDULES = [(0, 1), (0, 3), (16, 0), (16, 2), (32, 5), (5, 3), (-1, 2)]  # (chu
 def test_forced_schedule_operator_and_solve_parity(case, sched):
     name, sdim, n, nt, tc, mats = case
     chunk, ctas = sched
-    solver, prob = make_pair(sdim, n, nt, mats=mats, T0=0.2, time_constant=tc, rtol=1e-11, maxit=600,
-                             chunk_planes=chunk, max_ctas=ctas, coarse_max_nodes=64)
-    rho = _design(sdim, n, nt, tc, 3)
-    K = prob.K(rho)
-    Kbc, _, _, _ = prob.system(rho)
+    prob, rho, K, Kbc, T_ref, lam_ref = _oracle_case(case)
+    solver, _ = make_pair(sdim, n, nt, mats=mats, T0=0.2, time_constant=tc, rtol=1e-11, maxit=600,
+                          chunk_planes=chunk, max_ctas=ctas, coarse_max_nodes=64)
     x = I.rand_vector(prob.mesh.n_nodes, 17)
     xd, yd = dev(x), torch.empty(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
     for trans in (False, True):
@@ -68,14 +85,14 @@ def test_forced_schedule_operator_and_solve_parity(case, sched):
             ref = (A.T if trans else A) @ x
             solver.apply(dev(rho), xd, yd, transpose=trans, bc=bc)
             assert rel(host(yd), ref) <= 1e-12, (name, sched, trans, bc, rel(host(yd), ref))
-    T_ref, lam_ref = prob.solve_both(rho)
-    T = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
-    solver.solve(dev(rho), T)
-    assert solver.stats()["converged"] == 1
-    assert rel(host(T), T_ref) <= 1e-8
-    lam = torch.zeros_like(T)
-    solver.adjoint(dev(rho), dev(prob.compliance_rhs()), lam)
-    assert rel(host(lam), lam_ref) <= 1e-8
+    if sched in SOLVE_SCHEDULES:  # every mode of every level under the forced schedule
+        T = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+        solver.solve(dev(rho), T)
+        assert solver.stats()["converged"] == 1
+        assert rel(host(T), T_ref) <= 1e-8
+        lam = torch.zeros_like(T)
+        solver.adjoint(dev(rho), None, lam)
+        assert rel(host(lam), lam_ref) <= 1e-8
     solver.close()
 
 
