@@ -132,6 +132,9 @@ def parse():
     ap.add_argument("--nu-fine-nodes", type=int, default=-1,
                     help="coarse levels with at least this many nodes use the fine-level sweep counts (default: the "
                          "workload's)")
+    ap.add_argument("--timestepping", action="store_true",
+                    help="also time the GPU time-stepping baseline (st_timestep, backward Euler with nt steps and a "
+                         "spatial-MG PCG per step; time-constant workloads) against the space-time forward solve")
     ap.add_argument("--cpu-worker", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--cpu-reps", type=int, default=1, help=argparse.SUPPRESS)
     return ap.parse_args()
@@ -411,6 +414,23 @@ def run_cuda(args):
         "frac": step_bytes / (ms / 1e3) / 1e9 / peak,
         "model": "SURVEY.md sec. 8(d) per-iteration bytes (nu 2+2, m 20) x N_n x (forward + adjoint iterations)"}
 
+    # ---- GPU time-stepping baseline ---------------------
+    tsres = None
+    if args.timestepping and wl["tc"] and world == 1:
+        Tts = torch.empty((wl["nt"] + 1) * (wl["n"] + 1) ** wl["sdim"], dtype=torch.float64, device=dev)
+        with torch.cuda.stream(stream):
+            solver.timestep(rhos[0], wl["nt"], Tts)       # warm-up (graph capture)
+            tsr = [solver.timestep(rhos[k % len(rhos)], wl["nt"], Tts) for k in range(2)]
+        ts_ms = statistics.mean(x["ms"] for x in tsr)
+        st_fwd = statistics.mean(x[2] for x in its)
+        tsres = {"method": "backward Euler, nt steps, spatial-MG PCG per step (same rtol), CUDA graph per CG iteration",
+                 "steps": wl["nt"], "ms_forward": ts_ms, "cg_iterations": tsr[-1]["cg_iterations"],
+                 "max_step_iterations": tsr[-1]["max_step_iterations"],
+                 "space_time_forward_ms": st_fwd, "space_time_speedup_forward": ts_ms / st_fwd,
+                 "note": "forward solves only, same mesh / design / rtol; the paper's 52x (PAPER.md:712) compares "
+                         "whole design iterations on CPU clusters"}
+        del Tts
+
     # ---- end-to-end through the C ABI with pinned host buffers ------------------------------
     e2e = None
     if args.e2e_steps > 0 and design:
@@ -530,6 +550,8 @@ def run_cuda(args):
                    "device_mem_used_gb": round(mem_used / 1e9, 1)},
         "paper_context": PAPER_CONTEXT,
     }
+    if tsres is not None:
+        out["timestepping"] = tsres
     if rank == 0:
         print(json.dumps(out))
     solver.close()

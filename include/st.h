@@ -58,7 +58,12 @@ enum {
 };
 
 enum { ST_TIME_CONSTANT = 0, ST_SPACE_TIME = 1 };
-enum { ST_SRC_UNIFORM = 0, ST_SRC_SIN = 1 };
+/* Sources (rescaled units, R-7): UNIFORM Q~ = Q0 tau; SIN Q~ = Q0 tau (1 + a sin(w tau t));
+ * the paper's examples, Q0 given already rescaled (no tau factor): EX1 Q~ = 1/2 Q0 (1 - t)(1 + cos 50 t)
+ * (Example 1, Q0 = 100); EX2 Q~ = Q0 exp(-|x - x0(t)|^2 / (2 sigma^2)) with
+ * x0(t) = (1/2 + R cos(w tau t + pi/2), 1/2 + R sin(w tau t + pi/2)) (Example 2: Q0 = 1,
+ * sigma = 0.05, R = 0.25, w = pi, tau = 6; (2+1)D only). */
+enum { ST_SRC_UNIFORM = 0, ST_SRC_SIN = 1, ST_SRC_EX1 = 2, ST_SRC_EX2 = 3 };
 /* Smoothers: damped Jacobi (default); the paper's GMRES(k)-Jacobi smoother
  * (k = nu_pre / nu_post fixed steps, <= 24; one GPU). ST_SMOOTH_CHEBYSHEV is reserved
  * (ST_E_UNSUPPORTED). */
@@ -94,10 +99,12 @@ typedef struct {
   int32_t has_patch;  /* 0 => insulated everywhere except the IC                         */
   int32_t face;
   double center, halfwidth; /* fractions of L; BASELINE default 0.5, 0.05               */
+  int32_t all_walls;  /* 1: T = 0 on every spatial boundary node at all t (Example 2's cold
+                         walls) instead of the patch                         */
 } st_bcs_t;
 
-/* Source Q (physical units): UNIFORM Q0;  SIN: Q0 (1 + a sin(w t_phys)), t_phys = tau t. */
-typedef struct { int32_t kind; double Q0, a, w; } st_source_t;
+/* Source (kinds above): UNIFORM Q0;  SIN: Q0 (1 + a sin(w t_phys)), t_phys = tau t; EX1; EX2 (sigma, R). */
+typedef struct { int32_t kind; double Q0, a, w, sigma, R; } st_source_t;
 
 typedef struct {
   int32_t design_mode;      /* ST_TIME_CONSTANT | ST_SPACE_TIME                          */
@@ -287,6 +294,24 @@ int st_pnorm(st_ctx_t* ctx, const double* T, double P, double* phi, double* dphi
 /* out = x . y over the owned nodes of all ranks (e.g. the compliance f^T T). */
 int st_dot(st_ctx_t* ctx, const double* x, const double* y, double* out);
 
+/* ---- GPU time-stepping baseline (the comparison method of PAPER.md:620, 704-712) ----
+ * First-order backward difference (M_C / dt + K_k) T^{m+1} = (M_C / dt) T^m + F(t_{m+1}), dt = 1 / nsteps
+ * (rescaled), T^0 = T0 (0 on the sink / walls), on the context's spatial mesh with its materials, source
+ * (spatially uniform kinds UNIFORM / SIN / EX1) and spatial Dirichlet data; each step solved to the
+ * context's rtol by CG preconditioned with a spatial geometric-multigrid V-cycle (full spatial
+ * coarsening, Galerkin, damped Jacobi 2 + 2, dense coarsest), one CUDA graph launch per CG iteration.
+ * rho: the time-constant design (n^sdim, ST_TIME_CONSTANT contexts, one GPU). T: (nsteps + 1) planes
+ * of (n+1)^sdim nodes in the caller layout (nsteps = nt gives the space-time vector layout), device or
+ * host. Errors: ST_E_UNSUPPORTED (space-time design, slabs, EX2 source), ST_E_INVALID_ARG. */
+typedef struct {
+  int32_t steps;
+  int32_t max_step_iterations;   /* most CG iterations of one step                               */
+  int64_t cg_iterations;         /* total over the steps                                          */
+  double ms;                     /* device time of setup + all steps                             */
+  int64_t launches;              /* kernels launched (graph nodes counted)                       */
+} st_ts_stats_t;
+int st_timestep(st_ctx_t* ctx, const double* rho, int32_t nsteps, double* T, st_ts_stats_t* stats);
+
 int st_get_stats(const st_ctx_t* ctx, st_stats_t* s);
 int st_local_layout(const st_ctx_t* ctx, st_layout_t* layout);
 
@@ -304,8 +329,8 @@ typedef struct {
 int st_plan(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* bcs, const st_options_t* opts,
             int32_t rank, int32_t size, st_plan_t* plan);
 /* sizeof of the ABI structs (binding self-check): grid, materials, bcs, source, options, dist,
- * stats, hierarchy, layout, plan */
-int st_struct_sizes(int64_t out[10]);
+ * stats, hierarchy, layout, plan, ts_stats */
+int st_struct_sizes(int64_t out[11]);
 /* NCCL helpers (libnccl.so.2 is opened at run time): a unique id on one rank, broadcast by
  * the caller, then one communicator per rank. Return ST_OK or ST_E_NCCL. */
 int st_nccl_unique_id(char id[ST_NCCL_ID_BYTES]);

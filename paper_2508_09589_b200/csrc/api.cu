@@ -18,6 +18,12 @@
 
 using namespace st;
 
+// csrc/timestep.cu
+long long st_run_timestepping(const Geom& g0, const MatsDev& md, const st_source_t& src, double tau, double T0,
+                              const double* rho, int nsteps, double rtol, int maxit, int coarse_max_nodes,
+                              const Geom& gdense, double* Tout, cudaStream_t s, double* ms_out, long long* launches,
+                              int* max_its);
+
 namespace {
 thread_local std::string g_last_error;
 
@@ -175,7 +181,9 @@ long long nodes_of(const Geom& g) {
   return v;
 }
 Geom dense_of(const Geom& g) {
-  return make_geom(g.sd, g.n, g.nt, g.plo, g.phi, false, (int)std::lround(1.0 / g.dt), g.pg0);
+  Geom d = make_geom(g.sd, g.n, g.nt, g.plo, g.phi, false, (int)std::lround(1.0 / g.dt), g.pg0);
+  d.walls = g.walls;
+  return d;
 }
 
 // E' = W0^T E W0 + W1^T E W1 (linear-in-time prolongation, two fine layers per coarse layer)
@@ -228,7 +236,7 @@ void build_hierarchy(st_ctx* c) {
   int n = (int)c->grid.n, nt = (int)c->grid.nt;
   // sink patch on the fine level: nodes j with |j/n - center| <= halfwidth (R-4)
   int plo = 1, phi = 0;
-  if (c->bcs.has_patch) {
+  if (c->bcs.has_patch && !c->bcs.all_walls) {  // all_walls takes precedence (as the oracle's dirichlet)
     plo = n + 1;
     phi = -1;
     for (int j = 0; j <= n; ++j) {
@@ -280,7 +288,10 @@ void build_hierarchy(st_ctx* c) {
                                        std::to_string(c->lv.back().g.N) +
                                        " stored nodes > 4096): grid not divisible enough; use coarse_solver = "
                                        "ST_COARSE_GMRES (the paper's GMRES coarsest solve)"};
-  for (auto& Lv : c->lv) Lv.ntg = Lv.g.nt;
+  for (auto& Lv : c->lv) {
+    Lv.ntg = Lv.g.nt;
+    Lv.g.walls = c->bcs.all_walls ? 1 : 0;  // coarse walls = injection of the fine walls (R-23)
+  }
 }
 
 // Time slabs: the leading levels whose time extent splits into G equal
@@ -310,10 +321,12 @@ void assign_slabs(st_ctx* c) {
       Lv.a = r * Lv.nloc;
       const int ntl = Lv.nloc + (r < G - 1 ? 1 : 0);  // + ghost layer (except the last rank)
       Lv.g = make_geom(g.sd, g.n, ntl, g.plo, g.phi, true, Lv.ntg, Lv.a);
+      Lv.g.walls = g.walls;
     } else if (l == nd && nd > 0) {
       Lv.gather_in = true;
       const int nlc = Lv.ntg / G, ac = r * nlc;
       Lv.gs = make_geom(g.sd, g.n, nlc + (r < G - 1 ? 1 : 0), g.plo, g.phi, true, Lv.ntg, ac);
+      Lv.gs.walls = g.walls;
     }
   }
 }
@@ -664,6 +677,7 @@ void build_ops(st_ctx* c) {
       } else {  // space coarsening of every parent layer into mid, then time coarsening of mid
         OpDesc mop = Pv.op;
         mop.g = make_geom(c->sd, Lv.g.n, Pv.g.nt, Lv.g.plo, Lv.g.phi);
+        mop.g.walls = Lv.g.walls;
         mop.form = Lv.mid_ns == 5 ? FORM_B4 : FORM_MK;
         mop.nl = Pv.g.nt;
         mop.tvl = 1;
@@ -726,7 +740,9 @@ void build_ops(st_ctx* c) {
 // source vector f (Q~ = Q tau) into `out` (one write pass, per call: no
 // full-length vector is kept for it)
 void make_source(st_ctx* c, double* out) {
-  launch_source(c->lv[0].g, c->src.kind, c->src.Q0 * c->grid.tau, c->src.a, c->src.w, c->grid.tau, out, c->stream);
+  // UNIFORM / SIN: Q~ = Q tau; EX1 / EX2: Q0 is given already rescaled
+  const bool ex = c->src.kind == ST_SRC_EX1 || c->src.kind == ST_SRC_EX2;
+  launch_source(c->lv[0].g, c->src, ex ? c->src.Q0 : c->src.Q0 * c->grid.tau, c->grid.tau, out, c->stream);
   L(c);
   check_launch();
 }
@@ -1279,7 +1295,9 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
     if (!(mats->C_ins > 0) || !(mats->C_con > 0) || !(mats->k_ins > 0) || !(mats->k_con > 0))
       throw StErr{ST_E_INVALID_ARG, "material constants must be > 0"};
     if (bcs->has_patch && bcs->face != 0) throw StErr{ST_E_UNSUPPORTED, "only face 0 (x1 = 0) supported"};
-    if (src->kind != ST_SRC_UNIFORM && src->kind != ST_SRC_SIN) throw StErr{ST_E_UNSUPPORTED, "source kind"};
+    if (src->kind < ST_SRC_UNIFORM || src->kind > ST_SRC_EX2) throw StErr{ST_E_UNSUPPORTED, "source kind"};
+    if (src->kind == ST_SRC_EX2 && (grid->sdim != 2 || !(src->sigma > 0)))
+      throw StErr{ST_E_INVALID_ARG, "ST_SRC_EX2: (2+1)D grid and sigma > 0"};
     if (dist && dist->size > 1) {
       if (dist->rank < 0 || dist->rank >= dist->size) throw StErr{ST_E_INVALID_ARG, "rank out of range"};
       if (grid->nt % dist->size != 0) throw StErr{ST_E_DIVISIBILITY, "time slabs: nt must be divisible by the rank count"};
@@ -1363,6 +1381,7 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       c->voff = (long long)c->o0 * L0.g.P;
       c->Nown = (long long)c->nown * L0.g.P;
       c->gd0 = make_geom(c->sd, L0.g.n, c->nown - 1, L0.g.plo, L0.g.phi, false, L0.ntg, L0.g.pg0 + c->o0);
+      c->gd0.walls = L0.g.walls;
       c->Nd = nodes_of(c->gd0);
       long long nsp = 1;
       for (int d = 0; d < c->sd; ++d) nsp *= grid->n;
@@ -1700,6 +1719,51 @@ int st_bench_op(st_ctx_t* c, const double* rho, int level, int mode, int transpo
   });
 }
 
+int st_timestep(st_ctx_t* c, const double* rho, int32_t nsteps, double* T, st_ts_stats_t* stats) {
+  return guarded([&]() -> int {
+    if (!c || !rho || !T) throw StErr{ST_E_INVALID_ARG, "null argument"};
+    if (nsteps < 1) throw StErr{ST_E_INVALID_ARG, "nsteps must be >= 1"};
+    if (!c->tc) throw StErr{ST_E_UNSUPPORTED, "time stepping: time-constant designs only"};
+    if (c->comm.size > 1) throw StErr{ST_E_UNSUPPORTED, "time stepping: one GPU"};
+    if (c->src.kind == ST_SRC_EX2) throw StErr{ST_E_UNSUPPORTED, "time stepping: spatially uniform sources"};
+    CK(cudaSetDevice(c->device));
+    const double* r = rho_device(c, rho);
+    const long long Pd = c->gd0.P;
+    const long long nout = Pd * (nsteps + 1);
+    double* Td = T;
+    double* tmp = nullptr;
+    const bool host = !is_device_ptr(T);
+    if (host) {
+      dalloc(&tmp, (size_t)nout);
+      Td = tmp;
+    }
+    st_ts_stats_t st{};
+    double ms = 0.0;
+    long long nl = 0;
+    int worst = 0;
+    try {
+      st.cg_iterations = st_run_timestepping(c->lv[0].g, c->md, c->src, c->grid.tau, c->bcs.T0, r, nsteps, c->opt.rtol,
+                                             c->opt.maxit, (int)c->opt.coarse_max_nodes, c->gd0, Td, c->stream, &ms, &nl,
+                                             &worst);
+    } catch (const std::exception& e) {
+      cudaFree(tmp);
+      throw StErr{ST_E_CUDA, e.what()};
+    }
+    if (host) {
+      CK(cudaMemcpyAsync(T, tmp, (size_t)nout * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      cudaFree(tmp);
+    }
+    st.steps = nsteps;
+    st.ms = ms;
+    st.launches = nl;
+    st.max_step_iterations = worst;
+    L(c, nl);
+    if (stats) *stats = st;
+    return ST_OK;
+  });
+}
+
 int st_get_stats(const st_ctx_t* c, st_stats_t* s) {
   if (!c || !s) return ST_E_INVALID_ARG;
   *s = c->stats;
@@ -1786,12 +1850,13 @@ int st_plan(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* b
   });
 }
 
-int st_struct_sizes(int64_t out[10]) {
+int st_struct_sizes(int64_t out[11]) {
   if (!out) return ST_E_INVALID_ARG;
   out[0] = sizeof(st_grid_t); out[1] = sizeof(st_materials_t); out[2] = sizeof(st_bcs_t);
   out[3] = sizeof(st_source_t); out[4] = sizeof(st_options_t); out[5] = sizeof(st_dist_t);
   out[6] = sizeof(st_stats_t); out[7] = sizeof(st_hierarchy_t); out[8] = sizeof(st_layout_t);
   out[9] = sizeof(st_plan_t);
+  out[10] = sizeof(st_ts_stats_t);
   return ST_OK;
 }
 

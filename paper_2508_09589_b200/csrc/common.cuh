@@ -32,6 +32,7 @@ struct Geom {
   int plo, phi;  // sink patch: transverse node range at x1 = 0 (plo > phi: none)
   double dx, dt;
   int pg0;       // global index of local plane 0 (time slabs); 0 on one GPU
+  int walls;     // 1: every spatial boundary node is constrained (T = 0, Example 2's cold walls)
 };
 
 struct MatsDev {
@@ -100,18 +101,21 @@ __device__ __forceinline__ double dpowp(double r, double p) {  // d/dr r^p
 }
 
 // constrained node test (R-2, R-4): t = 0 plane, or sink patch at x1 = 0
-template <int SD> __device__ __forceinline__ bool is_cons(const Geom& g, const int* c, int p) {
-  if (p + g.pg0 == 0) return true;  // initial-condition plane (global t = 0)
+// spatial Dirichlet node (value 0 at all t): the sink patch, or with g.walls every boundary node
+template <int SD> __device__ __forceinline__ bool is_patch(const Geom& g, const int* c) {
+  if (g.walls) {
+    bool w = c[0] == 0 || c[0] == g.n || c[1] == 0 || c[1] == g.n;
+    if (SD == 3) w = w || c[2] == 0 || c[2] == g.n;
+    return w;
+  }
   if (c[0] != 0) return false;
   bool in = (c[1] >= g.plo && c[1] <= g.phi);
   if (SD == 3) in = in && (c[2] >= g.plo && c[2] <= g.phi);
   return in;
 }
-template <int SD> __device__ __forceinline__ bool is_patch(const Geom& g, const int* c) {
-  if (c[0] != 0) return false;
-  bool in = (c[1] >= g.plo && c[1] <= g.phi);
-  if (SD == 3) in = in && (c[2] >= g.plo && c[2] <= g.phi);
-  return in;
+template <int SD> __device__ __forceinline__ bool is_cons(const Geom& g, const int* c, int p) {
+  if (p + g.pg0 == 0) return true;  // initial-condition plane (global t = 0)
+  return is_patch<SD>(g, c);
 }
 
 template <int SD> __device__ __forceinline__ long long pidx(const Geom& g, const int* c) {

@@ -466,6 +466,7 @@ static void l2d_modes(const OpDesc& op, int mode, bool trans, bool mask, const d
 // returns false when the fast path does not cover the operator
 bool launch_op_fast2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                       double omega, cudaStream_t s) {
+  if (op.g.walls) return false;  // Example 2's cold walls: the generic kernels (is_cons)
   if (op.g.sd != 2) return false;
   if (mode == MODE_JAC0 && !mask) return false;
   if (op.form == FORM_RHO) {

@@ -1,6 +1,7 @@
 // kernels.h — host launchers of libst's CUDA kernels (internal).
 #pragma once
 #include <cuda_runtime.h>
+#include "st.h"
 #include "common.cuh"
 
 namespace st {
@@ -74,7 +75,7 @@ int gm_y_offset(int k);
 // k~(rho) = kins + dk rho^pk stored with a zero border, kt[t][gj+1][gi+1] (pitch n+2), plus a zero
 // layer nl; (nl+1) (n+2)^2 doubles. rho: [nl][n][n].
 void launch_ktilde(const double* rho, int n, int nl, const MatsDev& m, double* kt, cudaStream_t s);
-void launch_source(const Geom& g, int kind, double qscale, double a, double w, double tau, double* f, cudaStream_t s);
+void launch_source(const Geom& g, const st_source_t& src, double qscale, double tau, double* f, cudaStream_t s);
 void launch_mask_free(const Geom& g, const double* in, double* out, cudaStream_t s);       // out = m_f .* in
 void launch_copy_cons(const Geom& g, const double* src, double* dst, cudaStream_t s);     // dst_c = src_c
 void launch_relayout(const Geom& gs, const double* src, const Geom& gd, double* dst, cudaStream_t s);

@@ -1,6 +1,7 @@
 // misc.cu — source assembly, Dirichlet helpers, element sensitivities, dense coarsest solve.
 #include <algorithm>
 
+#include "st.h"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -10,8 +11,18 @@ namespace st {
 // f_a = sum_e int N_a Q~ dV for a spatially uniform source: exact spatial
 // integrals (dx/2 per adjacent element and direction) times 2-point Gauss in time per
 // element layer (R-5).
-// One CTA row per time plane (blockIdx.y): the temporal factor of the plane (4 Gauss points, the
-// sin of Q(t)) is evaluated once per CTA, then the plane's nodes are written with a grid-stride loop.
+// Temporal factor of a spatially uniform source (R-5: 2-point Gauss per element layer):
+// kind 0 UNIFORM, 1 SIN: qscale (1 + a sin(w tau t)); 2 EX1: 1/2 qscale (1 - t)(1 + cos 50 t)
+// (Example 1, t rescaled). t: global rescaled time.
+__device__ __forceinline__ double q_time(int kind, double qscale, double a, double w, double tau, double t) {
+  if (kind == 1) return qscale * (1.0 + a * sin(w * tau * t));
+  if (kind == 2) return 0.5 * qscale * (1.0 - t) * (1.0 + cos(50.0 * t));
+  return qscale;
+}
+
+// Spatially uniform sources (kinds 0-2): one CTA row per time plane (blockIdx.y); the plane's
+// temporal factor (4 Gauss points) is evaluated once per CTA, then the plane's nodes are written with
+// a grid-stride loop (exact spatial integrals: dx/2 per adjacent element and direction).
 template <int SD>
 __global__ void source_kernel(Geom g, int kind, double qscale, double a, double w, double tau, double* __restrict__ f) {
   __shared__ double ft_s;
@@ -26,8 +37,7 @@ __global__ void source_kernel(Geom g, int kind, double qscale, double a, double 
           const double sg = gp == 0 ? -s : s;
           const double tt = (l + g.pg0 + 0.5 + sg) * g.dt;  // global time of the Gauss point
           const double N = side == 0 ? (0.5 + sg) : (0.5 - sg);
-          const double Q = qscale * ((kind == 1) ? (1.0 + a * sin(w * tau * tt)) : 1.0);
-          ft += 0.5 * g.dt * N * Q;
+          ft += 0.5 * g.dt * N * q_time(kind, qscale, a, w, tau, tt);
         }
       }
       ft_s = ft;
@@ -46,6 +56,53 @@ __global__ void source_kernel(Geom g, int kind, double qscale, double a, double 
     }
     __syncthreads();
   }
+}
+
+// Example 2's moving Gaussian, (2+1)D: f_a = sum over the node's adjacent elements of
+// the 2 x 2 x 2-point Gauss quadrature of N_a Q~ (R-5), Q~ = Q0 exp(-|x - x0(t)|^2 / (2 s^2)),
+// x0(t) = (1/2 + R cos(w tau t + pi/2), 1/2 + R sin(w tau t + pi/2)) in rescaled coordinates.
+__global__ void source_ex2_kernel(Geom g, double q0, double w, double tau, double sig, double R, double* __restrict__ f) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= g.N) return;
+  const int p = (int)(idx / g.P);
+  int cc[3];
+  if (!pdecode<2>(g, idx % g.P, cc)) { f[idx] = 0.0; return; }
+  const double gq = 1.0 / sqrt(3.0);
+  const double det = 0.125 * g.dx * g.dx * g.dt;  // (dx/2)^2 (dt/2)
+  const double inv2s2 = 1.0 / (2.0 * sig * sig);
+  const double hp = 1.5707963267948966;
+  double acc = 0.0;
+  for (int bt = 0; bt < 2; ++bt) {
+    const int l = p - bt;  // element layer; the node's local time bit is bt
+    if (l < 0 || l >= g.nt) continue;
+    for (int qt = 0; qt < 2; ++qt) {
+      const double st = qt ? gq : -gq;
+      const double t = (l + g.pg0 + 0.5 * (1.0 + st)) * g.dt;
+      const double Nt = bt ? 0.5 * (1.0 + st) : 0.5 * (1.0 - st);
+      const double x10 = 0.5 + R * cos(w * tau * t + hp), x20 = 0.5 + R * sin(w * tau * t + hp);
+      for (int b2 = 0; b2 < 2; ++b2) {
+        const int e2 = cc[1] - b2;
+        if (e2 < 0 || e2 >= g.n) continue;
+        for (int b1 = 0; b1 < 2; ++b1) {
+          const int e1 = cc[0] - b1;
+          if (e1 < 0 || e1 >= g.n) continue;
+          for (int q2 = 0; q2 < 2; ++q2) {
+            const double s2 = q2 ? gq : -gq;
+            const double x2 = (e2 + 0.5 * (1.0 + s2)) * g.dx;
+            const double N2 = b2 ? 0.5 * (1.0 + s2) : 0.5 * (1.0 - s2);
+            for (int q1 = 0; q1 < 2; ++q1) {
+              const double s1 = q1 ? gq : -gq;
+              const double x1 = (e1 + 0.5 * (1.0 + s1)) * g.dx;
+              const double N1 = b1 ? 0.5 * (1.0 + s1) : 0.5 * (1.0 - s1);
+              const double r2 = (x1 - x10) * (x1 - x10) + (x2 - x20) * (x2 - x20);
+              acc += det * N1 * N2 * Nt * q0 * exp(-r2 * inv2s2);
+            }
+          }
+        }
+      }
+    }
+  }
+  f[idx] = acc;
 }
 
 __global__ void ktilde_kernel(const double* __restrict__ rho, int n, int nl, MatsDev m, double* __restrict__ kt) {
@@ -68,11 +125,15 @@ void launch_ktilde(const double* rho, int n, int nl, const MatsDev& m, double* k
   ktilde_kernel<<<(unsigned)blocks, 256, 0, s>>>(rho, n, nl, m, kt);
 }
 
-void launch_source(const Geom& g, int kind, double qscale, double a, double w, double tau, double* f, cudaStream_t s) {
+void launch_source(const Geom& g, const st_source_t& src, double qscale, double tau, double* f, cudaStream_t s) {
+  if (src.kind == ST_SRC_EX2) {
+    source_ex2_kernel<<<(unsigned)((g.N + 255) / 256), 256, 0, s>>>(g, qscale, src.w, tau, src.sigma, src.R, f);
+    return;
+  }
   const long long bx = std::min<long long>((g.P + 255) / 256, 64);
   const unsigned by = (unsigned)std::min<long long>(g.nt + 1, 65535);
-  if (g.sd == 2) source_kernel<2><<<dim3((unsigned)bx, by), 256, 0, s>>>(g, kind, qscale, a, w, tau, f);
-  else source_kernel<3><<<dim3((unsigned)bx, by), 256, 0, s>>>(g, kind, qscale, a, w, tau, f);
+  if (g.sd == 2) source_kernel<2><<<dim3((unsigned)bx, by), 256, 0, s>>>(g, src.kind, qscale, src.a, src.w, tau, f);
+  else source_kernel<3><<<dim3((unsigned)bx, by), 256, 0, s>>>(g, src.kind, qscale, src.a, src.w, tau, f);
 }
 
 // ---------------------------------------------------------------------------------------

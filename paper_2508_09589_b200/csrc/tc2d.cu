@@ -422,6 +422,7 @@ void ltc_modes(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, i
 // Masked (eliminated) operator only; false if the level is not covered.
 bool launch_op_tc2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                     double omega, cudaStream_t s) {
+  if (op.g.walls) return false;  // Example 2's cold walls: the generic kernels (is_cons)
   const Geom& g = op.g;
   if (g.sd != 2 || !mask) return false;
   const bool rho_tc = (op.form == FORM_RHO && op.rho_tc), mk_tc = (op.form == FORM_MK && !op.tvl);
@@ -449,6 +450,7 @@ bool launch_op_tc2d(const OpDesc& op, int mode, bool trans, bool mask, const dou
 // (same time planes, one GPU). false if not covered (then: prolongation kernel + plain sweep).
 bool launch_op_tc2d_pro(const OpDesc& op, const Geom& gc, bool trans, const double* x, const double* e,
                         const double* b, double* y, double omega, cudaStream_t s) {
+  if (op.g.walls) return false;  // Example 2's cold walls: the generic kernels (is_cons)
   const Geom& g = op.g;
   if (g.sd != 2 || gc.nt != g.nt || gc.nn != g.n / 2 + 1 || g.pg0 != 0 || gc.pg0 != 0) return false;
   const bool rho_tc = (op.form == FORM_RHO && op.rho_tc), mk_tc = (op.form == FORM_MK && !op.tvl);

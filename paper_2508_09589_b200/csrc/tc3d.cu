@@ -355,6 +355,7 @@ void lt3_modes(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, i
 // Masked (eliminated) operator on a (3+1)D time-constant level; false if not covered.
 bool launch_op_tc3d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                     double omega, cudaStream_t s) {
+  if (op.g.walls) return false;  // Example 2's cold walls: the generic kernels (is_cons)
   const Geom& g = op.g;
   if (g.sd != 3 || !mask) return false;
   const bool rho_tc = (op.form == FORM_RHO && op.rho_tc), mk_tc = (op.form == FORM_MK && !op.tvl);

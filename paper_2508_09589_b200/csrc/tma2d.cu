@@ -491,6 +491,7 @@ void lt2_modes(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, i
 
 bool launch_op_tma2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                      double omega, cudaStream_t s) {
+  if (op.g.walls) return false;  // Example 2's cold walls: the generic kernels (is_cons)
   const Geom& g = op.g;
   if (g.sd != 2) return false;
   const bool rho_tc = (op.form == FORM_RHO && op.rho_tc), rho_tv = (op.form == FORM_RHO && !op.rho_tc);

@@ -169,7 +169,7 @@ void launch_restrict(const Geom& gf, const Geom& gc, int kind, const double* rf,
 
 void launch_prolong_add(const Geom& gf, const Geom& gc, int kind, const double* ec, double* xf, cudaStream_t s) {
   // the paired kernel needs an even fine pitch (16-B aligned pairs): every internal vector has one
-  if (gf.sd == 2 && kind == KIND_SPACE && gf.nt + 1 <= 65535 && gf.pr % 2 == 0 && gf.P % 2 == 0) {
+  if (gf.sd == 2 && kind == KIND_SPACE && gf.nt + 1 <= 65535 && gf.pr % 2 == 0 && gf.P % 2 == 0 && !gf.walls) {
     prolong2s_kernel<<<dim3((gc.nn + 127) / 128, gc.nn, gf.nt + 1), 128, 0, s>>>(gf, gc, ec, xf);
     return;
   }

@@ -534,6 +534,7 @@ void ltv(const CUtensorMap& mx, const CUtensorMap& mb, const CUtensorMap& ml, co
 // Masked modes of the fine level of a space-time design with uniform capacity; false if not covered.
 bool launch_op_tv2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                     double omega, cudaStream_t s) {
+  if (op.g.walls) return false;  // Example 2's cold walls: the generic kernels (is_cons)
   const Geom& g = op.g;
   const bool rho_tv = op.form == FORM_RHO && !op.rho_tc && op.m.dC == 0.0;
   const bool mk_tv = op.form == FORM_MK && op.tvl && op.msep;

@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(HERE, "libst.so")
 ST_OK = 0
 ST_E_NOT_CONVERGED = -3
 ST_TIME_CONSTANT, ST_SPACE_TIME = 0, 1
-ST_SRC_UNIFORM, ST_SRC_SIN = 0, 1
+ST_SRC_UNIFORM, ST_SRC_SIN, ST_SRC_EX1, ST_SRC_EX2 = 0, 1, 2, 3
 ST_SMOOTH_JACOBI, ST_SMOOTH_GMRES = 0, 2  # st.h: the GMRES(k)-Jacobi smoother of the paper (one GPU)
 ST_KRYLOV_FGMRES, ST_KRYLOV_GMRES = 0, 1
 ST_COARSE_DENSE, ST_COARSE_GMRES = 0, 1
@@ -31,11 +31,12 @@ class Materials(C.Structure):
 
 class BCs(C.Structure):
     _fields_ = [("T0", C.c_double), ("has_patch", C.c_int32), ("face", C.c_int32),
-                ("center", C.c_double), ("halfwidth", C.c_double)]
+                ("center", C.c_double), ("halfwidth", C.c_double), ("all_walls", C.c_int32)]
 
 
 class Source(C.Structure):
-    _fields_ = [("kind", C.c_int32), ("Q0", C.c_double), ("a", C.c_double), ("w", C.c_double)]
+    _fields_ = [("kind", C.c_int32), ("Q0", C.c_double), ("a", C.c_double), ("w", C.c_double),
+                ("sigma", C.c_double), ("R", C.c_double)]
 
 
 class Options(C.Structure):
@@ -90,6 +91,11 @@ class Stats(C.Structure):
                 ("converged", C.c_int32), ("vcycles", C.c_int32), ("setups", C.c_int64)]
 
 
+class TsStats(C.Structure):
+    _fields_ = [("steps", C.c_int32), ("max_step_iterations", C.c_int32), ("cg_iterations", C.c_int64),
+                ("ms", C.c_double), ("launches", C.c_int64)]
+
+
 class Hierarchy(C.Structure):
     _fields_ = [("n_levels", C.c_int32), ("n", C.c_int64 * 32), ("nt", C.c_int64 * 32),
                 ("kind", C.c_int32 * 32), ("form", C.c_int32 * 32), ("nodes", C.c_int64 * 32),
@@ -100,7 +106,7 @@ EXPORTS = ["st_abi_version", "st_default_options", "st_setup", "st_destroy", "st
            "st_sensitivity", "st_apply", "st_vcycle", "st_rhs", "st_filter", "st_oc_update", "st_dot", "st_pnorm", "st_level_apply", "st_bench_op", "st_get_stats", "st_get_hierarchy",
            "st_local_layout", "st_nccl_unique_id", "st_nccl_comm_init", "st_nccl_comm_destroy", "st_plan",
            "st_struct_sizes",
-           "st_num_nodes", "st_num_design", "st_kernel_launches", "st_strerror", "st_last_error"]
+           "st_num_nodes", "st_num_design", "st_kernel_launches", "st_strerror", "st_last_error", "st_timestep"]
 
 _lib = None
 
@@ -138,6 +144,7 @@ def load_library(path: str = LIB_PATH):
     lib.st_level_apply.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
     lib.st_bench_op.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
     lib.st_get_stats.argtypes = [C.c_void_p, P(Stats)]
+    lib.st_timestep.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, P(TsStats)]
     lib.st_get_hierarchy.argtypes = [C.c_void_p, P(Hierarchy)]
     lib.st_local_layout.argtypes = [C.c_void_p, P(Layout)]
     lib.st_nccl_unique_id.argtypes = [C.c_char_p]
@@ -225,7 +232,7 @@ class TorchHostComm:
             return self._fail("allgather", e)
 
 
-STRUCTS = [Grid, Materials, BCs, Source, Options, Dist, Stats, Hierarchy, Layout, Plan]
+STRUCTS = [Grid, Materials, BCs, Source, Options, Dist, Stats, Hierarchy, Layout, Plan, TsStats]
 
 
 def plan(sdim, n, nt, rank=0, size=1, mats=(1.0, 1.0, 1.0, 1e-3, 1.0, 3.0), tau=1.0, L=1.0, has_patch=True,
@@ -238,7 +245,7 @@ def plan(sdim, n, nt, rank=0, size=1, mats=(1.0, 1.0, 1.0, 1e-3, 1.0, 3.0), tau=
         setattr(o, k, v)
     p = Plan()
     rc = lib.st_plan(C.byref(Grid(sdim, n, nt, L, tau)), C.byref(Materials(*mats)),
-                     C.byref(BCs(0.0, 1 if has_patch else 0, 0, 0.5, 0.05)), C.byref(o), rank, size, C.byref(p))
+                     C.byref(BCs(0.0, 1 if has_patch else 0, 0, 0.5, 0.05, 0)), C.byref(o), rank, size, C.byref(p))
     if rc != ST_OK:
         raise StError(rc, lib.st_last_error().decode())
     kinds = ["fine", "space", "time", "full"]
@@ -273,13 +280,15 @@ class Solver:
     def __init__(self, sdim, n, nt, mats=(1.0, 1.0, 1.0, 1e-3, 1.0, 3.0), T0=0.0, has_patch=True,
                  center=0.5, halfwidth=0.05, source=("uniform", 1.0, 0.0, 0.0), L=1.0, tau=1.0,
                  time_constant=False, stream=None, device=None, rank=0, size=1, host_comm=None,
-                 nccl_comm=None, **opts):
+                 nccl_comm=None, all_walls=False, **opts):
+        """source: (kind, Q0, a, w[, sigma, R]) with kind 'uniform' | 'sin' | 'ex1' | 'ex2' (st.h)."""
         self.lib = load_library()
         self.grid = Grid(sdim, n, nt, L, tau)
         self.mats = Materials(*mats)
-        self.bcs = BCs(T0, 1 if has_patch else 0, 0, center, halfwidth)
-        kind = {"uniform": ST_SRC_UNIFORM, "sin": ST_SRC_SIN}[source[0]]
-        self.src = Source(kind, *source[1:])
+        self.bcs = BCs(T0, 1 if has_patch else 0, 0, center, halfwidth, 1 if all_walls else 0)
+        kind = {"uniform": ST_SRC_UNIFORM, "sin": ST_SRC_SIN, "ex1": ST_SRC_EX1, "ex2": ST_SRC_EX2}[source[0]]
+        vals = list(source[1:]) + [0.0] * (5 - len(source[1:]))
+        self.src = Source(kind, *vals[:5])
         o = Options()
         self.lib.st_default_options(C.byref(o))
         o.design_mode = ST_TIME_CONSTANT if time_constant else ST_SPACE_TIME
@@ -394,6 +403,15 @@ class Solver:
     def rhs(self, rho, f=None, b=None):
         return self._check(self.lib.st_rhs(self.ctx, self._rho(rho), None if f is None else self._nodes(f, "f"),
                                            None if b is None else self._nodes(b, "b")))
+
+    def timestep(self, rho, nsteps, T):
+        """The GPU time-stepping baseline (st_timestep): backward Euler with nsteps steps; T receives the
+        (nsteps + 1) x (n+1)^sdim nodal temperatures. Returns st_ts_stats_t as a dict."""
+        st = TsStats()
+        plane = (int(self.grid.n) + 1) ** int(self.grid.sdim)
+        self._check(self.lib.st_timestep(self.ctx, self._rho(rho), int(nsteps), _ptr(T, plane * (nsteps + 1), "T"),
+                                         C.byref(st)))
+        return {k: getattr(st, k) for k, _ in TsStats._fields_}
 
     def stats(self):
         s = Stats()

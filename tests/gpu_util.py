@@ -9,13 +9,14 @@ CFG4_MATS = (0.1, 1.0, 1.0, 1e-4, 1.0, 3.0)       # k_min = 1e-4, c = 0.1 + 0.9 
 
 
 def make_pair(sdim, n, nt, mats=CFG1_MATS, T0=0.0, has_patch=True, source=("uniform", 1.0, 0.0, 0.0),
-              tau=1.0, time_constant=False, **opts):
+              tau=1.0, time_constant=False, all_walls=False, **opts):
+    """source: (kind, Q0, a, w[, sigma, R]) — the same tuple drives both sides."""
     import paper_2508_09589_b200 as S
     solver = S.Solver(sdim, n, nt, mats=mats, T0=T0, has_patch=has_patch, source=source, tau=tau,
-                      time_constant=time_constant, **opts)
-    kind = source[0]
-    src = O.Source(kind, source[1], source[2], source[3])
-    prob = O.Problem(O.Mesh(sdim, n, nt, tau=tau), O.Materials(*mats), O.BCs(T0=T0, has_patch=has_patch), src)
+                      time_constant=time_constant, all_walls=all_walls, **opts)
+    src = O.Source(*source)
+    prob = O.Problem(O.Mesh(sdim, n, nt, tau=tau), O.Materials(*mats),
+                     O.BCs(T0=T0, has_patch=has_patch, all_walls=all_walls), src)
     return solver, prob
 
 

@@ -70,7 +70,7 @@ def test_struct_layouts_match_binding():
     """The ctypes mirrors of every ABI struct have the C sizes (catches a field added on one side)."""
     from paper_2508_09589_b200 import st
     lib = st.load_library()
-    out = (ctypes.c_int64 * 10)()
+    out = (ctypes.c_int64 * 11)()
     assert lib.st_struct_sizes(out) == 0
     for cls, size in zip(st.STRUCTS, out):
         assert ctypes.sizeof(cls) == size, (cls.__name__, ctypes.sizeof(cls), size)

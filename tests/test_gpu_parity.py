@@ -440,3 +440,53 @@ def test_prolongation_fused_into_post_sweep_equals_separate_kernels(n, nt, desig
     assert rel(outs["0"][0], outs["1"][0]) <= 1e-12
     assert rel(outs["0"][1], outs["1"][1]) <= 1e-12
     assert launches["0"] < launches["1"], launches
+
+
+# ------------------------------------------------------------------ the paper's example presets
+PAPER_MATS = (0.5, 1.0, 2.0, 0.03, 3.0, 3.0)   # C 0.5 / 1, k 0.03 / 3, p_c 2, p_k 3
+EX_CASES = [
+    # Example 1: oscillating uniform source Q0 = 100, tau = 1, sink patch
+    ("ex1", 2, 16, 32, dict(source=("ex1", 100.0, 0.0, 0.0), tau=1.0)),
+    ("ex1-3d", 3, 6, 12, dict(source=("ex1", 100.0, 0.0, 0.0), tau=1.0)),
+    # Example 2: moving Gaussian, Q0 = 1, sigma 0.05, R 0.25, w = pi, tau = 6, cold walls
+    ("ex2", 2, 24, 48, dict(source=("ex2", 1.0, 0.0, np.pi, 0.05, 0.25), tau=6.0, all_walls=True, has_patch=False)),
+    ("ex2-T0", 2, 16, 24, dict(source=("ex2", 1.0, 0.0, np.pi, 0.05, 0.25), tau=6.0, all_walls=True, T0=0.3)),
+]
+
+
+@pytest.mark.parametrize("case", EX_CASES, ids=lambda c: c[0])
+def test_paper_example_presets_match_oracle(case):
+    """The sources of Examples 1 and 2 (ST_SRC_EX1 / ST_SRC_EX2, the latter by 2 x 2 x 2-point Gauss
+    quadrature of the moving Gaussian, R-5) and Example 2's cold walls (all_walls): RHS f,
+    operator, forward, adjoint (p-norm objective) and sensitivities equal the
+    oracle's."""
+    name, sdim, n, nt, kw = case
+    tc = sdim == 3
+    solver, prob = make_pair(sdim, n, nt, mats=PAPER_MATS, time_constant=tc, rtol=1e-11, maxit=600, **kw)
+    rho = I.rho_smooth((n,) * sdim, seed=3) if tc else I.rho_uniform((nt,) + (n,) * sdim, 3)
+    N = prob.mesh.n_nodes
+    f = torch.empty(N, dtype=torch.float64, device=DEV)
+    solver.rhs(dev(rho), f, None)
+    f_ref = prob.f()
+    assert rel(host(f), f_ref) <= 1e-13, rel(host(f), f_ref)
+    Kbc, _, _, _ = prob.system(rho)
+    x = I.rand_vector(N, 9)
+    y = torch.empty(N, dtype=torch.float64, device=DEV)
+    solver.apply(dev(rho), dev(x), y)
+    assert rel(host(y), Kbc @ x) <= 1e-12
+    T_ref = prob.forward(rho)
+    T = torch.zeros(N, dtype=torch.float64, device=DEV)
+    solver.solve(dev(rho), T)
+    assert rel(host(T), T_ref) <= 1e-8
+    phi_ref, g_ref = O.pnorm_objective(prob.mesh, T_ref, 20.0)
+    g = torch.empty_like(T)
+    solver.pnorm(T, 20.0, g)
+    lam = torch.zeros_like(T)
+    solver.adjoint(dev(rho), g, lam)
+    lam_ref = prob.adjoint(rho, g_ref)
+    assert rel(host(lam), lam_ref) <= 1e-8
+    dJ_ref = prob.sensitivity(rho, T_ref, lam_ref)
+    dJ = torch.empty(rho.size, dtype=torch.float64, device=DEV)
+    solver.sensitivity(dev(rho), T, lam, dJ)
+    assert rel(host(dJ).reshape(dJ_ref.shape), dJ_ref) <= 1e-7
+    solver.close()

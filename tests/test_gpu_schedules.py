@@ -251,3 +251,56 @@ def test_paper_solver_variant_with_inner_tolerances():
         assert rel(host(T), T_ref) <= 1e-8 and rel(host(lam), lam_ref) <= 1e-8
         solver.close()
     assert its[0][0] <= its[1][0] and its[0][1] <= its[1][1], its
+
+
+# ------------------------------------------------------------------ the GPU time-stepping baseline
+@pytest.mark.parametrize("sdim,n,nsteps,mats,T0,src", [
+    (2, 16, 16, CFG1_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0)),
+    (2, 32, 24, CFG4_MATS, 0.4, ("sin", 1.0, 1.0, 2 * np.pi)),
+    (2, 20, 12, (0.5, 1.0, 2.0, 0.03, 3.0, 3.0), 0.0, ("ex1", 100.0, 0.0, 0.0)),
+    (3, 8, 8, CFG4_MATS, 0.2, ("uniform", 1.0, 0.0, 0.0)),
+])
+def test_timestepping_baseline_matches_oracle_backward_euler(sdim, n, nsteps, mats, T0, src):
+    """st_timestep: the GPU backward-difference stepper with a
+    spatial-MG-preconditioned CG per step equals the oracle's direct backward Euler (oracle/timestep.py,
+    its own quadrature) at every time plane, to the solver tolerance."""
+    solver, prob = make_pair(sdim, n, nsteps, mats=mats, T0=T0, source=src, time_constant=True, rtol=1e-12,
+                             maxit=500)
+    rho = I.rho_smooth((n,) * sdim, seed=4)
+    T = torch.empty((nsteps + 1) * (n + 1) ** sdim, dtype=torch.float64, device=DEV)
+    st = solver.timestep(dev(rho), nsteps, T)
+    assert st["steps"] == nsteps and st["cg_iterations"] >= nsteps
+    C, k, _, _ = O.simp(rho.reshape(-1), prob.mats, prob.mesh)
+    cons, _ = O.dirichlet(prob.mesh, prob.bcs)
+    plane = (n + 1) ** sdim
+    qsrc = prob.src
+
+    def q_of_t(t):  # the oracle's rescaled source at time t (spatially uniform kinds)
+        return float(O.stfem._q_tilde(qsrc, prob.mesh, [np.zeros(1)] * sdim, np.array([t]))[0])
+    ref = O.backward_euler(n, sdim, C, k, q_of_t, nsteps, T0, cons[plane:2 * plane])
+    got = host(T).reshape(nsteps + 1, plane)
+    for m in range(nsteps + 1):
+        assert rel(got[m], ref[m]) <= 1e-9, (m, rel(got[m], ref[m]))
+    # host output buffer (library staging) gives the same result
+    Th = np.zeros((nsteps + 1) * plane)
+    solver.timestep(rho, nsteps, Th)
+    assert rel(Th, host(T)) <= 1e-14
+    solver.close()
+
+
+def test_timestepping_converges_to_the_space_time_solution():
+    """Both discretisations approach the same continuous solution: with nsteps = nt they differ by
+    O(dt) (first-order backward difference vs the stabilised space-time element), and the
+    gap shrinks under time refinement."""
+    n = 16
+    rho = I.rho_smooth((n, n), seed=1)
+    gaps = []
+    for nt in (16, 32, 64):
+        solver, prob = make_pair(2, n, nt, time_constant=True, rtol=1e-12, maxit=500)
+        T = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+        solver.solve(dev(rho), T)
+        Tts = torch.empty_like(T)
+        solver.timestep(dev(rho), nt, Tts)
+        gaps.append(rel(host(Tts), host(T)))
+        solver.close()
+    assert gaps[1] < gaps[0] and gaps[2] < gaps[1], gaps
