@@ -269,6 +269,7 @@ def run_cuda(args):
         obj = [S.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_comm = S.nccl_comm_init(obj[0], rank, world)
+        S.nccl_selftest(nccl_comm, rank, world)  # fail loudly before any timing if the transport is broken
     opts = solver_opts_for(wl, args)
     solver = S.Solver(wl["sdim"], wl["n"], wl["nt"], mats=wl["mats"], source=wl["source"], tau=wl["tau"],
                       time_constant=wl["tc"], stream=stream.cuda_stream, device=local, rtol=args.rtol, maxit=1000,

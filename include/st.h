@@ -336,6 +336,12 @@ int st_struct_sizes(int64_t out[11]);
 int st_nccl_unique_id(char id[ST_NCCL_ID_BYTES]);
 int st_nccl_comm_init(const char id[ST_NCCL_ID_BYTES], int32_t rank, int32_t size, void** comm);
 int st_nccl_comm_destroy(void* comm);
+/* Checks a communicator against (rank, size) (ncclCommCount / ncclCommUserRank; *nranks receives the
+ * count) and runs every NCCL call the slab path uses on it — ncclAllReduce, ncclAllGather and grouped
+ * ncclSend / ncclRecv with the ring neighbours (the rank itself when size = 1) — comparing the results.
+ * ST_OK or ST_E_NCCL (text in st_last_error). st_setup with ST_COMM_NCCL performs the count check and
+ * logs one line on rank 0. */
+int st_nccl_selftest(void* comm, int32_t rank, int32_t size, int32_t* nranks);
 int st_get_hierarchy(const st_ctx_t* ctx, st_hierarchy_t* h);
 int64_t st_num_nodes(const st_ctx_t* ctx);
 int64_t st_num_design(const st_ctx_t* ctx);

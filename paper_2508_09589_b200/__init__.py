@@ -6,7 +6,7 @@ only). There is no CPU fallback: importing the binding without the built library
 """
 from .st import (  # noqa: F401
     Grid, Materials, BCs, Source, Options, Solver, StError, load_library, TorchHostComm,
-    nccl_unique_id, nccl_comm_init,
+    nccl_unique_id, nccl_comm_init, nccl_selftest,
     ST_TIME_CONSTANT, ST_SPACE_TIME, ST_SRC_UNIFORM, ST_SRC_SIN, ST_COMM_NONE, ST_COMM_NCCL, ST_COMM_HOST,
 )
 from .design import design_loop  # noqa: F401,E402

@@ -1302,6 +1302,18 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       if (dist->rank < 0 || dist->rank >= dist->size) throw StErr{ST_E_INVALID_ARG, "rank out of range"};
       if (grid->nt % dist->size != 0) throw StErr{ST_E_DIVISIBILITY, "time slabs: nt must be divisible by the rank count"};
       if (dist->transport == ST_COMM_NCCL && !dist->nccl_comm) throw StErr{ST_E_INVALID_ARG, "NCCL transport needs nccl_comm"};
+      if (dist->transport == ST_COMM_NCCL) {  // the communicator must be the one the slabs assume
+        int cnt = -1, r = -1;
+        if (nccl_comm_count(dist->nccl_comm, &cnt, &r) != 0)
+          throw StErr{ST_E_NCCL, "ncclCommCount / ncclCommUserRank failed"};
+        if (cnt != dist->size || r != dist->rank)
+          throw StErr{ST_E_NCCL, "NCCL communicator has " + std::to_string(cnt) + " ranks (rank " + std::to_string(r) +
+                                     "), st_dist_t says " + std::to_string(dist->size) + " (rank " +
+                                     std::to_string(dist->rank) + ")"};
+        if (dist->rank == 0 || (opts && opts->verbose))
+          fprintf(stderr, "libst: time slabs over NCCL: ncclCommCount = %d, rank %d of %d, device %d\n", cnt, r,
+                  dist->size, dist->device);
+      }
       if (dist->transport == ST_COMM_HOST &&
           (!dist->host.sendrecv || !dist->host.allreduce_sum || !dist->host.allgather))
         throw StErr{ST_E_INVALID_ARG, "host transport needs sendrecv, allreduce_sum and allgather"};
@@ -1879,6 +1891,24 @@ int st_nccl_comm_init(const char id[ST_NCCL_ID_BYTES], int32_t rank, int32_t siz
 }
 
 int st_nccl_comm_destroy(void* comm) { return nccl_comm_destroy(comm) == 0 ? ST_OK : ST_E_NCCL; }
+
+int st_nccl_selftest(void* comm, int32_t rank, int32_t size, int32_t* nranks) {
+  return guarded([&]() -> int {
+    if (!comm || size < 1 || rank < 0 || rank >= size) throw StErr{ST_E_INVALID_ARG, "comm / rank / size"};
+    int cnt = -1, r = -1;
+    if (nccl_comm_count(comm, &cnt, &r) != 0) throw StErr{ST_E_NCCL, "ncclCommCount / ncclCommUserRank failed"};
+    if (nranks) *nranks = cnt;
+    if (cnt != size || r != rank)
+      throw StErr{ST_E_NCCL, "communicator has " + std::to_string(cnt) + " ranks (this is rank " + std::to_string(r) +
+                                 "), expected " + std::to_string(size) + " / " + std::to_string(rank)};
+    cudaStream_t s = nullptr;
+    CK(cudaStreamCreate(&s));
+    const std::string err = nccl_selftest(comm, rank, size, s);
+    cudaStreamDestroy(s);
+    if (!err.empty()) throw StErr{ST_E_NCCL, "NCCL self-test: " + err};
+    return ST_OK;
+  });
+}
 
 int64_t st_num_nodes(const st_ctx_t* c) { return c ? c->Nd : -1; }
 int64_t st_num_design(const st_ctx_t* c) { return c ? c->ndesign : -1; }

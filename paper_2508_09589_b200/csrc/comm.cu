@@ -15,6 +15,7 @@
 
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "comm.h"
 
@@ -33,6 +34,8 @@ typedef int (*p_ncclRecv)(void* buf, size_t count, int dtype, int peer, void* co
 typedef int (*p_ncclAllReduce)(const void* s, void* r, size_t count, int dtype, int op, void* comm, cudaStream_t st);
 typedef int (*p_ncclAllGather)(const void* s, void* r, size_t count, int dtype, void* comm, cudaStream_t st);
 typedef const char* (*p_ncclGetErrorString)(int);
+typedef int (*p_ncclCommCount)(void* comm, int* count);
+typedef int (*p_ncclCommUserRank)(void* comm, int* rank);
 constexpr int kNcclDouble = 8;  // ncclFloat64
 constexpr int kNcclSum = 0;
 
@@ -48,6 +51,8 @@ struct NcclApi {
   p_ncclAllReduce allReduce = nullptr;
   p_ncclAllGather allGather = nullptr;
   p_ncclGetErrorString errStr = nullptr;
+  p_ncclCommCount commCount = nullptr;
+  p_ncclCommUserRank commUserRank = nullptr;
 };
 
 NcclApi& nccl() {
@@ -69,6 +74,8 @@ NcclApi& nccl() {
   api.allReduce = (p_ncclAllReduce)dlsym(h, "ncclAllReduce");
   api.allGather = (p_ncclAllGather)dlsym(h, "ncclAllGather");
   api.errStr = (p_ncclGetErrorString)dlsym(h, "ncclGetErrorString");
+  api.commCount = (p_ncclCommCount)dlsym(h, "ncclCommCount");
+  api.commUserRank = (p_ncclCommUserRank)dlsym(h, "ncclCommUserRank");
   api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.groupStart && api.groupEnd && api.send &&
            api.recv && api.allReduce && api.allGather;
   return api;
@@ -122,6 +129,61 @@ int nccl_comm_init(const char* id_bytes, int rank, int size, void** comm) {
 int nccl_comm_destroy(void* comm) {
   if (!nccl().ok || !comm) return -1;
   return nccl().commDestroy(comm);
+}
+
+int nccl_comm_count(void* comm, int* count, int* rank) {
+  if (!nccl().ok || !comm || !nccl().commCount || !nccl().commUserRank) return -1;
+  if (nccl().commCount(comm, count) != 0) return -1;
+  if (nccl().commUserRank(comm, rank) != 0) return -1;
+  return 0;
+}
+
+std::string nccl_selftest(void* comm, int rank, int size, cudaStream_t s) {
+  NcclApi& api = nccl();
+  if (!api.ok) return "libnccl.so.2 not available";
+  const int n = 64;
+  double* d = nullptr;
+  if (cudaMalloc((void**)&d, (size_t)(5 + size) * n * sizeof(double)) != cudaSuccess) return "cudaMalloc";
+  double* a = d;              // allreduce: every rank contributes (rank + 1) * (i + 1)
+  double* g = d + n;          // allgather target: size * n
+  double* sl = g + size * n;  // send to rank - 1 (ring), receive from rank + 1
+  double* rl = sl + n;
+  double* sh = rl + n;        // send to rank + 1, receive from rank - 1
+  std::vector<double> h((size_t)(5 + size) * n, 0.0);  // a | g[size] | sl | rl | sh | rh
+  for (int i = 0; i < n; ++i) {
+    h[i] = (rank + 1.0) * (i + 1.0);
+    h[(size_t)(size + 1) * n + i] = 1000.0 * rank + i;      // sl
+    h[(size_t)(size + 3) * n + i] = -1000.0 * rank - i;     // sh
+  }
+  std::string err;
+  try {
+    cuda_check(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    nccl_check(api.allReduce(a, a, n, kNcclDouble, kNcclSum, comm, s), "ncclAllReduce");
+    nccl_check(api.allGather(a, g, n, kNcclDouble, comm, s), "ncclAllGather");
+    const int lo = (rank + size - 1) % size, hi = (rank + 1) % size;
+    double* rh = sh + n;
+    nccl_check(api.groupStart(), "ncclGroupStart");
+    nccl_check(api.send(sl, n, kNcclDouble, lo, comm, s), "ncclSend");
+    nccl_check(api.recv(rl, n, kNcclDouble, hi, comm, s), "ncclRecv");
+    nccl_check(api.send(sh, n, kNcclDouble, hi, comm, s), "ncclSend");
+    nccl_check(api.recv(rh, n, kNcclDouble, lo, comm, s), "ncclRecv");
+    nccl_check(api.groupEnd(), "ncclGroupEnd");
+    std::vector<double> o(h.size());
+    cuda_check(cudaMemcpyAsync(o.data(), d, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    const double tri = size * (size + 1) / 2.0;
+    for (int i = 0; i < n && err.empty(); ++i) {
+      if (o[i] != tri * (i + 1.0)) err = "allreduce value";
+      for (int r = 0; r < size && err.empty(); ++r)
+        if (o[(size_t)(1 + r) * n + i] != tri * (i + 1.0)) err = "allgather value";
+      if (err.empty() && o[(size_t)(size + 2) * n + i] != 1000.0 * hi + i) err = "send/recv (from rank + 1)";
+      if (err.empty() && o[(size_t)(size + 4) * n + i] != -1000.0 * lo - i) err = "send/recv (from rank - 1)";
+    }
+  } catch (const CommError& e) {
+    err = e.msg;
+  }
+  cudaFree(d);
+  return err;
 }
 
 void comm_release(Comm& c) {

@@ -25,6 +25,12 @@ bool nccl_available();
 int nccl_unique_id(char* out);                                  // ST_NCCL_ID_BYTES bytes
 int nccl_comm_init(const char* id, int rank, int size, void** comm);
 int nccl_comm_destroy(void* comm);
+// ncclCommCount / ncclCommUserRank of a communicator (-1 on failure)
+int nccl_comm_count(void* comm, int* count, int* rank);
+// exercise every NCCL entry point the slab path uses on a communicator (any size, including 1):
+// allreduce, allgather and a grouped send/recv exchange with the ring neighbours (self when size 1);
+// returns "" on success, else the first failure
+std::string nccl_selftest(void* comm, int rank, int size, cudaStream_t s);
 void comm_release(Comm& c);
 // halo planes with both time neighbours (count doubles each)
 void comm_halo(Comm& c, const double* send_lo, double* recv_lo, const double* send_hi, double* recv_hi,

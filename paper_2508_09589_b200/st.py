@@ -106,7 +106,7 @@ EXPORTS = ["st_abi_version", "st_default_options", "st_setup", "st_destroy", "st
            "st_sensitivity", "st_apply", "st_vcycle", "st_rhs", "st_filter", "st_oc_update", "st_dot", "st_pnorm", "st_level_apply", "st_bench_op", "st_get_stats", "st_get_hierarchy",
            "st_local_layout", "st_nccl_unique_id", "st_nccl_comm_init", "st_nccl_comm_destroy", "st_plan",
            "st_struct_sizes",
-           "st_num_nodes", "st_num_design", "st_kernel_launches", "st_strerror", "st_last_error", "st_timestep"]
+           "st_num_nodes", "st_num_design", "st_kernel_launches", "st_strerror", "st_last_error", "st_timestep", "st_nccl_selftest"]
 
 _lib = None
 
@@ -150,6 +150,7 @@ def load_library(path: str = LIB_PATH):
     lib.st_nccl_unique_id.argtypes = [C.c_char_p]
     lib.st_nccl_comm_init.argtypes = [C.c_char_p, C.c_int32, C.c_int32, P(C.c_void_p)]
     lib.st_nccl_comm_destroy.argtypes = [C.c_void_p]
+    lib.st_nccl_selftest.argtypes = [C.c_void_p, C.c_int32, C.c_int32, P(C.c_int32)]
     lib.st_plan.argtypes = [P(Grid), P(Materials), P(BCs), P(Options), C.c_int32, C.c_int32, P(Plan)]
     lib.st_struct_sizes.argtypes = [P(C.c_int64)]
     for name in ("st_num_nodes", "st_num_design", "st_kernel_launches"):
@@ -260,6 +261,16 @@ def nccl_unique_id():
     if lib.st_nccl_unique_id(buf) != ST_OK:
         raise StError(-7, lib.st_last_error().decode())
     return buf.raw
+
+
+def nccl_selftest(comm, rank: int, size: int) -> int:
+    """st_nccl_selftest: checks the communicator's rank count and runs allreduce / allgather / grouped
+    send-recv through the library's NCCL entry points; returns ncclCommCount."""
+    lib = load_library()
+    n = C.c_int32(-1)
+    if lib.st_nccl_selftest(comm, rank, size, C.byref(n)) != ST_OK:
+        raise StError(-7, lib.st_last_error().decode())
+    return n.value
 
 
 def nccl_comm_init(uid: bytes, rank: int, size: int):

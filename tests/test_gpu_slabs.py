@@ -39,10 +39,10 @@ def _worker(rank, size, port, case, q):
         dist.init_process_group("gloo", rank=rank, world_size=size, timeout=datetime.timedelta(seconds=180))
         torch.cuda.set_device(0)
         dev = torch.device("cuda:0")
-        sdim, n, nt, mats, T0, src, tau, design, tc, agg = case
+        sdim, n, nt, mats, T0, src, tau, design, tc, agg, opts = case
         hc = S.TorchHostComm() if size > 1 else None
         solver = S.Solver(sdim, n, nt, mats=mats, T0=T0, source=src, tau=tau, time_constant=tc, rank=rank,
-                          size=size, host_comm=hc, rtol=1e-10, maxit=400, agg_nodes=agg)
+                          size=size, host_comm=hc, rtol=1e-10, maxit=400, agg_nodes=agg, **opts)
         lay = solver.layout()
         rho = I.rho_uniform((n,) * sdim if tc else (nt,) + (n,) * sdim, 0) if design == "uniform" else \
             I.design_for(sdim, n, nt, design, 0)
@@ -110,12 +110,16 @@ def _run(case, size):
 
 
 CASES = {
-    # sdim, n, nt, mats, T0, source, tau, design, time-constant, agg_nodes
-    "cfg1": (2, 16, 16, CFG1_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0), 1.0, "uniform", False, 64),
-    "cfg2-replica": (2, 32, 32, CFG1_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0), 1.0, "smooth_tc", True, 64),
-    "cfg3-replica": (2, 32, 32, CFG1_MATS, 0.0, ("sin", 1.0, 1.0, 2 * np.pi), 1.0, "smooth_layers", False, 64),
-    "cfg4-replica": (3, 6, 12, CFG4_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0), 1.0, "smooth_tc", True, 64),
-    "T0-cfg4mats": (2, 12, 16, CFG4_MATS, 0.7, ("sin", 1.0, 1.0, 2 * np.pi), 1.0, "uniform", False, 64),
+    # sdim, n, nt, mats, T0, source, tau, design, time-constant, agg_nodes, options
+    "cfg1": (2, 16, 16, CFG1_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0), 1.0, "uniform", False, 64, {}),
+    "cfg2-replica": (2, 32, 32, CFG1_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0), 1.0, "smooth_tc", True, 64, {}),
+    "cfg3-replica": (2, 32, 32, CFG1_MATS, 0.0, ("sin", 1.0, 1.0, 2 * np.pi), 1.0, "smooth_layers", False, 64, {}),
+    # the bench's config-3 launch configuration (right-preconditioned GMRES(6), big coarse levels sweeping
+    # like the fine one) on slabs
+    "cfg3-bench-opts": (2, 32, 32, CFG1_MATS, 0.0, ("sin", 1.0, 1.0, 2 * np.pi), 1.0, "smooth_layers", False, 64,
+                        dict(krylov=1, restart=6, nu_fine_nodes=5000)),
+    "cfg4-replica": (3, 6, 12, CFG4_MATS, 0.0, ("uniform", 1.0, 0.0, 0.0), 1.0, "smooth_tc", True, 64, {}),
+    "T0-cfg4mats": (2, 12, 16, CFG4_MATS, 0.7, ("sin", 1.0, 1.0, 2 * np.pi), 1.0, "uniform", False, 64, {}),
 }
 
 
@@ -123,7 +127,7 @@ CASES = {
 @pytest.mark.parametrize("name", sorted(CASES))
 def test_time_slabs_match_oracle(name, size):
     case = CASES[name]
-    sdim, n, nt, mats, T0, src, tau, design, tc, agg = case
+    sdim, n, nt, mats, T0, src, tau, design, tc, agg, _ = case
     if nt % size:
         pytest.skip("nt not divisible")
     import paper_2508_09589_b200.st as stmod
