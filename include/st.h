@@ -287,6 +287,20 @@ int st_filter(st_ctx_t* ctx, const double* in, double* out, int transpose, doubl
  * volfrac. rho, dJ, rho_new: owned element layers. Lambda is written to *lambda_out if non-null. */
 int st_oc_update(st_ctx_t* ctx, const double* rho, const double* dJ, double volfrac, double move, double rho_min,
                  double* rho_new, double* lambda_out);
+/* ---- The paper's design regularisation --------------------
+ * PDE filter (K_f + M_f) g~ = T_f g on the space-time Q1 mesh with natural boundaries and
+ * d = diag(rx^2/12, ..., rt^2/12) in rescaled coordinates (the paper: rx = 2.4 dx, rt = 2.4 dt), the
+ * element value g~_e = mean of its nodal values (R-25), and the Heaviside projection
+ * g_bar = (tanh(beta eta) + tanh(beta (g~_e - eta))) / (tanh(beta eta) + tanh(beta (1 - eta)))
+ * (beta = 32, eta = 0.5 in the paper). gamma, gamma_e, gamma_bar: [nt][n]..[n] element fields of a
+ * space-time design (one GPU). gamma_e may be NULL. The filter system is solved by Jacobi-preconditioned
+ * CG to 1e-12 (st_get_stats iterations). */
+int st_pde_filter(st_ctx_t* ctx, const double* gamma, double rx, double rt, double beta, double eta,
+                  double* gamma_e, double* gamma_bar);
+/* Chain rule: dphi/dgamma = T_f^T (K_f + M_f)^-1 A^T (dg_bar/dg~ .* dphi/dg_bar), from the
+ * filtered element field gamma_e of st_pde_filter. */
+int st_pde_filter_grad(st_ctx_t* ctx, const double* gamma_e, const double* dphi_dgbar, double rx, double rt,
+                       double beta, double eta, double* dphi_dgamma);
 /* The paper's objective: phi = (sum_e Tavg_e^P)^(1/P) over all elements (all ranks),
  * Tavg_e the mean of the element's nodal temperatures (P = 20 in the paper), and, if dphidT is
  * non-null, its gradient on this rank's owned planes — the adjoint RHS. */

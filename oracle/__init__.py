@@ -24,3 +24,5 @@ from .stfem import *  # noqa: F401,F403
 from .hierarchy import algorithm1, d_eff  # noqa: F401
 from .timestep import backward_euler  # noqa: F401
 from .design import density_filter, oc_update, design_loop  # noqa: F401
+from .pdefilter import (filter_element_matrix, filter_matrices, projection, pde_filter,  # noqa: F401
+                        pde_filter_grad)

@@ -18,6 +18,12 @@
 
 using namespace st;
 
+// csrc/pdefilter.cu
+int st_run_pde_filter(int sd, int n, int nt, double rx, double rt, double beta, double eta, const double* gamma,
+                      double* ge, double* gb, double* const* vec, double* dd, double* hh, RedWs ws, cudaStream_t s);
+int st_run_pde_filter_grad(int sd, int n, int nt, double rx, double rt, double beta, double eta, const double* ge,
+                           const double* dphi, double* out, double* const* vec, double* dd, double* hh, RedWs ws,
+                           cudaStream_t s);
 // csrc/timestep.cu
 long long st_run_timestepping(const Geom& g0, const MatsDev& md, const st_source_t& src, double tau, double T0,
                               const double* rho, int nsteps, double rtol, int maxit, int coarse_max_nodes,
@@ -1772,6 +1778,89 @@ int st_timestep(st_ctx_t* c, const double* rho, int32_t nsteps, double* T, st_ts
     st.max_step_iterations = worst;
     L(c, nl);
     if (stats) *stats = st;
+    return ST_OK;
+  });
+}
+
+// ---- PDE filter + Heaviside projection (csrc/pdefilter.cu) ------------------------
+namespace {
+// six work vectors of >= Nd doubles: Krylov-pool slots (re-zeroed by pf_release), else allocations
+struct PfWork {
+  double* v[6] = {};
+  std::vector<double*> owned;
+  bool pooled = false;
+};
+PfWork pf_acquire(st_ctx* c) {
+  PfWork w;
+  const int slots = c->opt.restart + 1 + c->nz;
+  if (slots >= 6) {
+    for (int k = 0; k < 6; ++k) w.v[k] = pool(c, k);
+    w.pooled = true;
+  } else {
+    for (int k = 0; k < 6; ++k) {
+      dalloc(&w.v[k], (size_t)c->Nd);
+      w.owned.push_back(w.v[k]);
+    }
+  }
+  return w;
+}
+void pf_release(st_ctx* c, PfWork& w) {
+  if (w.pooled)  // the solver relies on zero pad entries in its pool vectors
+    for (int k = 0; k < 6; ++k) CK(cudaMemsetAsync(w.v[k], 0, (size_t)c->N * sizeof(double), c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (double* p : w.owned) cudaFree(p);
+}
+void pf_check(st_ctx* c, double rx, double rt, double beta, double eta) {
+  if (c->tc) throw StErr{ST_E_UNSUPPORTED, "PDE filter: space-time designs (a time-constant design is extruded)"};
+  if (c->comm.size > 1) throw StErr{ST_E_UNSUPPORTED, "PDE filter: one GPU"};
+  if (!(rx >= 0) || !(rt >= 0) || !(beta > 0) || !(eta > 0 && eta < 1))
+    throw StErr{ST_E_INVALID_ARG, "PDE filter: rx, rt >= 0, beta > 0, 0 < eta < 1"};
+}
+}  // namespace
+
+int st_pde_filter(st_ctx_t* c, const double* gamma, double rx, double rt, double beta, double eta, double* gamma_e,
+                  double* gamma_bar) {
+  return guarded([&]() -> int {
+    if (!c || !gamma || !gamma_bar) throw StErr{ST_E_INVALID_ARG, "null argument"};
+    pf_check(c, rx, rt, beta, eta);
+    CK(cudaSetDevice(c->device));
+    const long long ne = c->ndesign;
+    const double* g = in_ptr(c, gamma, ne, 1);
+    bool s1 = false, s2 = false;
+    double* gb = out_ptr(c, gamma_bar, ne, 2, false, &s1);
+    double* ge = gamma_e ? out_ptr(c, gamma_e, ne, 3, false, &s2) : nullptr;
+    PfWork w = pf_acquire(c);
+    const int its = st_run_pde_filter(c->sd, (int)c->grid.n, (int)c->grid.nt, rx, rt, beta, eta, g, ge, gb, w.v,
+                                      c->dsmall + 400, c->hsmall + 400, c->ws, c->stream);
+    L(c, 6 * its + 8);
+    check_launch();
+    pf_release(c, w);
+    if (s1) copy_back(c, gamma_bar, gb, ne);
+    if (s2) copy_back(c, gamma_e, ge, ne);
+    c->stats.iterations = its;
+    return ST_OK;
+  });
+}
+
+int st_pde_filter_grad(st_ctx_t* c, const double* gamma_e, const double* dphi_dgbar, double rx, double rt, double beta,
+                       double eta, double* dphi_dgamma) {
+  return guarded([&]() -> int {
+    if (!c || !gamma_e || !dphi_dgbar || !dphi_dgamma) throw StErr{ST_E_INVALID_ARG, "null argument"};
+    pf_check(c, rx, rt, beta, eta);
+    CK(cudaSetDevice(c->device));
+    const long long ne = c->ndesign;
+    const double* ge = in_ptr(c, gamma_e, ne, 1);
+    const double* dp = in_ptr(c, dphi_dgbar, ne, 2);
+    bool s1 = false;
+    double* out = out_ptr(c, dphi_dgamma, ne, 3, false, &s1);
+    PfWork w = pf_acquire(c);
+    const int its = st_run_pde_filter_grad(c->sd, (int)c->grid.n, (int)c->grid.nt, rx, rt, beta, eta, ge, dp, out,
+                                           w.v, c->dsmall + 400, c->hsmall + 400, c->ws, c->stream);
+    L(c, 6 * its + 8);
+    check_launch();
+    pf_release(c, w);
+    if (s1) copy_back(c, dphi_dgamma, out, ne);
+    c->stats.iterations = its;
     return ST_OK;
   });
 }

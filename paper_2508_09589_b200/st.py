@@ -106,7 +106,7 @@ EXPORTS = ["st_abi_version", "st_default_options", "st_setup", "st_destroy", "st
            "st_sensitivity", "st_apply", "st_vcycle", "st_rhs", "st_filter", "st_oc_update", "st_dot", "st_pnorm", "st_level_apply", "st_bench_op", "st_get_stats", "st_get_hierarchy",
            "st_local_layout", "st_nccl_unique_id", "st_nccl_comm_init", "st_nccl_comm_destroy", "st_plan",
            "st_struct_sizes",
-           "st_num_nodes", "st_num_design", "st_kernel_launches", "st_strerror", "st_last_error", "st_timestep", "st_nccl_selftest"]
+           "st_num_nodes", "st_num_design", "st_kernel_launches", "st_strerror", "st_last_error", "st_timestep", "st_nccl_selftest", "st_pde_filter", "st_pde_filter_grad"]
 
 _lib = None
 
@@ -140,6 +140,10 @@ def load_library(path: str = LIB_PATH):
     lib.st_oc_update.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_void_p,
                                  P(C.c_double)]
     lib.st_dot.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, P(C.c_double)]
+    lib.st_pde_filter.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double, C.c_void_p,
+                                  C.c_void_p]
+    lib.st_pde_filter_grad.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_double,
+                                       C.c_double, C.c_void_p]
     lib.st_pnorm.argtypes = [C.c_void_p, C.c_void_p, C.c_double, P(C.c_double), C.c_void_p]
     lib.st_level_apply.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
     lib.st_bench_op.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
@@ -380,6 +384,27 @@ class Solver:
         self._check(self.lib.st_oc_update(self.ctx, _ptr(rho, nown, "rho"), _ptr(dJ, nown, "dJ"), volfrac, move,
                                           rho_min, _ptr(rho_new, nown, "rho_new"), C.byref(lam)))
         return lam.value
+
+    def pde_filter(self, gamma, gamma_bar, gamma_e=None, rx=None, rt=None, beta=32.0, eta=0.5):
+        """The paper's PDE filter + Heaviside projection; radii default to 2.4 dx / 2.4 dt
+        (rescaled). Returns the filter's CG iterations."""
+        n, nt = int(self.grid.n), int(self.grid.nt)
+        rx = 2.4 / n if rx is None else rx
+        rt = 2.4 / nt if rt is None else rt
+        ne = self.n_design
+        self._check(self.lib.st_pde_filter(self.ctx, _ptr(gamma, ne, "gamma"), rx, rt, beta, eta,
+                                           _ptr(gamma_e, ne, "gamma_e"), _ptr(gamma_bar, ne, "gamma_bar")))
+        return self.stats()["iterations"]
+
+    def pde_filter_grad(self, gamma_e, dphi_dgbar, out, rx=None, rt=None, beta=32.0, eta=0.5):
+        """Chain rule of the filter + projection."""
+        n, nt = int(self.grid.n), int(self.grid.nt)
+        rx = 2.4 / n if rx is None else rx
+        rt = 2.4 / nt if rt is None else rt
+        ne = self.n_design
+        self._check(self.lib.st_pde_filter_grad(self.ctx, _ptr(gamma_e, ne, "gamma_e"), _ptr(dphi_dgbar, ne, "dphi"),
+                                                rx, rt, beta, eta, _ptr(out, ne, "out")))
+        return self.stats()["iterations"]
 
     def pnorm(self, T, P=20.0, grad=None):
         """phi = (sum_e Tavg_e^P)^(1/P); grad (optional) receives dphi/dT."""

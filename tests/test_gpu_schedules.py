@@ -304,3 +304,32 @@ def test_timestepping_converges_to_the_space_time_solution():
         gaps.append(rel(host(Tts), host(T)))
         solver.close()
     assert gaps[1] < gaps[0] and gaps[2] < gaps[1], gaps
+
+
+# ------------------------------------------------------------------ the paper's PDE filter + projection
+@pytest.mark.parametrize("sdim,n,nt,rfac", [(2, 16, 16, 2.4), (2, 40, 24, 2.4), (3, 6, 10, 2.4), (2, 12, 20, 6.0)])
+def test_pde_filter_projection_and_chain_rule_match_oracle(sdim, n, nt, rfac):
+    """st_pde_filter / st_pde_filter_grad: the filtered element
+    field, its projection and the chain-rule sensitivities equal the oracle's direct solves (CG to 1e-12);
+    the filter then feeds the state solve (the physical design of PAPER.md:552)."""
+    solver, prob = make_pair(sdim, n, nt, rtol=1e-11, maxit=500)
+    rng = np.random.default_rng(5)
+    g = rng.uniform(0.0, 1.0, (nt,) + (n,) * sdim)
+    rx, rt = rfac / n, rfac / nt
+    gb = torch.empty(g.size, dtype=torch.float64, device=DEV)
+    ge = torch.empty_like(gb)
+    its = solver.pde_filter(dev(g), gb, ge, rx=rx, rt=rt)
+    assert 0 < its <= 200
+    _, ge_ref, gb_ref = O.pde_filter(prob.mesh, g.reshape(-1), rx, rt)
+    assert rel(host(ge), ge_ref) <= 1e-10
+    assert rel(host(gb), gb_ref) <= 1e-9
+    w = rng.uniform(-1, 1, g.size)
+    out = torch.empty_like(gb)
+    solver.pde_filter_grad(ge, dev(w), out, rx=rx, rt=rt)
+    ref = O.pde_filter_grad(prob.mesh, ge_ref, w, rx, rt)
+    assert rel(host(out), ref) <= 1e-9
+    # the projected field is a valid design for the state solve
+    T = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
+    solver.solve(gb.clamp(1e-3, 1.0), T)
+    assert solver.stats()["converged"] == 1
+    solver.close()
