@@ -271,15 +271,38 @@ def run_cuda(args):
         nccl_comm = S.nccl_comm_init(obj[0], rank, world)
         S.nccl_selftest(nccl_comm, rank, world)  # fail loudly before any timing if the transport is broken
     opts = solver_opts_for(wl, args)
-    solver = S.Solver(wl["sdim"], wl["n"], wl["nt"], mats=wl["mats"], source=wl["source"], tau=wl["tau"],
-                      time_constant=wl["tc"], stream=stream.cuda_stream, device=local, rtol=args.rtol, maxit=1000,
-                      rank=rank, size=world, nccl_comm=nccl_comm, **opts)
-    N = solver.n_nodes            # this rank's owned nodes
-    nd = solver.n_design
     N_global = (wl["n"] + 1) ** wl["sdim"] * (wl["nt"] + 1)
     nsteps = args.warmup + args.steps
-    lay = solver.layout()
     big = N_global > 4e8          # config 3: one design on the device, a new one per step by rho <- 1.01 - rho
+    # memory plan: config 3 on one GPU uses ~180 of the B200's 183 GiB with GMRES(6). Should
+    # a box have less free memory, the restart length steps down (each step frees one 8.6 GB Krylov vector)
+    # rather than the run failing; the line reports the options actually used
+    mem_note = None
+    while True:
+        try:
+            solver = S.Solver(wl["sdim"], wl["n"], wl["nt"], mats=wl["mats"], source=wl["source"], tau=wl["tau"],
+                              time_constant=wl["tc"], stream=stream.cuda_stream, device=local, rtol=args.rtol,
+                              maxit=1000, rank=rank, size=world, nccl_comm=nccl_comm, **opts)
+            N = solver.n_nodes    # this rank's owned nodes
+            nd = solver.n_design
+            lay = solver.layout()
+            reserve = [torch.empty(n_, dtype=torch.float64, device=dev) for n_ in
+                       (N, N, nd if wl["tc"] else lay["n_layers"] * wl["n"] ** wl["sdim"], nd + 256 * 1024 * 1024 // 8)]
+            del reserve           # the caller's vectors fit next to the library's workspaces
+            break
+        except (S.StError, torch.OutOfMemoryError) as ex:
+            oom = isinstance(ex, torch.OutOfMemoryError) or getattr(ex, "code", 0) == -5
+            r = opts.get("restart", 16)
+            if not oom or r <= 2:
+                raise
+            try:
+                solver.close()
+            except Exception:  # noqa: BLE001
+                pass
+            solver = None
+            torch.cuda.empty_cache()
+            opts["restart"] = r - 1
+            mem_note = f"restart lowered to {r - 1} (device memory)"
     design = args.config == 5     # a step is one config-5 design iteration (R-13)
     t_gen = time.perf_counter()
     if wl["design"] == "const":
@@ -529,6 +552,7 @@ def run_cuda(args):
                    "parallelism": f"{world} time slabs (NCCL)" if world > 1 else "1 GPU",
                    "l2": "flushed (256 MB write) between steps" + ("; inputs (8.6 GB per vector) exceed L2" if big else ""),
                    "preconditioner": precond_desc(args, solver), "options": {k: v for k, v in opts.items()},
+                   "memory_note": mem_note,
                    "design_generation_s": round(t_gen, 1)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "fine-level damped-Jacobi sweep (" + ("tc2d_kernel, time-constant rho" if wl["tc"] and wl["sdim"] == 2
