@@ -54,13 +54,14 @@ WORKLOADS = {
             sdim=2, n=512, nt=512, mats=CFG1_MATS, tc=False, design="const", source=("uniform", 1.0, 0.0, 0.0),
             tau=1.0, opts={}, scaling="weak", bpd_iter=583.0, sweep_bpd=40.0),
     # BASELINE config 3 at full size: 1,076,890,625 DOFs (8.6 GB per vector). One GPU holds it with the
-    # memory plan of DESIGN.md sec. 6: right-preconditioned GMRES(6) (no Z vectors), the Krylov pool as
-    # the hooks' and the V-cycle's level-0 scratch, the compliance adjoint RHS generated in the library
+    # memory plan of DESIGN.md sec. 6: right-preconditioned GMRES(7) (no Z vectors; 188.9 of 192 GB),
+    # stepping down to GMRES(6) (180.2 GB) on a box with less free memory; the Krylov pool as the hooks'
+    # and the V-cycle's level-0 scratch, the compliance adjoint RHS generated in the library
     3: dict(name="config3: (2+1)D 1024^2x1024 elements (1,076,890,625 DOFs), an independent smooth field per "
                  "time layer (sigma 3, [0.01,1]), Q(t) = 1 + sin(2 pi t), k=1e-3+rho^3(1-1e-3), c=1, T=0 sink "
                  "patch (10% of x1=0), T0=0",
             sdim=2, n=1024, nt=1024, mats=CFG1_MATS, tc=False, design="smooth_layers", source=SIN_SRC, tau=1.0,
-            opts=dict(krylov=1, restart=6), scaling="strong", bpd_iter=580.0, sweep_bpd=40.0),
+            opts=dict(krylov=1, restart=7), scaling="strong", bpd_iter=580.0, sweep_bpd=40.0),
     # the 1/8 slab of config 3 on one GPU (round-1 "config 3 shape"): parity / profiling case
     33: dict(name="config3-shaped (1/8 of config 3 on one GPU): (2+1)D 512^2x512, an independent smooth field per "
                   "time layer, Q(t) = 1 + sin(2 pi t)", sdim=2, n=512, nt=512, mats=CFG1_MATS, tc=False,
@@ -289,6 +290,9 @@ def run_cuda(args):
             reserve = [torch.empty(n_, dtype=torch.float64, device=dev) for n_ in
                        (N, N, nd if wl["tc"] else lay["n_layers"] * wl["n"] ** wl["sdim"], nd + 256 * 1024 * 1024 // 8)]
             del reserve           # the caller's vectors fit next to the library's workspaces
+            free_b, _ = torch.cuda.mem_get_info(dev)
+            if big and free_b < 1.5e9 and opts.get("restart", 16) > 6:
+                raise torch.OutOfMemoryError("less than 1.5 GB of headroom")  # keep a margin: one step down
             break
         except (S.StError, torch.OutOfMemoryError) as ex:
             oom = isinstance(ex, torch.OutOfMemoryError) or getattr(ex, "code", 0) == -5

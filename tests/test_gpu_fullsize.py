@@ -167,5 +167,7 @@ def test_config3_fullsize_one_gpu_certified():
         pytest.skip("config 3 needs a 180 GB B200")
     wl = bench.WORKLOADS[3]
     rho = I.design_for(2, 1024, 1024, "smooth_layers", 0)
-    certify("config3", 2, 1024, 1024, False, "smooth_layers", wl["source"], CFG1_MATS, dict(wl["opts"]),
+    opts = dict(wl["opts"])
+    opts["restart"] = min(opts.get("restart", 6), 6)  # the bench's plan with its one-step memory margin
+    certify("config3", 2, 1024, 1024, False, "smooth_layers", wl["source"], CFG1_MATS, opts,
             rho=rho, nrows=1200, nel=1500)
