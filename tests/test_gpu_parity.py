@@ -320,7 +320,7 @@ def test_operator_parity_all_kernel_variants(variant, case):
                                                (3, 4, 6, True, CFG4_MATS)])
 def test_jacobi_weight_bound(sdim, n, nt, tc, mats):
     """The fine level's Gershgorin ratio equals max_i sum_j |A_ij| / |A_ii| of the
-    oracle's K_bc over free rows, bounds the spectral radius of D^-1 K_bc, and omega = min(cap, 1.8/R)."""
+    oracle's K_bc over free rows, bounds the spectral radius of D^-1 K_bc, and omega = min(cap, 1.9/R)."""
     solver, prob = make_pair(sdim, n, nt, mats=mats, time_constant=tc)
     rho = _rho(sdim, n, nt, "uniform", 2, tc)
     x = torch.zeros(prob.mesh.n_nodes, dtype=torch.float64, device=DEV)
