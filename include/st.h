@@ -151,6 +151,9 @@ typedef struct {
   int64_t nu_fine_nodes;    /* coarse levels with at least this many nodes use the fine-level sweep
                                counts nu_pre / nu_post instead of nu_coarse (their sweeps cost HBM
                                passes, not launch latency); 0 = level 0 only  */
+  int32_t pitch_align;      /* row pitch of the internal vectors rounded up to a multiple of this many
+                               doubles (even; 2 = 16-byte rows, the TMA minimum; default 4 = one
+                               DRAM sector)                                                     */
 } st_options_t;
 
 /* Distribution over time slabs. NULL or size == 1 => one GPU.

@@ -162,13 +162,17 @@ void dzalloc(double** p, size_t count) {
 // pad = true: internal layout with an even x1 row pitch (16-byte aligned rows and planes).
 // nt: local element layers; ntg (> 0): global layers of the level (dt = 1/ntg), pg0: global
 // index of local plane 0.
+// row-pitch alignment (doubles) of the padded internal layout while a context is being set up
+// (st_options_t pitch_align; st_setup / st_plan set it around build_hierarchy and assign_slabs)
+thread_local int t_pitch_align = 2;
+
 Geom make_geom(int sd, int n, int nt, int plo, int phi, bool pad = true, int ntg = 0, int pg0 = 0) {
   Geom g{};
   g.sd = sd;
   g.n = n;
   g.nn = n + 1;
   g.nt = nt;
-  g.pr = (pad && (g.nn % 2 == 1)) ? g.nn + 1 : g.nn;
+  g.pr = pad ? (g.nn + t_pitch_align - 1) / t_pitch_align * t_pitch_align : g.nn;
   g.P = g.pr;
   for (int d = 1; d < sd; ++d) g.P *= g.nn;
   g.N = g.P * (nt + 1);
@@ -682,7 +686,9 @@ void build_ops(st_ctx* c) {
         L(c);
       } else {  // space coarsening of every parent layer into mid, then time coarsening of mid
         OpDesc mop = Pv.op;
+        t_pitch_align = c->opt.pitch_align;
         mop.g = make_geom(c->sd, Lv.g.n, Pv.g.nt, Lv.g.plo, Lv.g.phi);
+        t_pitch_align = 2;
         mop.g.walls = Lv.g.walls;
         mop.form = Lv.mid_ns == 5 ? FORM_B4 : FORM_MK;
         mop.nl = Pv.g.nt;
@@ -1270,6 +1276,10 @@ void st_default_options(st_options_t* o) {
   // (levels 1-3: 2.7e8, 6.8e7, 1.7e7 nodes), config 5 247 -> 271, the 512^2 x 512 slab 486 -> 551;
   // configs 2 / 4 have no such coarse level (profiles/r02/nu_fine_nodes.log)
   o->nu_fine_nodes = 10000000;
+  // 32-byte rows: every TMA box row and every tile-row store starts on a DRAM sector (config-3 fine
+  // residual 7.80 -> 7.61 ms, sweep 6.79 -> 6.78 ms; 16 doubles: 7.44 / 6.76 ms but +1.4 % memory;
+  // profiles/r02/kbench_pitch.log)
+  o->pitch_align = 4;
 }
 
 const char* st_strerror(int code) {
@@ -1389,8 +1399,13 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       c->md.kins = mats->k_ins * scale;
       c->md.dk = (mats->k_con - mats->k_ins) * scale;
       c->md.pk = mats->p_k;
+      if (c->opt.pitch_align <= 0) c->opt.pitch_align = 4;
+      if (c->opt.pitch_align % 2 != 0 || c->opt.pitch_align > 64)
+        throw StErr{ST_E_INVALID_ARG, "pitch_align: an even number of doubles <= 64"};
+      t_pitch_align = c->opt.pitch_align;
       build_hierarchy(c);
       assign_slabs(c);
+      t_pitch_align = 2;
       setup_forms(c);
       const Level& L0 = c->lv[0];
       c->N = L0.g.N;

@@ -139,7 +139,7 @@ def test_options_defaults_and_knobs_are_options():
     assert o.kernel_family == st.ST_KERNELS_TMA and o.chunk_planes == 0 and o.max_ctas == 0
     assert o.fuse_prolong == 1 and o.fuse_restrict == 1
     assert o.omega_factor == 1.9 and o.dgks_eta == 0.1 and o.graph_max_nodes == 0 and o.smoother_rtol == 0.0
-    assert o.nu_fine_nodes == 10000000
+    assert o.nu_fine_nodes == 10000000 and o.pitch_align == 4
     hdr = open(os.path.join(ROOT, "include", "st.h")).read()
     for name in ("ST_KRYLOV_FGMRES", "ST_KRYLOV_GMRES", "ST_COARSE_DENSE", "ST_COARSE_GMRES", "ST_KERNELS_TMA",
                  "ST_KERNELS_CPASYNC", "ST_KERNELS_GENERIC", "ST_KERNELS_TMA2D"):
