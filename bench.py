@@ -56,12 +56,14 @@ WORKLOADS = {
     # BASELINE config 3 at full size: 1,076,890,625 DOFs (8.6 GB per vector). One GPU holds it with the
     # memory plan of DESIGN.md sec. 6: right-preconditioned GMRES(7) (no Z vectors; 188.9 of 192 GB),
     # stepping down to GMRES(6) (180.2 GB) on a box with less free memory; the Krylov pool as the hooks'
-    # and the V-cycle's level-0 scratch, the compliance adjoint RHS generated in the library
+    # and the V-cycle's level-0 scratch, the compliance adjoint RHS generated in the library. Sweeps 1 + 2 on
+    # the fine and big coarse levels (profiles/r02/nu_split_r02.log: 653 -> 693 MDOF/s at 14 + 14
+    # iterations; 2 + 2 stays the library default, better on configs 2, 4 and the 512^2 slab)
     3: dict(name="config3: (2+1)D 1024^2x1024 elements (1,076,890,625 DOFs), an independent smooth field per "
                  "time layer (sigma 3, [0.01,1]), Q(t) = 1 + sin(2 pi t), k=1e-3+rho^3(1-1e-3), c=1, T=0 sink "
                  "patch (10% of x1=0), T0=0",
             sdim=2, n=1024, nt=1024, mats=CFG1_MATS, tc=False, design="smooth_layers", source=SIN_SRC, tau=1.0,
-            opts=dict(krylov=1, restart=7), scaling="strong", bpd_iter=580.0, sweep_bpd=40.0),
+            opts=dict(krylov=1, restart=7, nu_pre=1), scaling="strong", bpd_iter=580.0, sweep_bpd=40.0),
     # the 1/8 slab of config 3 on one GPU (round-1 "config 3 shape"): parity / profiling case
     33: dict(name="config3-shaped (1/8 of config 3 on one GPU): (2+1)D 512^2x512, an independent smooth field per "
                   "time layer, Q(t) = 1 + sin(2 pi t)", sdim=2, n=512, nt=512, mats=CFG1_MATS, tc=False,
@@ -86,6 +88,10 @@ def solver_opts(args):
     nu = args.nu or (10 if args.smoother == "gmres" else 0)  # 0: the library defaults
     if nu:
         o["nu_pre"] = o["nu_post"] = nu
+    if args.nu_pre > 0:
+        o["nu_pre"] = args.nu_pre
+    if args.nu_post >= 0:
+        o["nu_post"] = args.nu_post
     if args.nu_coarse >= 0:
         o["nu_coarse"] = args.nu_coarse
     if args.omega > 0:
@@ -122,6 +128,8 @@ def parse():
                     help="jacobi: damped Jacobi nu+nu (default); gmres: the paper's GMRES(nu)-Jacobi smoother")
     ap.add_argument("--nu", type=int, default=0,
                     help="fine-level Jacobi sweeps / GMRES steps (default: the library's 2 for jacobi, 10 for gmres)")
+    ap.add_argument("--nu-pre", type=int, default=0, help="fine-level pre-smoothing sweeps (overrides --nu)")
+    ap.add_argument("--nu-post", type=int, default=-1, help="fine-level post-smoothing sweeps (overrides --nu)")
     ap.add_argument("--nu-coarse", type=int, default=-1,
                     help="Jacobi sweeps on the coarse levels (default: the library's 5; 0 = --nu)")
     ap.add_argument("--full-coarsening", action="store_true", help="the paper's full space-time coarsening")
