@@ -1740,7 +1740,7 @@ int st_bench_op(st_ctx_t* c, const double* rho, int level, int mode, int transpo
         set_fine_rho(c, rho);
         c->kt_design = false;
       }
-    } else {
+    } else if (!c->have_ops || c->lv[0].op.rho != rho) {  // as level 0: same pointer = same design (st.h)
       prepare(c, rho);
     }
     Level& Lv = c->lv[level];

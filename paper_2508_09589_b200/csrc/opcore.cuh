@@ -103,13 +103,17 @@ __device__ __forceinline__ double st_weight(const Geom& g, const double* __restr
                                             long long pn, int k) {
   constexpr int CEN = SG<SD>::CEN, NOFF = SG<SD>::NOFF;
   if (k >= CEN) return __ldg(base + (long long)(k - CEN) * g.P + pn);
+  // mirrored offset: the neighbour's forward coefficient. Branch-free (an outside neighbour reads the
+  // node's own entry and is masked), so the loads of a stencil issue back to back (latency-bound levels)
   int nb[3] = {0, 0, 0};
+  bool ok = true;
 #pragma unroll
   for (int d = 0; d < SD; ++d) {
     nb[d] = c[d] + SG<SD>::od(k, d);
-    if (nb[d] < 0 || nb[d] >= g.nn) return 0.0;
+    ok = ok && nb[d] >= 0 && nb[d] < g.nn;
   }
-  return __ldg(base + (long long)(NOFF - 1 - k - CEN) * g.P + pidx<SD>(g, nb));
+  const double v = __ldg(base + (long long)(NOFF - 1 - k - CEN) * g.P + (ok ? pidx<SD>(g, nb) : pn));
+  return ok ? v : 0.0;
 }
 
 template <int SD>

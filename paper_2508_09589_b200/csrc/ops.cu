@@ -9,6 +9,8 @@
 // Dirichlet elimination (R-1): A = m_f K m_f + m_c.
 // Fine level (FORM_RHO) is matrix-free: C_e, k~_e from rho by SIMP on the
 // fly, element matrices C (U (x) M_sp) + k~ (Tm (x) K_sp) (F1).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "opcore.cuh"
@@ -97,7 +99,7 @@ static void launch_t(const OpDesc& op, const double* x, const double* b, double*
   const Geom& g = op.g;
   dim3 blk(32, 4, 1);
   int rows = SD == 2 ? g.nn : g.nn * g.nn;
-  int chunk = choose_chunk(g);
+  int chunk = op.chunk > 0 ? std::min(op.chunk, g.nt + 1) : choose_chunk(g);
   dim3 grd((g.nn + 31) / 32, (rows + 3) / 4, (g.nt + 1 + chunk - 1) / chunk);
   op_kernel<SD, FORM, MODE, TRANS, MASK><<<grd, blk, 0, s>>>(op, x, b, y, omega, chunk);
 }
@@ -545,9 +547,84 @@ __global__ void gersh_kernel(OpDesc op, int pa, int pb, unsigned long long* __re
   }
 }
 
+// The same Gershgorin ratio for the (2+1)D fine level of a space-time design with uniform capacity
+// (configs 1, 3, 5), from the per-design k~ table (zero border: no element masks) with the Q1 weights
+// in closed form: per row the 8 element conductivities of the two adjacent layers, ~100 flops instead of
+// the generic kernel's per-weight element loops (config 3: 95 ms per design -> a few ms).
+__global__ void __launch_bounds__(256) gersh_tv2d_kernel(OpDesc op, int pa, int pb, unsigned long long* __restrict__ out) {
+  const Geom& g = op.g;
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double best = 0.0;
+  if (idx < g.P * (long long)(pb - pa + 1)) {
+    const int p = pa + (int)(idx / g.P);
+    int c[3] = {0, 0, 0};
+    if (pdecode<2>(g, idx % g.P, c) && !is_cons<2>(g, c, p)) {
+      const int i = c[0], j = c[1], n = g.n;
+      const long long w2 = n + 2;
+      const bool hasL = p >= 1, hasU = p < g.nt;
+      // k~ of the 4 elements (e = bx + 2 by: element (i - 1 + bx, j - 1 + by)) of layers p-1 and p
+      double kL[4], kU[4], cm[4];
+      for (int e = 0; e < 4; ++e) {
+        const int ei = i - 1 + (e & 1), ej = j - 1 + (e >> 1);
+        const long long col = (long long)(ej + 1) * w2 + (ei + 1);
+        kL[e] = hasL ? __ldg(op.kt + (long long)(p - 1) * w2 * w2 + col) : 0.0;
+        kU[e] = hasU ? __ldg(op.kt + (long long)p * w2 * w2 + col) : 0.0;
+        cm[e] = (ei >= 0 && ei < n && ej >= 0 && ej < n) ? 1.0 : 0.0;  // element inside (uniform capacity)
+      }
+      const double sm = op.m.Cins * g.dx * g.dx / 36.0, sk = 1.0 / 6.0;
+      double diag = 0.0, sum = 0.0;
+      for (int k = 0; k < 9; ++k) {
+        const int ox = (k % 3) - 1, oy = (k / 3) - 1;
+        const int nb[3] = {i + ox, j + oy, 0};
+        if (nb[0] < 0 || nb[0] > n || nb[1] < 0 || nb[1] > n) continue;
+        // elements holding both the node and the neighbour, and the Q1 weights by Hamming distance
+        double sL = 0.0, sU = 0.0, sM = 0.0;
+        for (int e = 0; e < 4; ++e) {
+          const int bx = e & 1, by = e >> 1;
+          if ((ox == 1 && bx != 1) || (ox == -1 && bx != 0) || (oy == 1 && by != 1) || (oy == -1 && by != 0)) continue;
+          sL += kL[e];
+          sU += kU[e];
+          sM += cm[e];
+        }
+        const int h = (ox != 0) + (oy != 0);
+        const double mw = sm * sM * (h == 0 ? 4.0 : (h == 1 ? 2.0 : 1.0));
+        const double kf = sk * (h == 0 ? 4.0 : (h == 1 ? -1.0 : -2.0));
+        const double KL = kf * sL, KU = kf * sU;
+        double wlo = 0.0, wmid = 0.0, whi = 0.0;
+        if (hasL) {
+          wlo = op.U[1][0] * mw + op.Tm[1][0] * KL;
+          wmid = op.U[1][1] * mw + op.Tm[1][1] * KL;
+        }
+        if (hasU) {
+          wmid += op.U[0][0] * mw + op.Tm[0][0] * KU;
+          whi = op.U[0][1] * mw + op.Tm[0][1] * KU;
+        }
+        if (k == 4) diag = wmid;
+        if (hasL && !is_cons<2>(g, nb, p - 1)) sum += fabs(wlo);
+        if (!is_cons<2>(g, nb, p)) sum += fabs(wmid);
+        if (hasU && !is_cons<2>(g, nb, p + 1)) sum += fabs(whi);
+      }
+      if (diag != 0.0) best = sum / fabs(diag);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_down_sync(0xffffffffu, best, o));
+  __shared__ double wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, wm[w]);
+    atomicMax(out, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
 void launch_gersh(const OpDesc& op, int pa, int pb, unsigned long long* out, cudaStream_t s) {
   long long total = op.g.P * (long long)(pb - pa + 1);
   if (total <= 0) return;
+  if (op.g.sd == 2 && op.form == FORM_RHO && !op.rho_tc && op.kt && op.m.dC == 0.0) {
+    gersh_tv2d_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(op, pa, pb, out);
+    return;
+  }
   unsigned grd = (unsigned)((total + 255) / 256);
 #define GK(SD, F) gersh_kernel<SD, F><<<grd, 256, 0, s>>>(op, pa, pb, out)
   if (op.g.sd == 2) {

@@ -29,4 +29,5 @@ with torch.cuda.stream(st):
     e0.record(st); s.bench_op(rho, level, mode, 10); e1.record(st)
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) / 10 * 1e3
-print(f"{' '.join(sys.argv[1:])}: us per launch {us:.2f} nodes {N} -> {32 * N / us / 1e3:.0f} GB/s (32 B/node)")
+print(f"{' '.join(sys.argv[1:])}: us per launch {us:.2f} nodes {N} -> {32 * N / us / 1e3:.0f} GB/s (32 B/node); "
+      f"rho setup {s.stats()['setup_ms']:.2f} ms; level {level}: {H[level]['n']}^{sdim} x {H[level]['nt']} {H[level]['kind']}")

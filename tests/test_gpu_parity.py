@@ -317,7 +317,10 @@ def test_operator_parity_all_kernel_variants(variant, case):
 
 
 @pytest.mark.parametrize("sdim,n,nt,tc,mats", [(2, 12, 10, True, CFG1_MATS), (2, 8, 12, False, CFG4_MATS),
-                                               (3, 4, 6, True, CFG4_MATS)])
+                                               (3, 4, 6, True, CFG4_MATS),
+                                               # uniform capacity, space-time design: the closed-form k~-table
+                                               # kernel (gersh_tv2d_kernel)
+                                               (2, 10, 12, False, CFG1_MATS), (2, 33 - 1, 6, False, CFG1_MATS)])
 def test_jacobi_weight_bound(sdim, n, nt, tc, mats):
     """The fine level's Gershgorin ratio equals max_i sum_j |A_ij| / |A_ii| of the
     oracle's K_bc over free rows, bounds the spectral radius of D^-1 K_bc, and omega = min(cap, 1.9/R)."""
