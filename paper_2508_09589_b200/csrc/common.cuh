@@ -156,6 +156,61 @@ __device__ __forceinline__ void work_segment(long long w, long long wend, long l
   *p1 = (rem < ce - *p0) ? *p0 + (int)rem : ce;
 }
 
+// Strided chunk schedule of the persistent stencil kernels tv2d / tc3r: the NP
+// planes are cut into nch balanced chunks of ~K planes; inside a chunk the tiles form groups of
+// G = gridDim.x consecutive tiles, and CTA b takes tile kG + b of every full group k for all the
+// chunk's planes (one segment per group), then an equal share of the (tile, plane) items of the last,
+// partial group (contiguous, tile-major). At any moment CTA b and its tile neighbours' CTAs work on
+// neighbouring tiles at about the same plane: the halo rows / columns two tiles share are requested
+// twice within a short interval and the second request hits L2 (the round-1 slice-per-CTA schedule put
+// a CTA's neighbour tiles 16 planes apart in time on the same CTA: ~10 % L2 hit rate at 1024^2 x 1024,
+// 1.8x the algorithmic DRAM reads, profiles/r02). nch = 1 (K = NP): one chunk.
+struct Sched {
+  long long tiles, w, we;
+  int NP, nch, c, cs, Kc, k, nfull;
+};
+__device__ __forceinline__ void sched_init(Sched& s, long long tiles, int NP, int K) {
+  s.tiles = tiles;
+  s.NP = NP;
+  s.nch = (NP + K - 1) / K;
+  s.c = -1;
+  s.w = s.we = 0;
+  s.cs = s.Kc = 0;
+  s.k = s.nfull = 0;
+}
+// next segment (tile, rows [p0, p1)) of this CTA; false when the CTA's work is done
+__device__ __forceinline__ bool sched_next(Sched& s, long long& tile, int& p0, int& p1) {
+  const long long G = gridDim.x, b = blockIdx.x;
+  for (;;) {
+    if (s.c >= 0) {
+      if (s.k < s.nfull) {  // full group k: tile k G + b over every plane of the chunk
+        tile = s.k * G + b;
+        p0 = s.cs;
+        p1 = s.cs + s.Kc;
+        ++s.k;
+        return true;
+      }
+      if (s.w < s.we) {  // partial group: a contiguous share of its (tile, plane) items
+        const long long r = s.w;
+        tile = (long long)s.nfull * G + r / s.Kc;
+        p0 = s.cs + (int)(r % s.Kc);
+        const long long rem = s.we - s.w;
+        p1 = (rem < s.cs + s.Kc - p0) ? p0 + (int)rem : s.cs + s.Kc;
+        s.w += p1 - p0;
+        return true;
+      }
+    }
+    if (++s.c >= s.nch) return false;
+    s.cs = (int)((long long)s.c * s.NP / s.nch);
+    s.Kc = (int)((long long)(s.c + 1) * s.NP / s.nch) - s.cs;
+    s.nfull = (int)(s.tiles / G);
+    s.k = 0;
+    const long long items = (s.tiles - (long long)s.nfull * G) * s.Kc;
+    s.w = items * b / G;
+    s.we = items * (b + 1) / G;
+  }
+}
+
 // planes per time chunk of a persistent stencil kernel's work list: the option when forced
 // (op.chunk > 0), one chunk (tile-major order) when chunking is off (op.chunk < 0), else the
 // kernel's automatic choice `auto_k` (only tv2d chunks automatically)

@@ -24,6 +24,9 @@ bool launch_op_tc2d_pro(const OpDesc& op, const Geom& gc, bool trans, const doub
 // tc3d.cu: (3+1)D TMA kernel for time-constant levels (fine from rho, stored MK), masked modes
 bool launch_op_tc3d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                     double omega, cudaStream_t s);
+// tc3r.cu: (3+1)D fine level of a time-constant design (element-layer products, full-row tiles)
+bool launch_op_tc3r(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
+                    double omega, cudaStream_t s);
 // tv2d.cu: fine level of a space-time design with uniform capacity (configs 1, 3, 5), masked modes
 bool launch_op_tv2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                     double omega, cudaStream_t s);

@@ -2,6 +2,8 @@
 // (classical Gram-Schmidt column h = V^T w together with ||w||^2), multi-AXPY with the new
 // norm, the solution update x += Z y, scaling. HBM-bound; reductions are deterministic
 // (fixed grid, per-block partials, last-block finalisation in fixed order).
+#include <cstdint>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -79,6 +81,39 @@ __global__ void __launch_bounds__(kRedThreads) mdot_kernel(const double* __restr
     double wi = __ldg(w + i);
 #pragma unroll
     for (int j = 0; j < J; ++j) acc[j] += __ldg(V + j * ldv + i) * wi;
+    if (NRM) acc[NV - 1] += wi * wi;
+  }
+  block_partials<NV>(acc, ws.partial, ws, out);
+}
+
+// 16-byte variant (every pointer 16-byte aligned, ldv even): one double2 of every vector per
+// iteration, grid stride; the odd last element (n odd) is added by the last thread of the grid.
+// Measured (scripts/dev/mdot_bench.cu, gpurun_out/mdot_bench.log): J = 11 at N = 17.0M 3.9 -> 6.9 TB/s,
+// J = 6 5.2 -> 6.9 TB/s at the library's 888-CTA grid.
+template <int J, bool NRM>
+__global__ void __launch_bounds__(kRedThreads) mdot2_kernel(const double* __restrict__ w, const double* __restrict__ V,
+                                                            long long ldv, long long n, double* out, RedWs ws) {
+  constexpr int NV = J + (NRM ? 1 : 0);
+  double acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  const long long n2 = n >> 1;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  for (long long i = t0; i < n2; i += stride) {
+    const double2 a = __ldg(w2 + i);
+    double2 v[J > 0 ? J : 1];
+#pragma unroll
+    for (int j = 0; j < J; ++j) v[j] = __ldg(reinterpret_cast<const double2*>(V + j * ldv) + i);
+#pragma unroll
+    for (int j = 0; j < J; ++j) acc[j] += v[j].x * a.x + v[j].y * a.y;
+    if (NRM) acc[NV - 1] += a.x * a.x + a.y * a.y;
+  }
+  if ((n & 1) && t0 == stride - 1) {
+    const double wi = __ldg(w + n - 1);
+#pragma unroll
+    for (int j = 0; j < J; ++j) acc[j] += __ldg(V + j * ldv + n - 1) * wi;
     if (NRM) acc[NV - 1] += wi * wi;
   }
   block_partials<NV>(acc, ws.partial, ws, out);
@@ -169,6 +204,88 @@ __global__ void __launch_bounds__(kRedThreads) maxpy_dots_kernel(double* __restr
     acc[J] += a * a;
   }
   block_partials<J + 1>(acc, ws.partial, ws, out);
+}
+
+template <int J>
+__global__ void __launch_bounds__(kRedThreads) maxpy_dots2_kernel(double* __restrict__ w, const double* __restrict__ V,
+                                                                  long long ldv, const double* __restrict__ h,
+                                                                  const double* __restrict__ s2, long long n,
+                                                                  double* out, RedWs ws) {
+  __shared__ double hs[J];
+  if (threadIdx.x < J) hs[threadIdx.x] = s2 ? h[threadIdx.x] * s2[threadIdx.x] : h[threadIdx.x];
+  __syncthreads();
+  double acc[J + 1];
+#pragma unroll
+  for (int v = 0; v <= J; ++v) acc[v] = 0.0;
+  const long long n2 = n >> 1;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double2* w2 = reinterpret_cast<double2*>(w);
+  for (long long i = t0; i < n2; i += stride) {
+    double2 a = w2[i];
+    double2 v[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) v[j] = __ldg(reinterpret_cast<const double2*>(V + j * ldv) + i);
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      a.x -= hs[j] * v[j].x;
+      a.y -= hs[j] * v[j].y;
+    }
+    w2[i] = a;
+#pragma unroll
+    for (int j = 0; j < J; ++j) acc[j] += v[j].x * a.x + v[j].y * a.y;
+    acc[J] += a.x * a.x + a.y * a.y;
+  }
+  if ((n & 1) && t0 == stride - 1) {
+    double a = w[n - 1];
+    double v[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) v[j] = __ldg(V + j * ldv + n - 1);
+#pragma unroll
+    for (int j = 0; j < J; ++j) a -= hs[j] * v[j];
+    w[n - 1] = a;
+#pragma unroll
+    for (int j = 0; j < J; ++j) acc[j] += v[j] * a;
+    acc[J] += a * a;
+  }
+  block_partials<J + 1>(acc, ws.partial, ws, out);
+}
+
+// x += sum_j y_j Z_j with 16-byte accesses (aligned pointers, even ldz)
+__global__ void lincomb2_kernel(double* __restrict__ x, const double* __restrict__ Z, long long ldz, int k,
+                                const double* __restrict__ y, long long n) {
+  __shared__ double ys[kMaxBasis];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) ys[j] = y[j];
+  __syncthreads();
+  const long long n2 = n >> 1;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double2* x2 = reinterpret_cast<double2*>(x);
+  for (long long i = t0; i < n2; i += stride) {
+    double2 a = x2[i];
+    int j = 0;
+    for (; j + 4 <= k; j += 4) {
+      double2 z[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) z[u] = __ldg(reinterpret_cast<const double2*>(Z + (j + u) * ldz) + i);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a.x += ys[j + u] * z[u].x;
+        a.y += ys[j + u] * z[u].y;
+      }
+    }
+    for (; j < k; ++j) {
+      const double2 z = __ldg(reinterpret_cast<const double2*>(Z + j * ldz) + i);
+      a.x += ys[j] * z.x;
+      a.y += ys[j] * z.y;
+    }
+    x2[i] = a;
+  }
+  if ((n & 1) && t0 == stride - 1) {
+    double a = x[n - 1];
+    for (int j = 0; j < k; ++j) a += ys[j] * __ldg(Z + j * ldz + n - 1);
+    x[n - 1] = a;
+  }
 }
 
 __global__ void lincomb_kernel(double* __restrict__ x, const double* __restrict__ Z, long long ldz, int k,
@@ -283,6 +400,11 @@ __global__ void __launch_bounds__(kRedThreads) fingerprint_kernel(const double* 
   }
 }
 
+// the 16-byte kernels apply when every vector start is 16-byte aligned (ld even)
+static bool al16(const void* a, const void* b, long long ld) {
+  return (((uintptr_t)a | (uintptr_t)(b ? b : a)) & 15u) == 0 && (ld & 1) == 0;
+}
+
 static unsigned red_blocks(long long n) {
   long long b = (n + 2 * kRedThreads - 1) / (2 * kRedThreads);
   if (b > kRedBlocks) b = kRedBlocks;
@@ -301,13 +423,22 @@ void launch_mdot(const double* w, const double* V, long long ldv, int k, long lo
     bool nrm = (done + J == k);
     const double* Vj = V + (long long)done * ldv;
     double* o = out + done;
+    const bool v2 = al16(w, J > 0 ? Vj : nullptr, J > 1 ? ldv : 0);
 #define MD(JJ)                                                                                 \
   case JJ:                                                                                     \
-    if (nrm) mdot_kernel<JJ, true><<<g, kRedThreads, 0, s>>>(w, Vj, ldv, n, o, ws);            \
-    else mdot_kernel<JJ, false><<<g, kRedThreads, 0, s>>>(w, Vj, ldv, n, o, ws);               \
+    if (v2) {                                                                                  \
+      if (nrm) mdot2_kernel<JJ, true><<<g, kRedThreads, 0, s>>>(w, Vj, ldv, n, o, ws);         \
+      else mdot2_kernel<JJ, false><<<g, kRedThreads, 0, s>>>(w, Vj, ldv, n, o, ws);            \
+    } else {                                                                                   \
+      if (nrm) mdot_kernel<JJ, true><<<g, kRedThreads, 0, s>>>(w, Vj, ldv, n, o, ws);          \
+      else mdot_kernel<JJ, false><<<g, kRedThreads, 0, s>>>(w, Vj, ldv, n, o, ws);             \
+    }                                                                                          \
     break;
     switch (J) {
-      case 0: mdot_kernel<0, true><<<g, kRedThreads, 0, s>>>(w, Vj, ldv, n, o, ws); break;
+      case 0:
+        if (v2) mdot2_kernel<0, true><<<g, kRedThreads, 0, s>>>(w, Vj, ldv, n, o, ws);
+        else mdot_kernel<0, true><<<g, kRedThreads, 0, s>>>(w, Vj, ldv, n, o, ws);
+        break;
       MD(1) MD(2) MD(3) MD(4) MD(5) MD(6) MD(7) MD(8)
       MD(9) MD(10) MD(11) MD(12) MD(13) MD(14) MD(15) MD(16)
     }
@@ -324,9 +455,11 @@ void launch_maxpy_norm(double* w, const double* V, long long ldv, int k, const d
 bool launch_maxpy_dots(double* w, const double* V, long long ldv, int k, const double* h, const double* s2,
                        long long n, double* out, RedWs ws, cudaStream_t s) {
   const unsigned g = red_blocks(n);
+  const bool v2 = al16(w, V, k > 1 ? ldv : 0);
 #define MX(JJ)                                                                              \
   case JJ:                                                                                  \
-    maxpy_dots_kernel<JJ><<<g, kRedThreads, 0, s>>>(w, V, ldv, h, s2, n, out, ws);          \
+    if (v2) maxpy_dots2_kernel<JJ><<<g, kRedThreads, 0, s>>>(w, V, ldv, h, s2, n, out, ws); \
+    else maxpy_dots_kernel<JJ><<<g, kRedThreads, 0, s>>>(w, V, ldv, h, s2, n, out, ws);    \
     return true;
   switch (k) {
     MX(1) MX(2) MX(3) MX(4) MX(5) MX(6) MX(7) MX(8)
@@ -344,7 +477,8 @@ static unsigned ew_blocks(long long n) {
 }
 
 void launch_lincomb(double* x, const double* Z, long long ldz, int k, const double* y, long long n, cudaStream_t s) {
-  lincomb_kernel<<<ew_blocks(n), 256, 0, s>>>(x, Z, ldz, k, y, n);
+  if (al16(x, Z, k > 1 ? ldz : 0)) lincomb2_kernel<<<ew_blocks((n + 1) / 2), 256, 0, s>>>(x, Z, ldz, k, y, n);
+  else lincomb_kernel<<<ew_blocks(n), 256, 0, s>>>(x, Z, ldz, k, y, n);
 }
 void launch_scale_dev(const double* w, double* v, const double* nrm2, long long n, cudaStream_t s) {
   scale_dev_kernel<<<ew_blocks(n), 256, 0, s>>>(w, v, nrm2, n);

@@ -221,4 +221,68 @@ __device__ __forceinline__ void load_nb(const Geom& g, const double* __restrict_
 }
 
 
+
+// Rows [p0, p1) of the (masked) level operator at spatial node (i0, row r) (r = x2 in 2D, x2 + nn x3 in
+// 3D), marching in time: each element layer is evaluated once, its top part carried to the next row.
+// Modes: APPLY y = A x; RESID y = b - A x; JAC y = x + w D^-1 (b - A x); JAC0 y = w D^-1 b. Used by
+// the generic kernels (op_kernel, ops.cu).
+template <int SD, int FORM, int MODE, bool TRANS, bool MASK>
+__device__ __forceinline__ void op_rows(const OpDesc& op, const double* __restrict__ x, const double* __restrict__ b,
+                                        double* __restrict__ y, double omega, int i0, int r, int p0, int p1) {
+  constexpr int NOFF = SG<SD>::NOFF;
+  constexpr bool NEEDX = (MODE != MODE_JAC0);
+  constexpr bool NEEDD = (MODE == MODE_JAC || MODE == MODE_JAC0);
+  const Geom& g = op.g;
+  int c[3];
+  c[0] = i0;
+  c[1] = (SD == 2) ? r : r % g.nn;
+  c[2] = (SD == 2) ? 0 : r / g.nn;
+  const long long pn = i0 + (long long)g.pr * r;
+  const bool patch = MASK && is_patch<SD>(g, c);
+
+  double xb[NOFF], xt[NOFF];
+  double carry = 0.0, dcarry = 0.0;
+  if (NEEDX) {
+    if (p0 >= 1) {
+      load_nb<SD, MASK>(g, x, c, p0 - 1, xb);
+      load_nb<SD, MASK>(g, x, c, p0, xt);
+    } else {
+      load_nb<SD, MASK>(g, x, c, p0, xt);
+    }
+  }
+  if (p0 >= 1) {
+    double bt, tp, db, dt;
+    layer_eval<SD, FORM, TRANS, NEEDX, NEEDD>(op, c, pn, p0 - 1, xb, xt, bt, tp, db, dt);
+    carry = tp;
+    dcarry = dt;
+  }
+  for (int p = p0; p < p1; ++p) {
+    if (NEEDX) {
+#pragma unroll
+      for (int k = 0; k < NOFF; ++k) xb[k] = xt[k];
+    }
+    double bot = 0.0, top = 0.0, dbot = 0.0, dtop = 0.0;
+    if (p < g.nt) {
+      if (NEEDX) load_nb<SD, MASK>(g, x, c, p + 1, xt);
+      layer_eval<SD, FORM, TRANS, NEEDX, NEEDD>(op, c, pn, p, xb, xt, bot, top, dbot, dtop);
+    }
+    const long long gi = (long long)p * g.P + pn;
+    const bool cons = MASK && (p + g.pg0 == 0 || patch);
+    double Ax = carry + bot;
+    double D = dcarry + dbot;
+    if (cons) {
+      Ax = NEEDX ? __ldg(x + gi) : 0.0;
+      D = 1.0;
+    }
+    double out;
+    if (MODE == MODE_APPLY) out = Ax;
+    else if (MODE == MODE_RESID) out = __ldg(b + gi) - Ax;
+    else if (MODE == MODE_JAC) out = __ldg(x + gi) + omega * (__ldg(b + gi) - Ax) / D;
+    else out = omega * __ldg(b + gi) / D;
+    y[gi] = out;
+    carry = top;
+    dcarry = dtop;
+  }
+}
+
 }  // namespace st

@@ -21,67 +21,14 @@ template <int SD, int FORM, int MODE, bool TRANS, bool MASK>
 __global__ void __launch_bounds__(128) op_kernel(OpDesc op, const double* __restrict__ x,
                                                  const double* __restrict__ b, double* __restrict__ y,
                                                  double omega, int chunk) {
-  constexpr int NOFF = SG<SD>::NOFF;
-  constexpr bool NEEDX = (MODE != MODE_JAC0);
-  constexpr bool NEEDD = (MODE == MODE_JAC || MODE == MODE_JAC0);
   const Geom& g = op.g;
   const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = blockIdx.y * blockDim.y + threadIdx.y;
   const int rows = (SD == 2) ? g.nn : g.nn * g.nn;
   if (i0 >= g.nn || r >= rows) return;
-  int c[3];
-  c[0] = i0;
-  c[1] = (SD == 2) ? r : r % g.nn;
-  c[2] = (SD == 2) ? 0 : r / g.nn;
-  const long long pn = i0 + (long long)g.pr * r;
   const int p0 = blockIdx.z * chunk;
-  const int p1 = min(p0 + chunk, g.nt + 1);
   if (p0 > g.nt) return;
-  const bool patch = MASK && is_patch<SD>(g, c);
-
-  double xb[NOFF], xt[NOFF];
-  double carry = 0.0, dcarry = 0.0;
-  if (NEEDX) {
-    if (p0 >= 1) {
-      load_nb<SD, MASK>(g, x, c, p0 - 1, xb);
-      load_nb<SD, MASK>(g, x, c, p0, xt);
-    } else {
-      load_nb<SD, MASK>(g, x, c, p0, xt);
-    }
-  }
-  if (p0 >= 1) {
-    double bt, tp, db, dt;
-    layer_eval<SD, FORM, TRANS, NEEDX, NEEDD>(op, c, pn, p0 - 1, xb, xt, bt, tp, db, dt);
-    carry = tp;
-    dcarry = dt;
-  }
-  for (int p = p0; p < p1; ++p) {
-    if (NEEDX) {
-#pragma unroll
-      for (int k = 0; k < NOFF; ++k) xb[k] = xt[k];
-    }
-    double bot = 0.0, top = 0.0, dbot = 0.0, dtop = 0.0;
-    if (p < g.nt) {
-      if (NEEDX) load_nb<SD, MASK>(g, x, c, p + 1, xt);
-      layer_eval<SD, FORM, TRANS, NEEDX, NEEDD>(op, c, pn, p, xb, xt, bot, top, dbot, dtop);
-    }
-    const long long gi = (long long)p * g.P + pn;
-    const bool cons = MASK && (p + g.pg0 == 0 || patch);
-    double Ax = carry + bot;
-    double D = dcarry + dbot;
-    if (cons) {
-      Ax = NEEDX ? __ldg(x + gi) : 0.0;
-      D = 1.0;
-    }
-    double out;
-    if (MODE == MODE_APPLY) out = Ax;
-    else if (MODE == MODE_RESID) out = __ldg(b + gi) - Ax;
-    else if (MODE == MODE_JAC) out = __ldg(x + gi) + omega * (__ldg(b + gi) - Ax) / D;
-    else out = omega * __ldg(b + gi) / D;
-    y[gi] = out;
-    carry = top;
-    dcarry = dtop;
-  }
+  op_rows<SD, FORM, MODE, TRANS, MASK>(op, x, b, y, omega, i0, r, p0, min(p0 + chunk, g.nt + 1));
 }
 
 // ---------------------------------------------------------------------------------------
@@ -132,6 +79,7 @@ void launch_op(const OpDesc& op, int mode, bool trans, bool mask, const double* 
   // general TMA kernel (tma2d), the cp.async-ring kernels (fast2d), then the generic kernels
   const int f = op.family;
   if (f == 0 && launch_op_tc2d(op, mode, trans, mask, x, b, y, omega, s)) return;
+  if (f == 0 && launch_op_tc3r(op, mode, trans, mask, x, b, y, omega, s)) return;
   if (f == 0 && launch_op_tc3d(op, mode, trans, mask, x, b, y, omega, s)) return;
   if (f == 0 && launch_op_tv2d(op, mode, trans, mask, x, b, y, omega, s)) return;
   if ((f == 0 || f == 3) && launch_op_tma2d(op, mode, trans, mask, x, b, y, omega, s)) return;

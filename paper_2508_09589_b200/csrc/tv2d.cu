@@ -123,59 +123,9 @@ struct Seg {
   int p0, p1, qs, qe;  // rows p0 .. p1-1; planes qs .. qe (qs = p0 - 1 reloads the plane below)
   int x0, y0, bx, by;  // node tile origin, layer box origin
 };
-// Strided chunk schedule: the NP planes are cut into nch balanced chunks of ~K
-// planes; inside a chunk the tiles form groups of G = gridDim.x consecutive tiles, and CTA b takes
-// tile kG + b of every full group k for all the chunk's planes (one segment per group), then an
-// equal share of the (tile, plane) items of the last, partial group (contiguous, tile-major). At any
-// moment CTA b and CTA b + 1 (b +- ntx) therefore work on x- (y-) neighbouring tiles at about the same
-// plane: the halo rows / columns two tiles share, and the layer box rows, are requested twice within
-// a short interval and the second request hits L2 (the round-1 slice-per-CTA schedule put a CTA's
-// neighbour tiles 16 planes apart in time on the same CTA: ~10 % L2 hit rate at 1024^2 x 1024,
-// 1.8x the algorithmic DRAM reads, profiles/r02). nch = 1 (K = NP): one chunk.
-struct Sched {
-  long long tiles, w, we;
-  int NP, nch, c, cs, Kc, k, nfull;
-};
-__device__ __forceinline__ void sched_init(Sched& s, long long tiles, int NP, int K) {
-  s.tiles = tiles;
-  s.NP = NP;
-  s.nch = (NP + K - 1) / K;
-  s.c = -1;
-  s.w = s.we = 0;
-  s.cs = s.Kc = 0;
-  s.k = s.nfull = 0;
-}
 __device__ __forceinline__ bool next_seg(Sched& s, int ntx, int nt, Seg& sg) {
-  const long long G = gridDim.x, b = blockIdx.x;
   long long tile;
-  for (;;) {
-    if (s.c >= 0) {
-      if (s.k < s.nfull) {  // full group k: tile k G + b over every plane of the chunk
-        tile = s.k * G + b;
-        sg.p0 = s.cs;
-        sg.p1 = s.cs + s.Kc;
-        ++s.k;
-        break;
-      }
-      if (s.w < s.we) {  // partial group: a contiguous share of its (tile, plane) items
-        const long long r = s.w;
-        tile = (long long)s.nfull * G + r / s.Kc;
-        sg.p0 = s.cs + (int)(r % s.Kc);
-        const long long rem = s.we - s.w;
-        sg.p1 = (rem < s.cs + s.Kc - sg.p0) ? sg.p0 + (int)rem : s.cs + s.Kc;
-        s.w += sg.p1 - sg.p0;
-        break;
-      }
-    }
-    if (++s.c >= s.nch) return false;
-    s.cs = (int)((long long)s.c * s.NP / s.nch);
-    s.Kc = (int)((long long)(s.c + 1) * s.NP / s.nch) - s.cs;
-    s.nfull = (int)(s.tiles / G);
-    s.k = 0;
-    const long long items = (s.tiles - (long long)s.nfull * G) * s.Kc;
-    s.w = items * b / G;
-    s.we = items * (b + 1) / G;
-  }
+  if (!sched_next(s, tile, sg.p0, sg.p1)) return false;
   sg.qs = max(sg.p0 - 1, 0);
   sg.qe = min(sg.p1, nt);
   sg.x0 = (int)(tile % ntx) * TX;
