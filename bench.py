@@ -141,6 +141,8 @@ def parse():
     ap.add_argument("--nu-fine-nodes", type=int, default=-1,
                     help="coarse levels with at least this many nodes use the fine-level sweep counts (default: the "
                          "workload's)")
+    ap.add_argument("--fuse-prolong", type=int, default=-1,
+                    help="prolongation fused into the first post-sweep (1) or separate kernels (0); default: the library's")
     ap.add_argument("--timestepping", action="store_true",
                     help="also time the GPU time-stepping baseline (st_timestep, backward Euler with nt steps and a "
                          "spatial-MG PCG per step; time-constant workloads) against the space-time forward solve")
@@ -247,6 +249,8 @@ def solver_opts_for(wl, args):
         o["coarse_max_nodes"] = args.coarse_max_nodes
     if args.nu_fine_nodes >= 0:
         o["nu_fine_nodes"] = args.nu_fine_nodes
+    if args.fuse_prolong >= 0:
+        o["fuse_prolong"] = args.fuse_prolong
     return o
 
 

@@ -57,6 +57,8 @@ struct Level {
   bool dense = false;
   double *A = nullptr, *Ainv = nullptr;
   int* info = nullptr;
+  int nf = 0;                                  // dense: free nodes (not pad, not constrained)
+  int *fidx = nullptr, *fpos = nullptr;        // dense: free stored indices [nf]; stored -> free position [N]
   // time slabs
   int ntg = 0;           // global element layers of the level
   bool dist = false;     // distributed in time slabs (else replicated on every rank)
@@ -509,9 +511,36 @@ void allocate(st_ctx* c) {
     dzalloc(&c->cgs, (size_t)gm_y_offset(k) + k + 32 + kMaxBasis + 64);
   } else {
     Lc.dense = true;
-    dalloc(&Lc.A, (size_t)Lc.g.N * Lc.g.N);
-    dalloc(&Lc.Ainv, (size_t)Lc.g.N * Lc.g.N);
+    // the free nodes of the coarsest level (host replica of pdecode / is_cons; the level is replicated:
+    // plane 0 is the initial-condition plane): the dense inverse excludes pad entries and the identity
+    // rows of constrained nodes (config 4: 248 of 600 stored entries, configs 2 / 3: 96 of 200)
+    const Geom& g = Lc.g;
+    std::vector<int> fidx, fpos((size_t)g.N, -1);
+    for (long long e = 0; e < g.N; ++e) {
+      const int p = (int)(e / g.P);
+      const long long pn = e % g.P;
+      const int c0 = (int)(pn % g.pr);
+      const long long t = pn / g.pr;
+      const int c1 = (int)(t % g.nn), c2 = c->sd == 3 ? (int)(t / g.nn) : 0;
+      if (c0 >= g.nn || p + g.pg0 == 0) continue;
+      bool patch;
+      if (g.walls) {
+        patch = c0 == 0 || c0 == g.n || c1 == 0 || c1 == g.n || (c->sd == 3 && (c2 == 0 || c2 == g.n));
+      } else {
+        patch = c0 == 0 && c1 >= g.plo && c1 <= g.phi && (c->sd == 2 || (c2 >= g.plo && c2 <= g.phi));
+      }
+      if (patch) continue;
+      fpos[(size_t)e] = (int)fidx.size();
+      fidx.push_back((int)e);
+    }
+    Lc.nf = (int)fidx.size();
+    dalloc(&Lc.A, (size_t)g.N * g.N);
+    dalloc(&Lc.Ainv, (size_t)std::max(Lc.nf, 1) * std::max(Lc.nf, 1));
     dalloc(&Lc.info, 1);
+    dalloc(&Lc.fidx, std::max<size_t>(fidx.size(), 1));
+    dalloc(&Lc.fpos, (size_t)g.N);
+    if (!fidx.empty()) CK(cudaMemcpy(Lc.fidx, fidx.data(), fidx.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(Lc.fpos, fpos.data(), fpos.size() * sizeof(int), cudaMemcpyHostToDevice));
   }
   CK(cudaEventCreate(&c->e0));
   CK(cudaEventCreate(&c->e1));
@@ -732,7 +761,8 @@ void build_ops(st_ctx* c) {
   if (Lc.dense) {
     CK(cudaMemsetAsync(Lc.A, 0, (size_t)Nc * Nc * sizeof(double), c->stream));
     launch_dense_assemble(Lc.op, Lc.A, c->stream);
-    launch_dense_invert(Lc.A, Lc.Ainv, (int)Nc, Lc.info, c->stream);
+    if (Lc.nf > 0) launch_dense_invert(Lc.A, Nc, Lc.fidx, Lc.nf, Lc.Ainv, Lc.info, c->stream);
+    else CK(cudaMemsetAsync(Lc.info, 0, sizeof(int), c->stream));
     L(c, 2);
     check_launch();
   }
@@ -896,7 +926,7 @@ void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_gr
   if (!rl) throw StErr{ST_E_INVALID_ARG, "internal: level-0 V-cycle without a residual scratch vector"};
   if (!in_graph && vcycle_graph(c, l, trans, b, x)) return;
   if (Lv.dense) {
-    launch_dense_solve(Lv.Ainv, (int)Lv.g.N, trans, b, x, c->stream);
+    launch_dense_solve(Lv.Ainv, Lv.nf, Lv.fidx, Lv.fpos, Lv.g.N, trans, b, x, c->stream);
     L(c);
     return;
   }
@@ -949,11 +979,14 @@ void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_gr
   // prolongation + correction, fused into the first post-sweep where the level kernel can read
   // x + P e itself (tc2d, space-coarsened next level, one GPU; options fuse_prolong = 0: separate kernels)
   int s0 = 0;
-  // not on level 0: there the fused sweep (201 us) costs more than sweep + prolongation (90 + 45 us;
-  // profiles/r01/launches_c2_v42_summary.txt) — the correction pass weighs on an issue-bound kernel
-  if (l > 0 && npost > 0 && c->opt.fuse_prolong && Nx.kind == KIND_SPACE && c->comm.size <= 1 &&
+  // tc2d: not on level 0: there the fused sweep (201 us) costs more than sweep + prolongation (90 + 45 us;
+  // profiles/r01/launches_c2_v42_summary.txt) — the correction pass weighs on an issue-bound kernel;
+  // tv2d: the fine level of a space-time design (configs 3, 5)
+  const double om = Lv.omega > 0.0 ? Lv.omega : c->opt.omega;
+  if (npost > 0 && c->opt.fuse_prolong && Nx.kind == KIND_SPACE && c->comm.size <= 1 &&
       c->opt.kernel_family == ST_KERNELS_TMA &&
-      launch_op_tc2d_pro(Lv.op, Nx.g, trans, cur, Nx.x, b, oth, Lv.omega > 0.0 ? Lv.omega : c->opt.omega, c->stream)) {
+      ((l > 0 && launch_op_tc2d_pro(Lv.op, Nx.g, trans, cur, Nx.x, b, oth, om, c->stream)) ||
+       (l == 0 && launch_op_tv2d_pro(Lv.op, Nx.g, trans, cur, Nx.x, b, oth, om, c->stream)))) {
     L(c);
     std::swap(cur, oth);
     s0 = 1;
@@ -1208,7 +1241,7 @@ void free_ctx(st_ctx* c) {
     if (Lv.st_owned && Lv.st) cudaFree(Lv.st);
     cudaFree(Lv.mid);
     cudaFree(Lv.gv);
-    cudaFree(Lv.A); cudaFree(Lv.Ainv); cudaFree(Lv.info);
+    cudaFree(Lv.A); cudaFree(Lv.Ainv); cudaFree(Lv.info); cudaFree(Lv.fidx); cudaFree(Lv.fpos);
   }
   for (double* p : c->vallocs) cudaFree(p);
   cudaFree(c->ws.partial); cudaFree(c->ws.counter);

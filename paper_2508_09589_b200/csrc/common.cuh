@@ -211,6 +211,33 @@ __device__ __forceinline__ bool sched_next(Sched& s, long long& tile, int& p0, i
   }
 }
 
+// Programmatic dependent launch (PDL) of the V-cycle's level kernels: launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, a kernel's CTAs may start (barrier init, smem
+// carve-up, tensor-map use) while the previous kernel in the stream drains; pdl_wait() — before the
+// kernel's first global-memory access — blocks until that kernel has completed and its writes are
+// visible (a no-op for a plain launch). On the latency-bound coarse levels this hides part of the
+// launch gap between consecutive kernels of the V-cycle's CUDA graph.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+#ifdef ST_NO_PDL
+  cfg.numAttrs = 0;  // A/B builds: plain stream-ordered launches
+#else
+  cfg.numAttrs = 1;
+#endif
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // planes per time chunk of a persistent stencil kernel's work list: the option when forced
 // (op.chunk > 0), one chunk (tile-major order) when chunking is off (op.chunk < 0), else the
 // kernel's automatic choice `auto_k` (only tv2d chunks automatically)

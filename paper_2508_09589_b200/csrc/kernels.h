@@ -30,6 +30,9 @@ bool launch_op_tc3r(const OpDesc& op, int mode, bool trans, bool mask, const dou
 // tv2d.cu: fine level of a space-time design with uniform capacity (configs 1, 3, 5), masked modes
 bool launch_op_tv2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                     double omega, cudaStream_t s);
+// fine-level damped-Jacobi sweep from x + P e, e the correction of a space-coarsened next level (one GPU)
+bool launch_op_tv2d_pro(const OpDesc& op, const Geom& gc, bool trans, const double* x, const double* e,
+                        const double* b, double* y, double omega, cudaStream_t s);
 void launch_rap_space(const OpDesc& fop, const Geom& gc, int nl, int ns, double* out, cudaStream_t s);
 void launch_rap_time(const OpDesc& fop, int nlc, double* out, cudaStream_t s);
 void launch_rho_to_mk(const OpDesc& fop, int tau, double* out, cudaStream_t s);
@@ -86,8 +89,13 @@ void launch_set_bc_values(const Geom& g, double T0, double* x, cudaStream_t s); 
 void launch_rhs_combine(const Geom& g, const double* f, const double* KxD, double T0, double* b, cudaStream_t s);
 void launch_xd(const Geom& g, double T0, double* x, cudaStream_t s);
 void launch_sensitivity(const OpDesc& op, const double* T, const double* lam, double* dJ, cudaStream_t s);
-void launch_dense_invert(double* A, double* Ainv, int n, int* info, cudaStream_t s);
-void launch_dense_solve(const double* Ainv, int n, bool trans, const double* b, double* x, cudaStream_t s);
+// dense coarsest level on its nf free nodes (fidx: free stored indices, fpos: stored index -> free
+// position or -1): Ainv = (A[fidx][fidx])^-1 (A: the assembled N x N operator); x = A^-1 b on the free
+// nodes, x = b elsewhere
+void launch_dense_invert(const double* A, long long N, const int* fidx, int nf, double* Ainv, int* info,
+                         cudaStream_t s);
+void launch_dense_solve(const double* Ainv, int nf, const int* fidx, const int* fpos, long long N, bool trans,
+                        const double* b, double* x, cudaStream_t s);
 
 // design.cu — config-5 design update (density filter, OC)
 void launch_filter(int sd, int n, int nl, int tdir, int lo_ok, int hi_ok, double r, const double* ghosted, double* out,

@@ -289,68 +289,15 @@ void launch_sensitivity(const OpDesc& op, const double* T, const double* lam, do
 }
 
 // ---------------------------------------------------------------------------------------
-// Dense coarsest level: Gauss-Jordan inverse with partial pivoting in one CTA (the level
-// has <= coarse_max_nodes nodes), then x = A^-1 b per V-cycle.
-__global__ void __launch_bounds__(1024) dense_invert_kernel(double* __restrict__ W, double* __restrict__ Ainv, int n,
-                                                            int* info) {
-  extern __shared__ double fac[];
-  __shared__ double bv[32];
-  __shared__ int bi[32];
-  const int tid = threadIdx.x, nth = blockDim.x;
-  for (long long i = tid; i < (long long)n * n; i += nth) Ainv[i] = ((i / n) == (i % n)) ? 1.0 : 0.0;
-  if (tid == 0) *info = 0;
-  __syncthreads();
-  for (int k = 0; k < n; ++k) {
-    // pivot search
-    double best = -1.0;
-    int bidx = k;
-    for (int i = k + tid; i < n; i += nth) {
-      double v = fabs(W[(long long)i * n + k]);
-      if (v > best) { best = v; bidx = i; }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      double ov = __shfl_down_sync(0xffffffffu, best, o);
-      int oi = __shfl_down_sync(0xffffffffu, bidx, o);
-      if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
-    }
-    if ((tid & 31) == 0) { bv[tid >> 5] = best; bi[tid >> 5] = bidx; }
-    __syncthreads();
-    if (tid == 0) {
-      double bb = bv[0];
-      int ii = bi[0];
-      for (int w = 1; w < nth / 32; ++w)
-        if (bv[w] > bb || (bv[w] == bb && bi[w] < ii)) { bb = bv[w]; ii = bi[w]; }
-      bi[0] = ii;
-      if (!(bb > 0.0)) *info = k + 1;
-    }
-    __syncthreads();
-    const int piv = bi[0];
-    if (piv != k) {
-      for (int j = tid; j < n; j += nth) {
-        double t1 = W[(long long)k * n + j]; W[(long long)k * n + j] = W[(long long)piv * n + j]; W[(long long)piv * n + j] = t1;
-        double t2 = Ainv[(long long)k * n + j]; Ainv[(long long)k * n + j] = Ainv[(long long)piv * n + j]; Ainv[(long long)piv * n + j] = t2;
-      }
-    }
-    __syncthreads();
-    const double d = W[(long long)k * n + k];
-    const double inv = (d != 0.0) ? 1.0 / d : 0.0;
-    __syncthreads();
-    for (int j = tid; j < n; j += nth) {
-      W[(long long)k * n + j] *= inv;
-      Ainv[(long long)k * n + j] *= inv;
-    }
-    for (int i = tid; i < n; i += nth) fac[i] = (i == k) ? 0.0 : W[(long long)i * n + k];
-    __syncthreads();
-    for (long long e = tid; e < (long long)n * n; e += nth) {
-      int i = (int)(e / n), j = (int)(e % n);
-      double f = fac[i];
-      if (f != 0.0) {
-        W[e] -= f * W[(long long)k * n + j];
-        Ainv[e] -= f * Ainv[(long long)k * n + j];
-      }
-    }
-    __syncthreads();
-  }
+// Dense coarsest level: the assembled eliminated operator restricted to the FREE nodes
+// (no pad entries, no constrained identity rows: those unknowns are x_c = b_c), inverted once per design
+// by Gauss-Jordan with partial pivoting in one CTA, then x = A^-1 b per V-cycle.
+__global__ void dense_gather_kernel(const double* __restrict__ A, long long N, const int* __restrict__ fidx, int nf,
+                                    double* __restrict__ Af) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)nf * nf) return;
+  const int i = (int)(e / nf), j = (int)(e % nf);
+  Af[e] = A[(long long)fidx[i] * N + fidx[j]];
 }
 
 // In-place Gauss-Jordan inversion with partial pivoting, the whole matrix in shared memory (n <= 160):
@@ -358,17 +305,23 @@ __global__ void __launch_bounds__(1024) dense_invert_kernel(double* __restrict__
 // a_kj = r_j, and for i != k: a_ik = 0, a_ij -= c_i r_j. The row swaps are undone at the end as
 // column swaps in reverse order. Same result as the augmented [A | I] elimination up to rounding,
 // with every access in shared memory (~1 us per pivot instead of ~11 us through L2).
+// SMEM = false (n <= 4096): the same steps in place on the global matrix (L2-resident), r and c in shared
+// memory.
 constexpr int kDenseSmemMax = 160;
-__global__ void __launch_bounds__(1024) dense_invert_smem_kernel(const double* __restrict__ A, double* __restrict__ Ainv,
-                                                                 int n, int* info) {
-  extern __shared__ double a[];  // [n][n], then r[n], c[n]
-  double* r = a + n * n;
+constexpr int kDenseMax = 4096;
+template <bool SMEM>
+__global__ void __launch_bounds__(1024) dense_invert_kernel(const double* __restrict__ A, double* __restrict__ Ainv,
+                                                            int n, int* info) {
+  extern __shared__ double dsm[];  // SMEM: [n][n], then r[n], c[n]; else r[n], c[n]
+  double* a = SMEM ? dsm : Ainv;
+  double* r = SMEM ? dsm + n * n : dsm;
   double* c = r + n;
-  __shared__ int perm[kDenseSmemMax];
+  __shared__ int perm[kDenseMax];
   __shared__ double bv[32];
   __shared__ int bi[32];
   const int tid = threadIdx.x, nth = blockDim.x;
-  for (int e = tid; e < n * n; e += nth) a[e] = A[e];
+  if (SMEM || A != Ainv)
+    for (int e = tid; e < n * n; e += nth) a[e] = A[e];
   if (tid == 0) *info = 0;
   __syncthreads();
   for (int k = 0; k < n; ++k) {
@@ -429,45 +382,63 @@ __global__ void __launch_bounds__(1024) dense_invert_smem_kernel(const double* _
       }
     __syncthreads();
   }
-  for (int e = tid; e < n * n; e += nth) Ainv[e] = a[e];
+  if (SMEM)
+    for (int e = tid; e < n * n; e += nth) Ainv[e] = a[e];
 }
 
-void launch_dense_invert(double* A, double* Ainv, int n, int* info, cudaStream_t s) {
-  if (n <= kDenseSmemMax) {
-    const size_t bytes = (size_t)(n * n + 2 * n) * sizeof(double);
+// A: the assembled N x N operator; fidx: the nf free stored indices; Ainv: nf x nf inverse (out)
+void launch_dense_invert(const double* A, long long N, const int* fidx, int nf, double* Ainv, int* info,
+                         cudaStream_t s) {
+  dense_gather_kernel<<<(unsigned)(((long long)nf * nf + 255) / 256), 256, 0, s>>>(A, N, fidx, nf, Ainv);
+  if (nf <= kDenseSmemMax) {
+    const size_t bytes = (size_t)(nf * nf + 2 * nf) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(dense_invert_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(dense_invert_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)((kDenseSmemMax * kDenseSmemMax + 2 * kDenseSmemMax) * sizeof(double)));
       attr = true;
     }
-    dense_invert_smem_kernel<<<1, 1024, bytes, s>>>(A, Ainv, n, info);
+    dense_invert_kernel<true><<<1, 1024, bytes, s>>>(Ainv, Ainv, nf, info);
     return;
   }
-  // augmented form through L2; the pivot column factors in shared memory (n <= kDenseMaxNodes = 4096:
-  // 32 KB, inside the default 48 KB; build_hierarchy rejects larger dense coarsest levels)
-  dense_invert_kernel<<<1, 1024, n * sizeof(double), s>>>(A, Ainv, n, info);
+  // in place through L2 (nf <= 4096: r, c 64 KB of dynamic shared memory)
+  static bool attr2 = false;
+  if (!attr2) {
+    cudaFuncSetAttribute(dense_invert_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(2 * kDenseMax * sizeof(double)));
+    attr2 = true;
+  }
+  dense_invert_kernel<false><<<1, 1024, 2 * nf * sizeof(double), s>>>(Ainv, Ainv, nf, info);
 }
 
-__global__ void dense_solve_kernel(const double* __restrict__ Ainv, int n, int trans, const double* __restrict__ b,
+// x = A^-1 b on the free nodes (fpos[e] = free position of stored entry e, or -1), x_e = b_e elsewhere
+// (constrained identity rows; pad entries, zero in both). One warp per stored entry.
+__global__ void dense_solve_kernel(const double* __restrict__ Ainv, int nf, const int* __restrict__ fidx,
+                                   const int* __restrict__ fpos, long long N, int trans, const double* __restrict__ b,
                                    double* __restrict__ x) {
-  // one warp per output entry
-  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (warp >= n) return;
+  pdl_wait();
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= N) return;
+  const int i = fpos[warp];
+  if (i < 0) {
+    if (lane == 0) x[warp] = b[warp];
+    return;
+  }
   double acc = 0.0;
   if (!trans)
-    for (int j = lane; j < n; j += 32) acc += Ainv[(long long)warp * n + j] * b[j];
+    for (int j = lane; j < nf; j += 32) acc += Ainv[(long long)i * nf + j] * b[fidx[j]];
   else
-    for (int j = lane; j < n; j += 32) acc += Ainv[(long long)j * n + warp] * b[j];
+    for (int j = lane; j < nf; j += 32) acc += Ainv[(long long)j * nf + i] * b[fidx[j]];
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
   if (lane == 0) x[warp] = acc;
 }
 
-void launch_dense_solve(const double* Ainv, int n, bool trans, const double* b, double* x, cudaStream_t s) {
-  int thr = 256;
-  unsigned grd = (unsigned)((n * 32 + thr - 1) / thr);
-  dense_solve_kernel<<<grd, thr, 0, s>>>(Ainv, n, trans ? 1 : 0, b, x);
+void launch_dense_solve(const double* Ainv, int nf, const int* fidx, const int* fpos, long long N, bool trans,
+                        const double* b, double* x, cudaStream_t s) {
+  const int thr = 256;
+  const unsigned grd = (unsigned)((N * 32 + thr - 1) / thr);
+  launch_pdl(dense_solve_kernel, dim3(grd), dim3(thr), 0, s, Ainv, nf, fidx, fpos, N, trans ? 1 : 0, b, x);
 }
 
 }  // namespace st

@@ -21,6 +21,7 @@ template <int SD, int FORM, int MODE, bool TRANS, bool MASK>
 __global__ void __launch_bounds__(128) op_kernel(OpDesc op, const double* __restrict__ x,
                                                  const double* __restrict__ b, double* __restrict__ y,
                                                  double omega, int chunk) {
+  pdl_wait();
   const Geom& g = op.g;
   const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = blockIdx.y * blockDim.y + threadIdx.y;
@@ -48,7 +49,7 @@ static void launch_t(const OpDesc& op, const double* x, const double* b, double*
   int rows = SD == 2 ? g.nn : g.nn * g.nn;
   int chunk = op.chunk > 0 ? std::min(op.chunk, g.nt + 1) : choose_chunk(g);
   dim3 grd((g.nn + 31) / 32, (rows + 3) / 4, (g.nt + 1 + chunk - 1) / chunk);
-  op_kernel<SD, FORM, MODE, TRANS, MASK><<<grd, blk, 0, s>>>(op, x, b, y, omega, chunk);
+  launch_pdl(op_kernel<SD, FORM, MODE, TRANS, MASK>, grd, blk, 0, s, op, x, b, y, omega, chunk);
 }
 
 template <int SD, int FORM>

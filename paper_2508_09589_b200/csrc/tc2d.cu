@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(NTH, CUNI ? ST_TC2D_MINB : 3)
     for (int k = 0; k < NB; ++k) mbar_init(&bar[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  pdl_wait();  // the previous kernel's writes (x, b, stencils) are visible from here on
   // spatial scales folded into the time factors (fine level: M = C dx^2/36 [..], K = 1/6 [..])
   const double sm = (SRC == 0) ? g.dx * g.dx * (1.0 / 36.0) * (CUNI ? op.m.Cins : 1.0) : (CUNI ? op.msc : 1.0);
   const double sk = (SRC == 0) ? (1.0 / 6.0) : 1.0;
@@ -397,7 +398,7 @@ void ltc(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, const d
   const long long ntx = (g.nn + TX - 1) / TX, nty = (g.nn + TY - 1) / TY;
   const long long wtot = ntx * nty * (g.nt + 1);
   const long long grid = persistent_grid(op, nsm, resident, wtot);
-  kern<<<(unsigned)grid, dim3(TX, TYT, 1), bytes, s>>>(mx, mb, me ? *me : mx, op, x, y, omega, wtot,
+  launch_pdl(kern, dim3((unsigned)grid), dim3(TX, TYT, 1), bytes, s, mx, mb, me ? *me : mx, op, x, y, omega, wtot,
                                                        chunk_planes(op, g.nt + 1, g.nt + 1), (int)ntx);
 }
 

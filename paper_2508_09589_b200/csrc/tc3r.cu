@@ -53,7 +53,8 @@ namespace t3r {
                      // two CTAs per SM at <= 144 registers)
 #endif
 constexpr int MAXT = 224;  // threads per CTA (7 warps)
-constexpr int MAXREG = ST_TC3R_R <= 2 ? 96 : 144;  // three (R = 2) / two (R >= 3) CTAs per SM
+constexpr int MAXREG = ST_TC3R_R <= 2 ? 96 : 128;  // three (R = 2) / two (R >= 3) CTAs per SM: at most
+                                                   // 4 warps x 32 x 128 registers on an SMSP (16384)
 template <int R> struct Cfg {
   static constexpr int NB = R <= 2 ? 4 : 3;  // ring depth (planes)
 };
@@ -128,6 +129,7 @@ __global__ void __maxnreg__(MAXREG)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();  // the previous kernel's writes are visible from here on
 
   const double sm = g.dx * g.dx * g.dx * (1.0 / 216.0);
   const double sk = g.dx * (1.0 / 36.0);
@@ -465,6 +467,8 @@ void lt3r(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, const 
   if (!attr) {
     attr = true;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    // two ~107 KB CTAs per SM need the largest shared-memory carve-out
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   }
   const int ntz = (g.nn + kR - 1) / kR;
   const int nth = (L.RY * g.nn + 31) / 32 * 32;
@@ -494,7 +498,7 @@ void lt3r(const CUtensorMap& mx, const CUtensorMap& mb, const OpDesc& op, const 
     }
   }
   const int kch = chunk_planes(op, NPl, NPl);
-  kern<<<(unsigned)grid, nth, bytes, s>>>(mx, mb, op, y, omega, wtot, kch, L);
+  launch_pdl(kern, dim3((unsigned)grid), dim3(nth), bytes, s, mx, mb, op, y, omega, wtot, kch, L);
 }
 }  // namespace
 

@@ -345,6 +345,7 @@ struct TsLevel {
   double omega = 0.8;
   double *D = nullptr, *Dinv = nullptr;
   int* info = nullptr;
+  int *fidx = nullptr, *fpos = nullptr;  // dense coarsest: every stored entry is an unknown (identity maps)
 };
 
 struct TsRun {
@@ -390,7 +391,7 @@ static void ts_op(TsRun& R, const TsLevel& Lv, int mode, const double* x, const 
 static void ts_vcycle(TsRun& R, int l, const double* b, double* x) {
   TsLevel& Lv = R.lv[l];
   if (Lv.Dinv) {
-    launch_dense_solve(Lv.Dinv, (int)Lv.g.P, false, b, x, R.s);
+    launch_dense_solve(Lv.Dinv, (int)Lv.g.P, Lv.fidx, Lv.fpos, Lv.g.P, false, b, x, R.s);
     ++R.launches;
     return;
   }
@@ -516,9 +517,18 @@ long long st_run_timestepping(const Geom& g0in, const MatsDev& md, const st_sour
     Lc.D = R.alloc(Pc * Pc);
     Lc.Dinv = R.alloc(Pc * Pc);
     Lc.info = (int*)R.alloc(1);
+    Lc.fidx = (int*)R.alloc((Pc + 1) / 2);
+    Lc.fpos = (int*)R.alloc((Pc + 1) / 2);
+    {
+      std::vector<int> iota((size_t)Pc);
+      for (long long e = 0; e < Pc; ++e) iota[(size_t)e] = (int)e;
+      cudaMemcpyAsync(Lc.fidx, iota.data(), Pc * sizeof(int), cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(Lc.fpos, iota.data(), Pc * sizeof(int), cudaMemcpyHostToDevice, s);
+      cudaStreamSynchronize(s);  // the host staging vector goes out of scope
+    }
     if (R.sd == 2) ts::dense_kernel<2><<<ts::nb(Pc), ts::BLK, 0, s>>>(Lc.g, Lc.A, Lc.D);
     else ts::dense_kernel<3><<<ts::nb(Pc), ts::BLK, 0, s>>>(Lc.g, Lc.A, Lc.D);
-    launch_dense_invert(Lc.D, Lc.Dinv, (int)Pc, Lc.info, s);
+    launch_dense_invert(Lc.D, Pc, Lc.fidx, (int)Pc, Lc.Dinv, Lc.info, s);
   }
   double hg[64];
   cudaMemcpyAsync(hg, gsh, 64 * sizeof(double), cudaMemcpyDeviceToHost, s);

@@ -14,6 +14,7 @@ namespace st {
 
 template <int SD, bool SP, bool TM>
 __global__ void restrict_kernel(Geom gf, Geom gc, const double* __restrict__ rf, double* __restrict__ rc) {
+  pdl_wait();
   long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= gc.N) return;
   restrict_node<SD, SP, TM>(gf, gc, rf, rc, idx);
@@ -21,6 +22,7 @@ __global__ void restrict_kernel(Geom gf, Geom gc, const double* __restrict__ rf,
 
 template <int SD, bool SP, bool TM>
 __global__ void prolong_kernel(Geom gf, Geom gc, const double* __restrict__ ec, double* __restrict__ xf) {
+  pdl_wait();
   long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= gf.N) return;
   prolong_node<SD, SP, TM>(gf, gc, ec, xf, idx);
@@ -33,6 +35,7 @@ __global__ void prolong_kernel(Geom gf, Geom gc, const double* __restrict__ ec, 
 // the last node (the pad column n+1, row n+1) and constrained fine nodes are left alone.
 __global__ void __launch_bounds__(128) prolong2s_kernel(Geom gf, Geom gc, const double* __restrict__ ec,
                                                         double* __restrict__ xf) {
+  pdl_wait();
   const int I = blockIdx.x * 128 + threadIdx.x, J = blockIdx.y, p = blockIdx.z;
   if (I >= gc.nn) return;
   if (p + gf.pg0 == 0) return;  // initial-condition plane: constrained
@@ -64,6 +67,7 @@ __global__ void __launch_bounds__(128) prolong2s_kernel(Geom gf, Geom gc, const 
 
 __global__ void __launch_bounds__(128) restrict2s_kernel(Geom gf, Geom gc, const double* __restrict__ rf,
                                                          double* __restrict__ rc) {
+  pdl_wait();
   const int I = blockIdx.x * 128 + threadIdx.x, J = blockIdx.y, Pp = blockIdx.z;
   if (I >= gc.pr) return;
   double* out = rc + (long long)Pp * gc.P + (long long)J * gc.pr + I;
@@ -90,13 +94,13 @@ __global__ void __launch_bounds__(128) restrict2s_kernel(Geom gf, Geom gc, const
 
 void launch_restrict(const Geom& gf, const Geom& gc, int kind, const double* rf, double* rc, cudaStream_t s) {
   if (gf.sd == 2 && kind == KIND_SPACE && gc.nt + 1 <= 65535) {
-    restrict2s_kernel<<<dim3((gc.pr + 127) / 128, gc.nn, gc.nt + 1), 128, 0, s>>>(gf, gc, rf, rc);
+    launch_pdl(restrict2s_kernel, dim3((gc.pr + 127) / 128, gc.nn, gc.nt + 1), dim3(128), 0, s, gf, gc, rf, rc);
     return;
   }
   int blk = 256;
   unsigned grd = (unsigned)((gc.N + blk - 1) / blk);
   bool SPc = (kind == KIND_SPACE || kind == KIND_FULL), TMc = (kind == KIND_TIME || kind == KIND_FULL);
-#define R(SD, A, B) restrict_kernel<SD, A, B><<<grd, blk, 0, s>>>(gf, gc, rf, rc)
+#define R(SD, A, B) launch_pdl(restrict_kernel<SD, A, B>, dim3(grd), dim3(blk), 0, s, gf, gc, rf, rc)
   if (gf.sd == 2) {
     if (SPc && TMc) R(2, true, true); else if (SPc) R(2, true, false); else R(2, false, true);
   } else {
@@ -111,10 +115,10 @@ void launch_prolong_add(const Geom& gf, const Geom& gc, int kind, const double* 
   bool SPc = (kind == KIND_SPACE || kind == KIND_FULL), TMc = (kind == KIND_TIME || kind == KIND_FULL);
   // the paired kernel needs an even fine pitch (16-B aligned pairs): every internal vector has one
   if (gf.sd == 2 && kind == KIND_SPACE && gf.nt + 1 <= 65535 && gf.pr % 2 == 0 && gf.P % 2 == 0 && !gf.walls) {
-    prolong2s_kernel<<<dim3((gc.nn + 127) / 128, gc.nn, gf.nt + 1), 128, 0, s>>>(gf, gc, ec, xf);
+    launch_pdl(prolong2s_kernel, dim3((gc.nn + 127) / 128, gc.nn, gf.nt + 1), dim3(128), 0, s, gf, gc, ec, xf);
     return;
   }
-#define PR(SD, A, B) prolong_kernel<SD, A, B><<<grd, blk, 0, s>>>(gf, gc, ec, xf)
+#define PR(SD, A, B) launch_pdl(prolong_kernel<SD, A, B>, dim3(grd), dim3(blk), 0, s, gf, gc, ec, xf)
   if (gf.sd == 2) {
     if (SPc && TMc) PR(2, true, true); else if (SPc) PR(2, true, false); else PR(2, false, true);
   } else {
