@@ -293,12 +293,13 @@ void build_hierarchy(st_ctx* c) {
     Ln.kind = kind;
     c->lv.push_back(Ln);
   }
-  // the dense coarsest inverse is one CTA's O(n^3) Gauss-Jordan (misc.cu): <= 4096 nodes (~0.5 s per
-  // design at the limit); larger coarsest levels need the iterative coarsest solve (ST_COARSE_GMRES)
-  if (c->opt.coarse_solver == ST_COARSE_DENSE && c->lv.back().g.N > 4096)
+  // the dense coarsest inverse is one CTA's O(n^3) Gauss-Jordan on the free nodes (misc.cu; n^3 x 16 B of
+  // L2 traffic: ~2 ms at config 4's 248, ~1 s at 2048): <= 2048 stored nodes; larger coarsest levels need
+  // the iterative coarsest solve (ST_COARSE_GMRES)
+  if (c->opt.coarse_solver == ST_COARSE_DENSE && c->lv.back().g.N > 2048)
     throw StErr{ST_E_DIVISIBILITY, "coarsest level too large for the dense solve (" +
                                        std::to_string(c->lv.back().g.N) +
-                                       " stored nodes > 4096): grid not divisible enough; use coarse_solver = "
+                                       " stored nodes > 2048): grid not divisible enough; use coarse_solver = "
                                        "ST_COARSE_GMRES (the paper's GMRES coarsest solve)"};
   for (auto& Lv : c->lv) {
     Lv.ntg = Lv.g.nt;
@@ -979,14 +980,13 @@ void vcycle(st_ctx* c, int l, bool trans, const double* b, double* x, bool in_gr
   // prolongation + correction, fused into the first post-sweep where the level kernel can read
   // x + P e itself (tc2d, space-coarsened next level, one GPU; options fuse_prolong = 0: separate kernels)
   int s0 = 0;
-  // tc2d: not on level 0: there the fused sweep (201 us) costs more than sweep + prolongation (90 + 45 us;
-  // profiles/r01/launches_c2_v42_summary.txt) — the correction pass weighs on an issue-bound kernel;
-  // tv2d: the fine level of a space-time design (configs 3, 5)
-  const double om = Lv.omega > 0.0 ? Lv.omega : c->opt.omega;
-  if (npost > 0 && c->opt.fuse_prolong && Nx.kind == KIND_SPACE && c->comm.size <= 1 &&
+  // not on level 0: there the fused sweep costs more than sweep + prolongation — tc2d: 201 vs 90 + 45 us
+  // (profiles/r01/launches_c2_v42_summary.txt), the correction pass weighs on an issue-bound kernel; the
+  // same fusion in tv2d (r02): config 3 689 -> 671 MDOF/s, the 512^2 x 512 slab 562 -> 556
+  // (profiles/r02/ab_r2.log)
+  if (l > 0 && npost > 0 && c->opt.fuse_prolong && Nx.kind == KIND_SPACE && c->comm.size <= 1 &&
       c->opt.kernel_family == ST_KERNELS_TMA &&
-      ((l > 0 && launch_op_tc2d_pro(Lv.op, Nx.g, trans, cur, Nx.x, b, oth, om, c->stream)) ||
-       (l == 0 && launch_op_tv2d_pro(Lv.op, Nx.g, trans, cur, Nx.x, b, oth, om, c->stream)))) {
+      launch_op_tc2d_pro(Lv.op, Nx.g, trans, cur, Nx.x, b, oth, Lv.omega > 0.0 ? Lv.omega : c->opt.omega, c->stream)) {
     L(c);
     std::swap(cur, oth);
     s0 = 1;

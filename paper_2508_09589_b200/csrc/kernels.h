@@ -30,9 +30,6 @@ bool launch_op_tc3r(const OpDesc& op, int mode, bool trans, bool mask, const dou
 // tv2d.cu: fine level of a space-time design with uniform capacity (configs 1, 3, 5), masked modes
 bool launch_op_tv2d(const OpDesc& op, int mode, bool trans, bool mask, const double* x, const double* b, double* y,
                     double omega, cudaStream_t s);
-// fine-level damped-Jacobi sweep from x + P e, e the correction of a space-coarsened next level (one GPU)
-bool launch_op_tv2d_pro(const OpDesc& op, const Geom& gc, bool trans, const double* x, const double* e,
-                        const double* b, double* y, double omega, cudaStream_t s);
 void launch_rap_space(const OpDesc& fop, const Geom& gc, int nl, int ns, double* out, cudaStream_t s);
 void launch_rap_time(const OpDesc& fop, int nlc, double* out, cudaStream_t s);
 void launch_rho_to_mk(const OpDesc& fop, int tau, double* out, cudaStream_t s);

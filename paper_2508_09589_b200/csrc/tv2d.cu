@@ -45,10 +45,6 @@ constexpr int RS0 = 320, RS1 = 1664;                     // layer slot: rho box 
 constexpr int NB0 = 6, NB1 = 4;                          // ring depth (planes)
 constexpr int NTH = TX * TYT;
 constexpr unsigned XBYTES = HX * HY * 8, BBYTES = TX * TY * 8;
-// prolongation fused into a Jacobi sweep (PRO, fine level): the coarse correction box of the
-// space-coarsened next level, coarse nodes (x0/2 - 2 .. x0/2 + 17) x (y0/2 - 1 .. y0/2 + 4), same plane
-constexpr int EW = 20, EH = 6, ES = 128;
-constexpr unsigned EBYTES = EW * EH * 8;
 
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned cnt) {
@@ -141,15 +137,11 @@ __device__ __forceinline__ bool next_seg(Sched& s, int ntx, int nt, Seg& sg) {
 
 // SRC: 0 = fine level from rho (the per-design k~ table op.kt, one entry per element and layer); 1 = stored per-layer
 // stiffness of a time-varying Galerkin space level (uniform capacity: the separable mass op.msc)
-// PRO (SRC 0, MODE_JAC): the sweep starts from x + P e, e the correction of the space-coarsened next
-// level (tme: its TMA map) — the V-cycle's prolongation + correction fused into the first post-sweep
-template <int SRC, int MODE, bool TRANS, bool PRO = false>
+template <int SRC, int MODE, bool TRANS>
 __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
     tv2d_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
-                const __grid_constant__ CUtensorMap tml, const __grid_constant__ CUtensorMap tme, OpDesc op,
-                const double* __restrict__ x, double* __restrict__ y, double omega, long long wtot, int kchunk,
-                int ntx) {
-  static_assert(!PRO || (MODE == MODE_JAC && SRC == 0), "prolongation is fused into fine-level Jacobi sweeps only");
+                const __grid_constant__ CUtensorMap tml, OpDesc op, const double* __restrict__ x,
+                double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx) {
   constexpr bool NX = (MODE != MODE_JAC0);
   constexpr bool NBV = (MODE != MODE_APPLY);
   constexpr bool ND = (MODE == MODE_JAC || MODE == MODE_JAC0);
@@ -162,7 +154,6 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
   double* xs = smem + 16;                    // [NB][XS]
   double* bs = xs + (NX ? NB * XS : 0);      // [NB][BS]
   double* ls = bs + (NBV ? NB * BS : 0);     // [NB][RS] layer boxes (layer q arrives with plane q)
-  double* es = ls + NB * RS;                 // [NB][ES] coarse correction boxes (PRO)
 
   const Geom& g = op.g;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
@@ -180,11 +171,11 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
   const double sm = SRC == 0 ? g.dx * g.dx * (1.0 / 36.0) * op.m.Cins : op.msc;
   const double sk = SRC == 0 ? 1.0 / 6.0 : 1.0;
   const double t00 = op.Tm[0][0] * sk, t01 = op.Tm[0][1] * sk, t11 = op.Tm[1][1] * sk;
-  const unsigned tx_plane = (NX ? XBYTES : 0u) + (NBV ? BBYTES : 0u) + (PRO ? EBYTES : 0u);
+  const unsigned tx_plane = (NX ? XBYTES : 0u) + (NBV ? BBYTES : 0u);
 
   // zero the ring once: box entries a thread reads outside the domain (clamped origin, masked
   // by 0) are then finite; the generic-proxy stores are ordered before the first TMA write
-  for (int k = tid; k < NB * ((NX ? XS : 0) + (NBV ? BS : 0) + RS + (PRO ? ES : 0)); k += NTH) xs[k] = 0.0;
+  for (int k = tid; k < NB * ((NX ? XS : 0) + (NBV ? BS : 0) + RS); k += NTH) xs[k] = 0.0;
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   __syncthreads();  // barriers initialised, ring zeroed
   pdl_wait();       // the previous kernel's writes are visible from here on
@@ -205,7 +196,6 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
     const bool hl = SRC == 0 || q < g.nt;  // layer q (SRC 0: layer nt of the padded k~ table is zero)
     mbar_expect_tx(&bar[slot], tx_plane - ((NBV && !wb) ? BBYTES : 0u) + (hl ? LBYTES : 0u));
     if (NX) tma3(xs + slot * XS, &tmx, &bar[slot], ps.x0, ps.y0, q);
-    if (PRO) tma3(es + slot * ES, &tme, &bar[slot], ps.x0 >> 1, ps.y0 >> 1, q);
     if (wb) tma3(bs + slot * BS, &tmb, &bar[slot], ps.x0, ps.y0, q);
     if (hl) {
       if (SRC == 0) tma3(ls + slot * RS, &tml, &bar[slot], ps.x0, ps.y0, q);  // padded: element x0-1 at x0
@@ -253,26 +243,6 @@ __global__ void __launch_bounds__(NTH, SRC == 0 ? 4 : 3)
       constexpr bool FIRST = decltype(first_tag)::value;
       mbar_wait(&bar[cur], (phase >> cur) & 1u);
       phase ^= 1u << cur;
-      if (PRO && q + g.pg0 > 0) {
-        // x += P e on the tile's in-domain, unconstrained nodes (the weights and order of
-        // prolong2s_kernel); entries outside the domain keep their zero or aliased values
-        double* xt = xs + cur * XS;
-        const double* et = es + cur * ES;
-        for (int e = tid; e < HY * (TX + 2); e += NTH) {
-          const int sr = e / (TX + 2), c = 1 + e % (TX + 2);
-          const int ii = x0 - 2 + c, jj = y0 - 1 + sr;
-          if (ii < 0 || ii > n || jj < 0 || jj > n) continue;
-          if (ii == 0 && jj >= g.plo && jj <= g.phi) continue;  // sink patch
-          const double* e0 = et + ((jj >> 1) - (y0 >> 1) + 1) * EW + ((ii >> 1) - (x0 >> 1) + 2);
-          double v;
-          if (!(ii & 1) && !(jj & 1)) v = e0[0];
-          else if (!(jj & 1)) v = 0.5 * (e0[0] + e0[1]);
-          else if (!(ii & 1)) v = 0.5 * (e0[0] + e0[EW]);
-          else v = 0.25 * ((e0[0] + e0[1]) + (e0[EW] + e0[EW + 1]));
-          xt[sr * HX + c] += v;
-        }
-        __syncthreads();
-      }
       const bool has = q < g.nt;
       const double* xq = xs + cur * XS + xo;
       double kn[RY + 1][2];
@@ -460,15 +430,15 @@ bool map4_tv(CUtensorMap* m, const void* base, unsigned long long nn, unsigned l
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int SRC, int MODE, bool TRANS, bool PRO = false>
+template <int SRC, int MODE, bool TRANS>
 void ltv(const CUtensorMap& mx, const CUtensorMap& mb, const CUtensorMap& ml, const OpDesc& op, const double* x,
-         double* y, double omega, cudaStream_t s, const CUtensorMap* me = nullptr) {
+         double* y, double omega, cudaStream_t s) {
   using namespace tv;
   const Geom& g = op.g;
-  auto kern = tv2d_kernel<SRC, MODE, TRANS, PRO>;
+  auto kern = tv2d_kernel<SRC, MODE, TRANS>;
   constexpr bool NX = (MODE != MODE_JAC0), NBV = (MODE != MODE_APPLY);
   constexpr int RS = SRC == 0 ? RS0 : RS1, NB = SRC == 0 ? NB0 : NB1;
-  constexpr size_t bytes = sizeof(double) * (16 + NB * ((NX ? XS : 0) + (NBV ? BS : 0) + RS + (PRO ? ES : 0)));
+  constexpr size_t bytes = sizeof(double) * (16 + NB * ((NX ? XS : 0) + (NBV ? BS : 0) + RS));
   static int resident = 0, nsm = 0;
   if (!resident) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -508,8 +478,7 @@ void ltv(const CUtensorMap& mx, const CUtensorMap& mb, const CUtensorMap& ml, co
   }
   // st_options_t chunk_planes overrides (parity tests force chunked schedules on small grids)
   const int kch = chunk_planes(op, NPl, kauto);
-  launch_pdl(kern, dim3((unsigned)grid), dim3(TX, TYT, 1), bytes, s, mx, mb, ml, me ? *me : mx, op, x, y, omega, wtot,
-             kch, (int)ntx);
+  launch_pdl(kern, dim3((unsigned)grid), dim3(TX, TYT, 1), bytes, s, mx, mb, ml, op, x, y, omega, wtot, kch, (int)ntx);
 }
 }  // namespace
 
@@ -552,32 +521,6 @@ bool launch_op_tv2d(const OpDesc& op, int mode, bool trans, bool mask, const dou
     C4(MODE_JAC0)
   }
 #undef C4
-  return true;
-}
-
-// Damped-Jacobi sweep of the fine level from x + P e (prolongation + correction fused into the first
-// post-smoothing sweep): e is the correction of the next level gc, a space coarsening of this one (same
-// time planes, one GPU). false if not covered (then: prolongation kernel + plain sweep).
-bool launch_op_tv2d_pro(const OpDesc& op, const Geom& gc, bool trans, const double* x, const double* e,
-                        const double* b, double* y, double omega, cudaStream_t s) {
-  if (op.g.walls) return false;
-  const Geom& g = op.g;
-  if (g.sd != 2 || gc.nt != g.nt || gc.nn != g.n / 2 + 1 || g.pg0 != 0 || gc.pg0 != 0 || g.nt < 1) return false;
-  if (!(op.form == FORM_RHO && !op.rho_tc && op.m.dC == 0.0 && op.kt)) return false;
-  if (op.U[0][0] != 0.0 || op.U[0][1] != 0.0 || op.U[1][0] != -1.0 || op.U[1][1] != 1.0) return false;
-  if (op.Tm[0][1] != op.Tm[1][0]) return false;
-  CUtensorMap mx{}, mb{}, ml{}, me{};
-  const unsigned long long nn = g.nn, s1 = (unsigned long long)g.pr * 8, s2 = (unsigned long long)g.P * 8;
-  if (!map3_tv(&mx, x - (g.pr + 2), (unsigned long long)g.pr + 2, nn + 1, g.nt + 1, s1, s2, tv::HX, tv::HY)) return false;
-  if (!map3_tv(&mb, b, nn, nn, g.nt + 1, s1, s2, tv::TX, tv::TY)) return false;
-  const unsigned long long w2 = (unsigned long long)g.n + 2;
-  if (!map3_tv(&ml, op.kt, w2, w2, g.nt + 1, w2 * 8, w2 * w2 * 8, tv::EX0, tv::EY)) return false;
-  // e: based like x (guarded internal vector): coordinate (X, Y, q) is coarse node (X - 2, Y - 1)
-  if (!map3_tv(&me, e - (gc.pr + 2), (unsigned long long)gc.pr + 2, (unsigned long long)gc.nn + 1, gc.nt + 1,
-               (unsigned long long)gc.pr * 8, (unsigned long long)gc.P * 8, tv::EW, tv::EH))
-    return false;
-  if (trans) ltv<0, MODE_JAC, true, true>(mx, mb, ml, op, x, y, omega, s, &me);
-  else ltv<0, MODE_JAC, false, true>(mx, mb, ml, op, x, y, omega, s, &me);
   return true;
 }
 
