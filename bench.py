@@ -573,7 +573,7 @@ def run_cuda(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "fine-level damped-Jacobi sweep (" + ("tc2d_kernel, time-constant rho" if wl["tc"] and wl["sdim"] == 2
                                                               else "tv2d_kernel, space-time rho, uniform capacity" if wl["sdim"] == 2
-                                                              else "tc3d_kernel, (3+1)D time-constant rho") + ")",
+                                                              else "tc3r_kernel, (3+1)D time-constant rho, element layers") + ")",
                      "bytes_per_launch": alg_bytes, "bytes_per_dof": wl["sweep_bpd"],
                      "bytes_source": "SURVEY.md sec. 8(d) damped-Jacobi sweep",
                      "min_bytes_per_launch": min_bytes, "min_frac": min_bytes / t_sweep / 1e9 / peak,

@@ -1,6 +1,5 @@
 #!/bin/bash
-# A/B: fine-level prolongation fusion (tv2d PRO) on / off and PDL on / off on configs 3 and 33; then the
-# tc3d row-tile variants (1 / 2 CTAs per SM) on config 4 and the 3D parity tests
+# A/B: fine-level prolongation fusion (tv2d PRO, since removed) on / off and PDL on / off on configs 3, 33, 2
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
 B=paper_2508_09589_b200
@@ -20,4 +19,3 @@ full "-DST_NO_PDL"
 bq c2_nopdl --config 2
 bq c33_nopdl --config 33 --fuse-prolong 1
 bq c3_nopdl --config 3 --fuse-prolong 1
-bash scripts/gpu_tc3d_r2.sh
