@@ -139,8 +139,6 @@ typedef struct {
                                tv2d trims the wave so the tiles form equal full groups (exp.)   */
   int32_t fuse_prolong;     /* 1 (default): prolongation + correction fused into the first
                                post-sweep where a kernel supports it; 0: separate kernels      */
-  int32_t fuse_restrict;    /* 1 (default): residual + restriction in one pass where a kernel
-                               supports it; 0: residual kernel + restriction kernel            */
   double omega_factor;      /* per-level Jacobi weight omega_l = min(omega, omega_factor / R_l)
                                (default 1.9)                                 */
   double dgks_eta;          /* FGMRES re-orthogonalisation when ||w'|| < dgks_eta ||w|| (0.1)   */

@@ -1300,7 +1300,6 @@ void st_default_options(st_options_t* o) {
   o->chunk_planes = 0;
   o->max_ctas = 0;
   o->fuse_prolong = 1;
-  o->fuse_restrict = 1;
   o->omega_factor = 1.9;
   o->dgks_eta = 0.1;
   o->graph_max_nodes = 0;

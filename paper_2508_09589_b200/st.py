@@ -47,7 +47,7 @@ class Options(C.Structure):
                 ("agg_nodes", C.c_int64), ("nu_coarse", C.c_int32),
                 ("krylov", C.c_int32), ("coarse_solver", C.c_int32), ("coarse_rtol", C.c_double),
                 ("coarse_maxit", C.c_int32), ("kernel_family", C.c_int32), ("chunk_planes", C.c_int32),
-                ("max_ctas", C.c_int32), ("fuse_prolong", C.c_int32), ("fuse_restrict", C.c_int32),
+                ("max_ctas", C.c_int32), ("fuse_prolong", C.c_int32),
                 ("omega_factor", C.c_double), ("dgks_eta", C.c_double), ("graph_max_nodes", C.c_int64),
                 ("smoother_rtol", C.c_double), ("nu_fine_nodes", C.c_int64),
                 ("pitch_align", C.c_int32)]

@@ -137,7 +137,7 @@ def test_options_defaults_and_knobs_are_options():
     assert o.krylov == st.ST_KRYLOV_FGMRES and o.coarse_solver == st.ST_COARSE_DENSE
     assert o.coarse_rtol == 1e-6 and o.coarse_maxit == 200
     assert o.kernel_family == st.ST_KERNELS_TMA and o.chunk_planes == 0 and o.max_ctas == 0
-    assert o.fuse_prolong == 1 and o.fuse_restrict == 1
+    assert o.fuse_prolong == 1
     assert o.omega_factor == 1.9 and o.dgks_eta == 0.1 and o.graph_max_nodes == 0 and o.smoother_rtol == 0.0
     assert o.nu_fine_nodes == 10000000 and o.pitch_align == 4
     hdr = open(os.path.join(ROOT, "include", "st.h")).read()
