@@ -74,7 +74,7 @@ enum { ST_SMOOTH_JACOBI = 0, ST_SMOOTH_CHEBYSHEV = 1, ST_SMOOTH_GMRES = 2 };
  * vectors — the memory plan of config 3 on one GPU). The GMRES smoother is not a
  * fixed linear map: ST_KRYLOV_GMRES requires ST_SMOOTH_JACOBI. */
 enum { ST_KRYLOV_FGMRES = 0, ST_KRYLOV_GMRES = 1 };
-/* Coarsest-level solver: exact dense inverse (default, <= 2048 stored nodes) or the paper's GMRES(<= coarse_maxit)
+/* Coarsest-level solver: exact dense inverse (default, <= 4096 stored nodes) or the paper's GMRES(<= coarse_maxit)
  * with Jacobi preconditioning to coarse_rtol (200 iterations, rtol 1e-6). */
 enum { ST_COARSE_DENSE = 0, ST_COARSE_GMRES = 1 };
 /* Stencil-kernel family (test / experiment hook; every family computes the same operator): the TMA

@@ -293,13 +293,14 @@ void build_hierarchy(st_ctx* c) {
     Ln.kind = kind;
     c->lv.push_back(Ln);
   }
-  // the dense coarsest inverse is one CTA's O(n^3) Gauss-Jordan on the free nodes (misc.cu; n^3 x 16 B of
-  // L2 traffic: ~2 ms at config 4's 248, ~1 s at 2048): <= 2048 stored nodes; larger coarsest levels need
-  // the iterative coarsest solve (ST_COARSE_GMRES)
-  if (c->opt.coarse_solver == ST_COARSE_DENSE && c->lv.back().g.N > 2048)
+  // the dense coarsest inverse is one CTA's O(n^3) Gauss-Jordan on the free nodes (misc.cu): <= 4096
+  // stored nodes (n^3 element updates at ~1.5e9 / s in one CTA: ~10 ms at config 4's 248 free nodes, a few
+  // seconds per design near the limit); larger coarsest levels need the iterative coarsest solve
+  // (ST_COARSE_GMRES)
+  if (c->opt.coarse_solver == ST_COARSE_DENSE && c->lv.back().g.N > 4096)
     throw StErr{ST_E_DIVISIBILITY, "coarsest level too large for the dense solve (" +
                                        std::to_string(c->lv.back().g.N) +
-                                       " stored nodes > 2048): grid not divisible enough; use coarse_solver = "
+                                       " stored nodes > 4096): grid not divisible enough; use coarse_solver = "
                                        "ST_COARSE_GMRES (the paper's GMRES coarsest solve)"};
   for (auto& Lv : c->lv) {
     Lv.ntg = Lv.g.nt;

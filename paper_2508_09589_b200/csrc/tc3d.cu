@@ -78,7 +78,10 @@ template <bool FACE0> __host__ __device__ constexpr int kslot(int k) {
                         // measured slower: 634 vs ~580 us per config-4 sweep
 #endif
 template <int SRC, int MODE, bool TRANS>
-__global__ void __launch_bounds__(NTH, SRC == 0 ? ST_TC3D_MINB : 1)
+#ifndef ST_TC3D_MINB1
+#define ST_TC3D_MINB1 1  // resident CTAs per SM of the stored-stencil variants (54 weights per node)
+#endif
+__global__ void __launch_bounds__(NTH, SRC == 0 ? ST_TC3D_MINB : ST_TC3D_MINB1)
     tc3d_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, OpDesc op,
                 const double* __restrict__ x, double* __restrict__ y, double omega, long long wtot, int kchunk, int ntx,
                 int nty) {

@@ -139,7 +139,7 @@ def test_st_plan_reproduces_the_paper_hierarchies():
         got = _plan_levels(2, cs["n"], cs["nt"], m, tau=cs["tau"], max_levels=cs["n_levels"], coarse_max_nodes=8,
                            coarse_solver=st.ST_COARSE_GMRES)
         assert [[a, b] for a, b, _ in got] == cs["levels"], cs["name"]
-    # the dense coarsest solve refuses them (more than 2048 stored nodes), with a clear error
+    # the dense coarsest solve refuses them (more than 4096 stored nodes), with a clear error
     cs = cases[0]
     with pytest.raises(st.StError, match="ST_COARSE_GMRES"):
         _plan_levels(2, cs["n"], cs["nt"], (cs["C_ins"], cs["C_con"], 1.0, cs["k_ins"], cs["k_con"], 3.0), tau=cs["tau"],
