@@ -219,24 +219,27 @@ void launch_rhs_combine(const Geom& g, const double* f, const double* KxD, doubl
 // Element sensitivities: dJ_e = -lambda_e^T (C' U(x)M_sp + k~' Tm(x)K_sp) T_e
 // with lambda = 0 on constrained nodes and full T. Time-constant rho: sum over layers
 // (transposed extrusion).
+// the element's nodal values of plane q: T and lambda (lambda = 0 at constrained nodes)
 template <int SD>
-__device__ double elem_sens(const OpDesc& op, const double* __restrict__ T, const double* __restrict__ lam,
-                            const int* a, int tau, double r) {
-  constexpr int NE = SG<SD>::NE;
-  const Geom& g = op.g;
-  double Tb[NE], Tt[NE], Lb[NE], Lt[NE];
+__device__ __forceinline__ void sens_plane(const Geom& g, const double* __restrict__ T, const double* __restrict__ lam,
+                                           const int* a, int q, double* Tq, double* Lq) {
 #pragma unroll
-  for (int b = 0; b < NE; ++b) {
+  for (int b = 0; b < SG<SD>::NE; ++b) {
     int c[3] = {0, 0, 0};
 #pragma unroll
     for (int d = 0; d < SD; ++d) c[d] = a[d] + ((b >> d) & 1);
-    long long pn = pidx<SD>(g, c);
-    long long ib = (long long)tau * g.P + pn, it = ib + g.P;
-    Tb[b] = __ldg(T + ib);
-    Tt[b] = __ldg(T + it);
-    Lb[b] = is_cons<SD>(g, c, tau) ? 0.0 : __ldg(lam + ib);
-    Lt[b] = is_cons<SD>(g, c, tau + 1) ? 0.0 : __ldg(lam + it);
+    const long long i = (long long)q * g.P + pidx<SD>(g, c);
+    Tq[b] = __ldg(T + i);
+    Lq[b] = is_cons<SD>(g, c, q) ? 0.0 : __ldg(lam + i);
   }
+}
+
+// dJ_e of element layer tau from the bottom (b) and top (t) nodal values
+template <int SD>
+__device__ __forceinline__ double elem_sens(const OpDesc& op, const double* Tb, const double* Tt, const double* Lb,
+                                            const double* Lt, double r) {
+  constexpr int NE = SG<SD>::NE;
+  const Geom& g = op.g;
   double gG = 0.0, gK1 = 0.0, gK2 = 0.0;
 #pragma unroll
   for (int b = 0; b < NE; ++b) {
@@ -255,35 +258,50 @@ __device__ double elem_sens(const OpDesc& op, const double* __restrict__ T, cons
   return -(dC * gG + dk * gK);
 }
 
+// one thread per (spatial element, chunk of kSensChunk layers), marching in time: the top plane's nodal
+// values of layer tau are the bottom plane's of layer tau + 1 (half the loads of one thread per element
+// and layer); time-constant rho: one chunk of all layers, summed
+constexpr int kSensChunk = 8;
 template <int SD>
 __global__ void sens_kernel(OpDesc op, const double* __restrict__ T, const double* __restrict__ lam,
                             double* __restrict__ dJ) {
+  constexpr int NE = SG<SD>::NE;
   const Geom& g = op.g;
   long long ne_sp = 1;
   for (int d = 0; d < SD; ++d) ne_sp *= g.n;
-  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long total = op.rho_tc ? ne_sp : ne_sp * g.nt;
-  if (idx >= total) return;
-  long long e = idx % ne_sp;
+  const int K = op.rho_tc ? g.nt : kSensChunk;
+  const long long nch = (g.nt + K - 1) / K;
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= ne_sp * nch) return;
+  const long long e = idx % ne_sp;
+  const int t0 = (int)(idx / ne_sp) * K, t1 = min(t0 + K, g.nt);
   int a[3] = {0, 0, 0};
   long long t = e;
   for (int d = 0; d < SD; ++d) { a[d] = (int)(t % g.n); t /= g.n; }
-  if (op.rho_tc) {
-    double r = __ldg(op.rho + e);
-    double acc = 0.0;
-    for (int tau = 0; tau < g.nt; ++tau) acc += elem_sens<SD>(op, T, lam, a, tau, r);
-    dJ[e] = acc;
-  } else {
-    int tau = (int)(idx / ne_sp);
-    dJ[idx] = elem_sens<SD>(op, T, lam, a, tau, __ldg(op.rho + idx));
+  double Tb[NE], Lb[NE], Tt[NE], Lt[NE];
+  sens_plane<SD>(g, T, lam, a, t0, Tb, Lb);
+  const double rtc = op.rho_tc ? __ldg(op.rho + e) : 0.0;
+  double acc = 0.0;
+  for (int tau = t0; tau < t1; ++tau) {
+    sens_plane<SD>(g, T, lam, a, tau + 1, Tt, Lt);
+    const long long ie = (long long)tau * ne_sp + e;
+    const double v = elem_sens<SD>(op, Tb, Tt, Lb, Lt, op.rho_tc ? rtc : __ldg(op.rho + ie));
+    if (op.rho_tc) acc += v;
+    else dJ[ie] = v;
+#pragma unroll
+    for (int b = 0; b < NE; ++b) {
+      Tb[b] = Tt[b];
+      Lb[b] = Lt[b];
+    }
   }
+  if (op.rho_tc) dJ[e] = acc;
 }
 
 void launch_sensitivity(const OpDesc& op, const double* T, const double* lam, double* dJ, cudaStream_t s) {
   long long ne_sp = 1;
   for (int d = 0; d < op.g.sd; ++d) ne_sp *= op.g.n;
-  long long total = op.rho_tc ? ne_sp : ne_sp * op.g.nt;
-  unsigned grd = (unsigned)((total + 127) / 128);
+  const long long nch = op.rho_tc ? 1 : (op.g.nt + kSensChunk - 1) / kSensChunk;
+  const unsigned grd = (unsigned)((ne_sp * nch + 127) / 128);
   if (op.g.sd == 2) sens_kernel<2><<<grd, 128, 0, s>>>(op, T, lam, dJ);
   else sens_kernel<3><<<grd, 128, 0, s>>>(op, T, lam, dJ);
 }

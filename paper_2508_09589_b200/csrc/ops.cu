@@ -522,6 +522,48 @@ __global__ void __launch_bounds__(256) gersh_tv2d_kernel(OpDesc op, int pa, int 
       }
       const double sm = op.m.Cins * g.dx * g.dx / 36.0, sk = 1.0 / 6.0;
       double diag = 0.0, sum = 0.0;
+      if (p >= 2 && i >= 2 && !g.walls && op.U[0][0] == 0.0 && op.U[0][1] == 0.0) {
+        // rows without a constrained neighbour (neither the t = 0 plane nor the sink patch at x1 = 0):
+        // the same weights, branch-free; neighbours outside the domain carry zero weight (their shared
+        // elements have k~ = 0 in the zero-bordered table and no capacity)
+        const double u10 = op.U[1][0], u11 = op.U[1][1];
+        const double t00 = op.Tm[0][0], t01 = op.Tm[0][1], t10 = op.Tm[1][0], t11 = op.Tm[1][1];
+        // sums over the elements shared by the node and the neighbour at offset (ox, oy):
+        // index a = ox + 1 along x1 (0: element column 0, 1: both, 2: column 1), likewise b for x2
+        double SL[3][3], SU[3][3], SM[3][3];
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            double l = 0.0, u = 0.0, m = 0.0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int bx = e & 1, by = e >> 1;
+              if ((a == 0 && bx != 0) || (a == 2 && bx != 1) || (b == 0 && by != 0) || (b == 2 && by != 1)) continue;
+              l += kL[e];
+              u += kU[e];
+              m += cm[e];
+            }
+            SL[b][a] = l;
+            SU[b][a] = u;
+            SM[b][a] = m;
+          }
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const int h = (a != 1) + (b != 1);
+            const double mw = sm * SM[b][a] * (h == 0 ? 4.0 : (h == 1 ? 2.0 : 1.0));
+            const double kf = sk * (h == 0 ? 4.0 : (h == 1 ? -1.0 : -2.0));
+            const double KL = kf * SL[b][a], KU = hasU ? kf * SU[b][a] : 0.0;
+            const double wlo = fma(u10, mw, t10 * KL);
+            const double wmid = fma(u11, mw, fma(t11, KL, t00 * KU));
+            const double whi = t01 * KU;
+            if (a == 1 && b == 1) diag = wmid;
+            sum += fabs(wlo) + fabs(wmid) + fabs(whi);
+          }
+        if (diag != 0.0) best = sum / fabs(diag);
+      } else
       for (int k = 0; k < 9; ++k) {
         const int ox = (k % 3) - 1, oy = (k / 3) - 1;
         const int nb[3] = {i + ox, j + oy, 0};

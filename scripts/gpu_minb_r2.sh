@@ -13,3 +13,6 @@ for v in "-DST_TC3D_MINB1=2" "-DST_TC3D_MINB1=1"; do
 done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:tc3r -s 3 -c 1 -o gpurun_out/ncu_tc3r_2cta \
   python scripts/prof_op.py 2 0 3 64 128 tc c4 > gpurun_out/ncu_tc3r_2cta.log 2>&1; echo "ncu tc3r rc=$?"
+rm -f paper_2508_09589_b200/build/tc3d.o; python -c "from paper_2508_09589_b200 import build as b; b.build()" > /dev/null 2>&1
+timeout 600 python -m pytest tests/test_gpu_schedules.py -m gpu -q -x -k "pde_filter" -p no:cacheprovider > gpurun_out/pytest_pf.log 2>&1; echo "pytest pde filter rc=$?"; tail -1 gpurun_out/pytest_pf.log
+for k in 1 2; do timeout 600 python bench.py --config 2 > gpurun_out/c2_rerun_$k.json 2>/dev/null; python -c "import json; d=json.load(open('gpurun_out/c2_rerun_$k.json')); s=d['solver']; print('config 2 rerun', round(d['value']/1e6,1), 'e2e', round(d['e2e']['value']/1e6,1), s['fwd_ms'], s['setup_ms'])"; done
