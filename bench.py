@@ -368,12 +368,8 @@ def run_cuda(args):
             solver.filter(dJt, dJd, transpose=True)
             solver.oc_update(rho_d, dJd, rnew)
             rho_d.copy_(rnew)
-        else:
-            solver.solve(rho, T)
-            a = solver.stats()
-            solver.adjoint(rho, None, lam)        # compliance: dphi/dT = f (R-8)
-            b = solver.stats()
-            solver.sensitivity(rho, T, lam, dJ)
+        else:  # st_design_step = st_solve + st_adjoint (compliance: dphi/dT = f, R-8) + st_sensitivity
+            a, b = solver.design_step(rho, None, T, lam, dJ)
         its.append((a["iterations"], b["iterations"], a["solve_ms"], b["solve_ms"], b["setup_ms"],
                     a["rel_residual"], b["rel_residual"], a["vcycles"], b["vcycles"]))
 
@@ -524,9 +520,7 @@ def run_cuda(args):
             flush.fill_(1.0)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            solver.solve(rho_h, T_h)
-            solver.adjoint(rho_h, None, lam_h)
-            solver.sensitivity(rho_h, T_h, lam_h, dJ_h)
+            solver.design_step(rho_h, None, T_h, lam_h, dJ_h)
             torch.cuda.synchronize()
             et.append(time.perf_counter() - t0)
         ems = statistics.mean(et) * 1e3
@@ -534,8 +528,8 @@ def run_cuda(args):
             t = torch.tensor([ems], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-        h2d = 3 * 8 * nd + 8 * N * 4          # rho x3; T in (solve, sens); lambda in (adjoint, sens)
-        d2h = 8 * N * 2 + 8 * ndj             # T, lambda, dJ
+        h2d = 8 * nd + 8 * N * 2              # rho once; T and lambda initial guesses (st_design_step)
+        d2h = 8 * N * 2 + 8 * ndj             # T (during the adjoint solve), lambda, dJ
         e2e = {"value": 2.0 * N_global / (ems / 1e3), "unit": "DOF/s", "ms_per_step": ems,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 

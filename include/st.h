@@ -122,7 +122,7 @@ typedef struct {
                                one CUDA graph launch per cycle                              */
   int32_t verbose;
   int64_t agg_nodes;        /* time slabs: agglomerate a level once it has fewer than this
-                               many nodes per rank (default 16384)                          */
+                               many nodes per rank (default 262144)                         */
   int32_t nu_coarse;        /* Jacobi sweeps (pre = post) on the coarse levels; 0 = nu_pre /
                                nu_post there too (default 5; nu_pre = nu_post = 2 on the fine
                                level: DESIGN.md sec. 9)                                     */
@@ -224,7 +224,7 @@ typedef struct {
 
 /* Fill `o` with the library defaults (rtol 1e-8, restart 16, FGMRES, Jacobi nu 2/2 on the fine level and
  * 5/5 on the coarse levels, weight cap 0.75, omega_factor 1.9, lambda_crit 0.5, coarse_max_nodes 400, dense
- * coarsest solve, agg_nodes 16384, TMA kernels, automatic chunking, both transfer fusions on). */
+ * coarsest solve, agg_nodes 262144, TMA kernels, automatic chunking, both transfer fusions on). */
 void st_default_options(st_options_t* o);
 
 /* Validate, run Algorithm 1, allocate all workspaces, assemble f on the device.
@@ -251,6 +251,19 @@ int st_adjoint(st_ctx_t* ctx, const double* rho, const double* dJdT, double* lam
  * summed through time for a time-constant design. */
 int st_sensitivity(st_ctx_t* ctx, const double* rho, const double* T, const double* lambda,
                    double* dJ);
+
+/* One design iteration's state work in one call (the per-iteration work of the
+ * optimisation loop of PAPER.md sec. 4): st_solve(rho, T), then st_adjoint(rho, dJdT, lambda), then
+ * st_sensitivity(rho, T, lambda, dJ), with identical arguments, layouts and results. rho is bound (and
+ * a host design copied to the device) once; T and lambda are in = initial guesses, out = solutions;
+ * dJdT = NULL selects the compliance. With HOST vectors the result copies overlap the next phase: T
+ * goes back to the host on a side stream during the adjoint solve, lambda during the sensitivities,
+ * and the sensitivities read T from its device copy (no second upload) — host traffic per call:
+ * rho, T, lambda (+ dJdT) in, T, lambda, dJ out. fwd_stats (nullable) receives the forward solve's
+ * statistics; st_get_stats afterwards reports the adjoint solve's. Returns ST_OK, or the first
+ * solve's ST_E_NOT_CONVERGED (both solves run, all outputs written), or an error. */
+int st_design_step(st_ctx_t* ctx, const double* rho, const double* dJdT, double* T, double* lambda,
+                   double* dJ, st_stats_t* fwd_stats);
 
 /* Test hook: y = K x (transpose = 0) or K^T x (1); bc = 1 applies the eliminated
  * operator m_f K m_f + m_c, bc = 0 the unconstrained K. */

@@ -119,6 +119,10 @@ struct st_ctx {
   st_stats_t stats{};
   long long launches = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  // st_design_step with host vectors: the side stream that copies results back while the next phase
+  // computes, and its ordering events (created on first use)
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_rdy[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
   // time slabs: rank, owned fine planes [o0, o0 + nown) of the local vector (o0 = 0 on rank 0,
   // else 1: local plane 0 is the ghost copy of the previous rank's last plane)
   Comm comm;
@@ -1261,9 +1265,66 @@ void free_ctx(st_ctx* c) {
     if (c->gexec[d]) cudaGraphExecDestroy(c->gexec[d]);
   if (c->e0) cudaEventDestroy(c->e0);
   if (c->e1) cudaEventDestroy(c->e1);
+  for (int k = 0; k < 2; ++k) {
+    if (c->ev_rdy[k]) cudaEventDestroy(c->ev_rdy[k]);
+    if (c->ev_done[k]) cudaEventDestroy(c->ev_done[k]);
+  }
+  if (c->cstream) cudaStreamDestroy(c->cstream);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
+
+// entries of dJ this rank writes (owned element layers; time-constant: the spatial design)
+long long sens_count(const st_ctx* c) {
+  const Level& L0 = c->lv[0];
+  long long nsp = 1;
+  for (int d = 0; d < c->sd; ++d) nsp *= c->grid.n;
+  return c->tc ? nsp : nsp * (L0.dist ? L0.nloc : L0.g.nt);
+}
+
+// dJ (device, sens_count entries) from the internal T and lambda (ghost planes refreshed)
+void sens_core(st_ctx* c, const double* r, const double* Ti, const double* li, double* dj) {
+  const Level& L0 = c->lv[0];
+  OpDesc op = L0.op;
+  op.rho = r;
+  op.g.nt = L0.dist ? L0.nloc : L0.g.nt;  // owned element layers
+  launch_sensitivity(op, Ti, li, dj, c->stream);
+  L(c);
+  check_launch();
+  if (c->tc) allreduce(c, dj, sens_count(c));  // time-constant design: sum through time over all slabs
+}
+
+// caller vector (host or device, dense owned planes) -> internal vector; a host vector is copied into
+// `scratch` (a free device buffer of >= Nd entries) first
+void pack_in_via(st_ctx* c, const double* user, double* internal, double* scratch, bool ghost) {
+  if (!user) throw StErr{ST_E_INVALID_ARG, "null pointer"};
+  const double* d = user;
+  if (!is_device_ptr(user)) {
+    CK(cudaMemcpyAsync(scratch, user, c->Nd * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    d = scratch;
+  }
+  launch_relayout(c->gd0, d, c->lv[0].g, internal + c->voff, c->stream);
+  L(c);
+  if (ghost) halo(c, 0, internal);
+}
+
+// side-stream copies of st_design_step: slot k's copy starts once the library stream reaches this
+// point (ev_rdy[k]) and runs beside whatever the library stream does next; side_wait(k) makes the
+// library stream wait for it (ev_done[k])
+void side_copy(st_ctx* c, int k, void* dst, const void* src, long long n, cudaMemcpyKind kind) {
+  if (!c->cstream) {
+    CK(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&c->ev_rdy[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming));
+    }
+  }
+  CK(cudaEventRecord(c->ev_rdy[k], c->stream));
+  CK(cudaStreamWaitEvent(c->cstream, c->ev_rdy[k], 0));
+  CK(cudaMemcpyAsync(dst, src, n * sizeof(double), kind, c->cstream));
+  CK(cudaEventRecord(c->ev_done[k], c->cstream));
+}
+void side_wait(st_ctx* c, int k) { CK(cudaStreamWaitEvent(c->stream, c->ev_done[k], 0)); }
 
 }  // namespace
 
@@ -1292,7 +1353,11 @@ void st_default_options(st_options_t* o) {
   o->full_coarsening = 0;
   o->use_graphs = 1;
   o->verbose = 0;
-  o->agg_nodes = 16384;
+  // 256 Ki nodes per rank: below that a distributed level's sweep (a few us per rank) costs less than
+  // the halo exchange each sweep needs (two NCCL plane messages, ~10-20 us), while the replicated
+  // level costs one all-gather per V-cycle; config 3 on 8 ranks gathers level 6 (65^2 x 257 nodes, 8.7 MB)
+  // instead of level 9 — 33 fewer exchanges per V-cycle
+  o->agg_nodes = 262144;
   o->krylov = ST_KRYLOV_FGMRES;
   o->coarse_solver = ST_COARSE_DENSE;
   o->coarse_rtol = 1e-6;
@@ -1417,7 +1482,7 @@ int st_setup(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* 
       }
       c->sd = grid->sdim;
       c->tc = (c->opt.design_mode == ST_TIME_CONSTANT);
-      if (c->opt.agg_nodes <= 0) c->opt.agg_nodes = 16384;
+      if (c->opt.agg_nodes <= 0) c->opt.agg_nodes = 262144;
       if (dist && dist->size > 1) {
         c->comm.rank = dist->rank;
         c->comm.size = dist->size;
@@ -1511,22 +1576,99 @@ int st_sensitivity(st_ctx_t* c, const double* rho, const double* T, const double
     double* li = pool(c, 1);
     pack_in(c, T, Ti, 1, true);
     pack_in(c, lambda, li, 2, true);
-    const Level& L0 = c->lv[0];
-    OpDesc op = L0.op;
-    op.rho = r;
-    op.g.nt = L0.dist ? L0.nloc : L0.g.nt;  // owned element layers
-    long long nsp = 1;
-    for (int d = 0; d < c->sd; ++d) nsp *= c->grid.n;
-    const long long ndj = c->tc ? nsp : nsp * op.g.nt;
+    const long long ndj = sens_count(c);
     bool staged = false;
     double* dj = out_ptr(c, dJ, ndj, 0, false, &staged);  // after the packs' relayouts (stream order)
-    launch_sensitivity(op, Ti, li, dj, c->stream);
-    L(c);
-    check_launch();
-    if (c->tc) allreduce(c, dj, ndj);  // time-constant design: sum through time over all slabs
+    sens_core(c, r, Ti, li, dj);
     if (staged) copy_back(c, dJ, dj, ndj);
     else CK(cudaStreamSynchronize(c->stream));
     return ST_OK;
+  });
+}
+
+int st_design_step(st_ctx_t* c, const double* rho, const double* dJdT, double* T, double* lambda, double* dJ,
+                   st_stats_t* fwd_stats) {
+  return guarded([&]() -> int {
+    if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
+    if (!T || !lambda || !dJ) throw StErr{ST_E_INVALID_ARG, "null pointer"};
+    CK(cudaSetDevice(c->device));
+    const bool hT = !is_device_ptr(T), hl = !is_device_ptr(lambda), hj = !is_device_ptr(dJ);
+    // host initial guesses go through the staging buffer S0 on the side stream: T0 while the design-
+    // dependent setup runs, lambda0 while the forward solve runs
+    double* S0 = (hT || hl) ? stage(c, 0, c->Nd) : nullptr;
+    if (hT) side_copy(c, 0, S0, T, c->Nd, cudaMemcpyHostToDevice);
+    // ---- forward solve (as st_solve); rho is bound (a host design uploaded) once for the whole step
+    prepare(c, rho);
+    const double* r = c->lv[0].op.rho;
+    make_forward_rhs(c, c->rhs);
+    if (hT) side_wait(c, 0);
+    launch_relayout(c->gd0, hT ? S0 : T, c->lv[0].g, c->xint + c->voff, c->stream);
+    L(c);
+    if (hl) side_copy(c, 1, S0, lambda, c->Nd, cudaMemcpyHostToDevice);  // after T0 left S0
+    launch_set_bc_values(c->lv[0].g, c->bcs.T0, c->xint, c->stream);
+    L(c);
+    halo(c, 0, c->xint);
+    const int rc1 = fgmres(c, false, c->rhs, c->xint);
+    st_stats_t s1 = c->stats;
+    // lambda0 (host) -> its internal layout in pool slot 1, freeing S0
+    if (hl) {
+      side_wait(c, 1);
+      launch_relayout(c->gd0, S0, c->lv[0].g, pool(c, 1) + c->voff, c->stream);
+      L(c);
+    }
+    // T -> its dense layout: the caller's device vector, or S0 (kept until the sensitivities; its
+    // copy to the host runs on the side stream during the adjoint solve)
+    const Geom go = owned_geom(c);
+    double* Td = hT ? S0 : T;
+    launch_relayout(go, c->xint + c->voff, c->gd0, Td, c->stream);
+    L(c);
+    if (hT) side_copy(c, 0, T, Td, c->Nd, cudaMemcpyDeviceToHost);
+    // ---- adjoint solve (as st_adjoint)
+    // (a pool slot used as a DENSE buffer is zeroed again afterwards: the level kernels read the pad
+    // entries of internal vectors, which must stay zero)
+    if (dJdT) {
+      pack_in_via(c, dJdT, c->rhs, pool(c, 0), false);
+      if (!is_device_ptr(dJdT)) CK(cudaMemsetAsync(pool(c, 0), 0, c->Nd * sizeof(double), c->stream));
+    } else {
+      make_source(c, c->rhs);
+    }
+    launch_mask_free(c->lv[0].g, c->rhs, c->rhs, c->stream);
+    L(c);
+    if (hl) CK(cudaMemcpyAsync(c->xint, pool(c, 1), c->N * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    else {
+      launch_relayout(c->gd0, lambda, c->lv[0].g, c->xint + c->voff, c->stream);
+      L(c);
+    }
+    launch_set_bc_values(c->lv[0].g, 0.0, c->xint, c->stream);
+    L(c);
+    halo(c, 0, c->xint);
+    const int rc2 = fgmres(c, true, c->rhs, c->xint);
+    // lambda -> dense (the caller's device vector, or pool slot 0 copied back on the side stream)
+    double* ld = hl ? pool(c, 0) : lambda;
+    launch_relayout(go, c->xint + c->voff, c->gd0, ld, c->stream);
+    L(c);
+    if (hl) side_copy(c, 1, lambda, ld, c->Nd, cudaMemcpyDeviceToHost);
+    // ---- sensitivities from the internal lambda (xint) and T re-laid out from its dense copy
+    halo(c, 0, c->xint);
+    double* Ti = pool(c, 1);
+    launch_relayout(c->gd0, Td, c->lv[0].g, Ti + c->voff, c->stream);
+    L(c);
+    halo(c, 0, Ti);
+    const long long ndj = sens_count(c);
+    double* dj = hj ? pool(c, 2) : dJ;
+    sens_core(c, r, Ti, c->xint, dj);
+    if (hj) {
+      CK(cudaMemcpyAsync(dJ, dj, ndj * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemsetAsync(dj, 0, ndj * sizeof(double), c->stream));
+    }
+    if (hl) {
+      side_wait(c, 1);
+      CK(cudaMemsetAsync(ld, 0, c->Nd * sizeof(double), c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->cstream) CK(cudaStreamSynchronize(c->cstream));
+    if (fwd_stats) *fwd_stats = s1;
+    return rc1 != ST_OK ? rc1 : rc2;
   });
 }
 
@@ -1971,7 +2113,7 @@ int st_plan(const st_grid_t* grid, const st_materials_t* mats, const st_bcs_t* b
     if (opts) c.opt = *opts;
     else st_default_options(&c.opt);
     if (c.opt.coarse_max_nodes < 8) c.opt.coarse_max_nodes = 8;
-    if (c.opt.agg_nodes <= 0) c.opt.agg_nodes = 16384;
+    if (c.opt.agg_nodes <= 0) c.opt.agg_nodes = 262144;
     c.sd = grid->sdim;
     c.comm.rank = rank;
     c.comm.size = size;

@@ -134,6 +134,8 @@ def load_library(path: str = LIB_PATH):
         getattr(lib, name).argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     lib.st_adjoint.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.st_sensitivity.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.st_design_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   P(Stats)]
     lib.st_apply.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]
     lib.st_rhs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.st_vcycle.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
@@ -366,6 +368,15 @@ class Solver:
     def sensitivity(self, rho, T, lam, dJ):
         return self._check(self.lib.st_sensitivity(self.ctx, self._rho(rho), self._nodes(T, "T"),
                                                    self._nodes(lam, "lambda"), _ptr(dJ, self._owned_design(), "dJ")))
+
+    def design_step(self, rho, dJdT, T, lam, dJ, allow_nc=False):
+        """st_design_step: forward solve, adjoint solve and sensitivities in one call (host vectors: result
+        copies overlap the next phase). Returns (forward stats, adjoint stats)."""
+        fs = Stats()
+        self._check(self.lib.st_design_step(self.ctx, self._rho(rho), self._nodes(dJdT, "dJdT"), self._nodes(T, "T"),
+                                            self._nodes(lam, "lambda"), _ptr(dJ, self._owned_design(), "dJ"),
+                                            C.byref(fs)), allow_nc)
+        return {k: getattr(fs, k) for k, _ in Stats._fields_}, self.stats()
 
     def apply(self, rho, x, y, transpose=False, bc=True):
         return self._check(self.lib.st_apply(self.ctx, self._rho(rho), self._nodes(x, "x"), self._nodes(y, "y"),

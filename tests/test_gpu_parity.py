@@ -495,3 +495,44 @@ def test_paper_example_presets_match_oracle(case):
     solver.sensitivity(dev(rho), T, lam, dJ)
     assert rel(host(dJ).reshape(dJ_ref.shape), dJ_ref) <= 1e-7
     solver.close()
+
+
+@pytest.mark.parametrize("case", [(2, 16, 16, CFG1_MATS, 0.0, "uniform", False, ("uniform", 1.0, 0.0, 0.0)),
+                                  (2, 32, 32, CFG1_MATS, 0.0, "smooth_tc", True, ("uniform", 1.0, 0.0, 0.0)),
+                                  (2, 12, 20, CFG4_MATS, 0.7, "uniform", False, ("sin", 1.0, 1.0, 2 * np.pi)),
+                                  (3, 6, 12, CFG4_MATS, 0.0, "smooth_tc", True, ("uniform", 1.0, 0.0, 0.0))],
+                         ids=["cfg1", "cfg2-replica", "nonzero-T0", "cfg4-replica"])
+@pytest.mark.parametrize("where", ["device", "host"])
+@pytest.mark.parametrize("rhs", ["compliance", "caller"])
+def test_design_step_matches_oracle_and_separate_calls(case, where, rhs):
+    """st_design_step (forward solve, adjoint solve, sensitivities in one call; host results copied
+    back on a side stream while the next phase runs) gives the oracle's T, lambda and dJ
+     and the same vectors as st_solve + st_adjoint + st_sensitivity."""
+    sdim, n, nt, mats, T0, design, tc, src = case
+    solver, prob = make_pair(sdim, n, nt, mats=mats, T0=T0, source=src, time_constant=tc, rtol=1e-10, maxit=400)
+    rho = _rho(sdim, n, nt, design, 0, tc).reshape(-1)
+    rho_o = rho.reshape(((n,) * sdim) if tc else ((nt,) + (n,) * sdim))
+    T_ref, lam_ref = prob.solve_both(rho_o)
+    dJ_ref = prob.sensitivity(rho_o, T_ref, lam_ref)
+    g = prob.compliance_rhs() if rhs == "caller" else None
+    N = prob.mesh.n_nodes
+    if where == "device":
+        mk = lambda a: dev(a)
+        back = host
+    else:
+        mk = lambda a: np.ascontiguousarray(a, dtype=np.float64).copy()
+        back = lambda a: a
+    T, lam, dJ = mk(np.zeros(N)), mk(np.zeros(N)), mk(np.zeros(rho.size))
+    fs, as_ = solver.design_step(mk(rho), None if g is None else mk(g), T, lam, dJ, allow_nc=True)
+    assert fs["converged"] == 1 and as_["converged"] == 1 and fs["rel_residual"] <= 1e-10, (fs, as_)
+    assert rel(back(T), T_ref) <= 1e-8, rel(back(T), T_ref)
+    assert rel(back(lam), lam_ref) <= 1e-8, rel(back(lam), lam_ref)
+    assert rel(back(dJ).reshape(dJ_ref.shape), dJ_ref) <= 1e-7
+    # the three separate calls from the same initial guesses: the same kernels in the same order
+    T2, lam2, dJ2 = mk(np.zeros(N)), mk(np.zeros(N)), mk(np.zeros(rho.size))
+    solver.solve(mk(rho), T2)
+    solver.adjoint(mk(rho), None if g is None else mk(g), lam2)
+    solver.sensitivity(mk(rho), T2, lam2, dJ2)
+    for a, b in ((T, T2), (lam, lam2), (dJ, dJ2)):
+        assert rel(back(a), back(b)) <= 1e-14, rel(back(a), back(b))
+    solver.close()

@@ -74,7 +74,13 @@ def _worker(rank, size, port, case, q):
         dJ = torch.zeros(nd, dtype=torch.float64, device=dev)
         solver.sensitivity(rd, T, lam, dJ)
         torch.cuda.synchronize()
-        out = dict(rank=rank, lay=lay, T=T.cpu().numpy(), lam=lam.cpu().numpy(), dJ=dJ.cpu().numpy(),
+        # st_design_step with HOST vectors on the slab (side-stream copies, ghost refreshes): the same
+        # vectors as the three calls above
+        Th, lh, jh = np.zeros(npl * P), np.zeros(npl * P), np.zeros(nd)
+        solver.design_step(np.ascontiguousarray(rho_loc).reshape(-1), np.ascontiguousarray(g), Th, lh, jh,
+                           allow_nc=True)
+        ds = max(rel(Th, T.cpu().numpy()), rel(lh, lam.cpu().numpy()), rel(jh, dJ.cpu().numpy()))
+        out = dict(rank=rank, lay=lay, T=T.cpu().numpy(), lam=lam.cpu().numpy(), dJ=dJ.cpu().numpy(), ds=ds,
                    Ax=Ax.cpu().numpy(), Mx=Mx.cpu().numpy(), Mtx=Mtx.cpu().numpy(),
                    its=(st_f["iterations"], st_a["iterations"]), conv=(st_f["converged"], st_a["converged"]))
         solver.close()
@@ -141,6 +147,7 @@ def test_time_slabs_match_oracle(name, size):
     for key, tol in (("Ax", 1e-13), ("Mx", 1e-12), ("Mtx", 1e-12)):
         got = np.concatenate([r[key] for r in res])
         assert rel(got, ref1[key]) <= tol, (key, rel(got, ref1[key]))
+    assert all(r["ds"] <= 1e-13 for r in res), [r["ds"] for r in res]  # st_design_step == 3 calls
     T = np.concatenate([r["T"] for r in res])
     lam = np.concatenate([r["lam"] for r in res])
     dJ = sum(r["dJ"] for r in res) / size if tc else np.concatenate([r["dJ"] for r in res])
