@@ -280,6 +280,14 @@ int st_rhs(st_ctx_t* ctx, const double* rho, double* f, double* b);
 int st_level_apply(st_ctx_t* ctx, const double* rho, int level, const double* x, double* y,
                    int transpose);
 
+/* Multigrid test hook: the transfer between level l and level l + 1 (linear
+ * interpolation P along the coarsened directions, restriction P^T). restrict_ = 1: out (level l + 1
+ * nodes) = P^T in (level l nodes), zero at the constrained coarse nodes; restrict_ = 0: out (level l
+ * nodes) = P in (level l + 1 nodes), zero at the constrained fine nodes. Vectors in the dense node
+ * order of their level (host or device). Single-rank contexts; ST_E_INVALID_ARG for the coarsest level. */
+int st_level_transfer(st_ctx_t* ctx, const double* rho, int level, const double* in, double* out,
+                      int restrict_);
+
 /* Benchmark hook: enqueue `reps` back-to-back launches of the level-l operator kernel in
  * mode (0 apply, 1 residual y = b - A x, 2 damped-Jacobi sweep, 3 first sweep from zero)
  * on the context's internal work vectors and return WITHOUT synchronising (the caller

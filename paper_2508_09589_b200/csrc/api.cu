@@ -411,7 +411,18 @@ void setup_forms(st_ctx* c) {
       Lv.st_owned = true;
     } else {  // KIND_TIME: Galerkin conduction, re-stabilised (upwind) capacity in time
       op.U[0][0] = 0.0; op.U[0][1] = 0.0; op.U[1][0] = -1.0; op.U[1][1] = 1.0;
-      if (!tv) {
+      if (!tv && po.form == FORM_RHO && c->sd == 3) {
+        // (3+1)D, time-constant design: the time-coarsened level is the fine discretisation on the
+        // doubled time step (nested spaces: the Galerkin time factor of the conduction term equals
+        // the coarse T_m; the capacity is re-stabilised, R-22), so it stays matrix-free from rho and
+        // runs the element-layer kernel (tc3r) instead of 2 x 27 stored weights per node (tc3d)
+        op.form = FORM_RHO;
+        op.rho_tc = 1;
+        op.nl = 1;
+        time_coarsen_factor(po.Tm, op.Tm);
+        Lv.st_owned = false;
+        ns = 2;
+      } else if (!tv) {
         op.form = FORM_MK;
         op.nl = 1;
         time_coarsen_factor(po.Tm, op.Tm);
@@ -599,8 +610,25 @@ void gather_planes(st_ctx* c, const Level& Nx, const double* part, double* full)
 
 // level-0 rho binding; a (2+1)D space-time fine level also gets its k~ table (one pass over the
 // design, read by tv2d instead of rho: the same bytes per sweep, no per-sweep rho^p)
+// every matrix-free level reads the design itself (level 0; (3+1)D time-constant: also the leading
+// time-coarsened levels). Captured V-cycle graphs hold the pointer: a new pointer drops them.
+void set_level_rho(st_ctx* c, const double* rho) {
+  bool coarse_moved = false;
+  for (size_t l = 0; l < c->lv.size(); ++l)
+    if (c->lv[l].op.form == FORM_RHO) {
+      if (l > 0 && c->lv[l].op.rho != rho) coarse_moved = true;
+      c->lv[l].op.rho = rho;
+    }
+  if (coarse_moved)
+    for (int d = 0; d < 2; ++d) {
+      if (c->gexec[d]) cudaGraphExecDestroy(c->gexec[d]);
+      c->gexec[d] = nullptr;
+      c->geager[d] = 0;
+    }
+}
+
 void set_fine_rho(st_ctx* c, const double* rho) {
-  c->lv[0].op.rho = rho;
+  set_level_rho(c, rho);
   if (c->kt) {
     launch_ktilde(rho, c->grid.n, c->lv[0].g.nt, c->lv[0].op.m, c->kt, c->stream);
     L(c);
@@ -620,7 +648,7 @@ const double* rho_device(st_ctx* c, const double* rho) {
 // rho -> level-0 operator pointer; returns true if rho changed since the last full setup
 bool bind_rho(st_ctx* c, const double* rho_in) {
   const double* rho = rho_device(c, rho_in);
-  c->lv[0].op.rho = rho;  // the per-design tables follow in prepare() when rho changed
+  set_level_rho(c, rho);  // the per-design tables follow in prepare() when rho changed
   // exact change detection: 128 bits of hash over the bit patterns (launch_fingerprint)
   unsigned long long* fp = reinterpret_cast<unsigned long long*>(c->dsmall + 500);
   launch_fingerprint(rho, c->ndesign, fp, c->stream);
@@ -738,7 +766,9 @@ void build_ops(st_ctx* c) {
       }
     } else if (Lv.kind == KIND_TIME) {
       if (!tv) {
-        if (Pv.op.form == FORM_RHO) {
+        if (Lv.op.form == FORM_RHO) {
+          // matrix-free from rho (set_level_rho): nothing to build
+        } else if (Pv.op.form == FORM_RHO) {
           launch_rho_to_mk(Pv.op, 0, Lv.st, c->stream);
           L(c);
         } else {
@@ -1724,6 +1754,43 @@ int st_level_apply(st_ctx_t* c, const double* rho, int level, const double* x, d
     check_launch();
     if (staged) copy_back(c, y, yd, nd);
     else CK(cudaStreamSynchronize(c->stream));
+    return ST_OK;
+  });
+}
+
+int st_level_transfer(st_ctx_t* c, const double* rho, int level, const double* in, double* out, int restrict_) {
+  return guarded([&]() -> int {
+    if (!c) throw StErr{ST_E_INVALID_ARG, "null ctx"};
+    if (level < 0 || level + 1 >= (int)c->lv.size()) throw StErr{ST_E_INVALID_ARG, "level out of range"};
+    if (c->comm.size > 1) throw StErr{ST_E_UNSUPPORTED, "st_level_transfer: single-rank contexts only"};
+    CK(cudaSetDevice(c->device));
+    prepare(c, rho);
+    Level& Lv = c->lv[level];
+    Level& Nx = c->lv[level + 1];
+    const Geom gdf = dense_of(Lv.g), gdc = dense_of(Nx.g);
+    const long long nf = nodes_of(Lv.g), ncn = nodes_of(Nx.g);
+    double* fine = level == 0 ? pool(c, 0) : Lv.x;
+    double* coarse = Nx.b;
+    bool staged = false;
+    if (restrict_) {  // out (level + 1) = m_c P^T in (level)
+      launch_relayout(gdf, in_ptr(c, in, nf, 1), Lv.g, fine, c->stream);
+      launch_restrict(Lv.g, Nx.g, Nx.kind, fine, coarse, c->stream);
+      double* od = out_ptr(c, out, ncn, 2, false, &staged);
+      launch_relayout(Nx.g, coarse, gdc, od, c->stream);
+      L(c, 3);
+      check_launch();
+      if (staged) copy_back(c, out, od, ncn);
+    } else {  // out (level) = m_f P in (level + 1): the correction added to a zero vector
+      launch_relayout(gdc, in_ptr(c, in, ncn, 1), Nx.g, coarse, c->stream);
+      CK(cudaMemsetAsync(fine, 0, (size_t)Lv.g.N * sizeof(double), c->stream));
+      launch_prolong_add(Lv.g, Nx.g, Nx.kind, coarse, fine, c->stream);
+      double* od = out_ptr(c, out, nf, 2, false, &staged);
+      launch_relayout(Lv.g, fine, gdf, od, c->stream);
+      L(c, 3);
+      check_launch();
+      if (staged) copy_back(c, out, od, nf);
+    }
+    if (!staged) CK(cudaStreamSynchronize(c->stream));
     return ST_OK;
   });
 }

@@ -104,7 +104,7 @@ class Hierarchy(C.Structure):
 
 
 EXPORTS = ["st_abi_version", "st_default_options", "st_setup", "st_destroy", "st_solve", "st_adjoint",
-           "st_sensitivity", "st_apply", "st_vcycle", "st_rhs", "st_filter", "st_oc_update", "st_dot", "st_pnorm", "st_level_apply", "st_bench_op", "st_get_stats", "st_get_hierarchy",
+           "st_sensitivity", "st_apply", "st_vcycle", "st_rhs", "st_filter", "st_oc_update", "st_dot", "st_pnorm", "st_level_apply", "st_level_transfer", "st_bench_op", "st_get_stats", "st_get_hierarchy",
            "st_local_layout", "st_nccl_unique_id", "st_nccl_comm_init", "st_nccl_comm_destroy", "st_plan",
            "st_struct_sizes",
            "st_num_nodes", "st_num_design", "st_kernel_launches", "st_strerror", "st_last_error", "st_timestep", "st_nccl_selftest", "st_pde_filter", "st_pde_filter_grad"]
@@ -149,6 +149,7 @@ def load_library(path: str = LIB_PATH):
                                        C.c_double, C.c_void_p]
     lib.st_pnorm.argtypes = [C.c_void_p, C.c_void_p, C.c_double, P(C.c_double), C.c_void_p]
     lib.st_level_apply.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
+    lib.st_level_transfer.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
     lib.st_bench_op.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
     lib.st_get_stats.argtypes = [C.c_void_p, P(Stats)]
     lib.st_timestep.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, P(TsStats)]
@@ -442,6 +443,16 @@ class Solver:
         nd = h[level]["nodes"]
         return self._check(self.lib.st_level_apply(self.ctx, self._rho(rho), level, _ptr(x, nd, "x"), _ptr(y, nd, "y"),
                                                    int(transpose)))
+
+    def level_transfer(self, rho, level, vin, vout, restrict=False):
+        """st_level_transfer: vout = P^T vin (level -> level + 1) or vout = P vin (level + 1 -> level)."""
+        h = self.hierarchy()
+        if not 0 <= level < len(h) - 1:
+            raise ValueError("level out of range")
+        nf, nc = h[level]["nodes"], h[level + 1]["nodes"]
+        a, b = (nf, nc) if restrict else (nc, nf)
+        return self._check(self.lib.st_level_transfer(self.ctx, self._rho(rho), level, _ptr(vin, a, "in"),
+                                                      _ptr(vout, b, "out"), int(bool(restrict))))
 
     def bench_op(self, rho, level, mode, reps, transpose=False):
         """Enqueue `reps` launches of the level operator kernel (internal work vectors) without

@@ -271,6 +271,52 @@ def test_coarse_operators(sdim, n, nt, tc, mats):
     solver.close()
 
 
+@pytest.mark.parametrize("sdim,n,nt,tc,opts", [(2, 16, 16, False, {}), (2, 40, 24, True, {}), (2, 8, 32, False, {}),
+                                                  (3, 4, 8, False, {}), (3, 8, 16, True, {}), (3, 10, 8, True, {}),
+                                                  (2, 16, 16, False, {"full_coarsening": 1}),
+                                                  (3, 8, 8, True, {"full_coarsening": 1}),
+                                                  (2, 16, 8, False, {"all_walls": True})])
+def test_transfer_parity(sdim, n, nt, tc, opts):
+    """Every level transfer equals the textbook linear interpolation P between the two node grids
+    (1 at coincident nodes, 1/2 to each neighbour along every coarsened direction,
+    Kronecker product over the directions) with the Dirichlet masks of DESIGN.md 'Coarse operators':
+    restriction m_c P^T r, prolongation m_f P e. Covers the space, time and full coarsening kernels of
+    both dimensions (the paired (2+1)D space kernels, the paired time kernels, the generic kernels)."""
+    opts = dict(opts)
+    walls = bool(opts.pop("all_walls", False))
+    solver, prob = make_pair(sdim, n, nt, mats=CFG4_MATS, time_constant=tc, all_walls=walls, **opts)
+    rho = dev(I.rho_uniform((n,) * sdim if tc else (nt,) + (n,) * sdim, 3))
+    H = solver.hierarchy()
+    kinds = set()
+    for l in range(len(H) - 1):
+        nf, ntf, nc, ntc, kind = H[l]["n"], H[l]["nt"], H[l + 1]["n"], H[l + 1]["nt"], H[l + 1]["kind"]
+        kinds.add(kind)
+        Ps = sp.identity((nf + 1) ** sdim, format="csr")
+        if kind in ("space", "full"):
+            Px = sp.csr_matrix(_P1(nf, "s"))
+            Ps = Px
+            for _ in range(sdim - 1):
+                Ps = sp.kron(Px, Ps)
+        Pt = sp.csr_matrix(_P1(ntf, "t")) if kind in ("time", "full") else sp.identity(ntf + 1)
+        P = sp.kron(Pt, Ps).tocsr()
+        assert P.shape == ((nf + 1) ** sdim * (ntf + 1), (nc + 1) ** sdim * (ntc + 1))
+        free = []
+        for (m, mt) in ((nf, ntf), (nc, ntc)):
+            cons, _ = O.dirichlet(O.Mesh(sdim, m, max(mt, 2)), O.BCs(all_walls=walls))
+            free.append((~cons[:(m + 1) ** sdim * (mt + 1)]).astype(float))
+        r = I.rand_vector(P.shape[0], 11 + l)
+        e = I.rand_vector(P.shape[1], 31 + l)
+        rc = torch.empty(P.shape[1], dtype=torch.float64, device=DEV)
+        xf = torch.empty(P.shape[0], dtype=torch.float64, device=DEV)
+        solver.level_transfer(rho, l, dev(r), rc, restrict=True)
+        solver.level_transfer(rho, l, dev(e), xf, restrict=False)
+        assert rel(host(rc), free[1] * (P.T @ r)) <= 1e-14, (l, H[l + 1], rel(host(rc), free[1] * (P.T @ r)))
+        assert rel(host(xf), free[0] * (P @ e)) <= 1e-14, (l, H[l + 1], rel(host(xf), free[0] * (P @ e)))
+    if not opts and n >= 8:
+        assert {"space", "time"} <= kinds, kinds
+    solver.close()
+
+
 def test_iteration_counts_reasonable():
     """Config-1 forward/adjoint converge in a modest number of outer iterations."""
     solver, prob = make_pair(2, 16, 16)
