@@ -4,15 +4,17 @@
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
 One STEP = one pass of the whole hot path on a fresh synthetic design:
-rho-dependent setup (Galerkin coarse operators, coarsest inverse, RHS), forward FGMRES+MG
+rho-dependent setup (Galerkin coarse operators, coarsest inverse, RHS), forward (F)GMRES+MG
 solve to true-residual rtol 1e-8 from T = 0, adjoint solve of the time-integrated thermal
-compliance (dJ/dT = f), element sensitivities. Workload at N = 1: BASELINE config 2
-(configs[1]): (2+1)D 256^2 x 256 elements, 16,974,593 space-time DOFs, time-constant smooth
-design. value = 2 N_n (forward + adjoint DOFs solved) per step time, summed over ranks.
-For N > 1 the space-time grid is split into N time slabs (one per GPU, NCCL over NVLink:
-halo planes, Krylov sums, agglomerated coarse levels) and the time extent
-grows with N (weak scaling in time, as BASELINE config 5): 256^2 x 256N elements, tau = N, the
-config-2 design; every rank holds a config-2-sized slab.
+compliance (dJ/dT = f), element sensitivities - one st_design_step call. Workload at N = 1:
+BASELINE config 3 (configs[2]) at full size: (2+1)D 1024^2 x 1024 elements, 1,076,890,625
+space-time DOFs, an independent smooth design per time layer, Q(t) = 1 + sin 2 pi t (the
+north_star's "largest config"; it fits one B200 with the memory plan of DESIGN.md sec. 6).
+--config 2|4|5|33 runs the other workloads. value = 2 N_n (forward + adjoint DOFs solved)
+per step time.
+For N > 1 the SAME problem is split into N time slabs (one per GPU, NCCL over NVLink: halo
+planes, Krylov sums, agglomerated coarse levels): strong scaling; config 5
+grows in time with N (weak scaling).
 Inputs are resident in HBM before the timed region; L2 is flushed (256 MB write) between
 steps. `e2e` repeats the step through the C ABI with pinned HOST buffers (copies inside).
 `--impl reference` times the CPU oracle (oracle/, SuperLU direct) on a bounded replica.
@@ -42,13 +44,16 @@ WORKLOADS = {
     2: dict(name="config2: (2+1)D 256^2x256 elements, time-constant smooth rho (sigma 3, [0.01,1]), "
                  "k=1e-3+rho^3(1-1e-3), c=1, Q=1, T=0 sink patch (10% of x1=0), T0=0",
             sdim=2, n=256, nt=256, mats=CFG1_MATS, tc=True, design="smooth_tc", source=("uniform", 1.0, 0.0, 0.0),
-            tau=1.0, opts={}, scaling="strong", bpd_iter=435.0, sweep_bpd=32.0),
+            # FGMRES(8): the same 10-13 iterations as FGMRES(16) with a cheaper Gram-Schmidt tail
+            # (profiles/r02/restart_ab.log: 704.6 -> 737.8 MDOF/s)
+            tau=1.0, opts=dict(restart=8), scaling="strong", bpd_iter=435.0, sweep_bpd=32.0),
     1: dict(name="config1: (2+1)D 16^3, rho~U[0.1,1] space-time", sdim=2, n=16, nt=16, mats=CFG1_MATS, tc=False,
             design="uniform", source=("uniform", 1.0, 0.0, 0.0), tau=1.0, opts={}, scaling="strong",
             bpd_iter=580.0, sweep_bpd=40.0),
     4: dict(name="config4: (3+1)D 64^3x128, time-constant smooth rho, c=0.1+0.9rho, k_min=1e-4", sdim=3, n=64,
             nt=128, mats=CFG4_MATS, tc=True, design="smooth_tc", source=("uniform", 1.0, 0.0, 0.0), tau=1.0,
-            opts={}, scaling="strong", bpd_iter=412.0, sweep_bpd=32.0),
+            # FGMRES(8): 25-31 iterations as with FGMRES(16) (profiles/r02/restart_ab.log: 220-222 -> 227 MDOF/s)
+            opts=dict(restart=8), scaling="strong", bpd_iter=412.0, sweep_bpd=32.0),
     5: dict(name="config5 (per GPU): (2+1)D 512^2x512, space-time design; a step = one OC design iteration "
                  "(density filter r=2, forward, adjoint, sensitivities, filter^T, OC volfrac 0.4) from rho=0.4",
             sdim=2, n=512, nt=512, mats=CFG1_MATS, tc=False, design="const", source=("uniform", 1.0, 0.0, 0.0),
