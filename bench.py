@@ -216,6 +216,29 @@ class ClockSampler:
                                        "-lms", "100", "-i", str(gpu_index)], stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
+        self.skip = 0
+
+    def wait_first(self, timeout_s: float = 5.0):
+        """Block until nvidia-smi has written its first sample: its start-up (NVML initialisation, which
+        stalls CUDA calls of this process for a few hundred ms) must not land in a short timed region
+        (config 2: 5 steps of 46 ms measured 74 ms each with the sampler started at the region's start)."""
+        if self.p is None:
+            return
+        t0 = time.time()
+        while time.time() - t0 < timeout_s:
+            try:
+                if os.path.getsize(self.f.name) > 0:
+                    return
+            except OSError:
+                return
+            time.sleep(0.02)
+
+    def mark(self):
+        """Start of the timed region: only the samples from here on (and the one just before) count."""
+        try:
+            self.skip = max(0, len(open(self.f.name).read().splitlines()) - 1)
+        except OSError:
+            self.skip = 0
 
     def stop(self):
         if self.p is None:
@@ -226,7 +249,7 @@ class ClockSampler:
         except subprocess.TimeoutExpired:
             self.p.kill()
         self.f.flush()
-        rows = [l.split(",") for l in open(self.f.name).read().splitlines() if l.strip()]
+        rows = [l.split(",") for l in open(self.f.name).read().splitlines()[self.skip:] if l.strip()]
         os.unlink(self.f.name)
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -378,6 +401,10 @@ def run_cuda(args):
         its.append((a["iterations"], b["iterations"], a["solve_ms"], b["solve_ms"], b["setup_ms"],
                     a["rel_residual"], b["rel_residual"], a["vcycles"], b["vcycles"]))
 
+    # the sampler runs from before the warm-up (its start-up stalls CUDA calls) and is read from the start
+    # of the timed region on
+    sampler = ClockSampler(local)
+    sampler.wait_first()
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
             r = rho_for(i)
@@ -391,7 +418,7 @@ def run_cuda(args):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        sampler = ClockSampler(local)
+        sampler.mark()
         l0 = solver.kernel_launches()
         times = []
         for k in range(args.steps):
