@@ -57,7 +57,8 @@ WORKLOADS = {
     5: dict(name="config5 (per GPU): (2+1)D 512^2x512, space-time design; a step = one OC design iteration "
                  "(density filter r=2, forward, adjoint, sensitivities, filter^T, OC volfrac 0.4) from rho=0.4",
             sdim=2, n=512, nt=512, mats=CFG1_MATS, tc=False, design="const", source=("uniform", 1.0, 0.0, 0.0),
-            tau=1.0, opts={}, scaling="weak", bpd_iter=583.0, sweep_bpd=40.0),
+            # FGMRES(8): as configs 2 and 4 (profiles/r02/restart_ab.log: 277.4 -> 289.9 MDOF/s, same iterations)
+            tau=1.0, opts=dict(restart=8), scaling="weak", bpd_iter=583.0, sweep_bpd=40.0),
     # BASELINE config 3 at full size: 1,076,890,625 DOFs (8.6 GB per vector). One GPU holds it with the
     # memory plan of DESIGN.md sec. 6: right-preconditioned GMRES(7) (no Z vectors; 188.9 of 192 GB),
     # stepping down to GMRES(6) (180.2 GB) on a box with less free memory; the Krylov pool as the hooks'
@@ -72,8 +73,8 @@ WORKLOADS = {
     # the 1/8 slab of config 3 on one GPU (round-1 "config 3 shape"): parity / profiling case
     33: dict(name="config3-shaped (1/8 of config 3 on one GPU): (2+1)D 512^2x512, an independent smooth field per "
                   "time layer, Q(t) = 1 + sin(2 pi t)", sdim=2, n=512, nt=512, mats=CFG1_MATS, tc=False,
-             design="smooth_layers", source=SIN_SRC, tau=1.0, opts={}, scaling="strong", bpd_iter=580.0,
-             sweep_bpd=40.0),
+             design="smooth_layers", source=SIN_SRC, tau=1.0, opts=dict(restart=8), scaling="strong", bpd_iter=580.0,
+             sweep_bpd=40.0),  # FGMRES(8): 577.9 -> 589.3 MDOF/s (profiles/r02/restart_ab.log)
 }
 DEFAULT_CONFIG = 3
 METRIC = "space-time DOFs solved/sec (FGMRES+MG to rtol 1e-8) & operator GB/s vs HBM peak"

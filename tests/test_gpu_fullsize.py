@@ -86,7 +86,8 @@ CASES = {
     # name: sdim, n, nt, time_constant, design, source, mats, solver options (bench's launch configuration)
     "config2": (2, 256, 256, True, "smooth_tc", ("uniform", 1.0, 0.0, 0.0), CFG1_MATS, {"restart": 8}),
     "config3-shaped-256": (2, 256, 256, False, "smooth_layers", ("sin", 1.0, 1.0, 2 * np.pi), CFG1_MATS, {}),
-    "config3-shaped-512": (2, 512, 512, False, "smooth_layers", ("sin", 1.0, 1.0, 2 * np.pi), CFG1_MATS, {}),
+    "config3-shaped-512": (2, 512, 512, False, "smooth_layers", ("sin", 1.0, 1.0, 2 * np.pi), CFG1_MATS,
+                           {"restart": 8}),
     "config4": (3, 64, 128, True, "smooth_tc", ("uniform", 1.0, 0.0, 0.0), CFG4_MATS, {"restart": 8}),
 }
 
